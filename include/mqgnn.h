@@ -1,0 +1,244 @@
+/*
+ * mqgnn.h — C-ABI of libmqgnn, the B200 (sm_100a) implementation of MQ-GNN's
+ * per-iteration GraphSAGE hot path.
+ *
+ * Conventions
+ *   - every entry point is extern "C", takes plain pointers/sizes, and returns
+ *     MQ_OK (0) or an MQ_ERR_* code; mq_last_error() holds the message
+ *     (thread-local).  No allocation happens behind the caller's back: all
+ *     device buffers are caller-owned and sized from the *_max bounds.
+ *   - `stream` is a cudaStream_t passed as void*.  All work is enqueued
+ *     asynchronously on it; entry points never synchronise, so a sequence of
+ *     calls can be captured into a CUDA graph.
+ *   - counts that are only known on the device (the frontier size of a hop,
+ *     the number of sampled edges) are passed as `const int32_t* n_dev`
+ *     pointers plus a host-side upper bound `n_max` that sizes the grid.
+ *   - node ids are int32 (all target shapes have < 2^31 nodes); CSR row offsets
+ *     and arc indices are int64.
+ *   - the graph handed to the sampler is the reference CSR with stored
+ *     self-loops removed (the reference drops the loop from every neighbour
+ *     list before sampling, samplers.py:162, and full_forward does the same,
+ *     nn.py:237-238); mq_strip_self_loops produces it.
+ *
+ * The reference (mqpipe, pure Python/NumPy) has no FFI; each function below
+ * names the reference Python function whose semantics it implements
+ * (paths relative to /root/reference/pkg/src/mqpipe/).
+ */
+#ifndef MQGNN_H
+#define MQGNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MQ_OK 0
+#define MQ_ERR_ARG 1
+#define MQ_ERR_CUDA 2
+#define MQ_ERR_STATE 3
+
+#define MQ_MAX_FANOUT 32
+
+/* --------------------------------------------------------------- library */
+int mq_version(void);
+const char* mq_last_error(void);
+/* Blocks until `stream` drains and reports any asynchronous kernel fault. */
+int mq_stream_check(void* stream);
+
+/* ------------------------------------------------------------ Philox draws
+ * The injected-draw contract that replaces numpy's PCG64 in
+ * samplers.py:172,174,177:  x_j = Philox4x32-10(key=(seed mod 2^32, epoch),
+ * ctr=(j>>2, row, hop, batch))[j&3].  Host and device share one
+ * implementation. */
+int mq_philox_fill_host(uint64_t seed, uint64_t epoch, uint32_t batch, uint32_t hop,
+                        uint32_t row, uint32_t count, uint32_t* out);
+int mq_philox_fill(uint64_t seed, uint64_t epoch, uint32_t batch, uint32_t hop,
+                   uint32_t row, uint32_t count, uint32_t* out_dev, void* stream);
+/* Positions chosen by the partial Fisher-Yates of `choice(pool, k)` over a
+ * pool of n (host reference of the device routine; k <= MQ_MAX_FANOUT). */
+int mq_fisher_yates_host(uint64_t seed, uint64_t epoch, uint32_t batch, uint32_t hop,
+                         uint32_t row, int64_t n, int32_t k, int64_t* pos_out);
+
+/* ------------------------------------------------------------ graph layout
+ * Replaces GraphCSR's read-only arrays (graph.py:28-91) on the device.
+ * mq_strip_self_loops: out_row_off[v] counts the arcs of rows < v with
+ * col != row; out_col receives them in CSR order.  `arc_flags_scratch` must
+ * hold mq_scan_scratch_bytes(n_arcs) bytes. */
+int64_t mq_scan_scratch_bytes(int64_t n_max);
+int mq_strip_self_loops(const int64_t* row_off, const int32_t* col, int64_t n_nodes,
+                        int64_t n_arcs, int64_t* out_row_off, int32_t* out_col,
+                        void* scratch, void* stream);
+
+/* ---------------------------------------------------- GNS cache residency
+ * Per-epoch residency index that makes the per-row hot/cold split of
+ * node_wise_block (samplers.py:168-175) O(fanout) instead of a full row scan:
+ *   hot_arc[]  = indices (ascending) of every arc whose head is resident,
+ *   hot_off[v] = number of hot arcs before row v (so row v's hot arcs are
+ *                hot_arc[hot_off[v] .. hot_off[v+1])), length n_nodes+1.
+ * resident_bits is a bitmap over node ids (CacheState.cached_mask,
+ * cache.py:20-38).  *n_hot_dev receives the hot arc count.  hot_arc must hold
+ * n_arcs entries (worst case). */
+int mq_residency_index(const int64_t* row_off, const int32_t* col, int64_t n_nodes,
+                       int64_t n_arcs, const uint32_t* resident_bits, int64_t* hot_arc,
+                       int64_t* hot_off, int64_t* n_hot_dev, void* scratch, void* stream);
+/* slot_of[v] = rank of v among resident nodes (ascending id) or -1; the HBM
+ * cache table row of a hit (cache.py:131 searchsorted).  scratch as above
+ * with n_max = n_nodes. */
+int mq_residency_slots(const uint32_t* resident_bits, int64_t n_nodes, int32_t* slot_of,
+                       int32_t* n_resident_dev, void* scratch, void* stream);
+
+/* ------------------------------------------------------------- sampling
+ * One hop of node_wise_block, SAGE arm (samplers.py:142-210): for dst row r,
+ * v = dst[r], nbrs = row v (self loops already stripped), n = |nbrs|:
+ *   n <= fanout           -> all neighbours in CSR order
+ *   hot index given       -> |hot| >= fanout ? choice(hot, fanout)
+ *                                            : hot ++ choice(cold, fanout-|hot|)
+ *   otherwise             -> choice(nbrs, fanout)
+ * with choice() the injected Philox Fisher-Yates.  Writes node ids to
+ * nbr[r*fanout + i] and the count to cnt[r].  hot_arc/hot_off may be NULL
+ * (no cache).  If key_dev is non-NULL the stream key is read on the device
+ * (key_dev = {seed mod 2^32, epoch, batch}) instead of the by-value
+ * seed/epoch/batch, so one captured CUDA graph serves every batch. */
+int mq_sample_hop(const int64_t* row_off, const int32_t* col, const int64_t* hot_arc,
+                  const int64_t* hot_off, const int32_t* dst, const int32_t* n_dst_dev,
+                  int32_t n_dst_max, int32_t fanout, uint64_t seed, uint64_t epoch,
+                  uint32_t batch, uint32_t hop, const uint32_t* key_dev, int32_t* nbr,
+                  int32_t* cnt, void* stream);
+
+/* Relabel + block emit (samplers.py:155-156, 186-200): src_ids = dst ids
+ * followed by newly seen ids in first-occurrence (row, pick) order; rows/cols
+ * are the block triplets, vals[e] = float32(1.0 / s_row).  row_ptr has
+ * n_dst+1 entries (CSR view of the triplets).  counts_dev[0] = n_src,
+ * counts_dev[1] = nnz.  dpos_tbl / first_tbl are node-indexed int32 tables
+ * that must hold -1 / INT32_MAX on entry and are restored on exit.
+ * scratch: mq_relabel_scratch_bytes(n_dst_max, fanout). */
+int64_t mq_relabel_scratch_bytes(int32_t n_dst_max, int32_t fanout);
+int mq_relabel(const int32_t* dst, const int32_t* n_dst_dev, int32_t n_dst_max,
+               const int32_t* nbr, const int32_t* cnt, int32_t fanout, int32_t* dpos_tbl,
+               int32_t* first_tbl, int32_t* row_ptr, int32_t* rows, int32_t* cols,
+               float* vals, int32_t* src_ids, int32_t* counts_dev, void* scratch,
+               void* stream);
+
+/* --------------------------------------------------------------- gather
+ * gather_features / lookup (cache.py:111-134, runtime.py:127-143):
+ *   out[i, :d] = slot_of[id] >= 0 ? cache_tbl[slot_of[id]] : store[id]
+ * store may be a device table or a pinned host table (UVA pointer) — the
+ * host-miss path.  slot_of may be NULL (everything served from store).
+ * hit_miss[0] += hits, hit_miss[1] += misses (counted only when slot_of is
+ * given).  Row pitches are in floats and must be multiples of 4. */
+int mq_gather(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
+              const float* store, int32_t store_pitch, const int32_t* ids,
+              const int32_t* n_dev, int32_t n_max, int32_t d, float* out,
+              int32_t out_pitch, unsigned long long* hit_miss, void* stream);
+
+/* ---------------------------------------------------------- SAGE numerics
+ * block_apply (nn.py:79-89): agg[r] = sum over the row's triplets, in order,
+ * of float32(val) * h[col] — sequential fp32 adds, bit-identical to np.add.at. */
+int mq_spmm_fwd(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh,
+                int32_t d, float* agg, int32_t ldagg, void* stream);
+
+/* block_apply_t + the self-path add (nn.py:92-98, 171-174):
+ * dh[c] = sum_{e: col[e]=c} val[e] * dt[row[e], :d] + (c < n_dst ? dt[c, d:2d] : 0),
+ * then, if mask_h != NULL, dh[c] *= (mask_h[c] > 0) (the ReLU mask of the
+ * layer below, nn.py:167; mask_h is that layer's activation).
+ * dh must be zeroed by this call's caller-visible semantics: the function
+ * clears rows [0, n_src) itself. */
+int mq_spmm_bwd(const int32_t* rows, const int32_t* cols, const float* vals,
+                const int32_t* counts_dev /* [n_src, nnz] */, int32_t nnz_max,
+                const int32_t* n_dst_dev, int32_t n_src_max, const float* dt, int32_t lddt,
+                int32_t d, const float* mask_h, int32_t ldm, float* dh, int32_t lddh,
+                void* stream);
+
+/* sage_forward transform (nn.py:126-131): z = [agg | h_dst] @ W with W
+ * (2*d_in, d_out) row-major.  z (pre-activation) and/or relu_out (max(z, 0))
+ * are written when non-NULL; hidden layers only need relu_out because the
+ * backward mask (pre > 0) equals (relu(pre) > 0). */
+int mq_sage_linear_fwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                       const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                       int32_t d_out, float* z, int32_t ldz, float* relu_out, int32_t ldr,
+                       void* stream);
+
+/* backward (nn.py:167-170): dW = [agg | h_dst]^T @ dz (deterministic split-K,
+ * scratch: mq_linear_bwd_w_scratch_bytes) and, if dt != NULL, dt = dz @ W^T. */
+int64_t mq_linear_bwd_w_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out);
+int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                       const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                       int32_t d_out, const float* dz, int32_t lddz, float* dW, float* dt,
+                       int32_t lddt, void* scratch, void* stream);
+
+/* batch_loss (nn.py:141-156): summed max-shifted softmax-CE over n rows;
+ * dlogits = softmax - onehot; loss_out[0] += loss (f64);  nonfinite[0] |= 1
+ * when any dlogit is NaN/Inf (FloatingPointError, nn.py:74-76). */
+int mq_softmax_ce(const float* logits, int32_t ld, const int32_t* labels,
+                  const int32_t* n_dev, int32_t n_max, int32_t n_classes, float* dlogits,
+                  int32_t lddl, double* loss_out, int32_t* nonfinite, void* stream);
+
+/* Device-side batch plan for graph replay (runtime.py:95-124): window
+ * k = cursor[0]++, batch id j = k*world + rank (round-robin deal),
+ * targets = perm[j*batch_size .. min(n_perm, (j+1)*batch_size)),
+ * n_targets[0] = that length (0 when this rank has no batch in window k),
+ * key_dev[2] = j.  key_dev[0..1] (seed, epoch) are left untouched. */
+int mq_batch_setup(const int32_t* perm, int64_t n_perm, int32_t batch_size, int32_t world,
+                   int32_t rank, int32_t* cursor_dev, int32_t* targets, int32_t* n_targets_dev,
+                   uint32_t* key_dev, void* stream);
+
+/* End-of-step bookkeeping for graph replay: loss_ring[(cursor[0]-1) mod
+ * ring_len] = loss_acc[0]; loss_acc[0] = 0 (EpochStats.losses,
+ * runtime.py:72-92, read back once per epoch instead of per batch). */
+int mq_step_commit(double* loss_acc, const int32_t* cursor_dev, double* loss_ring,
+                   int32_t ring_len, void* stream);
+
+/* labels[i] = all_labels[ids[i]] (build_minibatch target_labels, samplers.py:532) */
+int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_t* n_dev,
+                     int32_t n_max, int32_t* out, void* stream);
+
+/* adam_step (nn.py:191-206) over one flat parameter vector.  The gradient is
+ * grad32 (f32) or grad64 * grad_scale cast to f32 (the RaCoM f64 window mean,
+ * racom.py:47-57, 81-87); when grad_scale == 0 the scale is 1/grad64[n], the
+ * all-reduced contributor count packed by mq_pack_grads (expected[k],
+ * runtime.py:115-116).  step_dev is incremented on device; bias[2*(t-1)],
+ * bias[2*(t-1)+1] hold float32(1 - 0.9**t), float32(1 - 0.999**t) for
+ * t = 1..bias_len; lr is float32(learning_rate).  nonfinite[0] |= 1 on a
+ * non-finite weight. */
+int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
+            double grad_scale, int64_t n, int32_t* step_dev, const float* bias,
+            int32_t bias_len, float lr, int32_t* nonfinite, void* stream);
+/* sgd_step (nn.py:209-215) */
+int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale,
+           int64_t n, int32_t* step_dev, float lr, int32_t* nonfinite, void* stream);
+/* out64[i] = (double)grad[i] for i < n and out64[n] = (n_targets_dev[0] > 0):
+ * one f64 buffer carries the window's gradient sum and contributor count
+ * through a single all-reduce. */
+int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, double* out64,
+                  void* stream);
+
+/* RaCoM packing for the NCCL collectives (racom.py:47-57, 118-139):
+ * out64[i] = (double)in32[i];  out32[i] = (float)(in64[i] * scale). */
+int mq_f32_to_f64(const float* in32, double* out64, int64_t n, void* stream);
+int mq_f64_to_f32(const double* in64, double scale, float* out32, int64_t n, void* stream);
+
+/* ------------------------------------------------------------- utilities */
+/* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */
+int mq_scan_i32(const int32_t* in, const int32_t* n_dev, int32_t n_max, int32_t* out,
+                void* scratch, void* stream);
+
+/* ---------------------------------------------------- kernel timing hooks
+ * Bench instrumentation: when enabled, each kernel launch is bracketed by
+ * CUDA events on its stream; mq_prof_read returns per-kernel totals (ms) and
+ * launch counts.  Must be disabled while capturing a CUDA graph. */
+int mq_prof_enable(int on);
+int mq_prof_reset(void);
+int mq_prof_num_kernels(void);
+const char* mq_prof_kernel_name(int id);
+int mq_prof_read(double* total_ms, int64_t* launches, int32_t n);
+/* Number of kernel launches issued through this library since the last
+ * reset (counted whether or not timing is enabled). */
+int64_t mq_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MQGNN_H */

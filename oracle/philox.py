@@ -1,0 +1,99 @@
+"""Philox4x32-10 counter-based generator and the injected-draw contract.
+
+Third-party algorithm: Random123 Philox4x32-10 (Salmon et al., SC'11; the
+Random123 1.x headers, ``philox.h``).  Not vendored in ``/root/reference``; the
+reference samples with NumPy's PCG64 ``Generator.choice`` (``samplers.py:172,
+174,177``), whose draw count per call is data dependent and therefore cannot be
+replayed in parallel.  Parity is defined under *injected draws*
+(SURVEY.md §8c):
+
+    x_j = Philox4x32-10(key=(seed mod 2^32, epoch),
+                        ctr=(j >> 2, row, hop, batch_id))[j & 3]
+
+and ``choice(pool, k, replace=False)`` is a partial Fisher-Yates over pool
+positions with ``r = j + ((x_j * (n - j)) >> 32)``.
+
+Pinned by the Random123 known-answer vectors (``tests/golden/philox_kat.json``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+M0 = np.uint64(0xD2511F53)
+M1 = np.uint64(0xCD9E8D57)
+W0 = 0x9E3779B9
+W1 = 0xBB67AE85
+MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr, key):
+    """Vectorised Philox4x32-10.
+
+    ctr: uint32-compatible array shaped (..., 4); key: (..., 2).
+    Returns uint32 array (..., 4).
+    """
+    c = np.asarray(ctr, dtype=np.uint64) & MASK32
+    k = np.asarray(key, dtype=np.uint64) & MASK32
+    c0, c1, c2, c3 = (c[..., i].copy() for i in range(4))
+    k0, k1 = k[..., 0].copy(), k[..., 1].copy()
+    k0 = np.broadcast_to(k0, c0.shape).copy()
+    k1 = np.broadcast_to(k1, c0.shape).copy()
+    for rnd in range(10):
+        if rnd:
+            k0 = (k0 + np.uint64(W0)) & MASK32
+            k1 = (k1 + np.uint64(W1)) & MASK32
+        p0 = M0 * c0
+        p1 = M1 * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & MASK32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & MASK32
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+    return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
+
+
+def draws(seed: int, epoch: int, batch_id: int, hop: int, row: int,
+          count: int) -> np.ndarray:
+    """The first ``count`` uint32 draws x_0..x_{count-1} of one row stream."""
+    if count <= 0:
+        return np.empty(0, dtype=np.uint32)
+    blocks = (count + 3) // 4
+    ctr = np.zeros((blocks, 4), dtype=np.uint64)
+    ctr[:, 0] = np.arange(blocks, dtype=np.uint64)
+    ctr[:, 1] = row & 0xFFFFFFFF
+    ctr[:, 2] = hop & 0xFFFFFFFF
+    ctr[:, 3] = batch_id & 0xFFFFFFFF
+    key = np.array([seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF], dtype=np.uint64)
+    return philox4x32_10(ctr, key).reshape(-1)[:count]
+
+
+def fisher_yates_positions(x: np.ndarray, n: int, k: int) -> list:
+    """Pool positions chosen by a partial Fisher-Yates shuffle.
+
+    For pick j: r = j + ((x_j * (n - j)) >> 32); swap positions j and r and
+    emit the element now at j.  A sparse map replaces the O(n) array.
+    """
+    if k > n:
+        raise ValueError(f"cannot take {k} of {n} without replacement")
+    swapped: dict = {}
+    out = []
+    for j in range(k):
+        r = j + ((int(x[j]) * (n - j)) >> 32)
+        a = swapped.get(j, j)
+        b = swapped.get(r, r)
+        out.append(b)
+        swapped[r] = a
+    return out
+
+
+class RowStream:
+    """Duck-typed ``rng`` whose ``choice`` draws from one Philox row stream."""
+
+    def __init__(self, seed, epoch, batch_id, hop, row):
+        self.key = (seed, epoch, batch_id, hop, row)
+
+    def choice(self, a, size, replace=False):
+        if replace:
+            raise ValueError("the injected-draw contract is WOR only")
+        a = np.asarray(a)
+        x = draws(*self.key, count=size)
+        return a[fisher_yates_positions(x, a.size, size)]

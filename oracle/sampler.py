@@ -1,0 +1,159 @@
+"""CPU restatement of GNS-biased node-wise sampling (SAGE arm) — test oracle.
+
+Follows ``mqpipe/samplers.py`` of the reference:
+
+* ``node_wise_block``   — ``samplers.py:142-210`` (SAGE arm ``:192-200``)
+* ``sample_node_wise``  — ``samplers.py:213-226`` (extended with per-hop fanouts)
+* ``build_minibatch``   — ``samplers.py:502-540`` (node-wise dispatch only)
+* ``digest``            — ``samplers.py:63-72``
+
+The reference's ``rng.choice`` is replaced by the injected Philox row stream
+(``oracle.philox``), the contract under which the reference itself produced
+the golden vectors in ``tests/golden``.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+from .philox import draws, fisher_yates_positions
+
+
+class OracleBlock:
+    __slots__ = ("rows", "cols", "values", "src_ids", "dst_ids", "dst_in_src")
+
+    def __init__(self, rows, cols, values, src_ids, dst_ids):
+        self.rows = rows
+        self.cols = cols
+        self.values = values
+        self.src_ids = src_ids
+        self.dst_ids = dst_ids
+        self.dst_in_src = np.arange(dst_ids.size, dtype=np.int64)
+
+    @property
+    def effective_values(self):
+        return self.values
+
+    @property
+    def num_dst(self):
+        return int(self.dst_ids.size)
+
+    @property
+    def num_src(self):
+        return int(self.src_ids.size)
+
+
+def _choice(pool: np.ndarray, k: int, key) -> np.ndarray:
+    """Injected ``rng.choice(pool, size=k, replace=False)`` (samplers.py:172-177)."""
+    x = draws(*key, count=k)
+    return pool[fisher_yates_positions(x, pool.size, k)]
+
+
+def node_wise_block(row_offsets, col_indices, dst_ids, fanout: int, *, seed: int,
+                    epoch: int, batch_id: int, hop: int, cached_mask=None):
+    """One SAGE block (samplers.py:142-210, arch == 'sage')."""
+    dst_ids = np.asarray(dst_ids, dtype=np.int64)
+    src_list = list(dst_ids.tolist())
+    # last occurrence wins, as with the dict comprehension at samplers.py:156
+    src_pos = {int(v): i for i, v in enumerate(dst_ids)}
+    rows, cols, vals = [], [], []
+    for r, v in enumerate(dst_ids.tolist()):
+        nbrs = col_indices[row_offsets[v]:row_offsets[v + 1]]
+        nbrs = nbrs[nbrs != v]                      # samplers.py:162
+        n = nbrs.size
+        key = (seed, epoch, batch_id, hop, r)
+        if n <= fanout:                             # :164-167
+            sampled = nbrs
+        elif cached_mask is not None:               # :168-175
+            hot_sel = cached_mask[nbrs]
+            hot, cold = nbrs[hot_sel], nbrs[~hot_sel]
+            if hot.size >= fanout:
+                sampled = _choice(hot, fanout, key)
+            else:
+                sampled = np.concatenate(
+                    [hot, _choice(cold, fanout - hot.size, key)])
+        else:                                       # :176-177
+            sampled = _choice(nbrs, fanout, key)
+        s = sampled.size
+        for u in sampled.tolist():                  # :192-200
+            if u not in src_pos:
+                src_pos[u] = len(src_list)
+                src_list.append(u)
+            rows.append(r)
+            cols.append(src_pos[u])
+            vals.append(1.0 / s)
+    return OracleBlock(np.asarray(rows, dtype=np.int64),
+                       np.asarray(cols, dtype=np.int64),
+                       np.asarray(vals, dtype=np.float64),
+                       np.asarray(src_list, dtype=np.int64), dst_ids)
+
+
+def sample_node_wise(row_offsets, col_indices, targets, fanouts, *, seed, epoch,
+                     batch_id, cached_mask=None):
+    """Hop chaining top-down, blocks returned bottom-up (samplers.py:213-226).
+
+    ``fanouts[h]`` is applied at hop h counted from the seeds.
+    """
+    dst = np.asarray(targets, dtype=np.int64)
+    if dst.size == 0:
+        raise ValueError("empty target set")        # SamplingError in the reference
+    blocks = []
+    for hop, f in enumerate(fanouts):
+        blk = node_wise_block(row_offsets, col_indices, dst, int(f), seed=seed,
+                              epoch=epoch, batch_id=batch_id, hop=hop,
+                              cached_mask=cached_mask)
+        blocks.append(blk)
+        dst = blk.src_ids
+    blocks.reverse()
+    return blocks
+
+
+class OracleMiniBatch:
+    def __init__(self, batch_id, epoch, target_ids, target_labels, layers,
+                 input_ids, features, hits, misses):
+        self.batch_id = batch_id
+        self.epoch = epoch
+        self.target_ids = target_ids
+        self.target_labels = target_labels
+        self.layers = tuple(layers)
+        self.input_ids = input_ids
+        self.features = features
+        self.cache_hits = hits
+        self.cache_misses = misses
+
+    def digest(self) -> str:
+        """SHA-256 over ids, triplets and features (samplers.py:63-72)."""
+        return digest_of(self.target_ids, self.layers, self.features)
+
+
+def digest_of(target_ids, layers, features) -> str:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(target_ids, dtype=np.int64).tobytes())
+    for blk in layers:
+        h.update(np.ascontiguousarray(blk.rows, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(blk.cols, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(blk.values, dtype=np.float64).tobytes())
+        h.update(np.ascontiguousarray(blk.src_ids, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(blk.dst_ids, dtype=np.int64).tobytes())
+    if features is not None:
+        h.update(np.ascontiguousarray(features, dtype=np.float32).tobytes())
+    return h.hexdigest()
+
+
+def build_minibatch(row_offsets, col_indices, features, labels, targets, fanouts,
+                    *, seed, epoch, batch_id, cached_mask=None):
+    """Node-wise arm of build_minibatch (samplers.py:502-540)."""
+    targets = np.asarray(targets, dtype=np.int64)
+    blocks = sample_node_wise(row_offsets, col_indices, targets, fanouts,
+                              seed=seed, epoch=epoch, batch_id=batch_id,
+                              cached_mask=cached_mask)
+    kept = blocks[-1].dst_ids
+    input_ids = blocks[0].src_ids
+    hits = misses = 0
+    if cached_mask is not None and input_ids.size:
+        hits = int(np.count_nonzero(cached_mask[input_ids]))
+        misses = int(input_ids.size - hits)
+    return OracleMiniBatch(batch_id, epoch, kept, labels[kept], blocks,
+                           input_ids, features[input_ids].copy(), hits, misses)

@@ -1,0 +1,113 @@
+"""ctypes binding of libmqgnn.so (the C-ABI in include/mqgnn.h).
+
+The product path has no CPU fallback: if the library is missing or a call
+fails, an ``MQError`` is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libmqgnn.so"
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+U32 = C.c_uint32
+U64 = C.c_uint64
+F32 = C.c_float
+F64 = C.c_double
+
+# name -> (restype, argtypes); mirrors include/mqgnn.h one to one
+SIGNATURES = {
+    "mq_version": (C.c_int, []),
+    "mq_last_error": (C.c_char_p, []),
+    "mq_stream_check": (C.c_int, [P]),
+    "mq_philox_fill_host": (C.c_int, [U64, U64, U32, U32, U32, U32, P]),
+    "mq_philox_fill": (C.c_int, [U64, U64, U32, U32, U32, U32, P, P]),
+    "mq_fisher_yates_host": (C.c_int, [U64, U64, U32, U32, U32, I64, I32, P]),
+    "mq_scan_scratch_bytes": (I64, [I64]),
+    "mq_strip_self_loops": (C.c_int, [P, P, I64, I64, P, P, P, P]),
+    "mq_residency_index": (C.c_int, [P, P, I64, I64, P, P, P, P, P, P]),
+    "mq_residency_slots": (C.c_int, [P, I64, P, P, P, P]),
+    "mq_sample_hop": (C.c_int, [P, P, P, P, P, P, I32, I32, U64, U64, U32, U32, P, P, P, P]),
+    "mq_batch_setup": (C.c_int, [P, I64, I32, I32, I32, P, P, P, P, P]),
+    "mq_step_commit": (C.c_int, [P, P, P, I32, P]),
+    "mq_relabel_scratch_bytes": (I64, [I32, I32]),
+    "mq_relabel": (C.c_int, [P, P, I32, P, P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "mq_gather": (C.c_int, [P, I32, P, P, I32, P, P, I32, I32, P, I32, P, P]),
+    "mq_spmm_fwd": (C.c_int, [P, P, P, P, I32, P, I32, I32, P, I32, P]),
+    "mq_spmm_bwd": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, I32, P, I32, P, I32, P]),
+    "mq_sage_linear_fwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, I32, P]),
+    "mq_linear_bwd_w_scratch_bytes": (I64, [I32, I32, I32]),
+    "mq_sage_linear_bwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, P, I32,
+                                     P, P]),
+    "mq_softmax_ce": (C.c_int, [P, I32, P, P, I32, I32, P, I32, P, P, P]),
+    "mq_gather_labels": (C.c_int, [P, P, P, I32, P, P]),
+    "mq_adam": (C.c_int, [P, P, P, P, P, F64, I64, P, P, I32, F32, P, P]),
+    "mq_sgd": (C.c_int, [P, P, P, F64, I64, P, F32, P, P]),
+    "mq_f32_to_f64": (C.c_int, [P, P, I64, P]),
+    "mq_pack_grads": (C.c_int, [P, I64, P, P, P]),
+    "mq_f64_to_f32": (C.c_int, [P, F64, P, I64, P]),
+    "mq_scan_i32": (C.c_int, [P, P, I32, P, P, P]),
+    "mq_prof_enable": (C.c_int, [C.c_int]),
+    "mq_prof_reset": (C.c_int, []),
+    "mq_prof_num_kernels": (C.c_int, []),
+    "mq_prof_kernel_name": (C.c_char_p, [C.c_int]),
+    "mq_prof_read": (C.c_int, [P, P, I32]),
+    "mq_launch_count": (I64, []),
+}
+
+_INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
+               if res is C.c_int and name not in ("mq_version", "mq_prof_num_kernels")}
+
+
+class MQError(RuntimeError):
+    """A libmqgnn call failed (argument, CUDA or state error)."""
+
+
+class _Lib:
+    def __init__(self, path: Path):
+        if not path.exists():
+            raise MQError(
+                f"{path} is missing: build it with `python -m paper_2601_04707_b200._build` "
+                "(there is no CPU fallback)")
+        self.path = path
+        self.dll = C.CDLL(str(path))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(self.dll, name)
+            fn.restype = res
+            fn.argtypes = args
+
+    def __getattr__(self, name):
+        fn = getattr(self.dll, name)
+        if name not in _INT_STATUS:
+            return fn
+
+        def checked(*args):
+            rc = fn(*args)
+            if rc != 0:
+                msg = self.dll.mq_last_error().decode(errors="replace")
+                raise MQError(f"{name} failed ({rc}): {msg}")
+            return rc
+
+        return checked
+
+
+_LIB = None
+
+
+def lib() -> _Lib:
+    global _LIB
+    if _LIB is None:
+        _LIB = _Lib(Path(os.environ.get("MQGNN_LIB", LIB_PATH)))
+    return _LIB
+
+
+def ptr(t) -> int | None:
+    """Raw device/host address of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()

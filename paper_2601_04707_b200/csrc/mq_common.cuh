@@ -1,0 +1,161 @@
+// Shared device/host helpers for libmqgnn (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/mqgnn.h"
+#include "mq_kernels.h"
+
+namespace mq {
+
+// ---------------------------------------------------------------------------
+// error plumbing: every C-ABI entry returns MQ_OK or an error code and leaves a
+// message readable through mq_last_error() (thread-local).
+
+void set_error(const char* fmt, ...);
+
+#define MQ_CHECK_ARG(cond, ...)                  \
+  do {                                           \
+    if (!(cond)) {                               \
+      ::mq::set_error(__VA_ARGS__);              \
+      return MQ_ERR_ARG;                         \
+    }                                            \
+  } while (0)
+
+#define MQ_CUDA(call)                                                       \
+  do {                                                                      \
+    cudaError_t _e = (call);                                                \
+    if (_e != cudaSuccess) {                                                \
+      ::mq::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,            \
+                      cudaGetErrorString(_e));                              \
+      return MQ_ERR_CUDA;                                                   \
+    }                                                                       \
+  } while (0)
+
+#define MQ_LAUNCH_CHECK(name)                                               \
+  do {                                                                      \
+    cudaError_t _e = cudaGetLastError();                                    \
+    if (_e != cudaSuccess) {                                                \
+      ::mq::set_error("launch %s: %s", name, cudaGetErrorString(_e));       \
+      return MQ_ERR_CUDA;                                                   \
+    }                                                                       \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kNumSMs = 148;
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------
+// per-kernel event timing (bench instrumentation; off by default, never used
+// while a stream is being captured into a CUDA graph)
+
+struct ProfScope {
+  int id;
+  cudaStream_t s;
+  bool on;
+  cudaEvent_t a, b;
+  ProfScope(int kernel_id, cudaStream_t stream);
+  ~ProfScope();
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Random123 constants), shared host/device so that host and GPU
+// draws are identical by construction.
+
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi,
+                                                   uint32_t& lo) {
+#ifdef __CUDA_ARCH__
+  hi = __umulhi(a, b);
+  lo = a * b;
+#else
+  uint64_t p = (uint64_t)a * (uint64_t)b;
+  hi = (uint32_t)(p >> 32);
+  lo = (uint32_t)p;
+#endif
+}
+
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
+    U4 n;
+    n.x = hi1 ^ c.y ^ k0;
+    n.y = lo1;
+    n.z = hi0 ^ c.w ^ k1;
+    n.w = lo0;
+    c = n;
+  }
+  return c;
+}
+
+// Draw x_j of the row stream (seed, epoch, batch, hop, row) — SURVEY §8c.
+struct RowStream {
+  uint32_t k0, k1, row, hop, batch;
+  U4 cur;
+  uint32_t blk;
+  __host__ __device__ __forceinline__ RowStream(uint64_t seed, uint64_t epoch, uint32_t batch_,
+                                                uint32_t hop_, uint32_t row_)
+      : k0((uint32_t)seed), k1((uint32_t)epoch), row(row_), hop(hop_), batch(batch_),
+        blk(0xFFFFFFFFu) {}
+  __host__ __device__ __forceinline__ uint32_t draw(uint32_t j) {
+    uint32_t b = j >> 2;
+    if (b != blk) {
+      U4 c{b, row, hop, batch};
+      cur = philox4x32_10(c, k0, k1);
+      blk = b;
+    }
+    switch (j & 3) {
+      case 0: return cur.x;
+      case 1: return cur.y;
+      case 2: return cur.z;
+      default: return cur.w;
+    }
+  }
+};
+
+// Partial Fisher-Yates over pool positions [0, n): writes k positions to pos[].
+// r = j + ((x_j * (n - j)) >> 32); swap(j, r); emit element at j. The sparse map
+// only ever holds the k swapped-in targets (keys >= j), kept in registers.
+template <int MAXK, class IdxT>
+__host__ __device__ __forceinline__ void fisher_yates(RowStream& rs, IdxT n, int k, IdxT* pos) {
+  IdxT key[MAXK];
+  IdxT val[MAXK];
+  int used = 0;
+  for (int j = 0; j < k; ++j) {
+    uint64_t x = rs.draw((uint32_t)j);
+    IdxT r = (IdxT)(j + (int64_t)((x * (uint64_t)(n - j)) >> 32));
+    IdxT a = (IdxT)j, b = r;
+    int ia = -1, ib = -1;
+    for (int t = 0; t < used; ++t) {
+      if (key[t] == (IdxT)j) ia = t;
+      if (key[t] == r) ib = t;
+    }
+    if (ia >= 0) a = val[ia];
+    if (ib >= 0) b = val[ib];
+    pos[j] = b;
+    if (ib >= 0) {
+      val[ib] = a;
+    } else {
+      key[used] = r;
+      val[used] = a;
+      ++used;
+    }
+  }
+}
+
+}  // namespace mq

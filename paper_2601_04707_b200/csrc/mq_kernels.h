@@ -1,0 +1,42 @@
+// Kernel ids for the timing hooks (mq_prof_*).
+#pragma once
+
+#define MQ_KERNEL_LIST(X)                         \
+  X(K_PHILOX, "philox_fill")                      \
+  X(K_SCAN, "scan")                               \
+  X(K_STRIP_FLAGS, "strip_self_loops")            \
+  X(K_RESIDENCY_COMPACT, "residency_compact")     \
+  X(K_RESIDENCY_OFFSETS, "residency_offsets")     \
+  X(K_RESIDENCY_SLOTS, "residency_slots")         \
+  X(K_SAMPLE, "sample_hop")                       \
+  X(K_RELABEL_MARK, "relabel_mark")               \
+  X(K_RELABEL_FIRST, "relabel_first")             \
+  X(K_RELABEL_FLAG, "relabel_flag_scan")          \
+  X(K_RELABEL_EMIT, "relabel_emit")               \
+  X(K_RELABEL_COLS, "relabel_cols")               \
+  X(K_RELABEL_CLEAN, "relabel_clean")             \
+  X(K_GATHER, "gather")                           \
+  X(K_SPMM_FWD, "spmm_fwd")                       \
+  X(K_SPMM_BWD_INIT, "spmm_bwd_init")             \
+  X(K_SPMM_BWD, "spmm_bwd_scatter")               \
+  X(K_SPMM_BWD_MASK, "spmm_bwd_mask")             \
+  X(K_LINEAR_FWD, "linear_fwd")                   \
+  X(K_LINEAR_BWD_W, "linear_bwd_w")               \
+  X(K_LINEAR_BWD_W_REDUCE, "linear_bwd_w_reduce") \
+  X(K_LINEAR_BWD_X, "linear_bwd_x")               \
+  X(K_SOFTMAX_CE, "softmax_ce")                   \
+  X(K_LABELS, "gather_labels")                    \
+  X(K_ADAM, "adam")                               \
+  X(K_SGD, "sgd")                                 \
+  X(K_STEP_BUMP, "step_bump")                     \
+  X(K_CONVERT, "convert")                         \
+  X(K_BATCH_SETUP, "batch_setup")
+
+namespace mq {
+enum KernelId {
+#define MQ_KENUM(e, s) e,
+  MQ_KERNEL_LIST(MQ_KENUM)
+#undef MQ_KENUM
+      K_COUNT
+};
+}  // namespace mq

@@ -1,0 +1,275 @@
+// Loss, optimizers, RaCoM packing and the exported scan.
+//
+// Reference: mqpipe/nn.py:141-156 (batch_loss), nn.py:191-215 (adam_step /
+// sgd_step), racom.py:47-57,118-139 (f64 accumulation).  The optimizer update
+// mirrors NumPy 2's float32 arithmetic with Python-float (weak) scalars
+// operation by operation, with explicit round-to-nearest intrinsics so that
+// no FMA contraction changes a rounding: the update is bit-identical to the
+// reference given the same gradient.
+#include "mq_common.cuh"
+#include "mq_scan.cuh"
+
+namespace mq {
+
+__device__ __forceinline__ bool finite_f(float x) { return isfinite(x); }
+
+// One warp per target row; summed loss accumulated in f64.
+__global__ void softmax_ce_kernel(const float* __restrict__ logits, int ld,
+                                  const int32_t* __restrict__ labels,
+                                  const int32_t* __restrict__ n_dev, int C, float* __restrict__ dl,
+                                  int lddl, double* __restrict__ loss_out,
+                                  int32_t* __restrict__ nonfinite) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x / 32;
+  const int n = *n_dev;
+  double wloss = 0.0;
+  int bad = 0;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
+    const float* x = logits + (int64_t)r * ld;
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = fmaxf(m, x[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32) s += expf(x[c] - m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float logd = logf(s);
+    const int lab = labels[r];
+    float* g = dl + (int64_t)r * lddl;
+    for (int c = lane; c < C; c += 32) {
+      const float sh = x[c] - m;
+      float p = expf(sh) / s;
+      if (c == lab) {
+        p -= 1.f;
+        wloss += -(double)(sh - logd);
+      }
+      g[c] = p;
+      bad |= !finite_f(p);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wloss += __shfl_xor_sync(0xffffffffu, wloss, o);
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (lane == 0) {
+    if (wloss != 0.0) atomicAdd(loss_out, wloss);
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+__global__ void step_bump_kernel(int32_t* step) { *step += 1; }
+
+__global__ void step_commit_kernel(double* loss_acc, const int32_t* cursor, double* ring,
+                                   int ring_len) {
+  int k = cursor[0] - 1;
+  k = ((k % ring_len) + ring_len) % ring_len;
+  ring[k] = loss_acc[0];
+  loss_acc[0] = 0.0;
+}
+
+__device__ __forceinline__ float load_grad(const float* g32, const double* g64, double scale,
+                                           int64_t i) {
+  return g32 ? g32[i] : (float)(g64[i] * scale);
+}
+
+// scale == 0 selects the packed contributor count g64[n] (mq_pack_grads)
+__device__ __forceinline__ double grad_scale_of(const double* g64, double scale, int64_t n) {
+  return (g64 != nullptr && scale == 0.0) ? 1.0 / g64[n] : scale;
+}
+
+__global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                            const float* __restrict__ g32, const double* __restrict__ g64,
+                            double scale, int64_t n, const int32_t* __restrict__ step,
+                            const float* __restrict__ bias, int bias_len, float lr,
+                            int32_t* __restrict__ nonfinite) {
+  const int t = *step;
+  if (t < 1 || t > bias_len) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
+    return;
+  }
+  const float bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
+  scale = grad_scale_of(g64, scale, n);
+  const float b1 = (float)0.9, b2 = (float)0.999;
+  const float c1 = (float)(1.0 - 0.9), c2 = (float)(1.0 - 0.999), eps = (float)1e-8;
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float g = load_grad(g32, g64, scale, i);
+    float mi = __fmul_rn(m[i], b1);                         // m *= beta1
+    mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
+    float vi = __fmul_rn(v[i], b2);                         // v *= beta2
+    vi = __fadd_rn(vi, __fmul_rn(__fmul_rn(c2, g), g));     // v += (1-beta2)*g*g
+    const float mh = __fdiv_rn(mi, bc1);                    // m / (1 - beta1**t)
+    const float vh = __fdiv_rn(vi, bc2);                    // v / (1 - beta2**t)
+    const float upd = __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps));
+    const float wi = __fsub_rn(w[i], upd);                  // w -= lr*mh/(sqrt(vh)+eps)
+    m[i] = mi;
+    v[i] = vi;
+    w[i] = wi;
+    bad |= !finite_f(wi);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
+                           const double* __restrict__ g64, double scale, int64_t n, float lr,
+                           int32_t* __restrict__ nonfinite) {
+  scale = grad_scale_of(g64, scale, n);
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float wi = __fsub_rn(w[i], __fmul_rn(lr, load_grad(g32, g64, scale, i)));
+    w[i] = wi;
+    bad |= !finite_f(wi);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+__global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+
+__global__ void pack_grads_kernel(const float* __restrict__ a, int64_t n,
+                                  const int32_t* __restrict__ n_targets, double* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = i < n ? (double)a[i] : (n_targets[0] > 0 ? 1.0 : 0.0);
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, double scale, float* __restrict__ b,
+                                  int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)(a[i] * scale);
+}
+
+inline int elem_blocks(int64_t n) {
+  int b = ceil_div(n < 1 ? 1 : n, 256);
+  return b > kNumSMs * 8 ? kNumSMs * 8 : b;
+}
+
+}  // namespace mq
+
+using namespace mq;
+
+extern "C" {
+
+int mq_softmax_ce(const float* logits, int32_t ld, const int32_t* labels, const int32_t* n_dev,
+                  int32_t n_max, int32_t n_classes, float* dlogits, int32_t lddl, double* loss_out,
+                  int32_t* nonfinite, void* stream) {
+  MQ_CHECK_ARG(logits && labels && n_dev && dlogits && loss_out && nonfinite,
+               "mq_softmax_ce: null pointer");
+  MQ_CHECK_ARG(n_classes >= 1 && ld >= n_classes && lddl >= n_classes, "mq_softmax_ce: bad dims");
+  if (n_max <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  int blocks = ceil_div(n_max, 8);
+  if (blocks > kNumSMs * 4) blocks = kNumSMs * 4;
+  {
+    ProfScope ps(K_SOFTMAX_CE, s);
+    softmax_ce_kernel<<<blocks, 256, 0, s>>>(logits, ld, labels, n_dev, n_classes, dlogits, lddl,
+                                             loss_out, nonfinite);
+  }
+  MQ_LAUNCH_CHECK("softmax_ce");
+  return MQ_OK;
+}
+
+int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
+            double grad_scale, int64_t n, int32_t* step_dev, const float* bias, int32_t bias_len,
+            float lr, int32_t* nonfinite, void* stream) {
+  MQ_CHECK_ARG(w && m && v && step_dev && bias && nonfinite, "mq_adam: null pointer");
+  MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_adam: exactly one gradient source");
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_STEP_BUMP, s);
+    step_bump_kernel<<<1, 1, 0, s>>>(step_dev);
+  }
+  MQ_LAUNCH_CHECK("step_bump");
+  if (n <= 0) return MQ_OK;
+  {
+    ProfScope ps(K_ADAM, s);
+    adam_kernel<<<elem_blocks(n), 256, 0, s>>>(w, m, v, grad32, grad64, grad_scale, n, step_dev,
+                                               bias, bias_len, lr, nonfinite);
+  }
+  MQ_LAUNCH_CHECK("adam");
+  return MQ_OK;
+}
+
+int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale, int64_t n,
+           int32_t* step_dev, float lr, int32_t* nonfinite, void* stream) {
+  MQ_CHECK_ARG(w && step_dev && nonfinite, "mq_sgd: null pointer");
+  MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_sgd: exactly one gradient source");
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_STEP_BUMP, s);
+    step_bump_kernel<<<1, 1, 0, s>>>(step_dev);
+  }
+  MQ_LAUNCH_CHECK("step_bump");
+  if (n <= 0) return MQ_OK;
+  {
+    ProfScope ps(K_SGD, s);
+    sgd_kernel<<<elem_blocks(n), 256, 0, s>>>(w, grad32, grad64, grad_scale, n, lr, nonfinite);
+  }
+  MQ_LAUNCH_CHECK("sgd");
+  return MQ_OK;
+}
+
+int mq_step_commit(double* loss_acc, const int32_t* cursor_dev, double* loss_ring,
+                   int32_t ring_len, void* stream) {
+  MQ_CHECK_ARG(loss_acc && cursor_dev && loss_ring && ring_len > 0, "mq_step_commit: bad args");
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_STEP_BUMP, s);
+    step_commit_kernel<<<1, 1, 0, s>>>(loss_acc, cursor_dev, loss_ring, ring_len);
+  }
+  MQ_LAUNCH_CHECK("step_commit");
+  return MQ_OK;
+}
+
+int mq_f32_to_f64(const float* in32, double* out64, int64_t n, void* stream) {
+  MQ_CHECK_ARG(in32 && out64, "mq_f32_to_f64: null pointer");
+  if (n <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_CONVERT, s);
+    f32_to_f64_kernel<<<elem_blocks(n), 256, 0, s>>>(in32, out64, n);
+  }
+  MQ_LAUNCH_CHECK("f32_to_f64");
+  return MQ_OK;
+}
+
+int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, double* out64,
+                  void* stream) {
+  MQ_CHECK_ARG(grad && n_targets_dev && out64, "mq_pack_grads: null pointer");
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_CONVERT, s);
+    pack_grads_kernel<<<elem_blocks(n + 1), 256, 0, s>>>(grad, n, n_targets_dev, out64);
+  }
+  MQ_LAUNCH_CHECK("pack_grads");
+  return MQ_OK;
+}
+
+int mq_f64_to_f32(const double* in64, double scale, float* out32, int64_t n, void* stream) {
+  MQ_CHECK_ARG(in64 && out32, "mq_f64_to_f32: null pointer");
+  if (n <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_CONVERT, s);
+    f64_to_f32_kernel<<<elem_blocks(n), 256, 0, s>>>(in64, scale, out32, n);
+  }
+  MQ_LAUNCH_CHECK("f64_to_f32");
+  return MQ_OK;
+}
+
+int mq_scan_i32(const int32_t* in, const int32_t* n_dev, int32_t n_max, int32_t* out,
+                void* scratch, void* stream) {
+  MQ_CHECK_ARG(in && n_dev && out && scratch, "mq_scan_i32: null pointer");
+  return launch_scan(LoadI32{in, n_dev, 0}, StoreOffsets<int32_t>{out}, n_max < 1 ? 1 : n_max,
+                     scratch, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+"""Preallocated device workspaces for one training step and its CUDA graph.
+
+Every buffer of the per-iteration path is sized
+once from host-side upper bounds, so a whole step — batch setup, L hops of
+sample + relabel, feature gather, forward, loss, backward, optimizer — is a
+fixed sequence of C-ABI launches with no host synchronisation and can be
+captured into one CUDA graph.  Counts that only the device knows (frontier
+sizes, nnz) travel as device scalars.
+
+Bounds for batch B and per-hop fanouts f_h (hop 0 at the seeds):
+  n_dst_0 = B,  n_src_h = min(n_dst_h (1 + f_h), n_dst_h + |V|),
+  n_dst_{h+1} = n_src_h,  nnz_h <= n_dst_h f_h.
+Layer l (bottom-up) consumes hop L-1-l.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import lib, ptr
+from .graph import DeviceGraph, round_up
+
+
+@dataclass
+class HopBounds:
+    fanout: int
+    n_dst_max: int
+    n_src_max: int
+
+    @property
+    def nnz_max(self) -> int:
+        return self.n_dst_max * self.fanout
+
+
+def hop_bounds(batch_size: int, fanouts, num_nodes: int) -> list:
+    out = []
+    nd = batch_size
+    for f in fanouts:
+        ns = min(nd * (1 + f), nd + num_nodes)
+        out.append(HopBounds(int(f), nd, ns))
+        nd = ns
+    return out
+
+
+class HopBuffers:
+    """Device outputs of one hop of sample + relabel (one Block)."""
+
+    def __init__(self, b: HopBounds, device):
+        i32 = dict(dtype=torch.int32, device=device)
+        self.bounds = b
+        self.nbr = torch.zeros(max(b.nnz_max, 1), **i32)
+        self.cnt = torch.zeros(max(b.n_dst_max, 1), **i32)
+        self.row_ptr = torch.zeros(b.n_dst_max + 1, **i32)
+        self.rows = torch.zeros(max(b.nnz_max, 1), **i32)
+        self.cols = torch.zeros(max(b.nnz_max, 1), **i32)
+        self.vals = torch.zeros(max(b.nnz_max, 1), dtype=torch.float32, device=device)
+        self.src_ids = torch.zeros(max(b.n_src_max, 1), **i32)
+        self.counts = torch.zeros(2, **i32)  # [n_src, nnz]
+
+
+class SampleWorkspace:
+    """Targets + the hop chain (sample_node_wise, samplers.py:213-226)."""
+
+    def __init__(self, g: DeviceGraph, fanouts, batch_size: int):
+        if not fanouts:
+            raise ValueError("need at least one hop")
+        if any(f < 1 or f > 32 for f in fanouts):
+            raise ValueError("fanouts must lie in [1, 32]")
+        dev = g.device
+        self.graph = g
+        self.fanouts = tuple(int(f) for f in fanouts)
+        self.batch_size = int(batch_size)
+        self.bounds = hop_bounds(self.batch_size, self.fanouts, g.num_nodes)
+        self.targets = torch.zeros(max(self.batch_size, 1), dtype=torch.int32, device=dev)
+        self.n_targets = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.key = torch.zeros(3, dtype=torch.int32, device=dev)  # uint32 seed, epoch, batch
+        self.hops = [HopBuffers(b, dev) for b in self.bounds]
+        scr = max(int(lib().mq_relabel_scratch_bytes(b.n_dst_max, b.fanout)) for b in self.bounds)
+        self.scratch = torch.zeros(scr, dtype=torch.uint8, device=dev)
+
+    # device scalars for hop h
+    def n_dst_dev(self, h: int) -> torch.Tensor:
+        return self.n_targets if h == 0 else self.hops[h - 1].counts[0:1]
+
+    def dst(self, h: int) -> torch.Tensor:
+        return self.targets if h == 0 else self.hops[h - 1].src_ids
+
+    @property
+    def input_ids(self) -> torch.Tensor:
+        return self.hops[-1].src_ids
+
+    @property
+    def n_input_dev(self) -> torch.Tensor:
+        return self.hops[-1].counts[0:1]
+
+    def launch(self, cache, stream, *, seed=0, epoch=0, batch=0, key_on_device=False):
+        g = self.graph
+        L = lib()
+        hot_arc = ptr(cache.hot_arc) if cache is not None else None
+        hot_off = ptr(cache.hot_off) if cache is not None else None
+        key = ptr(self.key) if key_on_device else None
+        for h, (hb, b) in enumerate(zip(self.hops, self.bounds)):
+            L.mq_sample_hop(ptr(g.row_off), ptr(g.col), hot_arc, hot_off, ptr(self.dst(h)),
+                            ptr(self.n_dst_dev(h)), b.n_dst_max, b.fanout, seed & 0xFFFFFFFF,
+                            epoch & 0xFFFFFFFF, batch & 0xFFFFFFFF, h, key, ptr(hb.nbr),
+                            ptr(hb.cnt), stream)
+            L.mq_relabel(ptr(self.dst(h)), ptr(self.n_dst_dev(h)), b.n_dst_max, ptr(hb.nbr),
+                         ptr(hb.cnt), b.fanout, ptr(g.dpos), ptr(g.first), ptr(hb.row_ptr),
+                         ptr(hb.rows), ptr(hb.cols), ptr(hb.vals), ptr(hb.src_ids),
+                         ptr(hb.counts), ptr(self.scratch), stream)
+
+
+class DeviceModel:
+    """Flat fp32 parameters + Adam moments (ModelState, nn.py:19-53)."""
+
+    def __init__(self, weights, learning_rate: float, device, step_count: int = 0,
+                 m=None, v=None, bias_len: int = 1 << 16):
+        self.shapes = [tuple(int(x) for x in w.shape) for w in weights]
+        self.offsets = np.cumsum([0] + [a * b for a, b in self.shapes]).tolist()
+        n = self.offsets[-1]
+        self.num_params = n
+        self.device = device
+        self.learning_rate = float(learning_rate)
+        self.flat_w = torch.zeros(n, dtype=torch.float32, device=device)
+        self.flat_m = torch.zeros(n, dtype=torch.float32, device=device)
+        self.flat_v = torch.zeros(n, dtype=torch.float32, device=device)
+        self.flat_g = torch.zeros(n, dtype=torch.float32, device=device)
+        for i, w in enumerate(weights):
+            self.weight(i).copy_(_t(w, device))
+            if m is not None:
+                self.view(self.flat_m, i).copy_(_t(m[i], device))
+            if v is not None:
+                self.view(self.flat_v, i).copy_(_t(v[i], device))
+        self.step_dev = torch.tensor([step_count], dtype=torch.int32, device=device)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=device)
+        self.bias_len = 0
+        self.bias = None
+        self.ensure_bias(max(bias_len, step_count + 1))
+        self.host_steps = step_count
+
+    def ensure_bias(self, steps: int):
+        """float32(1 - beta1**t), float32(1 - beta2**t) for t = 1..steps, computed
+        with Python floats exactly as nn.py:202-203 does."""
+        if steps <= self.bias_len:
+            return
+        t = np.arange(1, steps + 1, dtype=np.float64)
+        tab = np.empty((steps, 2), dtype=np.float32)
+        tab[:, 0] = np.array([1 - 0.9 ** int(k) for k in t], dtype=np.float64).astype(np.float32)
+        tab[:, 1] = np.array([1 - 0.999 ** int(k) for k in t], dtype=np.float64).astype(np.float32)
+        self.bias = torch.as_tensor(tab.reshape(-1), device=self.device)
+        self.bias_len = steps
+
+    def view(self, flat, i):
+        a, b = self.shapes[i]
+        return flat[self.offsets[i]:self.offsets[i + 1]].view(a, b)
+
+    def weight(self, i):
+        return self.view(self.flat_w, i)
+
+    def grad(self, i):
+        return self.view(self.flat_g, i)
+
+    @property
+    def num_layers(self):
+        return len(self.shapes)
+
+    @property
+    def lr32(self) -> float:
+        return float(np.float32(self.learning_rate))
+
+
+def _t(a, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.float32)
+    return torch.as_tensor(np.asarray(a, dtype=np.float32), device=device)
+
+
+class TrainWorkspace:
+    """Activation / gradient buffers of one SAGE step over a SampleWorkspace."""
+
+    def __init__(self, sw: SampleWorkspace, dims, num_classes: int):
+        g = sw.graph
+        dev = g.device
+        L = len(sw.fanouts)
+        if len(dims) != L + 1:
+            raise ValueError("dims must list input, hidden..., classes")
+        self.sw = sw
+        self.dims = list(dims)
+        self.L = L
+        self.C = num_classes
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.x0 = torch.zeros((max(sw.bounds[-1].n_src_max, 1), g.pitch), **f32)
+        self.ld_in = [g.pitch] + [round_up(d, 4) for d in self.dims[1:L]]
+        self.agg, self.act, self.dt, self.dh = [], [None], [], []
+        for l in range(L):
+            b = sw.bounds[L - 1 - l]
+            self.agg.append(torch.zeros((max(b.n_dst_max, 1), self.ld_in[l]), **f32))
+            if l + 1 < L:
+                self.act.append(torch.zeros((max(b.n_dst_max, 1), self.ld_in[l + 1]), **f32))
+            if l > 0:
+                self.dt.append(torch.zeros((max(b.n_dst_max, 1), 2 * self.dims[l]), **f32))
+                self.dh.append(torch.zeros((max(b.n_src_max, 1), self.ld_in[l]), **f32))
+            else:
+                self.dt.append(None)
+                self.dh.append(None)
+        B = sw.batch_size
+        self.logits = torch.zeros((max(B, 1), num_classes), **f32)
+        self.dlogits = torch.zeros((max(B, 1), num_classes), **f32)
+        self.labels = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        scr = max(int(lib().mq_linear_bwd_w_scratch_bytes(sw.bounds[L - 1 - l].n_dst_max,
+                                                          self.dims[l], self.dims[l + 1]))
+                  for l in range(L))
+        self.scratch = torch.zeros(scr // 4 + 1, **f32)
+
+    def h_in(self, l):
+        return self.x0 if l == 0 else self.act[l]
+
+    def launch_gather(self, cache, stream):
+        g, sw = self.sw.graph, self.sw
+        b = sw.bounds[-1]
+        if cache is None:
+            lib().mq_gather(None, 0, None, ptr(g.features), g.pitch, ptr(sw.input_ids),
+                            ptr(sw.n_input_dev), b.n_src_max, g.feature_dim, ptr(self.x0), g.pitch,
+                            None, stream)
+        else:
+            lib().mq_gather(ptr(cache.table), g.pitch, ptr(cache.slot_of), ptr(g.features), g.pitch,
+                            ptr(sw.input_ids), ptr(sw.n_input_dev), b.n_src_max, g.feature_dim,
+                            ptr(self.x0), g.pitch, ptr(cache.hit_miss), stream)
+
+    def launch_forward(self, model: DeviceModel, stream):
+        sw = self.sw
+        L = self.L
+        for l in range(L):
+            h = L - 1 - l
+            hb, b = sw.hops[h], sw.bounds[h]
+            nd = sw.n_dst_dev(h)
+            hin = self.h_in(l)
+            lib().mq_spmm_fwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals), ptr(nd), b.n_dst_max,
+                              ptr(hin), self.ld_in[l], self.dims[l], ptr(self.agg[l]),
+                              self.ld_in[l], stream)
+            W = model.weight(l)
+            if l + 1 < L:
+                lib().mq_sage_linear_fwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],
+                                         ptr(nd), b.n_dst_max, self.dims[l], ptr(W),
+                                         self.dims[l + 1], None, 0, ptr(self.act[l + 1]),
+                                         self.ld_in[l + 1], stream)
+            else:
+                lib().mq_sage_linear_fwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],
+                                         ptr(nd), b.n_dst_max, self.dims[l], ptr(W),
+                                         self.dims[l + 1], ptr(self.logits), self.C, None, 0,
+                                         stream)
+
+    def launch_loss(self, model: DeviceModel, stream):
+        g, sw = self.sw.graph, self.sw
+        lib().mq_gather_labels(ptr(g.labels), ptr(sw.targets), ptr(sw.n_targets), sw.batch_size,
+                               ptr(self.labels), stream)
+        lib().mq_softmax_ce(ptr(self.logits), self.C, ptr(self.labels), ptr(sw.n_targets),
+                            sw.batch_size, self.C, ptr(self.dlogits), self.C, ptr(self.loss),
+                            ptr(model.nonfinite), stream)
+
+    def launch_backward(self, model: DeviceModel, stream):
+        sw = self.sw
+        L = self.L
+        dz, lddz = self.dlogits, self.C
+        for l in range(L - 1, -1, -1):
+            h = L - 1 - l
+            hb, b = sw.hops[h], sw.bounds[h]
+            nd = sw.n_dst_dev(h)
+            hin = self.h_in(l)
+            d_in, d_out = self.dims[l], self.dims[l + 1]
+            dt = self.dt[l]
+            lib().mq_sage_linear_bwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],
+                                     ptr(nd), b.n_dst_max, d_in, ptr(model.weight(l)), d_out,
+                                     ptr(dz), lddz, ptr(model.grad(l)), ptr(dt), 2 * d_in,
+                                     ptr(self.scratch), stream)
+            if l > 0:
+                lib().mq_spmm_bwd(ptr(hb.rows), ptr(hb.cols), ptr(hb.vals), ptr(hb.counts),
+                                  b.nnz_max, ptr(nd), b.n_src_max, ptr(dt), 2 * d_in, d_in,
+                                  ptr(hin), self.ld_in[l], ptr(self.dh[l]), self.ld_in[l], stream)
+                dz, lddz = self.dh[l], self.ld_in[l]
+
+    @staticmethod
+    def launch_optimizer(model: DeviceModel, optimizer: str, stream, grad64=None, scale=1.0):
+        g32 = None if grad64 is not None else ptr(model.flat_g)
+        g64 = ptr(grad64) if grad64 is not None else None
+        if optimizer == "adam":
+            lib().mq_adam(ptr(model.flat_w), ptr(model.flat_m), ptr(model.flat_v), g32, g64, scale,
+                          model.num_params, ptr(model.step_dev), ptr(model.bias), model.bias_len,
+                          model.lr32, ptr(model.nonfinite), stream)
+        elif optimizer == "sgd":
+            lib().mq_sgd(ptr(model.flat_w), g32, g64, scale, model.num_params,
+                         ptr(model.step_dev), model.lr32, ptr(model.nonfinite), stream)
+        else:
+            raise ValueError(f"unknown optimizer {optimizer!r}")
+
+
+def current_stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream

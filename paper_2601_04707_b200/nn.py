@@ -1,0 +1,260 @@
+"""Drop-in SAGE numerics API backed by the CUDA kernels.
+
+Mirrors ``mqpipe/nn.py``:
+
+* ``ModelState``/``init_model`` — ``nn.py:19-71`` (Glorot uniform drawn with the
+  reference's own NumPy generator, so weights are identical for a seed)
+* ``forward``/``sage_forward``  — ``nn.py:116-138``
+* ``batch_loss``                — ``nn.py:141-156``
+* ``backward``                  — ``nn.py:159-180``
+* ``loss_and_grads``            — ``nn.py:183-188``
+* ``adam_step``/``sgd_step``    — ``nn.py:191-215``
+* ``accuracy``                  — ``nn.py:253-256``
+
+Parameters live in one flat fp32 device buffer (``engine.DeviceModel``);
+``weights``, ``m`` and ``v`` are views into it.  Non-finite results raise
+``FloatingPointError`` like the reference (``nn.py:74-76``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import lib, ptr
+from .engine import DeviceModel, current_stream
+from .graph import round_up
+
+ADAM_BETA1 = 0.9
+ADAM_BETA2 = 0.999
+ADAM_EPS = 1e-8
+
+
+class ModelState:
+    """Weights plus Adam moments for one replica (flat device storage)."""
+
+    def __init__(self, weights, arch: str = "sage", learning_rate: float = 0.001,
+                 step_count: int = 0, m=None, v=None, device=None):
+        if arch != "sage":
+            raise NotImplementedError("the B200 path implements the GraphSAGE arch")
+        dev = torch.device(device or (weights[0].device if isinstance(weights[0], torch.Tensor)
+                                      and weights[0].is_cuda else "cuda"))
+        self.arch = arch
+        self.dev = DeviceModel(weights, learning_rate, dev, step_count, m, v)
+
+    # reference-compatible views
+    @property
+    def weights(self):
+        return [self.dev.weight(i) for i in range(self.dev.num_layers)]
+
+    @property
+    def m(self):
+        return [self.dev.view(self.dev.flat_m, i) for i in range(self.dev.num_layers)]
+
+    @property
+    def v(self):
+        return [self.dev.view(self.dev.flat_v, i) for i in range(self.dev.num_layers)]
+
+    @property
+    def learning_rate(self):
+        return self.dev.learning_rate
+
+    @learning_rate.setter
+    def learning_rate(self, lr):
+        self.dev.learning_rate = float(lr)
+
+    @property
+    def step_count(self) -> int:
+        return self.dev.host_steps
+
+    @property
+    def dtype(self):
+        return torch.float32
+
+    @property
+    def device(self):
+        return self.dev.device
+
+    def copy(self) -> "ModelState":
+        return ModelState([w.clone() for w in self.weights], self.arch, self.learning_rate,
+                          self.step_count, [m.clone() for m in self.m],
+                          [v.clone() for v in self.v], device=self.device)
+
+    def to_numpy(self):
+        return ([w.cpu().numpy() for w in self.weights], [m.cpu().numpy() for m in self.m],
+                [v.cpu().numpy() for v in self.v])
+
+
+def glorot_weights(feature_dim, hidden_dim, num_classes, num_layers=2, seed=0):
+    """Same draws as nn.py:56-71 (NumPy default_rng(seed), SAGE fan-in 2x)."""
+    rng = np.random.default_rng(seed)
+    dims = [feature_dim] + [hidden_dim] * (num_layers - 1) + [num_classes]
+    out = []
+    for l in range(num_layers):
+        fan_in, fan_out = dims[l] * 2, dims[l + 1]
+        limit = np.sqrt(6.0 / (fan_in + fan_out))
+        out.append(rng.uniform(-limit, limit, size=(fan_in, fan_out)).astype(np.float32))
+    return out
+
+
+def init_model(feature_dim: int, hidden_dim: int, num_classes: int, num_layers: int = 2,
+               arch: str = "sage", seed: int = 0, learning_rate: float = 0.001,
+               dtype=np.float32, device=None) -> ModelState:
+    if np.dtype(dtype) != np.float32:
+        raise NotImplementedError("the device path trains in float32 (nn.py default)")
+    w = glorot_weights(feature_dim, hidden_dim, num_classes, num_layers, seed)
+    return ModelState(w, arch=arch, learning_rate=learning_rate, device=device)
+
+
+def _check(state: ModelState, name: str):
+    flag = int(state.dev.nonfinite.item())
+    if flag & 1:
+        state.dev.nonfinite.zero_()
+        raise FloatingPointError(f"{name} contains NaN or Inf")
+    if flag & 2:
+        state.dev.nonfinite.zero_()
+        raise RuntimeError("Adam bias-correction table exhausted")
+
+
+def _finite_or_raise(name, t):
+    if not bool(torch.isfinite(t).all()):
+        raise FloatingPointError(f"{name} contains NaN or Inf")
+
+
+def _pitched(x: torch.Tensor, ld: int) -> torch.Tensor:
+    """Copy [n, d] into a zero-padded [n, ld] buffer (16-byte aligned rows)."""
+    n, d = x.shape
+    if x.is_contiguous() and d == ld:
+        return x
+    out = torch.zeros((max(n, 1), ld), dtype=torch.float32, device=x.device)
+    out[:n, :d] = x
+    return out
+
+
+def sage_forward(batch, state: ModelState, return_cache: bool = False):
+    """Per layer: agg = segment-mean SpMM, z = [agg | h_dst] W, ReLU except last."""
+    dev = state.device
+    stream = current_stream(dev)
+    h = batch.features.to(device=dev, dtype=torch.float32)
+    cache = {"inputs": [], "pre": []}
+    L = len(batch.layers)
+    for l, blk in enumerate(batch.layers):
+        d_in = int(h.shape[1])
+        ld = round_up(d_in, 4)
+        hp = _pitched(h, ld)
+        nd = blk.num_dst
+        nd_dev = torch.tensor([nd], dtype=torch.int32, device=dev)
+        agg = torch.zeros((max(nd, 1), ld), dtype=torch.float32, device=dev)
+        lib().mq_spmm_fwd(ptr(blk.row_ptr), ptr(blk.cols), ptr(blk.values), ptr(nd_dev), nd,
+                          ptr(hp), ld, d_in, ptr(agg), ld, stream)
+        W = state.weights[l]
+        d_out = int(W.shape[1])
+        z = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev)
+        r = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev) if l < L - 1 else None
+        lib().mq_sage_linear_fwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,
+                                 ptr(z), d_out, ptr(r), d_out, stream)
+        cache["inputs"].append((hp, agg, blk, nd_dev, d_in))
+        cache["pre"].append(z[:nd])
+        h = r[:nd] if l < L - 1 else z[:nd]
+    _finite_or_raise("sage_forward output", h)
+    return (h, cache) if return_cache else h
+
+
+forward = sage_forward
+
+
+def batch_loss(logits: torch.Tensor, labels):
+    """Summed softmax-CE and dlogits (nn.py:141-156)."""
+    dev = logits.device
+    n, C = logits.shape
+    lab = torch.as_tensor(labels).to(device=dev, dtype=torch.int32).contiguous()
+    logits = logits.contiguous().to(torch.float32)
+    n_dev = torch.tensor([n], dtype=torch.int32, device=dev)
+    dl = torch.empty((max(n, 1), C), dtype=torch.float32, device=dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib().mq_softmax_ce(ptr(logits), C, ptr(lab), ptr(n_dev), n, C, ptr(dl), C, ptr(loss), ptr(bad),
+                        current_stream(dev))
+    if int(bad.item()):
+        raise FloatingPointError("batch_loss contains NaN or Inf")
+    return float(loss.item()), dl[:n]
+
+
+def backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
+    """Weight gradients, last layer first (nn.py:159-180)."""
+    dev = state.device
+    stream = current_stream(dev)
+    L = len(batch.layers)
+    grads = [None] * L
+    dz = dlogits.contiguous().to(torch.float32)
+    lddz = int(dz.shape[1])
+    for l in range(L - 1, -1, -1):
+        hp, agg, blk, nd_dev, d_in = cache["inputs"][l]
+        ld = int(hp.shape[1])
+        nd = blk.num_dst
+        W = state.weights[l]
+        d_out = int(W.shape[1])
+        dW = torch.empty_like(W)
+        scr = torch.empty(int(lib().mq_linear_bwd_w_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+                          dtype=torch.float32, device=dev)
+        dt = torch.empty((max(nd, 1), 2 * d_in), dtype=torch.float32, device=dev) if l > 0 else None
+        lib().mq_sage_linear_bwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,
+                                 ptr(dz), lddz, ptr(dW), ptr(dt), 2 * d_in, ptr(scr), stream)
+        grads[l] = dW
+        if l > 0:
+            ns = blk.num_src
+            counts = torch.tensor([ns, blk.nnz], dtype=torch.int32, device=dev)
+            dh = torch.empty((max(ns, 1), ld), dtype=torch.float32, device=dev)
+            lib().mq_spmm_bwd(ptr(blk.rows), ptr(blk.cols), ptr(blk.values), ptr(counts), blk.nnz,
+                              ptr(nd_dev), ns, ptr(dt), 2 * d_in, d_in, ptr(hp), ld, ptr(dh), ld,
+                              stream)
+            dz, lddz = dh, ld
+    for g in grads:
+        _finite_or_raise("backward", g)
+    return grads
+
+
+def loss_and_grads(batch, state: ModelState):
+    logits, cache = forward(batch, state, return_cache=True)
+    loss, dlogits = batch_loss(logits, batch.target_labels)
+    grads = backward(batch, state, cache, dlogits)
+    return loss, grads, logits
+
+
+def _flat_grad(state: ModelState, grads):
+    g = state.dev.flat_g
+    for i, gi in enumerate(grads):
+        state.dev.grad(i).copy_(torch.as_tensor(gi).to(device=g.device, dtype=torch.float32)
+                                if not isinstance(gi, torch.Tensor) else gi.to(torch.float32))
+    return g
+
+
+def adam_step(state: ModelState, grads: list) -> ModelState:
+    """Bias-corrected Adam, bit-identical op order to nn.py:191-206."""
+    _flat_grad(state, grads)
+    d = state.dev
+    d.ensure_bias(d.host_steps + 1)
+    lib().mq_adam(ptr(d.flat_w), ptr(d.flat_m), ptr(d.flat_v), ptr(d.flat_g), None, 1.0,
+                  d.num_params, ptr(d.step_dev), ptr(d.bias), d.bias_len, d.lr32,
+                  ptr(d.nonfinite), current_stream(d.device))
+    d.host_steps += 1
+    _check(state, "adam_step")
+    return state
+
+
+def sgd_step(state: ModelState, grads: list) -> ModelState:
+    _flat_grad(state, grads)
+    d = state.dev
+    lib().mq_sgd(ptr(d.flat_w), ptr(d.flat_g), None, 1.0, d.num_params, ptr(d.step_dev), d.lr32,
+                 ptr(d.nonfinite), current_stream(d.device))
+    d.host_steps += 1
+    _check(state, "sgd_step")
+    return state
+
+
+def accuracy(logits, labels) -> float:
+    logits = torch.as_tensor(logits)
+    if logits.shape[0] == 0:
+        return 0.0
+    lab = torch.as_tensor(labels, device=logits.device)
+    return float((logits.argmax(dim=1) == lab.long()).float().mean().item())
