@@ -159,19 +159,15 @@ __global__ void __launch_bounds__(128) sample_hop_kernel(
       fisher_yates<MAXK, int>(rs, nh, fanout, pos);
       for (int j = 0; j < fanout; ++j) out[j] = __ldg(&col[hot_arc[hb + pos[j]]]);
     } else {
-      int hp[MAXK];  // row positions of the hot arcs (ascending)
-      for (int i = 0; i < nh; ++i) {
-        int64_t a = hot_arc[hb + i];
-        hp[i] = (int)(a - beg);
-        out[i] = __ldg(&col[a]);
-      }
+      for (int i = 0; i < nh; ++i) out[i] = __ldg(&col[hot_arc[hb + i]]);
       const int k = fanout - nh;
       fisher_yates<MAXK, int>(rs, n - nh, k, pos);
       for (int j = 0; j < k; ++j) {
-        // cold rank -> row position: skip the hot positions at or before it
+        // cold rank -> row position: skip every hot position h_i with
+        // h_i - i <= rank (the hot positions are ascending)
         const int rr = pos[j];
         int c = 0;
-        for (int i = 0; i < nh; ++i) c += (hp[i] - i <= rr) ? 1 : 0;
+        for (int i = 0; i < nh; ++i) c += ((int)(hot_arc[hb + i] - beg) - i <= rr) ? 1 : 0;
         out[nh + j] = __ldg(&col[beg + rr + c]);
       }
     }

@@ -1,0 +1,235 @@
+"""One replica's per-iteration hot path as captured CUDA graphs.
+
+A step = batch setup (device-side plan), L hops of sample + relabel, feature
+gather, SAGE forward, summed softmax-CE, backward and the optimizer — the
+``_run_epoch_serial`` per-batch body of the reference (``runtime.py:294-323``)
+with the RaCoM window apply (``runtime.py:167-195``) folded in.  Everything is
+enqueued through the C-ABI on one stream; after an eager warm-up the sequence
+is captured once and replayed per batch, so a step costs one graph launch.
+
+Multi-replica (RaCoM) steps split the graph in two around the gradient
+exchange: compute graph -> f64 all-reduce of [grads | contributor count]
+(NCCL in production, gloo/in-process in tests) -> update graph.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import lib, ptr
+from .engine import SampleWorkspace, TrainWorkspace
+
+
+class StepRunner:
+    """Per-iteration path for one replica on one GPU."""
+
+    def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
+                 optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
+                 exchange=None, use_graph: bool = True, ring_len: int = 1 << 16):
+        if optimizer not in ("adam", "sgd"):
+            raise ValueError(f"unknown optimizer {optimizer!r}")
+        self.g = g
+        self.model = model
+        self.dm = model.dev
+        self.cache = cache
+        self.optimizer = optimizer
+        self.seed = int(seed)
+        self.world, self.rank = int(world), int(rank)
+        self.exchange = exchange
+        self.use_graph = use_graph
+        dev = g.device
+        self.device = dev
+        self.sw = SampleWorkspace(g, fanouts, batch_size)
+        dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
+        if dims[-1] != g.num_classes:
+            raise ValueError("model output width must equal num_classes")
+        self.tw = TrainWorkspace(self.sw, dims, g.num_classes)
+        self.num_train = int(num_train)
+        self.perm = torch.zeros(max(self.num_train, 1), dtype=torch.int32, device=dev)
+        self.cursor = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ring_len = int(ring_len)
+        self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
+        self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
+                       if exchange is not None else None)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graphs = {}
+        self.windows_done = 0
+        self.epoch = 0
+
+    # ---------------------------------------------------------------- epochs
+    def begin_epoch(self, epoch: int, perm: np.ndarray):
+        """Upload this epoch's shuffled train ids (plan_epoch, runtime.py:95-117)."""
+        perm = np.asarray(perm)
+        if perm.size != self.num_train:
+            raise ValueError("permutation length changed; build a new StepRunner")
+        with torch.cuda.stream(self.stream):
+            self.perm.copy_(torch.as_tensor(perm.astype(np.int32)), non_blocking=False)
+            self.cursor.zero_()
+            self.sw.key.copy_(torch.tensor([self.seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF, 0],
+                                           dtype=torch.int64).to(torch.int32))
+        self.epoch = epoch
+        self.windows_done = 0
+        n_windows = -(-self.num_train // (self.sw.batch_size * self.world))
+        self.dm.ensure_bias(self.dm.host_steps + n_windows + 8)
+
+    # --------------------------------------------------------------- enqueue
+    def _enqueue_setup(self, s):
+        lib().mq_batch_setup(ptr(self.perm), self.num_train, self.sw.batch_size, self.world,
+                             self.rank, ptr(self.cursor), ptr(self.sw.targets),
+                             ptr(self.sw.n_targets), ptr(self.sw.key), s)
+
+    def _enqueue_compute(self, s, commit=True):
+        self.sw.launch(self.cache, s, key_on_device=True)
+        self.tw.launch_gather(self.cache, s)
+        self.tw.launch_forward(self.dm, s)
+        self.tw.launch_loss(self.dm, s)
+        if commit:
+            lib().mq_step_commit(ptr(self.tw.loss), ptr(self.cursor), ptr(self.loss_ring),
+                                 self.ring_len, s)
+        self.tw.launch_backward(self.dm, s)
+        if self.grad64 is not None:
+            lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(self.sw.n_targets),
+                                ptr(self.grad64), s)
+
+    def _enqueue_update(self, s):
+        if self.grad64 is None:
+            self.tw.launch_optimizer(self.dm, self.optimizer, s)
+        else:  # scale 0: divide by the all-reduced contributor count (expected[k])
+            self.tw.launch_optimizer(self.dm, self.optimizer, s, grad64=self.grad64, scale=0.0)
+
+    def _phases(self):
+        if self.grad64 is None:
+            return {"full": lambda s: (self._enqueue_setup(s), self._enqueue_compute(s),
+                                       self._enqueue_update(s))}
+        return {"compute": lambda s: (self._enqueue_setup(s), self._enqueue_compute(s)),
+                "update": self._enqueue_update}
+
+    # ----------------------------------------------------------------- graphs
+    def _snapshot(self):
+        d = self.dm
+        return [t.clone() for t in (d.flat_w, d.flat_m, d.flat_v, d.step_dev, self.cursor,
+                                    self.loss_ring)] + (
+            [self.cache.hit_miss.clone()] if self.cache is not None else [])
+
+    def _restore(self, snap):
+        d = self.dm
+        targets = [d.flat_w, d.flat_m, d.flat_v, d.step_dev, self.cursor, self.loss_ring] + (
+            [self.cache.hit_miss] if self.cache is not None else [])
+        for t, v in zip(targets, snap):
+            t.copy_(v)
+
+    def capture(self):
+        """Eager warm-up (state restored afterwards), then capture each phase."""
+        if self.graphs:
+            return
+        phases = self._phases()
+        with torch.cuda.stream(self.stream):
+            snap = self._snapshot()
+            s = self.stream.cuda_stream
+            for fn in phases.values():
+                fn(s)
+                if self.exchange is not None and fn is phases.get("compute"):
+                    pass  # warm-up only: no collective
+            self.stream.synchronize()
+            self._restore(snap)
+            self.tw.loss.zero_()
+            self.dm.nonfinite.zero_()
+            self.stream.synchronize()
+        for name, fn in phases.items():
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=self.stream):
+                fn(torch.cuda.current_stream().cuda_stream)
+            self.graphs[name] = graph
+        torch.cuda.synchronize(self.device)
+
+    def kernels_per_step(self) -> int:
+        """Number of libmqgnn kernel launches one step enqueues."""
+        lib().mq_prof_reset()
+        before = lib().mq_launch_count()
+        with torch.cuda.stream(self.stream):
+            snap = self._snapshot()
+            for fn in self._phases().values():
+                fn(self.stream.cuda_stream)
+            self.stream.synchronize()
+            self._restore(snap)
+            self.tw.loss.zero_()
+        return int(lib().mq_launch_count() - before)
+
+    # ------------------------------------------------------------------ step
+    def step(self):
+        """One window of this replica (async; nothing is read back)."""
+        with torch.cuda.stream(self.stream):
+            if self.grad64 is None:
+                if self.use_graph:
+                    self.graphs["full"].replay()
+                else:
+                    self._phases()["full"](self.stream.cuda_stream)
+            else:
+                if self.use_graph:
+                    self.graphs["compute"].replay()
+                else:
+                    self._phases()["compute"](self.stream.cuda_stream)
+                self.exchange.allreduce_sum(self.grad64, self.stream)
+                if self.use_graph:
+                    self.graphs["update"].replay()
+                else:
+                    self._enqueue_update(self.stream.cuda_stream)
+        self.dm.host_steps += 1
+        self.windows_done += 1
+
+    def losses(self, n_windows: int) -> np.ndarray:
+        self.stream.synchronize()
+        return self.loss_ring[:n_windows].cpu().numpy()
+
+    def check_finite(self):
+        self.stream.synchronize()
+        flag = int(self.dm.nonfinite.item())
+        if flag:
+            self.dm.nonfinite.zero_()
+            if flag & 2:
+                raise RuntimeError("Adam bias-correction table exhausted")
+            raise FloatingPointError("training step produced NaN or Inf")
+
+    # ------------------------------------------------- host-input (e2e) path
+    def capture_host_input(self):
+        """Graph variant that reads targets staged by the host (no device plan)."""
+        if "host" in self.graphs:
+            return
+        if self.grad64 is not None:
+            raise NotImplementedError("host-input steps are single-replica")
+
+        def fn(s):
+            self._enqueue_compute(s, commit=False)
+            self._enqueue_update(s)
+        with torch.cuda.stream(self.stream):
+            snap = self._snapshot()
+            fn(self.stream.cuda_stream)
+            self.stream.synchronize()
+            self._restore(snap)
+            self.tw.loss.zero_()
+            self.stream.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=self.stream):
+            fn(torch.cuda.current_stream().cuda_stream)
+        self.graphs["host"] = graph
+        self._stage = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        self._loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+
+    def step_from_host(self, targets_pinned: torch.Tensor, batch_id: int) -> float:
+        """H2D the batch's targets, run the step, D2H its loss (synchronous)."""
+        n = int(targets_pinned.numel())
+        with torch.cuda.stream(self.stream):
+            self.sw.targets[:n].copy_(targets_pinned, non_blocking=True)
+            self._stage[0] = n
+            self._stage[1] = self.seed & 0x7FFFFFFF
+            self._stage[2] = self.epoch
+            self._stage[3] = batch_id
+            self.sw.n_targets.copy_(self._stage[0:1], non_blocking=True)
+            self.sw.key.copy_(self._stage[1:4], non_blocking=True)
+            self.graphs["host"].replay()
+            self._loss_host.copy_(self.tw.loss, non_blocking=True)
+            self.tw.loss.zero_()
+        self.stream.synchronize()
+        self.dm.host_steps += 1
+        return float(self._loss_host[0])
