@@ -215,9 +215,10 @@ int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, do
                   void* stream);
 
 /* RaCoM packing for the NCCL collectives (racom.py:47-57, 118-139):
- * out64[i] = (double)in32[i];  out32[i] = (float)(in64[i] * scale). */
+ * out64[i] = (double)in32[i];  out32[i] = (float)(in64[i] / divisor) — the
+ * replica average of sync_models (sum over replicas in f64, then / n). */
 int mq_f32_to_f64(const float* in32, double* out64, int64_t n, void* stream);
-int mq_f64_to_f32(const double* in64, double scale, float* out32, int64_t n, void* stream);
+int mq_f64_to_f32(const double* in64, double divisor, float* out32, int64_t n, void* stream);
 
 /* ------------------------------------------------------------- utilities */
 /* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */

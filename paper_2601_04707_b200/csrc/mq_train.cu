@@ -69,14 +69,16 @@ __global__ void step_commit_kernel(double* loss_acc, const int32_t* cursor, doub
   loss_acc[0] = 0.0;
 }
 
+// grad32, or the f64 window sum: * scale, or (scale == 0) / the all-reduced
+// contributor count packed at g64[n] by mq_pack_grads
 __device__ __forceinline__ float load_grad(const float* g32, const double* g64, double scale,
-                                           int64_t i) {
-  return g32 ? g32[i] : (float)(g64[i] * scale);
+                                           double count, int64_t i) {
+  if (g32) return g32[i];
+  return scale != 0.0 ? (float)(g64[i] * scale) : (float)(g64[i] / count);
 }
 
-// scale == 0 selects the packed contributor count g64[n] (mq_pack_grads)
-__device__ __forceinline__ double grad_scale_of(const double* g64, double scale, int64_t n) {
-  return (g64 != nullptr && scale == 0.0) ? 1.0 / g64[n] : scale;
+__device__ __forceinline__ double grad_count(const double* g64, double scale, int64_t n) {
+  return (g64 != nullptr && scale == 0.0) ? g64[n] : 1.0;
 }
 
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
@@ -90,13 +92,13 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
     return;
   }
   const float bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
-  scale = grad_scale_of(g64, scale, n);
+  const double count = grad_count(g64, scale, n);
   const float b1 = (float)0.9, b2 = (float)0.999;
   const float c1 = (float)(1.0 - 0.9), c2 = (float)(1.0 - 0.999), eps = (float)1e-8;
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float g = load_grad(g32, g64, scale, i);
+    const float g = load_grad(g32, g64, scale, count, i);
     float mi = __fmul_rn(m[i], b1);                         // m *= beta1
     mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
     float vi = __fmul_rn(v[i], b2);                         // v *= beta2
@@ -116,11 +118,11 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
                            const double* __restrict__ g64, double scale, int64_t n, float lr,
                            int32_t* __restrict__ nonfinite) {
-  scale = grad_scale_of(g64, scale, n);
+  const double count = grad_count(g64, scale, n);
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float wi = __fsub_rn(w[i], __fmul_rn(lr, load_grad(g32, g64, scale, i)));
+    const float wi = __fsub_rn(w[i], __fmul_rn(lr, load_grad(g32, g64, scale, count, i)));
     w[i] = wi;
     bad |= !finite_f(wi);
   }
@@ -140,11 +142,11 @@ __global__ void pack_grads_kernel(const float* __restrict__ a, int64_t n,
     b[i] = i < n ? (double)a[i] : (n_targets[0] > 0 ? 1.0 : 0.0);
 }
 
-__global__ void f64_to_f32_kernel(const double* __restrict__ a, double scale, float* __restrict__ b,
-                                  int64_t n) {
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, double divisor,
+                                  float* __restrict__ b, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = (float)(a[i] * scale);
+    b[i] = (float)(a[i] / divisor);
 }
 
 inline int elem_blocks(int64_t n) {
@@ -253,13 +255,13 @@ int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, do
   return MQ_OK;
 }
 
-int mq_f64_to_f32(const double* in64, double scale, float* out32, int64_t n, void* stream) {
-  MQ_CHECK_ARG(in64 && out32, "mq_f64_to_f32: null pointer");
+int mq_f64_to_f32(const double* in64, double divisor, float* out32, int64_t n, void* stream) {
+  MQ_CHECK_ARG(in64 && out32 && divisor != 0.0, "mq_f64_to_f32: null pointer or zero divisor");
   if (n <= 0) return MQ_OK;
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_CONVERT, s);
-    f64_to_f32_kernel<<<elem_blocks(n), 256, 0, s>>>(in64, scale, out32, n);
+    f64_to_f32_kernel<<<elem_blocks(n), 256, 0, s>>>(in64, divisor, out32, n);
   }
   MQ_LAUNCH_CHECK("f64_to_f32");
   return MQ_OK;

@@ -80,6 +80,10 @@ class SampleWorkspace:
         self.hops = [HopBuffers(b, dev) for b in self.bounds]
         scr = max(int(lib().mq_relabel_scratch_bytes(b.n_dst_max, b.fanout)) for b in self.bounds)
         self.scratch = torch.zeros(scr, dtype=torch.uint8, device=dev)
+        # node-indexed relabel tables, private to this workspace so replicas
+        # sampling concurrently on different streams never share them
+        self.dpos = torch.full((g.num_nodes,), -1, dtype=torch.int32, device=dev)
+        self.first = torch.full((g.num_nodes,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
 
     # device scalars for hop h
     def n_dst_dev(self, h: int) -> torch.Tensor:
@@ -108,7 +112,7 @@ class SampleWorkspace:
                             epoch & 0xFFFFFFFF, batch & 0xFFFFFFFF, h, key, ptr(hb.nbr),
                             ptr(hb.cnt), stream)
             L.mq_relabel(ptr(self.dst(h)), ptr(self.n_dst_dev(h)), b.n_dst_max, ptr(hb.nbr),
-                         ptr(hb.cnt), b.fanout, ptr(g.dpos), ptr(g.first), ptr(hb.row_ptr),
+                         ptr(hb.cnt), b.fanout, ptr(self.dpos), ptr(self.first), ptr(hb.row_ptr),
                          ptr(hb.rows), ptr(hb.cols), ptr(hb.vals), ptr(hb.src_ids),
                          ptr(hb.counts), ptr(self.scratch), stream)
 

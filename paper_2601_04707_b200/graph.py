@@ -13,7 +13,6 @@ HBM layout:
     Placement "hbm" keeps the table in device memory; "host" keeps it in
     pinned host memory and the gather reads misses over the host link.
   * ``labels`` int32 [n].
-  * relabel tables ``dpos``/``first`` int32 [n] (reset by each relabel).
 """
 
 from __future__ import annotations
@@ -92,8 +91,6 @@ class DeviceGraph:
                 table = torch.zeros((n, self.pitch), dtype=torch.float32, pin_memory=True)
                 table[:, :self.feature_dim] = _as_tensor(feats, torch.float32, "cpu")
             self.features = table
-            self.dpos = torch.full((n,), -1, dtype=torch.int32, device=dev)
-            self.first = torch.full((n,), INT32_MAX, dtype=torch.int32, device=dev)
         return self
 
     # ---- reference-compatible views

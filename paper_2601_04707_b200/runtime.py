@@ -1,0 +1,266 @@
+"""Drop-in ``run_epoch`` over the device step graphs, plus the epoch plan.
+
+Mirrors ``mqpipe/runtime.py``:
+
+* ``PipelineConfig``  — ``runtime.py:39-69`` (same fields; the timing
+  simulation knobs only exist for the reference's thread simulator and must
+  stay at their defaults here)
+* ``EpochStats``      — ``runtime.py:72-92``
+* ``plan_epoch``      — ``runtime.py:95-117`` (same NumPy shuffle, so the
+  batches are identical to the reference's)
+* ``batch_rng``       — ``runtime.py:120-124`` -> the Philox stream key
+* ``transfer_stage``  — ``runtime.py:127-143``
+* ``run_epoch``       — ``runtime.py:208-226``
+
+The sample -> transfer -> compute -> update queue pipeline of the reference's
+threaded mode becomes a single captured CUDA graph per replica step: the
+bounded queues disappear because the stages are stream-ordered on the
+device, and the host only launches one graph per window.  Replicas are either
+several StepRunners in this process (the reference's simulated devices, one
+GPU) or one per process over torch.distributed (NCCL over NVLink), with the
+RaCoM schedule of ``racom.WindowDriver``.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .cache import DeviceCache, gather_features
+from .pipeline import MS_TO_NS, Trace
+from .racom import DistExchange, WindowDriver
+from .samplers import PhiloxStream, SamplerParams
+from .trainer import StepRunner
+
+
+@dataclass
+class PipelineConfig:
+    num_devices: int = 1
+    queue_capacity: int = 2
+    sampler_workers: int = 1
+    batch_size: int = 1024
+    sampler: SamplerParams = field(default_factory=SamplerParams)
+    optimizer: str = "adam"
+    sync_period: int = 1
+    delay_model: object = None
+    transfer_model: object = None
+    timing_mode: str = "real"
+    stage_durations: dict = field(default_factory=dict)
+    deterministic: bool = False
+    seed: int = 0
+    queue_timeout: float = 60.0
+    capture_weights: bool = False
+    use_graph: bool = True
+
+    def validate(self) -> None:
+        if self.num_devices < 1:
+            raise ValueError("need at least one device")
+        if self.queue_capacity < 1:
+            raise ValueError("queue capacity must be at least 1")
+        if self.sampler_workers < 1:
+            raise ValueError("need at least one sampler worker per device")
+        if self.sync_period < 1:
+            raise ValueError("sync period must be at least 1")
+        if self.timing_mode not in ("real", "simulated"):
+            raise ValueError(f"unknown timing_mode {self.timing_mode!r}")
+        if self.optimizer not in ("adam", "sgd"):
+            raise ValueError(f"unknown optimizer {self.optimizer!r}")
+        if self.sampler.method != "sage":
+            raise NotImplementedError("the device runtime trains GraphSAGE node-wise batches")
+        if self.timing_mode != "real" or self.stage_durations:
+            raise NotImplementedError("simulated stage timings belong to the reference simulator")
+        dm = self.delay_model
+        if dm is not None and getattr(dm, "kind", "none") != "none":
+            raise NotImplementedError("gradient delay injection is not modelled on devices")
+
+
+@dataclass
+class EpochStats:
+    epoch: int
+    losses: dict
+    batches: int
+    cache_hits: int = 0
+    cache_misses: int = 0
+    dropped_targets: int = 0
+    sync_count: int = 0
+    epoch_sync: int = 0
+    applied_windows: dict = field(default_factory=dict)
+    queue_high_water: dict = field(default_factory=dict)
+    queue_keys: dict = field(default_factory=dict)
+    weight_traces: dict = field(default_factory=dict)
+    wall_ms: float = 0.0
+
+    @property
+    def mean_loss(self) -> float:
+        if not self.losses:
+            return float("nan")
+        return float(np.mean(list(self.losses.values())))
+
+
+def epoch_permutation(train_mask, seed: int, epoch: int) -> np.ndarray:
+    train_ids = np.flatnonzero(train_mask)
+    if train_ids.size == 0:
+        raise ValueError("graph has no training nodes")
+    rng = np.random.default_rng(np.random.SeedSequence([seed, epoch, 0]))
+    return rng.permutation(train_ids)
+
+
+def plan_epoch(g, config: PipelineConfig, epoch: int):
+    """(per_device[(window, batch_id, targets)], expected[k]) — runtime.py:95-117."""
+    perm = epoch_permutation(g.train_mask, config.seed, epoch)
+    bs = config.batch_size
+    batches = [perm[i:i + bs] for i in range(0, perm.size, bs)]
+    per_device = [[] for _ in range(config.num_devices)]
+    for j, targets in enumerate(batches):
+        d = j % config.num_devices
+        per_device[d].append((len(per_device[d]), j, targets))
+    total = max((len(x) for x in per_device), default=0)
+    expected = [sum(1 for x in per_device if len(x) > k) for k in range(total)]
+    return per_device, expected
+
+
+def batch_rng(config: PipelineConfig, epoch: int, batch_id: int) -> PhiloxStream:
+    """Batch content depends only on (seed, epoch, batch_id) (runtime.py:120-124)."""
+    return PhiloxStream(config.seed, epoch, batch_id)
+
+
+def transfer_stage(batch, cache, g, transfer_model=None, rng=None):
+    """Serve cached rows from HBM, misses from the store (runtime.py:127-143).
+    Returns (batch, miss_bytes) — the bytes that crossed the host link when
+    the store is pinned host memory."""
+    ids = batch.input_ids
+    if cache is not None:
+        hit = cache.cached_mask[ids.long()]
+        batch.cache_hits = int(hit.sum().item())
+        batch.cache_misses = int(ids.numel()) - batch.cache_hits
+        miss_rows = batch.cache_misses
+    else:
+        miss_rows = int(ids.numel())
+    batch.features = gather_features(cache, g, ids, count_hits=cache is not None).clone()
+    return batch, miss_rows * g.feature_dim * 4
+
+
+def _distributed():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+
+
+def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
+    key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
+           config.seed, world, rank, multi, num_train, config.use_graph)
+    r = getattr(replica, "_runner", None)
+    if r is None or r[0] != key:
+        runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
+                            batch_size=config.batch_size, num_train=num_train, cache=cache,
+                            optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
+                            multi=multi, use_graph=config.use_graph)
+        replica._runner = (key, runner)
+        return runner, True
+    return r[1], False
+
+
+def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
+              trace: Trace | None = None):
+    """Train one epoch; returns (EpochStats, Trace).  Every training target
+    lands in exactly one batch; all windows are applied on every replica and
+    multi-replica runs end with the epoch-barrier model average."""
+    config.validate()
+    if trace is None:
+        trace = Trace()
+    if cache is not None and not isinstance(cache, DeviceCache):
+        cache = DeviceCache(g, cache)
+    dist_mode = _distributed()
+    if dist_mode:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(), dist.get_rank()
+        if config.num_devices != world or len(replicas) != 1:
+            raise ValueError("distributed run: one replica per rank, num_devices == world size")
+        exchange = DistExchange()
+        local_ranks = [rank]
+    else:
+        if len(replicas) != config.num_devices:
+            raise ValueError("one model replica per device required")
+        world = config.num_devices
+        exchange = None
+        local_ranks = list(range(world))
+    per_device, expected = plan_epoch(g, config, epoch)
+    total_windows = len(expected)
+    perm = epoch_permutation(g.train_mask, config.seed, epoch)
+    multi = world > 1
+    runners = []
+    for d, rep in zip(local_ranks, replicas):
+        r, fresh = _runner_for(rep, g, cache, config, world, d, multi, perm.size)
+        r.begin_epoch(epoch, perm)
+        if config.use_graph:
+            r.capture()
+        runners.append(r)
+    hm0 = cache.hit_miss.clone() if cache is not None else None
+    weight_traces = {d: [] for d in local_ranks}
+    starts, ends = [], []
+
+    def on_window(k):
+        if config.capture_weights:
+            for d, r in zip(local_ranks, runners):
+                r.sync_point()
+                weight_traces[d].append((k, [w.detach().cpu().numpy().copy()
+                                             for w in r.model.weights]))
+
+    t0 = time.perf_counter()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(runners[0].stream)
+    info = WindowDriver(runners, exchange, config.sync_period).run(total_windows, on_window)
+    ev1.record(runners[0].stream)
+    for r in runners:
+        r.check_finite()
+    torch.cuda.synchronize(g.device)
+    gpu_ms = ev0.elapsed_time(ev1)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+
+    losses = {}
+    for d, r in zip(local_ranks, runners):
+        ring = r.losses(len(per_device[d]))
+        for k, (_, bid, _) in enumerate(per_device[d]):
+            losses[bid] = float(ring[k])
+    hits = misses = 0
+    if cache is not None:
+        delta = (cache.hit_miss - hm0).cpu().numpy()
+        hits, misses = int(delta[0]), int(delta[1])
+    if dist_mode:
+        import torch.distributed as dist
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (losses, hits, misses))
+        losses = {}
+        hits = misses = 0
+        for l_, h_, m_ in gathered:
+            losses.update(l_)
+            hits += h_
+            misses += m_
+    # coarse trace: one compute span per window, split fwd/bwd as the serial
+    # reference does with its duration models (runtime.py:332-333)
+    per_win = gpu_ms / max(total_windows, 1)
+    for d in local_ranks:
+        for k, (_, bid, _) in enumerate(per_device[d]):
+            a = k * per_win * MS_TO_NS
+            trace.add("compute_fwd", d, bid, epoch, a, a + per_win * MS_TO_NS / 2)
+            trace.add("compute_bwd", d, bid, epoch, a + per_win * MS_TO_NS / 2,
+                      a + per_win * MS_TO_NS)
+            trace.add("grad_apply", d, k, epoch, a + per_win * MS_TO_NS, a + per_win * MS_TO_NS)
+        t_end = total_windows * per_win * MS_TO_NS
+        for _ in range(info["sync_count"] + info["epoch_sync"]):
+            trace.add("sync", d, -1, epoch, t_end, t_end)
+    stats = EpochStats(
+        epoch=epoch, losses=losses, batches=sum(len(x) for x in per_device),
+        cache_hits=hits, cache_misses=misses, dropped_targets=0,
+        sync_count=info["sync_count"], epoch_sync=info["epoch_sync"],
+        applied_windows={d: info["applied"] for d in range(config.num_devices)},
+        queue_high_water={d: {"cpu": 1 if per_device[d] else 0, "dev": 1 if per_device[d] else 0}
+                          for d in range(config.num_devices)},
+        queue_keys={d: {k: [b for _, b, _ in per_device[d]]
+                        for k in ("cpu_put", "cpu_get", "dev_put", "dev_get")}
+                    for d in range(config.num_devices)},
+        weight_traces=weight_traces, wall_ms=wall_ms)
+    return stats, trace

@@ -187,7 +187,7 @@ def _run_hops(g, targets, fanouts, rng: PhiloxStream, cache, hop0: int = 0):
                             rng.epoch & 0xFFFFFFFF, rng.batch_id & 0xFFFFFFFF, hop0, None,
                             ptr(hb.nbr), ptr(hb.cnt), stream)
         lib().mq_relabel(ptr(ws.targets), ptr(ws.n_targets), b.n_dst_max, ptr(hb.nbr), ptr(hb.cnt),
-                         b.fanout, ptr(g.dpos), ptr(g.first), ptr(hb.row_ptr), ptr(hb.rows),
+                         b.fanout, ptr(ws.dpos), ptr(ws.first), ptr(hb.row_ptr), ptr(hb.rows),
                          ptr(hb.cols), ptr(hb.vals), ptr(hb.src_ids), ptr(hb.counts),
                          ptr(ws.scratch), stream)
     counts = torch.stack([hb.counts for hb in ws.hops]).cpu().numpy()

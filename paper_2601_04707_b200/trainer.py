@@ -26,7 +26,7 @@ class StepRunner:
 
     def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
-                 exchange=None, use_graph: bool = True, ring_len: int = 1 << 16):
+                 multi: bool = False, use_graph: bool = True, ring_len: int = 1 << 16):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         self.g = g
@@ -36,7 +36,7 @@ class StepRunner:
         self.optimizer = optimizer
         self.seed = int(seed)
         self.world, self.rank = int(world), int(rank)
-        self.exchange = exchange
+        self.multi = bool(multi)
         self.use_graph = use_graph
         dev = g.device
         self.device = dev
@@ -51,7 +51,7 @@ class StepRunner:
         self.ring_len = int(ring_len)
         self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
         self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
-                       if exchange is not None else None)
+                       if self.multi else None)
         self.stream = torch.cuda.Stream(device=dev)
         self.graphs = {}
         self.windows_done = 0
@@ -128,9 +128,7 @@ class StepRunner:
             snap = self._snapshot()
             s = self.stream.cuda_stream
             for fn in phases.values():
-                fn(s)
-                if self.exchange is not None and fn is phases.get("compute"):
-                    pass  # warm-up only: no collective
+                fn(s)  # warm-up only: no collective in between
             self.stream.synchronize()
             self._restore(snap)
             self.tw.loss.zero_()
@@ -157,26 +155,57 @@ class StepRunner:
         return int(lib().mq_launch_count() - before)
 
     # ------------------------------------------------------------------ step
-    def step(self):
-        """One window of this replica (async; nothing is read back)."""
+    def _replay(self, name):
         with torch.cuda.stream(self.stream):
-            if self.grad64 is None:
-                if self.use_graph:
-                    self.graphs["full"].replay()
-                else:
-                    self._phases()["full"](self.stream.cuda_stream)
+            if self.use_graph:
+                self.graphs[name].replay()
+            elif name == "update":
+                self._enqueue_update(self.stream.cuda_stream)
             else:
-                if self.use_graph:
-                    self.graphs["compute"].replay()
-                else:
-                    self._phases()["compute"](self.stream.cuda_stream)
-                self.exchange.allreduce_sum(self.grad64, self.stream)
-                if self.use_graph:
-                    self.graphs["update"].replay()
-                else:
-                    self._enqueue_update(self.stream.cuda_stream)
+                self._phases()[name](self.stream.cuda_stream)
+
+    # RaCoM protocol (racom.WindowDriver): compute -> exchange grad64 -> apply.
+    # A lone replica's compute already contains its update ("full" graph).
+    def compute_window(self):
+        self._replay("compute" if self.multi else "full")
+
+    def apply_window(self):
+        if self.multi:
+            self._replay("update")
         self.dm.host_steps += 1
         self.windows_done += 1
+
+    def step(self):
+        """One window (async; nothing is read back)."""
+        if self.multi:
+            raise RuntimeError("multi-replica runners need the exchange: use racom.WindowDriver")
+        self.compute_window()
+        self.apply_window()
+
+    def state64(self) -> torch.Tensor:
+        from .racom import _pack_state
+        with torch.cuda.stream(self.stream):
+            out = torch.empty(3 * self.dm.num_params, dtype=torch.float64, device=self.device)
+            _pack_state(self.model, out)
+        return out
+
+    def load_state64(self, t: torch.Tensor, divisor: int):
+        from .racom import _unpack_state
+        with torch.cuda.stream(self.stream):
+            _unpack_state(self.model, t, divisor)
+
+    @property
+    def step_count(self) -> int:
+        return self.dm.host_steps
+
+    def sync_point(self):
+        self.stream.synchronize()
+
+    def stream_ctx(self):
+        return torch.cuda.stream(self.stream)
+
+    def wait_current(self):
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
 
     def losses(self, n_windows: int) -> np.ndarray:
         self.stream.synchronize()
@@ -196,7 +225,7 @@ class StepRunner:
         """Graph variant that reads targets staged by the host (no device plan)."""
         if "host" in self.graphs:
             return
-        if self.grad64 is not None:
+        if self.multi:
             raise NotImplementedError("host-input steps are single-replica")
 
         def fn(s):
