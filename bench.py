@@ -1,0 +1,502 @@
+#!/usr/bin/env python
+"""Benchmark: seed nodes/s of MQ-GNN's per-iteration GraphSAGE training step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--shape reddit|products|cfg1] [--no-cpu-baseline]
+
+A step = one RaCoM window on every rank: device-side batch plan, 2 hops of
+GNS-cache-biased sampling + relabel, feature gather, SAGE forward, summed
+softmax-CE, backward, (f64 gradient all-reduce when N > 1) and Adam — the
+per-batch body of the reference's run_epoch (mqpipe/runtime.py:294-323).
+
+Workload (BASELINE.json configs[1]): Reddit-shaped synthetic power-law graph,
+232,965 nodes, 114M arcs, 602-d features, 41 classes, fanouts [10, 5],
+batch 1024, hidden 64, 1% degree-mode GNS cache, Adam lr 1e-3.  Graph,
+features and cache are resident in HBM before timing (``value``); ``e2e``
+is the same metric through the public host-buffer entry point
+(StepRunner.step_from_host: pinned H2D of the batch's targets, one graph
+launch, D2H of the loss, every step).  Inputs (1.1 GB of CSR + features)
+exceed the 126 MB L2, so no explicit flush is done.
+
+``--impl reference`` times the CPU oracle port of the reference path
+(oracle/, restated from mqpipe and pinned to reference-generated golden
+vectors) on this host's cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "seed nodes/sec & epoch time at 1/2/4/8 B200; sample/gather/SpMM GB/s vs HBM"
+UNIT = "seed nodes/s"
+SHAPE_DESC = {
+    "reddit": "reddit-shaped: 232,965 nodes / 114M arcs / 602-d / 41 classes, SAGE 2-layer "
+              "fanout [10,5], batch 1024, hidden 64, 1% GNS degree cache (BASELINE configs[1])",
+    "products": "ogbn-products-shaped: 2,449,029 nodes / 62M arcs / 100-d / 47 classes, SAGE "
+                "3-layer fanout [15,10,5], batch 1024, hidden 64, 1% GNS walk-free degree cache",
+    "cfg1": "cfg1: 10k nodes / 100k arcs / 64-d / 4 classes, SAGE 2-layer fanout [10,5], "
+            "batch 1024, hidden 64, 1% GNS degree cache (BASELINE configs[0])",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default="reddit", choices=list(SHAPE_DESC))
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--hidden", type=int, default=64)
+    ap.add_argument("--cache-fraction", type=float, default=0.01)
+    ap.add_argument("--feature-placement", default="hbm", choices=["hbm", "host"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------- inputs
+def build_inputs(args, device):
+    """Synthetic graph (GPU generator when a GPU exists) + degree-mode cache mask."""
+    from paper_2601_04707_b200 import synth
+    t0 = time.perf_counter()
+    sg, fanouts = synth.generate_shape(args.shape, seed=args.seed, device=device)
+    t_gen = time.perf_counter() - t0
+    return sg, fanouts, t_gen
+
+
+def cache_mask_from(sg, fraction, seed):
+    """Degree-mode residency exactly as refresh_cache (cache.py:79-108):
+    ceil(f*|V|) ids drawn WOR with probability ~ in-degree (cache.py:41-48)."""
+    from paper_2601_04707_b200.cache import weighted_sample_without_replacement
+    import torch
+    col = sg.col_indices
+    n = sg.num_nodes
+    if isinstance(col, torch.Tensor):
+        indeg = torch.bincount(col.long(), minlength=n).double().cpu().numpy()
+    else:
+        indeg = np.bincount(col, minlength=n).astype(np.float64)
+    probs = indeg / indeg.sum()
+    budget = int(math.ceil(fraction * n))
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0, 8]))
+    chosen = weighted_sample_without_replacement(probs, budget, rng)
+    mask = np.zeros(n, dtype=bool)
+    mask[chosen] = True
+    return mask
+
+
+def host_arrays(sg):
+    import torch
+
+    def h(a, dt):
+        if isinstance(a, torch.Tensor):
+            return a.detach().cpu().numpy().astype(dt, copy=False)
+        return np.asarray(a).astype(dt, copy=False)
+    return (h(sg.row_offsets, np.int64), h(sg.col_indices, np.int64),
+            h(sg.features, np.float32), h(sg.labels, np.int32))
+
+
+# ---------------------------------------------------------------- CPU oracle
+def cpu_oracle_run(ro, col, feats, labels, mask, perm, fanouts, args, budget_s, max_batches):
+    """The oracle's per-batch path (sample -> gather -> fwd/bwd -> Adam)."""
+    from oracle import nn as onn
+    from oracle import sampler as osamp
+    model = onn.init_model(feats.shape[1], args.hidden, int(labels.max()) + 1,
+                           num_layers=len(fanouts), seed=args.seed, learning_rate=1e-3)
+    B = args.batch
+    seeds = 0
+    t0 = time.perf_counter()
+    nb = 0
+    for j in range(max_batches):
+        tg = perm[j * B:(j + 1) * B]
+        if tg.size == 0:
+            break
+        mb = osamp.build_minibatch(ro, col, feats, labels, tg, fanouts, seed=args.seed, epoch=0,
+                                   batch_id=j, cached_mask=mask)
+        _, grads, _ = onn.loss_and_grads(mb.layers, mb.features, mb.target_labels, model.weights)
+        onn.adam_step(model, grads)
+        seeds += tg.size
+        nb += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return seeds, nb, dt
+
+
+def cores_used():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:  # pragma: no cover
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxs.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxs) if maxs else None, "samples": len(sms),
+                "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_table():
+    """Per-launch DRAM bytes of each kernel from the committed ncu capture."""
+    files = sorted((ROOT / "profiles").glob("traffic_*.json"))
+    if not files:
+        return {}
+    return json.loads(files[-1].read_text())
+
+
+# ------------------------------------------------------------------- arms
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import torch
+    device = "cuda" if torch.cuda.is_available() else None
+    sg, fanouts, t_gen = build_inputs(args, device)
+    mask = cache_mask_from(sg, args.cache_fraction, args.seed)
+    ro, col, feats, labels = host_arrays(sg)
+    from paper_2601_04707_b200.runtime import epoch_permutation
+    perm = epoch_permutation(np.asarray(sg.train_mask), args.seed, 0)
+    del sg
+    if device:
+        torch.cuda.empty_cache()
+    # warm-up batches are not timed; each timed step is one batch, capped so
+    # the whole arm stays within a few minutes
+    w = min(args.warmup, 2)
+    cpu_oracle_run(ro, col, feats, labels, mask, perm, fanouts, args, 60.0, w)
+    budget = float(os.environ.get("MQ_REF_BUDGET_S", 90.0))
+    seeds, nb, dt = cpu_oracle_run(ro, col, feats, labels, mask, perm[w * args.batch:], fanouts,
+                                   args, budget, args.steps)
+    value = seeds / dt
+    cores = cores_used()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": nb, "warmup": w, "ms_per_step": dt * 1e3 / max(nb, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": SHAPE_DESC[args.shape],
+                                        "parallelism": "cpu oracle, rank 0 only"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{nb} batches x {args.batch} seeds of the {args.shape} "
+                                   f"workload (oracle/ NumPy restatement of mqpipe, pinned to "
+                                   f"reference golden vectors), {dt:.1f} s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200._lib import lib
+    from paper_2601_04707_b200.roofline import step_flops, step_models
+    from paper_2601_04707_b200.runtime import epoch_permutation
+
+    setup = {}
+    sg, fanouts, setup["graph_gen_s"] = build_inputs(args, f"cuda:{local}")
+    t0 = time.perf_counter()
+    g = mq.DeviceGraph.from_csr(sg, device=dev, feature_placement=args.feature_placement)
+    torch.cuda.synchronize()
+    setup["upload_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mask = cache_mask_from(sg, args.cache_fraction, args.seed)
+    cache = mq.DeviceCache(g, mask, args.cache_fraction)
+    torch.cuda.synchronize()
+    setup["cache_refresh_s"] = time.perf_counter() - t0
+    model = mq.init_model(g.feature_dim, args.hidden, g.num_classes, num_layers=len(fanouts),
+                          seed=args.seed, learning_rate=1e-3, device=dev)
+    n_train = int(g.train_mask.sum())
+    windows = -(-n_train // (args.batch * world))
+    runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=args.batch, num_train=n_train,
+                           cache=cache, optimizer="adam", seed=args.seed, world=world, rank=rank,
+                           multi=world > 1)
+    exchange = mq.DistExchange() if world > 1 else None
+    driver = mq.WindowDriver([runner], exchange, sync_period=1)
+    t0 = time.perf_counter()
+    runner.capture()
+    setup["capture_s"] = time.perf_counter() - t0
+    epoch = [0]
+    runner.begin_epoch(0, epoch_permutation(g.train_mask, args.seed, 0))
+    seeds_done = [0]
+    plan_sizes = np.minimum(args.batch, np.maximum(
+        0, n_train - np.arange(windows * world) * args.batch))
+
+    def one_window():
+        if runner.windows_done >= windows:
+            epoch[0] += 1
+            runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
+        k = runner.windows_done
+        for r in range(world):
+            seeds_done[0] += int(plan_sizes[k * world + r])
+        if world == 1:
+            runner.step()
+        else:
+            runner.compute_window()
+            driver._reduce([runner.grad64])
+            runner.apply_window()
+
+    for _ in range(args.warmup):
+        one_window()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    seeds_done[0] = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(runner.stream)
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        one_window()
+    ev1.record(runner.stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    runner.check_finite()
+    value = seeds_done[0] / (ms_max / 1e3)
+
+    # -------- per-kernel profile (eager, instrumented, same workload) --------
+    per_kernel = {}
+    n_kernels = runner.kernels_per_step()
+    if rank == 0:
+        L = lib()
+        L.mq_prof_reset()
+        L.mq_prof_enable(1)
+        bytes_acc: dict = {}
+        flops_acc: dict = {}
+        prof_ev0 = torch.cuda.Event(enable_timing=True)
+        prof_ev1 = torch.cuda.Event(enable_timing=True)
+        dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
+        prof_step_ms = []
+        for _ in range(args.profile_steps):
+            if runner.windows_done >= windows:
+                epoch[0] += 1
+                runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
+            prof_ev0.record(runner.stream)
+            with torch.cuda.stream(runner.stream):
+                for fn in runner._phases().values():
+                    fn(runner.stream.cuda_stream)
+            prof_ev1.record(runner.stream)
+            runner.dm.host_steps += 1
+            runner.windows_done += 1
+            c = runner.read_counts()
+            prof_step_ms.append(prof_ev0.elapsed_time(prof_ev1))
+            for name, lst in step_models(c, dims, fanouts, True, runner.dm.num_params,
+                                         g.num_classes).items():
+                bytes_acc[name] = bytes_acc.get(name, 0.0) + sum(lst)
+            for name, f in step_flops(c, dims, fanouts).items():
+                flops_acc[name] = flops_acc.get(name, 0.0) + f
+        L.mq_prof_enable(0)
+        nk = L.mq_prof_num_kernels()
+        tot = np.zeros(nk, dtype=np.float64)
+        cnt = np.zeros(nk, dtype=np.int64)
+        L.mq_prof_read(tot.ctypes.data, cnt.ctypes.data, nk)
+        all_ms = float(tot.sum())
+        for i in range(nk):
+            if cnt[i] == 0:
+                continue
+            name = L.mq_prof_kernel_name(i).decode()
+            b = bytes_acc.get(name)
+            per_kernel[name] = {
+                "ms_per_step": tot[i] / args.profile_steps,
+                "launches_per_step": cnt[i] / args.profile_steps,
+                "share": tot[i] / all_ms,
+                "avg_launch_us": tot[i] / cnt[i] * 1e3,
+                "gbps": (b / (tot[i] / 1e3) / 1e9) if b else None,
+                "bytes_per_launch": (b / cnt[i]) if b else None,
+                "tflops": (flops_acc[name] / (tot[i] / 1e3) / 1e12) if name in flops_acc else None,
+            }
+    # ----------------------------- e2e through the host-buffer entry point ---
+    e2e = None
+    if world == 1:
+        runner.capture_host_input()
+        perm_e2e = epoch_permutation(g.train_mask, args.seed, 100)
+        B = args.batch
+        nb = min(args.e2e_steps, len(perm_e2e) // B)
+        host_batches = [torch.from_numpy(perm_e2e[j * B:(j + 1) * B].astype(np.int32)).pin_memory()
+                        for j in range(nb)]
+        for j in range(min(5, nb)):
+            runner.step_from_host(host_batches[j], j)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(runner.stream)
+        seeds = 0
+        for j in range(nb):
+            runner.step_from_host(host_batches[j], j)
+            seeds += int(host_batches[j].numel())
+        e1.record(runner.stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        e2e = {"value": seeds / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * B + 16,
+               "d2h_bytes_per_step": 8, "steps": nb, "ms_per_step": e2e_ms / nb,
+               "entry": "StepRunner.step_from_host (pinned targets H2D, graph, loss D2H)"}
+    runner.check_finite()
+
+    # ----------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ro, col, feats, labels = host_arrays(sg)
+        perm = epoch_permutation(g.train_mask, args.seed, 0)
+        seeds, nbat, dt = cpu_oracle_run(ro, col, feats, labels, mask, perm, fanouts, args,
+                                         args.cpu_seconds, 10_000)
+        cpu = {"value": seeds / dt, "unit": UNIT, "cores": cores_used(), "kind": "port",
+               "sample": f"{nbat} batches x {args.batch} seeds of the same workload through the "
+                         f"oracle (NumPy restatement of mqpipe's per-batch path), {dt:.1f} s"}
+
+    if rank == 0:
+        hbm, peak_kind = measured_peaks()
+        sample_like = {k: v for k, v in per_kernel.items()}
+        dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms_per_step"]) if per_kernel else None
+        traffic = traffic_table()
+        roof = None
+        if dom:
+            name, kd = dom
+            achieved = kd["gbps"]
+            t = traffic.get(name)
+            roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm,
+                    "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+                    "traffic": t, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                    "algorithmic_bytes_per_launch": kd["bytes_per_launch"],
+                    "avg_launch_us": kd["avg_launch_us"], "share_of_step": kd["share"]}
+        focus = {}
+        for nm in ("sample_hop", "gather", "spmm_fwd", "spmm_bwd_scatter", "linear_fwd",
+                   "linear_bwd_w", "residency_compact"):
+            if nm in sample_like:
+                focus[nm] = {"gbps": sample_like[nm]["gbps"],
+                             "frac_hbm": (sample_like[nm]["gbps"] / hbm
+                                          if sample_like[nm]["gbps"] else None),
+                             "share": sample_like[nm]["share"],
+                             "avg_launch_us": sample_like[nm]["avg_launch_us"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Chung-Lu power law, exponent 2.1, N(0,1) features, teacher "
+                    "labels; random-init weights)",
+            "config": {"workload": SHAPE_DESC[args.shape], "nodes": g.num_nodes,
+                       "arcs": g.num_edges, "feature_dim": g.feature_dim,
+                       "classes": g.num_classes, "fanouts": list(fanouts), "batch": args.batch,
+                       "hidden": args.hidden, "cache_fraction": args.cache_fraction,
+                       "optimizer": "adam", "feature_placement": args.feature_placement,
+                       "parallelism": f"dp{world} (RaCoM sync P=1)" if world > 1 else "dp1",
+                       "l2": "inputs larger than L2 (CSR+features ~1.1 GB), no flush",
+                       "cuda_graph": True},
+            "epoch_ms": ms_max / args.steps * windows, "windows_per_epoch": windows,
+            "roofline": roof, "kernels": focus,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": n_kernels * args.steps, "kernels_per_step": n_kernels,
+            "wall_s_timed": t_wall, "setup": setup,
+        }
+        print(json.dumps(line), flush=True)
+        if os.environ.get("MQ_BENCH_KERNELS"):
+            print(json.dumps({"per_kernel": per_kernel}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -51,11 +51,31 @@ def philox4x32_10(ctr, key):
     return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
 
 
+def _philox_scalar(c0, c1, c2, c3, k0, k1):
+    """Python-int Philox4x32-10 (same rounds; cheaper than NumPy for one block)."""
+    m = 0xFFFFFFFF
+    for rnd in range(10):
+        if rnd:
+            k0 = (k0 + W0) & m
+            k1 = (k1 + W1) & m
+        p0 = 0xD2511F53 * c0
+        p1 = 0xCD9E8D57 * c2
+        c0, c1, c2, c3 = ((p1 >> 32) ^ c1 ^ k0, p1 & m, (p0 >> 32) ^ c3 ^ k1, p0 & m)
+    return c0, c1, c2, c3
+
+
 def draws(seed: int, epoch: int, batch_id: int, hop: int, row: int,
           count: int) -> np.ndarray:
     """The first ``count`` uint32 draws x_0..x_{count-1} of one row stream."""
     if count <= 0:
         return np.empty(0, dtype=np.uint32)
+    if count <= 64:
+        out = []
+        k0, k1 = seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF
+        for b in range((count + 3) // 4):
+            out.extend(_philox_scalar(b, row & 0xFFFFFFFF, hop & 0xFFFFFFFF,
+                                      batch_id & 0xFFFFFFFF, k0, k1))
+        return np.array(out[:count], dtype=np.uint32)
     blocks = (count + 3) // 4
     ctr = np.zeros((blocks, 4), dtype=np.uint64)
     ctr[:, 0] = np.arange(blocks, dtype=np.uint64)

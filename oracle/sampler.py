@@ -18,7 +18,7 @@ import hashlib
 
 import numpy as np
 
-from .philox import draws, fisher_yates_positions
+from .philox import draws, fisher_yates_positions, philox4x32_10
 
 
 class OracleBlock:
@@ -45,10 +45,23 @@ class OracleBlock:
         return int(self.src_ids.size)
 
 
-def _choice(pool: np.ndarray, k: int, key) -> np.ndarray:
+def _choice(pool: np.ndarray, k: int, key, x=None) -> np.ndarray:
     """Injected ``rng.choice(pool, size=k, replace=False)`` (samplers.py:172-177)."""
-    x = draws(*key, count=k)
+    if x is None:
+        x = draws(*key, count=k)
     return pool[fisher_yates_positions(x, pool.size, k)]
+
+
+def _row_draws(n_rows, count, seed, epoch, batch_id, hop):
+    """x_0..x_{count-1} of every row stream of a hop, vectorised: [n_rows, count]."""
+    blocks = (count + 3) // 4
+    ctr = np.zeros((n_rows, blocks, 4), dtype=np.uint64)
+    ctr[:, :, 0] = np.arange(blocks, dtype=np.uint64)[None, :]
+    ctr[:, :, 1] = np.arange(n_rows, dtype=np.uint64)[:, None] & np.uint64(0xFFFFFFFF)
+    ctr[:, :, 2] = hop & 0xFFFFFFFF
+    ctr[:, :, 3] = batch_id & 0xFFFFFFFF
+    key = np.array([seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF], dtype=np.uint64)
+    return philox4x32_10(ctr, key).reshape(n_rows, blocks * 4)[:, :count]
 
 
 def node_wise_block(row_offsets, col_indices, dst_ids, fanout: int, *, seed: int,
@@ -59,6 +72,7 @@ def node_wise_block(row_offsets, col_indices, dst_ids, fanout: int, *, seed: int
     # last occurrence wins, as with the dict comprehension at samplers.py:156
     src_pos = {int(v): i for i, v in enumerate(dst_ids)}
     rows, cols, vals = [], [], []
+    xs = _row_draws(dst_ids.size, fanout, seed, epoch, batch_id, hop) if dst_ids.size else None
     for r, v in enumerate(dst_ids.tolist()):
         nbrs = col_indices[row_offsets[v]:row_offsets[v + 1]]
         nbrs = nbrs[nbrs != v]                      # samplers.py:162
@@ -70,12 +84,12 @@ def node_wise_block(row_offsets, col_indices, dst_ids, fanout: int, *, seed: int
             hot_sel = cached_mask[nbrs]
             hot, cold = nbrs[hot_sel], nbrs[~hot_sel]
             if hot.size >= fanout:
-                sampled = _choice(hot, fanout, key)
+                sampled = _choice(hot, fanout, key, xs[r])
             else:
                 sampled = np.concatenate(
-                    [hot, _choice(cold, fanout - hot.size, key)])
+                    [hot, _choice(cold, fanout - hot.size, key, xs[r])])
         else:                                       # :176-177
-            sampled = _choice(nbrs, fanout, key)
+            sampled = _choice(nbrs, fanout, key, xs[r])
         s = sampled.size
         for u in sampled.tolist():                  # :192-200
             if u not in src_pos:

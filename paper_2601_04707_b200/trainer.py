@@ -63,11 +63,15 @@ class StepRunner:
         perm = np.asarray(perm)
         if perm.size != self.num_train:
             raise ValueError("permutation length changed; build a new StepRunner")
+        # stream-ordered and host-asynchronous: pinned staging + non_blocking
+        # copies, so an epoch boundary does not drain the step pipeline
+        staged = torch.from_numpy(perm.astype(np.int32)).pin_memory()
+        key = torch.from_numpy(np.array([self.seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF, 0],
+                                        dtype=np.uint32).view(np.int32)).pin_memory()
         with torch.cuda.stream(self.stream):
-            self.perm.copy_(torch.as_tensor(perm.astype(np.int32)), non_blocking=False)
+            self.perm.copy_(staged, non_blocking=True)
             self.cursor.zero_()
-            self.sw.key.copy_(torch.tensor([self.seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF, 0],
-                                           dtype=torch.int64).to(torch.int32))
+            self.sw.key.copy_(key, non_blocking=True)
         self.epoch = epoch
         self.windows_done = 0
         n_windows = -(-self.num_train // (self.sw.batch_size * self.world))
@@ -207,6 +211,17 @@ class StepRunner:
     def wait_current(self):
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
 
+    def read_counts(self) -> dict:
+        """Device counts of the last step: targets and (n_dst, n_src, nnz) per hop."""
+        self.stream.synchronize()
+        c = torch.cat([self.sw.n_targets] + [hb.counts for hb in self.sw.hops]).cpu().tolist()
+        hops, nd = [], c[0]
+        for h in range(len(self.sw.hops)):
+            ns, nnz = c[1 + 2 * h], c[2 + 2 * h]
+            hops.append((nd, ns, nnz))
+            nd = ns
+        return {"n_targets": c[0], "hops": hops}
+
     def losses(self, n_windows: int) -> np.ndarray:
         self.stream.synchronize()
         return self.loss_ring[:n_windows].cpu().numpy()
@@ -250,10 +265,9 @@ class StepRunner:
         n = int(targets_pinned.numel())
         with torch.cuda.stream(self.stream):
             self.sw.targets[:n].copy_(targets_pinned, non_blocking=True)
-            self._stage[0] = n
-            self._stage[1] = self.seed & 0x7FFFFFFF
-            self._stage[2] = self.epoch
-            self._stage[3] = batch_id
+            self._stage.numpy().view(np.uint32)[:] = (n, self.seed & 0xFFFFFFFF,
+                                                      self.epoch & 0xFFFFFFFF,
+                                                      batch_id & 0xFFFFFFFF)
             self.sw.n_targets.copy_(self._stage[0:1], non_blocking=True)
             self.sw.key.copy_(self._stage[1:4], non_blocking=True)
             self.graphs["host"].replay()
