@@ -367,12 +367,8 @@ def run_ours(args):
                 epoch[0] += 1
                 runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
             prof_ev0.record(runner.stream)
-            with torch.cuda.stream(runner.stream):
-                for fn in runner._phases().values():
-                    fn(runner.stream.cuda_stream)
+            runner.eager_window()
             prof_ev1.record(runner.stream)
-            runner.dm.host_steps += 1
-            runner.windows_done += 1
             c = runner.read_counts()
             prof_step_ms.append(prof_ev0.elapsed_time(prof_ev1))
             for name, lst in step_models(c, dims, fanouts, True, runner.dm.num_params,
@@ -407,24 +403,23 @@ def run_ours(args):
         perm_e2e = epoch_permutation(g.train_mask, args.seed, 100)
         B = args.batch
         nb = min(args.e2e_steps, len(perm_e2e) // B)
-        host_batches = [torch.from_numpy(perm_e2e[j * B:(j + 1) * B].astype(np.int32)).pin_memory()
-                        for j in range(nb)]
-        for j in range(min(5, nb)):
-            runner.step_from_host(host_batches[j], j)
+        host_batches = [(j, torch.from_numpy(perm_e2e[j * B:(j + 1) * B].astype(np.int32))
+                         .pin_memory()) for j in range(nb)]
+        for _ in runner.run_host_batches(host_batches[:5]):
+            pass
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(runner.stream)
         seeds = 0
-        for j in range(nb):
-            runner.step_from_host(host_batches[j], j)
-            seeds += int(host_batches[j].numel())
+        for bid, _loss in runner.run_host_batches(host_batches):
+            seeds += int(host_batches[bid][1].numel())
         e1.record(runner.stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
         e2e = {"value": seeds / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * B + 16,
                "d2h_bytes_per_step": 8, "steps": nb, "ms_per_step": e2e_ms / nb,
-               "entry": "StepRunner.step_from_host (pinned targets H2D, graph, loss D2H)"}
+               "entry": "StepRunner.run_host_batches (per batch: pinned targets H2D, graph, loss D2H)"}
     runner.check_finite()
 
     # ----------------------------------------------------------- CPU baseline

@@ -154,15 +154,18 @@ int mq_spmm_bwd(const int32_t* rows, const int32_t* cols, const float* vals,
 /* sage_forward transform (nn.py:126-131): z = [agg | h_dst] @ W with W
  * (2*d_in, d_out) row-major.  z (pre-activation) and/or relu_out (max(z, 0))
  * are written when non-NULL; hidden layers only need relu_out because the
- * backward mask (pre > 0) equals (relu(pre) > 0). */
+ * backward mask (pre > 0) equals (relu(pre) > 0).  agg and h share one
+ * 16-byte-aligned pitch (ldagg == ldh).  Persistent split-K GEMM whose split
+ * count is chosen on the device from m; the fixed-order split reduction makes
+ * results deterministic.  scratch: mq_linear_scratch_bytes. */
+int64_t mq_linear_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out);
 int mq_sage_linear_fwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
                        const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
                        int32_t d_out, float* z, int32_t ldz, float* relu_out, int32_t ldr,
-                       void* stream);
+                       void* scratch, void* stream);
 
-/* backward (nn.py:167-170): dW = [agg | h_dst]^T @ dz (deterministic split-K,
- * scratch: mq_linear_bwd_w_scratch_bytes) and, if dt != NULL, dt = dz @ W^T. */
-int64_t mq_linear_bwd_w_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out);
+/* backward (nn.py:167-170): dW = [agg | h_dst]^T @ dz and, if dt != NULL,
+ * dt = dz @ W^T (same kernel family and scratch as the forward). */
 int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
                        const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
                        int32_t d_out, const float* dz, int32_t lddz, float* dW, float* dt,
@@ -184,10 +187,11 @@ int mq_batch_setup(const int32_t* perm, int64_t n_perm, int32_t batch_size, int3
                    int32_t rank, int32_t* cursor_dev, int32_t* targets, int32_t* n_targets_dev,
                    uint32_t* key_dev, void* stream);
 
-/* End-of-step bookkeeping for graph replay: loss_ring[(cursor[0]-1) mod
- * ring_len] = loss_acc[0]; loss_acc[0] = 0 (EpochStats.losses,
- * runtime.py:72-92, read back once per epoch instead of per batch). */
-int mq_step_commit(double* loss_acc, const int32_t* cursor_dev, double* loss_ring,
+/* End-of-step bookkeeping for graph replay: with k = key_dev[2] / world (the
+ * window of the batch just trained), loss_ring[k mod ring_len] = loss_acc[0];
+ * loss_acc[0] = 0 (EpochStats.losses, runtime.py:72-92, read back once per
+ * epoch instead of per batch). */
+int mq_step_commit(double* loss_acc, const uint32_t* key_dev, int32_t world, double* loss_ring,
                    int32_t ring_len, void* stream);
 
 /* labels[i] = all_labels[ids[i]] (build_minibatch target_labels, samplers.py:532) */

@@ -34,14 +34,14 @@ SIGNATURES = {
     "mq_residency_slots": (C.c_int, [P, I64, P, P, P, P]),
     "mq_sample_hop": (C.c_int, [P, P, P, P, P, P, I32, I32, U64, U64, U32, U32, P, P, P, P]),
     "mq_batch_setup": (C.c_int, [P, I64, I32, I32, I32, P, P, P, P, P]),
-    "mq_step_commit": (C.c_int, [P, P, P, I32, P]),
+    "mq_step_commit": (C.c_int, [P, P, I32, P, I32, P]),
     "mq_relabel_scratch_bytes": (I64, [I32, I32]),
     "mq_relabel": (C.c_int, [P, P, I32, P, P, I32, P, P, P, P, P, P, P, P, P, P]),
     "mq_gather": (C.c_int, [P, I32, P, P, I32, P, P, I32, I32, P, I32, P, P]),
     "mq_spmm_fwd": (C.c_int, [P, P, P, P, I32, P, I32, I32, P, I32, P]),
     "mq_spmm_bwd": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, I32, P, I32, P, I32, P]),
-    "mq_sage_linear_fwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, I32, P]),
-    "mq_linear_bwd_w_scratch_bytes": (I64, [I32, I32, I32]),
+    "mq_sage_linear_fwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, I32, P, P]),
+    "mq_linear_scratch_bytes": (I64, [I32, I32, I32]),
     "mq_sage_linear_bwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, P, I32,
                                      P, P]),
     "mq_softmax_ce": (C.c_int, [P, I32, P, P, I32, I32, P, I32, P, P, P]),

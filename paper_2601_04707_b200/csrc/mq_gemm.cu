@@ -1,15 +1,22 @@
 // Dense SAGE layer transforms: z = [agg | h_dst] W, dW = [agg | h_dst]^T dz,
 // dt = dz W^T (mqpipe/nn.py:126-131, 167-170).
 //
-// fp32 SIMT tiles with FMA accumulation.  The reference trains in fp32 and
-// north_star pins these contractions at rel 1e-5, which TF32 tensor-core math
-// (10-bit mantissa) cannot meet; the concat is never materialised — the A
-// loader reads the agg and self halves from their own buffers.
+// fp32 FMA on the CUDA cores: the reference trains in fp32 and north_star pins
+// these contractions at rel 1e-5, which single-pass TF32 tensor-core math
+// (10-bit mantissa) cannot meet.  The shapes are skinny (N = 41..128) with a
+// row count M that only the device knows (the sampled frontier), so the
+// kernel is a persistent split-K GEMM whose split factor is chosen ON THE
+// DEVICE from M to fill all 148 SMs, followed by a deterministic fixed-order
+// split reduction fused with the epilogue (ReLU / store / dW row scatter).
+// The concat is never materialised: the K (or M) index space is padded to
+// [0, P) -> agg, [P, 2P) -> h with P the 16-byte-aligned row pitch, so every
+// operand load is a float4.
 #include "mq_common.cuh"
 
 namespace mq {
 
-constexpr int BM = 64, BN = 64, BK = 16, kGemmThreads = 256;
+constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 256;
+constexpr int kMaxSplits = 16;
 
 struct Dims {
   const int32_t* m_dev;  // if set, M = *m_dev (else m)
@@ -21,128 +28,171 @@ struct Dims {
   __device__ int K() const { return k_dev ? *k_dev : k; }
 };
 
-// A(i, k) of z = [agg | h] W: k contiguous
+__device__ __forceinline__ float4 ld4_guard(const float* p, int n_valid) {
+  // n_valid in [0, 4]: elements beyond are zero
+  if (n_valid >= 4 && ((uintptr_t)p & 15) == 0) return __ldg(reinterpret_cast<const float4*>(p));
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < 4 && i < n_valid; ++i) v[i] = __ldg(p + i);
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// ---- operand loaders: load4(i, k) returns A(i, k..k+3) / B(k.., j) as float4
+// A(i, k) of z = [agg | h] W over the padded k space (k contiguous)
 struct ALoadConcat {
   static constexpr bool kKContig = true;
   const float* agg;
-  int lda;
   const float* h;
-  int ldh;
-  int d_in;
-  __device__ float operator()(int i, int k) const {
-    return k < d_in ? __ldg(&agg[(int64_t)i * lda + k]) : __ldg(&h[(int64_t)i * ldh + (k - d_in)]);
+  int ld;  // common pitch P of agg and h (multiple of 4)
+  __device__ float4 load4(int i, int k, int K) const {  // K = 2P
+    if (k >= K) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* p = k < ld ? agg + (int64_t)i * ld + k : h + (int64_t)i * ld + (k - ld);
+    return __ldg(reinterpret_cast<const float4*>(p));
   }
 };
-// A(o, r) = [agg | h](r, o) for dW (output row o over 2*d_in, reduction r over rows): o contiguous
+// A(o, r) = [agg | h](r, o) for dW (o over the padded 2P, r over rows): o contiguous
 struct ALoadConcatT {
   static constexpr bool kKContig = false;
   const float* agg;
-  int lda;
   const float* h;
-  int ldh;
-  int d_in;
-  __device__ float operator()(int o, int r) const {
-    return o < d_in ? __ldg(&agg[(int64_t)r * lda + o]) : __ldg(&h[(int64_t)r * ldh + (o - d_in)]);
+  int ld;
+  __device__ float4 load4m(int o, int r) const {  // o..o+3 at row r
+    const float* p = o < ld ? agg + (int64_t)r * ld + o : h + (int64_t)r * ld + (o - ld);
+    return __ldg(reinterpret_cast<const float4*>(p));
   }
 };
-// plain row-major matrix, element (i, k) at p[i*ld + k]
+// row-major A (i, k) = p[i*ld + k], k contiguous, K columns valid
 struct ALoadRow {
   static constexpr bool kKContig = true;
   const float* p;
   int ld;
-  __device__ float operator()(int i, int k) const { return __ldg(&p[(int64_t)i * ld + k]); }
+  __device__ float4 load4(int i, int k, int K) const {
+    return ld4_guard(p + (int64_t)i * ld + k, K - k);
+  }
 };
-// B(k, j) = p[k*ld + j]: j contiguous
+// B(k, j) of z = [agg | h] W: padded k -> W row, j contiguous, N columns
+struct BLoadW {
+  const float* W;
+  int ld;    // pitch P of the concat halves
+  int d_in;  // real rows per half
+  int N;
+  __device__ float4 load4(int k, int j) const {
+    int row;
+    if (k < ld) {
+      if (k >= d_in) return make_float4(0.f, 0.f, 0.f, 0.f);
+      row = k;
+    } else {
+      if (k - ld >= d_in) return make_float4(0.f, 0.f, 0.f, 0.f);
+      row = d_in + (k - ld);
+    }
+    return ld4_guard(W + (int64_t)row * N + j, N - j);
+  }
+};
+// B(r, j) = dz[r*ld + j] for dW: j contiguous
 struct BLoadRow {
-  static constexpr bool kKContig = false;
   const float* p;
   int ld;
-  __device__ float operator()(int k, int j) const { return __ldg(&p[(int64_t)k * ld + j]); }
+  int N;
+  __device__ float4 load4(int k, int j) const { return ld4_guard(p + (int64_t)k * ld + j, N - j); }
 };
-// B(k, j) = p[j*ld + k] (transposed weight): k contiguous
-struct BLoadT {
-  static constexpr bool kKContig = true;
-  const float* p;
-  int ld;
-  __device__ float operator()(int k, int j) const { return __ldg(&p[(int64_t)j * ld + k]); }
-};
-
-struct EpiLinearFwd {
-  float* z;
-  int ldz;
-  float* relu;
-  int ldr;
-  __device__ void operator()(int i, int j, float v, int) const {
-    if (z) z[(int64_t)i * ldz + j] = v;
-    if (relu) relu[(int64_t)i * ldr + j] = v > 0.f ? v : 0.f;
-  }
-};
-struct EpiStore {
-  float* c;
-  int ldc;
-  __device__ void operator()(int i, int j, float v, int) const { c[(int64_t)i * ldc + j] = v; }
-};
-struct EpiPartial {
-  float* part;  // [splits][M][N]
-  int M, N;
-  __device__ void operator()(int i, int j, float v, int z) const {
-    part[((int64_t)z * M + i) * N + j] = v;
+// B(k, j) = W[j*ld + k] (dt = dz W^T: k over d_out, j over 2*d_in)
+struct BLoadWT {
+  const float* W;
+  int ld;  // d_out
+  int K;   // d_out
+  int N;   // 2*d_in
+  __device__ float4 load4(int k, int j) const {
+    float v[4];
+    for (int t = 0; t < 4; ++t)
+      v[t] = (j + t < N && k < K) ? __ldg(W + (int64_t)(j + t) * ld + k) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
   }
 };
 
-// C[M, N] = sum_k A(i,k) B(k,j) over the k-range of split blockIdx.z.
-template <class AL, class BL, class Epi>
-__global__ void __launch_bounds__(kGemmThreads) sgemm_kernel(AL A, BL B, Epi epi, Dims dims,
-                                                             int k_chunk) {
-  __shared__ __align__(16) float As[BK][BM + 4];
-  __shared__ __align__(16) float Bs[BK][BN + 4];
+struct Split {
+  int tiles_m, tiles_n, S, k_chunk;
+};
+
+__device__ __forceinline__ Split choose_split(int M, int N, int K, int grid, int s_cap) {
+  Split s;
+  s.tiles_m = (M + GBM - 1) / GBM;
+  s.tiles_n = (N + GBN - 1) / GBN;
+  const int tiles = max(1, s.tiles_m * s.tiles_n);
+  const int kb = max(1, (K + GBK - 1) / GBK);
+  int S = (grid + tiles - 1) / tiles;
+  S = max(1, min(S, min(s_cap, kb)));
+  const int per = (kb + S - 1) / S;  // k blocks per split
+  s.k_chunk = per * GBK;
+  s.S = (K + s.k_chunk - 1) / s.k_chunk;
+  if (s.S < 1) s.S = 1;
+  return s;
+}
+
+// Persistent split-K tile loop; partial tile sums go to part[s][M_ld][N].
+template <class AL, class BL>
+__global__ void __launch_bounds__(GTHREADS, 2)
+    sgemm_splitk_kernel(AL A, BL B, Dims dims, int s_cap, float* __restrict__ part, int m_ld) {
+  __shared__ __align__(16) float As[2][GBK][GBM + 4];
+  __shared__ __align__(16) float Bs[2][GBK][GBN + 4];
   const int M = dims.M(), N = dims.n, K = dims.K();
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int kb = blockIdx.z * k_chunk;
-  const int ke = min(K, kb + k_chunk);
-  const bool live = m0 < M;
+  const Split sp = choose_split(M, N, K, gridDim.x, s_cap);
+  const int items = sp.tiles_m * sp.tiles_n * sp.S;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  if (live) {
-    for (int k0 = kb; k0 < ke; k0 += BK) {
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int s = w % sp.S;
+    const int t = w / sp.S;
+    const int m0 = (t / sp.tiles_n) * GBM, n0 = (t % sp.tiles_n) * GBN;
+    const int kb = s * sp.k_chunk, ke = min(K, kb + sp.k_chunk);
+    float acc[4][4];
 #pragma unroll
-      for (int q = 0; q < (BM * BK) / kGemmThreads; ++q) {
-        const int idx = tid + q * kGemmThreads;
-        int mi, ki;
-        if (AL::kKContig) {
-          mi = idx / BK;
-          ki = idx % BK;
-        } else {
-          mi = idx % BM;
-          ki = idx / BM;
-        }
-        const int gm = m0 + mi, gk = k0 + ki;
-        As[ki][mi] = (gm < M && gk < ke) ? A(gm, gk) : 0.f;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+    // per-thread load slots: one float4 of A and one of B per BK step
+    float4 ra, rb;
+    auto load_tiles = [&](int k0) {
+      if constexpr (AL::kKContig) {
+        const int mi = tid >> 2, kq = (tid & 3) * 4;
+        const int gm = m0 + mi, gk = k0 + kq;
+        ra = (gm < M && gk < ke) ? A.load4(gm, gk, ke) : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        const int ki = tid >> 4, mq4 = (tid & 15) * 4;
+        const int gk = k0 + ki, gm = m0 + mq4;
+        ra = (gk < ke && gm < M) ? A.load4m(gm, gk) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-#pragma unroll
-      for (int q = 0; q < (BN * BK) / kGemmThreads; ++q) {
-        const int idx = tid + q * kGemmThreads;
-        int ni, ki;
-        if (BL::kKContig) {
-          ni = idx / BK;
-          ki = idx % BK;
-        } else {
-          ni = idx % BN;
-          ki = idx / BN;
-        }
-        const int gn = n0 + ni, gk = k0 + ki;
-        Bs[ki][ni] = (gn < N && gk < ke) ? B(gk, gn) : 0.f;
+      {
+        const int ki = tid >> 4, nq = (tid & 15) * 4;
+        const int gk = k0 + ki, gn = n0 + nq;
+        rb = (gk < ke && gn < N) ? B.load4(gk, gn) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      __syncthreads();
+    };
+    auto store_tiles = [&](int buf) {
+      if constexpr (AL::kKContig) {
+        const int mi = tid >> 2, kq = (tid & 3) * 4;
+        As[buf][kq + 0][mi] = ra.x;
+        As[buf][kq + 1][mi] = ra.y;
+        As[buf][kq + 2][mi] = ra.z;
+        As[buf][kq + 3][mi] = ra.w;
+      } else {
+        const int ki = tid >> 4, mq4 = (tid & 15) * 4;
+        *reinterpret_cast<float4*>(&As[buf][ki][mq4]) = ra;
+      }
+      const int ki = tid >> 4, nq = (tid & 15) * 4;
+      *reinterpret_cast<float4*>(&Bs[buf][ki][nq]) = rb;
+    };
+
+    int buf = 0;
+    load_tiles(kb);
+    store_tiles(0);
+    __syncthreads();
+    for (int k0 = kb; k0 < ke; k0 += GBK) {
+      const bool more = k0 + GBK < ke;
+      if (more) load_tiles(k0 + GBK);
 #pragma unroll
-      for (int k = 0; k < BK; ++k) {
-        const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      for (int k = 0; k < GBK; ++k) {
+        const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
         const float av[4] = {a.x, a.y, a.z, a.w};
         const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -150,39 +200,102 @@ __global__ void __launch_bounds__(kGemmThreads) sgemm_kernel(AL A, BL B, Epi epi
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
       }
+      if (more) store_tiles(buf ^ 1);
       __syncthreads();
+      buf ^= 1;
     }
-  }
-  if (!live) return;
+    float* out = part + (int64_t)s * m_ld * N;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gm = m0 + ty * 4 + i;
-    if (gm >= M) continue;
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + ty * 4 + i;
+      if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gn = n0 + tx * 4 + j;
-      if (gn < N) epi(gm, gn, acc[i][j], blockIdx.z);
+      for (int j = 0; j < 4; ++j) {
+        const int gn = n0 + tx * 4 + j;
+        if (gn < N) out[(int64_t)gm * N + gn] = acc[i][j];
+      }
     }
+    __syncthreads();
   }
 }
 
-// dW[i] = sum over splits, in split order (deterministic)
-__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t mn,
-                                     float* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mn;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * mn + i];
-    out[i] = s;
+// ---- split reduction + epilogues (fixed split order: deterministic)
+struct EpiLinearFwd {
+  float* z;
+  int ldz;
+  float* relu;
+  int ldr;
+  __device__ void operator()(int i, int j, float v) const {
+    if (z) z[(int64_t)i * ldz + j] = v;
+    if (relu) relu[(int64_t)i * ldr + j] = v > 0.f ? v : 0.f;
+  }
+};
+struct EpiStore {
+  float* c;
+  int ldc;
+  __device__ void operator()(int i, int j, float v) const { c[(int64_t)i * ldc + j] = v; }
+};
+// padded concat row o -> dW row (skip the pad rows)
+struct EpiDW {
+  float* dW;
+  int ld;  // pitch P
+  int d_in;
+  int N;
+  __device__ void operator()(int o, int j, float v) const {
+    int row;
+    if (o < ld) {
+      if (o >= d_in) return;
+      row = o;
+    } else {
+      if (o - ld >= d_in) return;
+      row = d_in + (o - ld);
+    }
+    dW[(int64_t)row * N + j] = v;
+  }
+};
+
+template <class Epi>
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, Dims dims, int grid_gemm,
+                                     int s_cap, int m_ld, Epi epi) {
+  const int M = dims.M(), N = dims.n, K = dims.K();
+  const Split sp = choose_split(M, N, K, grid_gemm, s_cap);
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    float v = 0.f;
+    for (int s = 0; s < sp.S; ++s) v += part[((int64_t)s * m_ld + i) * N + j];
+    epi(i, j, v);
   }
 }
 
-constexpr int kBwdWSplitRows = 256;  // reduction rows per split of the dW GEMM
+constexpr int kGemmGrid = kNumSMs * 2;
 
-inline int bwd_w_splits(int m_max) {
-  int s = ceil_div(m_max < 1 ? 1 : m_max, kBwdWSplitRows);
-  return s < 1 ? 1 : s;
+template <class AL, class BL, class Epi>
+int run_gemm(const AL& A, const BL& B, const Epi& epi, Dims dims, int m_max, int k_max, int s_cap,
+             float* part, cudaStream_t s, int kid_gemm, int kid_red) {
+  const int tiles_max = ceil_div(m_max < 1 ? 1 : m_max, GBM) * ceil_div(dims.n, GBN);
+  (void)k_max;
+  int grid = kGemmGrid;
+  if (grid > tiles_max * s_cap) grid = tiles_max * s_cap;
+  if (grid < 1) grid = 1;
+  {
+    ProfScope ps(kid_gemm, s);
+    sgemm_splitk_kernel<AL, BL><<<grid, GTHREADS, 0, s>>>(A, B, dims, s_cap, part, m_max);
+  }
+  MQ_LAUNCH_CHECK("sgemm_splitk");
+  int64_t mn = (int64_t)(m_max < 1 ? 1 : m_max) * dims.n;
+  int rb = ceil_div(mn, 256);
+  if (rb > kNumSMs * 4) rb = kNumSMs * 4;
+  {
+    ProfScope ps(kid_red, s);
+    splitk_reduce_kernel<Epi><<<rb, 256, 0, s>>>(part, dims, grid, s_cap, m_max, epi);
+  }
+  MQ_LAUNCH_CHECK("splitk_reduce");
+  return MQ_OK;
 }
+
+inline int pitch_of(int d) { return (d + 3) / 4 * 4; }
 
 }  // namespace mq
 
@@ -190,29 +303,34 @@ using namespace mq;
 
 extern "C" {
 
+int64_t mq_linear_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out) {
+  const int64_t m = m_max < 1 ? 1 : m_max;
+  const int64_t P2 = 2 * pitch_of(d_in);
+  int64_t fwd = kMaxSplits * m * d_out;
+  int64_t bww = kMaxSplits * P2 * d_out;
+  int64_t bwx = (int64_t)((d_out + GBK - 1) / GBK) * m * 2 * d_in;
+  int64_t mx = fwd > bww ? fwd : bww;
+  mx = mx > bwx ? mx : bwx;
+  return mx * (int64_t)sizeof(float);
+}
+
 int mq_sage_linear_fwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
                        const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
                        int32_t d_out, float* z, int32_t ldz, float* relu_out, int32_t ldr,
-                       void* stream) {
-  MQ_CHECK_ARG(agg && h && m_dev && W && (z || relu_out), "mq_sage_linear_fwd: null pointer");
+                       void* scratch, void* stream) {
+  MQ_CHECK_ARG(agg && h && m_dev && W && (z || relu_out) && scratch,
+               "mq_sage_linear_fwd: null pointer");
   MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && (!z || ldz >= d_out) && (!relu_out || ldr >= d_out),
                "mq_sage_linear_fwd: bad dims");
+  MQ_CHECK_ARG(ldagg == ldh && ldagg % 4 == 0 && ldagg >= d_in &&
+                   ((uintptr_t)agg | (uintptr_t)h) % 16 == 0,
+               "mq_sage_linear_fwd: agg and h need one 16-byte-aligned pitch >= d_in");
   if (m_max <= 0) return MQ_OK;
   cudaStream_t s = as_stream(stream);
-  Dims dims{m_dev, 0, nullptr, 2 * d_in, d_out};
-  dim3 grid(ceil_div(m_max, BM), ceil_div(d_out, BN), 1);
-  {
-    ProfScope ps(K_LINEAR_FWD, s);
-    sgemm_kernel<<<grid, kGemmThreads, 0, s>>>(ALoadConcat{agg, ldagg, h, ldh, d_in},
-                                               BLoadRow{W, d_out},
-                                               EpiLinearFwd{z, ldz, relu_out, ldr}, dims, 2 * d_in);
-  }
-  MQ_LAUNCH_CHECK("linear_fwd");
-  return MQ_OK;
-}
-
-int64_t mq_linear_bwd_w_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out) {
-  return (int64_t)bwd_w_splits(m_max) * 2 * d_in * d_out * sizeof(float);
+  Dims dims{m_dev, 0, nullptr, 2 * ldagg, d_out};
+  return run_gemm(ALoadConcat{agg, h, ldagg}, BLoadW{W, ldagg, d_in, d_out},
+                  EpiLinearFwd{z, ldz, relu_out, ldr}, dims, m_max, 2 * ldagg, kMaxSplits,
+                  reinterpret_cast<float*>(scratch), s, K_LINEAR_FWD, K_LINEAR_FWD_REDUCE);
 }
 
 int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
@@ -222,36 +340,27 @@ int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t 
   MQ_CHECK_ARG(agg && h && m_dev && W && dz && dW && scratch, "mq_sage_linear_bwd: null pointer");
   MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && lddz >= d_out && (!dt || lddt >= 2 * d_in),
                "mq_sage_linear_bwd: bad dims");
+  MQ_CHECK_ARG(ldagg == ldh && ldagg % 4 == 0 && ldagg >= d_in &&
+                   ((uintptr_t)agg | (uintptr_t)h) % 16 == 0,
+               "mq_sage_linear_bwd: agg and h need one 16-byte-aligned pitch >= d_in");
   cudaStream_t s = as_stream(stream);
-  const int mo = 2 * d_in;
-  const int splits = bwd_w_splits(m_max);
   float* part = reinterpret_cast<float*>(scratch);
+  const int P = ldagg;
   {
-    // dW partials: output (2*d_in x d_out), reduction over the m rows in splits
-    Dims dims{nullptr, mo, m_dev, 0, d_out};
-    dim3 grid(ceil_div(mo, BM), ceil_div(d_out, BN), splits);
-    ProfScope ps(K_LINEAR_BWD_W, s);
-    sgemm_kernel<<<grid, kGemmThreads, 0, s>>>(ALoadConcatT{agg, ldagg, h, ldh, d_in},
-                                               BLoadRow{dz, lddz}, EpiPartial{part, mo, d_out},
-                                               dims, kBwdWSplitRows);
+    // dW over the padded concat rows: M = 2P (static), reduction over the m rows
+    Dims dims{nullptr, 2 * P, m_dev, 0, d_out};
+    int rc = run_gemm(ALoadConcatT{agg, h, P}, BLoadRow{dz, lddz, d_out},
+                      EpiDW{dW, P, d_in, d_out}, dims, 2 * P, m_max, kMaxSplits, part, s,
+                      K_LINEAR_BWD_W, K_LINEAR_BWD_W_REDUCE);
+    if (rc) return rc;
   }
-  MQ_LAUNCH_CHECK("linear_bwd_w");
-  {
-    int64_t mn = (int64_t)mo * d_out;
-    int blocks = ceil_div(mn, 256);
-    if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
-    ProfScope ps(K_LINEAR_BWD_W_REDUCE, s);
-    reduce_splits_kernel<<<blocks, 256, 0, s>>>(part, splits, mn, dW);
-  }
-  MQ_LAUNCH_CHECK("linear_bwd_w_reduce");
   if (dt != nullptr && m_max > 0) {
-    Dims dims{m_dev, 0, nullptr, d_out, mo};
-    dim3 grid(ceil_div(m_max, BM), ceil_div(mo, BN), 1);
-    ProfScope ps(K_LINEAR_BWD_X, s);
-    sgemm_kernel<<<grid, kGemmThreads, 0, s>>>(ALoadRow{dz, lddz}, BLoadT{W, d_out},
-                                               EpiStore{dt, lddt}, dims, d_out);
+    Dims dims{m_dev, 0, nullptr, d_out, 2 * d_in};
+    int rc = run_gemm(ALoadRow{dz, lddz}, BLoadWT{W, d_out, d_out, 2 * d_in}, EpiStore{dt, lddt},
+                      dims, m_max, d_out, (d_out + GBK - 1) / GBK, part, s, K_LINEAR_BWD_X,
+                      K_LINEAR_BWD_X_REDUCE);
+    if (rc) return rc;
   }
-  MQ_LAUNCH_CHECK("linear_bwd_x");
   return MQ_OK;
 }
 

@@ -24,6 +24,8 @@
   X(K_LINEAR_BWD_W, "linear_bwd_w")               \
   X(K_LINEAR_BWD_W_REDUCE, "linear_bwd_w_reduce") \
   X(K_LINEAR_BWD_X, "linear_bwd_x")               \
+  X(K_LINEAR_FWD_REDUCE, "linear_fwd_reduce")     \
+  X(K_LINEAR_BWD_X_REDUCE, "linear_bwd_x_reduce") \
   X(K_SOFTMAX_CE, "softmax_ce")                   \
   X(K_LABELS, "gather_labels")                    \
   X(K_ADAM, "adam")                               \

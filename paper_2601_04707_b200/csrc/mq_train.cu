@@ -61,10 +61,9 @@ __global__ void softmax_ce_kernel(const float* __restrict__ logits, int ld,
 
 __global__ void step_bump_kernel(int32_t* step) { *step += 1; }
 
-__global__ void step_commit_kernel(double* loss_acc, const int32_t* cursor, double* ring,
+__global__ void step_commit_kernel(double* loss_acc, const uint32_t* key, int world, double* ring,
                                    int ring_len) {
-  int k = cursor[0] - 1;
-  k = ((k % ring_len) + ring_len) % ring_len;
+  int k = (int)((key[2] / (uint32_t)world) % (uint32_t)ring_len);
   ring[k] = loss_acc[0];
   loss_acc[0] = 0.0;
 }
@@ -219,13 +218,14 @@ int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scal
   return MQ_OK;
 }
 
-int mq_step_commit(double* loss_acc, const int32_t* cursor_dev, double* loss_ring,
+int mq_step_commit(double* loss_acc, const uint32_t* key_dev, int32_t world, double* loss_ring,
                    int32_t ring_len, void* stream) {
-  MQ_CHECK_ARG(loss_acc && cursor_dev && loss_ring && ring_len > 0, "mq_step_commit: bad args");
+  MQ_CHECK_ARG(loss_acc && key_dev && loss_ring && ring_len > 0 && world >= 1,
+               "mq_step_commit: bad args");
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_STEP_BUMP, s);
-    step_commit_kernel<<<1, 1, 0, s>>>(loss_acc, cursor_dev, loss_ring, ring_len);
+    step_commit_kernel<<<1, 1, 0, s>>>(loss_acc, key_dev, world, loss_ring, ring_len);
   }
   MQ_LAUNCH_CHECK("step_commit");
   return MQ_OK;

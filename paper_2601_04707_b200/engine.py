@@ -84,6 +84,10 @@ class SampleWorkspace:
         # sampling concurrently on different streams never share them
         self.dpos = torch.full((g.num_nodes,), -1, dtype=torch.int32, device=dev)
         self.first = torch.full((g.num_nodes,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        # this slot's transfer-stage outputs: gathered input rows and target labels
+        self.x0 = torch.zeros((max(self.bounds[-1].n_src_max, 1), g.pitch), dtype=torch.float32,
+                              device=dev)
+        self.labels = torch.zeros(max(self.batch_size, 1), dtype=torch.int32, device=dev)
 
     # device scalars for hop h
     def n_dst_dev(self, h: int) -> torch.Tensor:
@@ -183,7 +187,12 @@ def _t(a, device):
 
 
 class TrainWorkspace:
-    """Activation / gradient buffers of one SAGE step over a SampleWorkspace."""
+    """Activation / gradient buffers of one SAGE step.
+
+    The per-batch inputs (hop CSR blocks, gathered features ``x0``, labels)
+    live in a SampleWorkspace "slot"; every launch method takes the slot it
+    consumes so two slots can be double-buffered (prep of batch k+1 while
+    batch k trains)."""
 
     def __init__(self, sw: SampleWorkspace, dims, num_classes: int):
         g = sw.graph
@@ -196,7 +205,6 @@ class TrainWorkspace:
         self.L = L
         self.C = num_classes
         f32 = dict(dtype=torch.float32, device=dev)
-        self.x0 = torch.zeros((max(sw.bounds[-1].n_src_max, 1), g.pitch), **f32)
         self.ld_in = [g.pitch] + [round_up(d, 4) for d in self.dims[1:L]]
         self.agg, self.act, self.dt, self.dh = [], [None], [], []
         for l in range(L):
@@ -213,36 +221,43 @@ class TrainWorkspace:
         B = sw.batch_size
         self.logits = torch.zeros((max(B, 1), num_classes), **f32)
         self.dlogits = torch.zeros((max(B, 1), num_classes), **f32)
-        self.labels = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
-        scr = max(int(lib().mq_linear_bwd_w_scratch_bytes(sw.bounds[L - 1 - l].n_dst_max,
-                                                          self.dims[l], self.dims[l + 1]))
+        scr = max(int(lib().mq_linear_scratch_bytes(sw.bounds[L - 1 - l].n_dst_max,
+                                                    self.dims[l], self.dims[l + 1]))
                   for l in range(L))
         self.scratch = torch.zeros(scr // 4 + 1, **f32)
 
-    def h_in(self, l):
-        return self.x0 if l == 0 else self.act[l]
+    @property
+    def x0(self):
+        return self.sw.x0
 
-    def launch_gather(self, cache, stream):
-        g, sw = self.sw.graph, self.sw
+    def h_in(self, l, sw=None):
+        return (sw or self.sw).x0 if l == 0 else self.act[l]
+
+    @staticmethod
+    def launch_gather(sw: SampleWorkspace, cache, stream):
+        """transfer_stage (runtime.py:127-143) + target labels (samplers.py:532)."""
+        g = sw.graph
         b = sw.bounds[-1]
         if cache is None:
             lib().mq_gather(None, 0, None, ptr(g.features), g.pitch, ptr(sw.input_ids),
-                            ptr(sw.n_input_dev), b.n_src_max, g.feature_dim, ptr(self.x0), g.pitch,
+                            ptr(sw.n_input_dev), b.n_src_max, g.feature_dim, ptr(sw.x0), g.pitch,
                             None, stream)
         else:
             lib().mq_gather(ptr(cache.table), g.pitch, ptr(cache.slot_of), ptr(g.features), g.pitch,
                             ptr(sw.input_ids), ptr(sw.n_input_dev), b.n_src_max, g.feature_dim,
-                            ptr(self.x0), g.pitch, ptr(cache.hit_miss), stream)
+                            ptr(sw.x0), g.pitch, ptr(cache.hit_miss), stream)
+        lib().mq_gather_labels(ptr(g.labels), ptr(sw.targets), ptr(sw.n_targets), sw.batch_size,
+                               ptr(sw.labels), stream)
 
-    def launch_forward(self, model: DeviceModel, stream):
-        sw = self.sw
+    def launch_forward(self, model: DeviceModel, stream, sw=None):
+        sw = sw or self.sw
         L = self.L
         for l in range(L):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
             nd = sw.n_dst_dev(h)
-            hin = self.h_in(l)
+            hin = self.h_in(l, sw)
             lib().mq_spmm_fwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals), ptr(nd), b.n_dst_max,
                               ptr(hin), self.ld_in[l], self.dims[l], ptr(self.agg[l]),
                               self.ld_in[l], stream)
@@ -251,30 +266,28 @@ class TrainWorkspace:
                 lib().mq_sage_linear_fwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],
                                          ptr(nd), b.n_dst_max, self.dims[l], ptr(W),
                                          self.dims[l + 1], None, 0, ptr(self.act[l + 1]),
-                                         self.ld_in[l + 1], stream)
+                                         self.ld_in[l + 1], ptr(self.scratch), stream)
             else:
                 lib().mq_sage_linear_fwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],
                                          ptr(nd), b.n_dst_max, self.dims[l], ptr(W),
                                          self.dims[l + 1], ptr(self.logits), self.C, None, 0,
-                                         stream)
+                                         ptr(self.scratch), stream)
 
-    def launch_loss(self, model: DeviceModel, stream):
-        g, sw = self.sw.graph, self.sw
-        lib().mq_gather_labels(ptr(g.labels), ptr(sw.targets), ptr(sw.n_targets), sw.batch_size,
-                               ptr(self.labels), stream)
-        lib().mq_softmax_ce(ptr(self.logits), self.C, ptr(self.labels), ptr(sw.n_targets),
+    def launch_loss(self, model: DeviceModel, stream, sw=None):
+        sw = sw or self.sw
+        lib().mq_softmax_ce(ptr(self.logits), self.C, ptr(sw.labels), ptr(sw.n_targets),
                             sw.batch_size, self.C, ptr(self.dlogits), self.C, ptr(self.loss),
                             ptr(model.nonfinite), stream)
 
-    def launch_backward(self, model: DeviceModel, stream):
-        sw = self.sw
+    def launch_backward(self, model: DeviceModel, stream, sw=None):
+        sw = sw or self.sw
         L = self.L
         dz, lddz = self.dlogits, self.C
         for l in range(L - 1, -1, -1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
             nd = sw.n_dst_dev(h)
-            hin = self.h_in(l)
+            hin = self.h_in(l, sw)
             d_in, d_out = self.dims[l], self.dims[l + 1]
             dt = self.dt[l]
             lib().mq_sage_linear_bwd(ptr(self.agg[l]), self.ld_in[l], ptr(hin), self.ld_in[l],

@@ -151,8 +151,10 @@ def sage_forward(batch, state: ModelState, return_cache: bool = False):
         d_out = int(W.shape[1])
         z = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev)
         r = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev) if l < L - 1 else None
+        scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+                          dtype=torch.float32, device=dev)
         lib().mq_sage_linear_fwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,
-                                 ptr(z), d_out, ptr(r), d_out, stream)
+                                 ptr(z), d_out, ptr(r), d_out, ptr(scr), stream)
         cache["inputs"].append((hp, agg, blk, nd_dev, d_in))
         cache["pre"].append(z[:nd])
         h = r[:nd] if l < L - 1 else z[:nd]
@@ -195,7 +197,7 @@ def backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
         W = state.weights[l]
         d_out = int(W.shape[1])
         dW = torch.empty_like(W)
-        scr = torch.empty(int(lib().mq_linear_bwd_w_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+        scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
                           dtype=torch.float32, device=dev)
         dt = torch.empty((max(nd, 1), 2 * d_in), dtype=torch.float32, device=dev) if l > 0 else None
         lib().mq_sage_linear_bwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,

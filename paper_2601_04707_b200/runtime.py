@@ -54,6 +54,7 @@ class PipelineConfig:
     queue_timeout: float = 60.0
     capture_weights: bool = False
     use_graph: bool = True
+    pipeline: bool = True   # prep of batch k+1 overlaps training of batch k
 
     def validate(self) -> None:
         if self.num_devices < 1:
@@ -150,13 +151,14 @@ def _distributed():
 
 def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
     key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
-           config.seed, world, rank, multi, num_train, config.use_graph)
+           config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline)
     r = getattr(replica, "_runner", None)
     if r is None or r[0] != key:
         runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
                             batch_size=config.batch_size, num_train=num_train, cache=cache,
                             optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
-                            multi=multi, use_graph=config.use_graph)
+                            multi=multi, use_graph=config.use_graph,
+                            pipeline=config.pipeline)
         replica._runner = (key, runner)
         return runner, True
     return r[1], False
@@ -191,15 +193,16 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
     perm = epoch_permutation(g.train_mask, config.seed, epoch)
     multi = world > 1
     runners = []
+    # counters before the pipeline prologue, which already gathers batch 0
+    torch.cuda.synchronize(g.device)
+    hm0 = cache.hit_miss.clone() if cache is not None else None
     for d, rep in zip(local_ranks, replicas):
         r, fresh = _runner_for(rep, g, cache, config, world, d, multi, perm.size)
         r.begin_epoch(epoch, perm)
         if config.use_graph:
             r.capture()
         runners.append(r)
-    hm0 = cache.hit_miss.clone() if cache is not None else None
     weight_traces = {d: [] for d in local_ranks}
-    starts, ends = [], []
 
     def on_window(k):
         if config.capture_weights:

@@ -1,15 +1,21 @@
-"""One replica's per-iteration hot path as captured CUDA graphs.
+"""One replica's per-iteration hot path as captured, pipelined CUDA graphs.
 
 A step = batch setup (device-side plan), L hops of sample + relabel, feature
-gather, SAGE forward, summed softmax-CE, backward and the optimizer — the
-``_run_epoch_serial`` per-batch body of the reference (``runtime.py:294-323``)
-with the RaCoM window apply (``runtime.py:167-195``) folded in.  Everything is
-enqueued through the C-ABI on one stream; after an eager warm-up the sequence
-is captured once and replayed per batch, so a step costs one graph launch.
+gather ("prep": the reference's sample + transfer stages, samplers.py:502-540
+and runtime.py:127-143) followed by SAGE forward, summed softmax-CE,
+backward and the optimizer ("train": nn.py:116-206 and the RaCoM window
+apply, runtime.py:167-195).
 
-Multi-replica (RaCoM) steps split the graph in two around the gradient
-exchange: compute graph -> f64 all-reduce of [grads | contributor count]
-(NCCL in production, gloo/in-process in tests) -> update graph.
+The multi-queue pipeline of MQ-GNN (sample -> transfer -> compute -> update,
+runtime.py:380-612) is expressed with two CUDA streams inside ONE graph per
+step: the prep of batch k+1 runs on the prep stream into the other of two
+double-buffered slots while batch k trains on the train stream; the graph
+joins both branches, so the host launches one graph per window and never
+synchronises.  Queue depth is the slot count (2).
+
+Multi-replica (RaCoM) steps split the graph around the gradient exchange:
+[prep k+1 || train k + pack] -> f64 all-reduce of [grads | contributor
+count] (NCCL in production, gloo / in-process in tests) -> update graph.
 """
 
 from __future__ import annotations
@@ -26,7 +32,8 @@ class StepRunner:
 
     def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
-                 multi: bool = False, use_graph: bool = True, ring_len: int = 1 << 16):
+                 multi: bool = False, use_graph: bool = True, pipeline: bool = True,
+                 ring_len: int = 1 << 16):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         self.g = g
@@ -38,28 +45,36 @@ class StepRunner:
         self.world, self.rank = int(world), int(rank)
         self.multi = bool(multi)
         self.use_graph = use_graph
+        self.pipeline = bool(pipeline)
         dev = g.device
         self.device = dev
-        self.sw = SampleWorkspace(g, fanouts, batch_size)
+        self.slots = [SampleWorkspace(g, fanouts, batch_size)
+                      for _ in range(2 if self.pipeline else 1)]
+        self.sw = self.slots[0]
         dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
         if dims[-1] != g.num_classes:
             raise ValueError("model output width must equal num_classes")
         self.tw = TrainWorkspace(self.sw, dims, g.num_classes)
         self.num_train = int(num_train)
+        self.batch_size = int(batch_size)
         self.perm = torch.zeros(max(self.num_train, 1), dtype=torch.int32, device=dev)
         self.cursor = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ring_len = int(ring_len)
         self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
         self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
                        if self.multi else None)
-        self.stream = torch.cuda.Stream(device=dev)
+        self.stream = torch.cuda.Stream(device=dev)       # train stream
+        self.prep_stream = torch.cuda.Stream(device=dev)  # sample + transfer stream
         self.graphs = {}
+        self.launches_per_phase = {}
         self.windows_done = 0
         self.epoch = 0
+        self._primed = False
 
     # ---------------------------------------------------------------- epochs
     def begin_epoch(self, epoch: int, perm: np.ndarray):
-        """Upload this epoch's shuffled train ids (plan_epoch, runtime.py:95-117)."""
+        """Upload this epoch's shuffled train ids (plan_epoch, runtime.py:95-117)
+        and, when pipelined, prepare batch 0 (the pipeline prologue)."""
         perm = np.asarray(perm)
         if perm.size != self.num_train:
             raise ValueError("permutation length changed; build a new StepRunner")
@@ -71,29 +86,45 @@ class StepRunner:
         with torch.cuda.stream(self.stream):
             self.perm.copy_(staged, non_blocking=True)
             self.cursor.zero_()
-            self.sw.key.copy_(key, non_blocking=True)
+            for sw in self.slots:
+                sw.key.copy_(key, non_blocking=True)
         self.epoch = epoch
         self.windows_done = 0
-        n_windows = -(-self.num_train // (self.sw.batch_size * self.world))
+        n_windows = -(-self.num_train // (self.batch_size * self.world))
         self.dm.ensure_bias(self.dm.host_steps + n_windows + 8)
+        self._primed = False
+        if self.pipeline and self.graphs:
+            self._prologue()
+
+    def _prologue(self):
+        with torch.cuda.stream(self.stream):
+            if self.use_graph:
+                self.graphs["prologue"].replay()
+            else:
+                self._enqueue_prep(self.slots[0], self.stream.cuda_stream)
+        self._primed = True
 
     # --------------------------------------------------------------- enqueue
-    def _enqueue_setup(self, s):
-        lib().mq_batch_setup(ptr(self.perm), self.num_train, self.sw.batch_size, self.world,
-                             self.rank, ptr(self.cursor), ptr(self.sw.targets),
-                             ptr(self.sw.n_targets), ptr(self.sw.key), s)
+    def _enqueue_setup(self, sw, s):
+        lib().mq_batch_setup(ptr(self.perm), self.num_train, self.batch_size, self.world,
+                             self.rank, ptr(self.cursor), ptr(sw.targets), ptr(sw.n_targets),
+                             ptr(sw.key), s)
 
-    def _enqueue_compute(self, s, commit=True):
-        self.sw.launch(self.cache, s, key_on_device=True)
-        self.tw.launch_gather(self.cache, s)
-        self.tw.launch_forward(self.dm, s)
-        self.tw.launch_loss(self.dm, s)
+    def _enqueue_prep(self, sw, s, setup=True):
+        if setup:
+            self._enqueue_setup(sw, s)
+        sw.launch(self.cache, s, key_on_device=True)
+        self.tw.launch_gather(sw, self.cache, s)
+
+    def _enqueue_train(self, sw, s, commit=True):
+        self.tw.launch_forward(self.dm, s, sw)
+        self.tw.launch_loss(self.dm, s, sw)
         if commit:
-            lib().mq_step_commit(ptr(self.tw.loss), ptr(self.cursor), ptr(self.loss_ring),
+            lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world, ptr(self.loss_ring),
                                  self.ring_len, s)
-        self.tw.launch_backward(self.dm, s)
+        self.tw.launch_backward(self.dm, s, sw)
         if self.grad64 is not None:
-            lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(self.sw.n_targets),
+            lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(sw.n_targets),
                                 ptr(self.grad64), s)
 
     def _enqueue_update(self, s):
@@ -102,76 +133,116 @@ class StepRunner:
         else:  # scale 0: divide by the all-reduced contributor count (expected[k])
             self.tw.launch_optimizer(self.dm, self.optimizer, s, grad64=self.grad64, scale=0.0)
 
+    def _fork_join(self, s_train, prep_fn, train_fn):
+        """prep_fn on the prep stream in parallel with train_fn on s_train."""
+        cur = torch.cuda.current_stream(self.device)
+        self.prep_stream.wait_stream(cur)
+        with torch.cuda.stream(self.prep_stream):
+            prep_fn(self.prep_stream.cuda_stream)
+        train_fn(s_train)
+        cur.wait_stream(self.prep_stream)
+
     def _phases(self):
-        if self.grad64 is None:
-            return {"full": lambda s: (self._enqueue_setup(s), self._enqueue_compute(s),
-                                       self._enqueue_update(s))}
-        return {"compute": lambda s: (self._enqueue_setup(s), self._enqueue_compute(s)),
-                "update": self._enqueue_update}
+        """name -> fn(stream) for every graph this runner captures."""
+        ph = {}
+        if not self.pipeline:
+            sw = self.slots[0]
+
+            def full(s):
+                self._enqueue_prep(sw, s)
+                self._enqueue_train(sw, s)
+                if not self.multi:
+                    self._enqueue_update(s)
+            ph["step0" if not self.multi else "compute0"] = full
+        else:
+            ph["prologue"] = lambda s: self._enqueue_prep(self.slots[0], s)
+            for i in (0, 1):
+                cur, nxt = self.slots[i], self.slots[1 - i]
+
+                def step(s, cur=cur, nxt=nxt):
+                    def train(st):
+                        self._enqueue_train(cur, st)
+                        if not self.multi:
+                            self._enqueue_update(st)
+                    self._fork_join(s, lambda sp: self._enqueue_prep(nxt, sp), train)
+                ph[("step" if not self.multi else "compute") + str(i)] = step
+        if self.multi:
+            ph["update"] = self._enqueue_update
+        return ph
 
     # ----------------------------------------------------------------- graphs
-    def _snapshot(self):
+    def _state_tensors(self):
         d = self.dm
-        return [t.clone() for t in (d.flat_w, d.flat_m, d.flat_v, d.step_dev, self.cursor,
-                                    self.loss_ring)] + (
-            [self.cache.hit_miss.clone()] if self.cache is not None else [])
+        ts = [d.flat_w, d.flat_m, d.flat_v, d.step_dev, self.cursor, self.loss_ring]
+        if self.cache is not None:
+            ts.append(self.cache.hit_miss)
+        return ts
 
-    def _restore(self, snap):
-        d = self.dm
-        targets = [d.flat_w, d.flat_m, d.flat_v, d.step_dev, self.cursor, self.loss_ring] + (
-            [self.cache.hit_miss] if self.cache is not None else [])
-        for t, v in zip(targets, snap):
-            t.copy_(v)
-
-    def capture(self):
-        """Eager warm-up (state restored afterwards), then capture each phase."""
-        if self.graphs:
-            return
-        phases = self._phases()
+    def _warm(self):
+        """Run every phase once eagerly (module loading, first-touch) and
+        restore all mutable state afterwards."""
+        snap = [t.clone() for t in self._state_tensors()]
         with torch.cuda.stream(self.stream):
-            snap = self._snapshot()
-            s = self.stream.cuda_stream
-            for fn in phases.values():
-                fn(s)  # warm-up only: no collective in between
-            self.stream.synchronize()
-            self._restore(snap)
-            self.tw.loss.zero_()
-            self.dm.nonfinite.zero_()
-            self.stream.synchronize()
-        for name, fn in phases.items():
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=self.stream):
-                fn(torch.cuda.current_stream().cuda_stream)
-            self.graphs[name] = graph
-        torch.cuda.synchronize(self.device)
-
-    def kernels_per_step(self) -> int:
-        """Number of libmqgnn kernel launches one step enqueues."""
-        lib().mq_prof_reset()
-        before = lib().mq_launch_count()
-        with torch.cuda.stream(self.stream):
-            snap = self._snapshot()
             for fn in self._phases().values():
                 fn(self.stream.cuda_stream)
-            self.stream.synchronize()
-            self._restore(snap)
-            self.tw.loss.zero_()
-        return int(lib().mq_launch_count() - before)
+        torch.cuda.synchronize(self.device)
+        for t, v in zip(self._state_tensors(), snap):
+            t.copy_(v)
+        self.tw.loss.zero_()
+        self.dm.nonfinite.zero_()
+        torch.cuda.synchronize(self.device)
 
-    # ------------------------------------------------------------------ step
+    def capture(self):
+        """Eager warm-up (state restored), then capture each phase as a graph."""
+        if self.graphs:
+            return
+        self._warm()
+        self.launches_per_phase = {}
+        for name, fn in self._phases().items():
+            graph = torch.cuda.CUDAGraph()
+            before = lib().mq_launch_count()
+            with torch.cuda.graph(graph, stream=self.stream):
+                fn(torch.cuda.current_stream().cuda_stream)
+            self.launches_per_phase[name] = int(lib().mq_launch_count() - before)
+            self.graphs[name] = graph
+        torch.cuda.synchronize(self.device)
+        if self.pipeline and not self._primed:
+            self._prologue()
+
+    def kernels_per_step(self) -> int:
+        """libmqgnn kernel launches in one steady-state step (counted while the
+        step's graphs were captured)."""
+        ph = self.launches_per_phase
+        if self.multi:
+            return ph.get("compute0", 0) + ph.get("update", 0)
+        return ph.get("step0", 0)
+
+    def eager_window(self):
+        """One window enqueued eagerly (not from the graphs) — used by the bench
+        to time each kernel with CUDA events; same kernels, same buffers."""
+        g = self.use_graph
+        self.use_graph = False
+        try:
+            self.compute_window()
+            if not self.multi:
+                self.apply_window()
+        finally:
+            self.use_graph = g
+
     def _replay(self, name):
         with torch.cuda.stream(self.stream):
             if self.use_graph:
                 self.graphs[name].replay()
-            elif name == "update":
-                self._enqueue_update(self.stream.cuda_stream)
             else:
                 self._phases()[name](self.stream.cuda_stream)
 
     # RaCoM protocol (racom.WindowDriver): compute -> exchange grad64 -> apply.
-    # A lone replica's compute already contains its update ("full" graph).
+    # A lone replica's compute already contains its update ("step" graph).
     def compute_window(self):
-        self._replay("compute" if self.multi else "full")
+        if self.pipeline and not self._primed:
+            self._prologue()
+        i = self.windows_done % 2 if self.pipeline else 0
+        self._replay(("compute" if self.multi else "step") + str(i))
 
     def apply_window(self):
         if self.multi:
@@ -211,12 +282,14 @@ class StepRunner:
     def wait_current(self):
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
 
-    def read_counts(self) -> dict:
-        """Device counts of the last step: targets and (n_dst, n_src, nnz) per hop."""
-        self.stream.synchronize()
-        c = torch.cat([self.sw.n_targets] + [hb.counts for hb in self.sw.hops]).cpu().tolist()
+    def read_counts(self, slot: int | None = None) -> dict:
+        """Device counts of a slot's batch: targets and (n_dst, n_src, nnz) per hop."""
+        torch.cuda.synchronize(self.device)
+        sw = self.slots[slot if slot is not None else
+                        ((self.windows_done - 1) % 2 if self.pipeline else 0)]
+        c = torch.cat([sw.n_targets] + [hb.counts for hb in sw.hops]).cpu().tolist()
         hops, nd = [], c[0]
-        for h in range(len(self.sw.hops)):
+        for h in range(len(sw.hops)):
             ns, nnz = c[1 + 2 * h], c[2 + 2 * h]
             hops.append((nd, ns, nnz))
             nd = ns
@@ -237,42 +310,108 @@ class StepRunner:
 
     # ------------------------------------------------- host-input (e2e) path
     def capture_host_input(self):
-        """Graph variant that reads targets staged by the host (no device plan)."""
-        if "host" in self.graphs:
+        """Graphs whose prep reads targets staged by the host (no device plan):
+        slot i trains while the other slot's host-staged batch is prepared."""
+        if "host0" in self.graphs:
             return
         if self.multi:
             raise NotImplementedError("host-input steps are single-replica")
-
-        def fn(s):
-            self._enqueue_compute(s, commit=False)
-            self._enqueue_update(s)
-        with torch.cuda.stream(self.stream):
-            snap = self._snapshot()
-            fn(self.stream.cuda_stream)
-            self.stream.synchronize()
-            self._restore(snap)
-            self.tw.loss.zero_()
-            self.stream.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=self.stream):
-            fn(torch.cuda.current_stream().cuda_stream)
-        self.graphs["host"] = graph
-        self._stage = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        self._stage = [torch.zeros(4, dtype=torch.int32, pin_memory=True) for _ in self.slots]
         self._loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        phases = {}
+        if not self.pipeline:
+            sw = self.slots[0]
+
+            def host0(s):
+                self._enqueue_prep(sw, s, setup=False)
+                self._enqueue_train(sw, s, commit=False)
+                self._enqueue_update(s)
+            phases["host0"] = host0
+        else:
+            phases["hostpro"] = lambda s: self._enqueue_prep(self.slots[0], s, setup=False)
+            for i in (0, 1):
+                cur, nxt = self.slots[i], self.slots[1 - i]
+
+                def hstep(s, cur=cur, nxt=nxt):
+                    def train(st):
+                        self._enqueue_train(cur, st, commit=False)
+                        self._enqueue_update(st)
+                    self._fork_join(s, lambda sp: self._enqueue_prep(nxt, sp, setup=False), train)
+                phases[f"host{i}"] = hstep
+        snap = [t.clone() for t in self._state_tensors()]
+        with torch.cuda.stream(self.stream):
+            for fn in phases.values():
+                fn(self.stream.cuda_stream)
+        torch.cuda.synchronize(self.device)
+        for t, v in zip(self._state_tensors(), snap):
+            t.copy_(v)
+        self.tw.loss.zero_()
+        torch.cuda.synchronize(self.device)
+        for name, fn in phases.items():
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=self.stream):
+                fn(torch.cuda.current_stream().cuda_stream)
+            self.graphs[name] = graph
+        torch.cuda.synchronize(self.device)
+
+    def _stage_batch(self, slot: int, targets_pinned: torch.Tensor, batch_id: int):
+        sw = self.slots[slot]
+        n = int(targets_pinned.numel())
+        st = self._stage[slot]
+        st.numpy().view(np.uint32)[:] = (n, self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF,
+                                        batch_id & 0xFFFFFFFF)
+        sw.targets[:n].copy_(targets_pinned, non_blocking=True)
+        sw.n_targets.copy_(st[0:1], non_blocking=True)
+        sw.key.copy_(st[1:4], non_blocking=True)
+
+    def run_host_batches(self, batches):
+        """Public host-buffer entry point (one replica): for each pinned int32
+        target batch (batch_id, targets) the step H2D-copies its inputs, trains,
+        and D2H-reads its summed loss.  With pipelining, batch k+1 is staged and
+        prepared while batch k trains; every batch still gets its own H2D copy
+        and its own loss read-back.  Yields (batch_id, loss)."""
+        batches = list(batches)
+        if not batches:
+            return
+        with torch.cuda.stream(self.stream):
+            if not self.pipeline:
+                for bid, t in batches:
+                    self._stage_batch(0, t, bid)
+                    self.graphs["host0"].replay()
+                    self._loss_host.copy_(self.tw.loss, non_blocking=True)
+                    self.tw.loss.zero_()
+                    self.stream.synchronize()
+                    self.dm.host_steps += 1
+                    yield bid, float(self._loss_host[0])
+                return
+            # the host runs one step ahead: step k's loss is read back (its own
+            # D2H + event wait) right after step k+1 has been launched
+            if not hasattr(self, "_loss_ring_host"):
+                self._loss_ring_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
+                self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            self._stage_batch(0, batches[0][1], batches[0][0])
+            self.graphs["hostpro"].replay()
+            pending = None
+            for k, (bid, t) in enumerate(batches):
+                cur, nxt = k % 2, 1 - (k % 2)
+                if k + 1 < len(batches):
+                    self._stage_batch(nxt, batches[k + 1][1], batches[k + 1][0])
+                else:  # nothing left to prepare: an empty batch keeps the graph fixed
+                    self.slots[nxt].n_targets.zero_()
+                self.graphs[f"host{cur}"].replay()
+                self._loss_ring_host[cur:cur + 1].copy_(self.tw.loss, non_blocking=True)
+                self.tw.loss.zero_()
+                self._loss_ev[cur].record(self.stream)
+                self.dm.host_steps += 1
+                if pending is not None:
+                    pbid, pslot = pending
+                    self._loss_ev[pslot].synchronize()
+                    yield pbid, float(self._loss_ring_host[pslot])
+                pending = (bid, cur)
+            pbid, pslot = pending
+            self._loss_ev[pslot].synchronize()
+            yield pbid, float(self._loss_ring_host[pslot])
 
     def step_from_host(self, targets_pinned: torch.Tensor, batch_id: int) -> float:
-        """H2D the batch's targets, run the step, D2H its loss (synchronous)."""
-        n = int(targets_pinned.numel())
-        with torch.cuda.stream(self.stream):
-            self.sw.targets[:n].copy_(targets_pinned, non_blocking=True)
-            self._stage.numpy().view(np.uint32)[:] = (n, self.seed & 0xFFFFFFFF,
-                                                      self.epoch & 0xFFFFFFFF,
-                                                      batch_id & 0xFFFFFFFF)
-            self.sw.n_targets.copy_(self._stage[0:1], non_blocking=True)
-            self.sw.key.copy_(self._stage[1:4], non_blocking=True)
-            self.graphs["host"].replay()
-            self._loss_host.copy_(self.tw.loss, non_blocking=True)
-            self.tw.loss.zero_()
-        self.stream.synchronize()
-        self.dm.host_steps += 1
-        return float(self._loss_host[0])
+        """Single synchronous step from one host batch (no cross-step overlap)."""
+        return next(iter(self.run_host_batches([(batch_id, targets_pinned)])))[1]

@@ -42,7 +42,7 @@ def test_version_and_scratch_queries(L):
     assert L.mq_scan_scratch_bytes(1) > 0
     assert L.mq_scan_scratch_bytes(10**8) > L.mq_scan_scratch_bytes(10**4)
     assert L.mq_relabel_scratch_bytes(1024, 10) > 0
-    assert L.mq_linear_bwd_w_scratch_bytes(2722, 602, 64) >= 2 * 602 * 64 * 4
+    assert L.mq_linear_scratch_bytes(2722, 602, 64) >= 2 * 602 * 64 * 4
     assert L.mq_prof_num_kernels() > 20
     names = {L.mq_prof_kernel_name(i).decode() for i in range(L.mq_prof_num_kernels())}
     assert {"sample_hop", "gather", "spmm_fwd", "linear_fwd", "adam"} <= names
