@@ -171,6 +171,56 @@ int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t 
                        int32_t d_out, const float* dz, int32_t lddz, float* dW, float* dt,
                        int32_t lddt, void* scratch, void* stream);
 
+/* ------------------------------------------------ fused training step
+ * The StepRunner's SAGE step.  Hidden layers are evaluated
+ * transform-first — the reference's z = [A h | h_dst] W (nn.py:126-131)
+ * re-associated as Y = h [W_top | W_bot], z = A Y_top + Y_bot — so the wide
+ * input features are never aggregated; the last layer is one fused kernel.
+ *
+ * mq_sage_transform: y (m x 2*d_out, row-major, ld 2*d_out) = h[:, :d_in] [W_top | W_bot],
+ *   W (2*d_in x d_out) as in the reference.  m = *m_dev (<= m_max).
+ * scratch for transform / transform_bwd: mq_sage_fused_scratch_bytes. */
+int64_t mq_sage_fused_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out);
+int mq_sage_transform(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, float* y, void* scratch,
+                      void* stream);
+/* act[r, :d_out] = relu(sum_e val_e y[col_e, :d_out] + y[r, d_out:2 d_out]) for
+ * r < *n_dst_dev (pad columns up to ldact zeroed); then zero the rows
+ * [0, *zeroK_rows_dev) x zeroK_row_floats of zero0 / zero1 (either may be NULL)
+ * — the backward's scatter targets, cleared here so they cost no launch. */
+int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                      const int32_t* n_dst_dev, int32_t n_dst_max, const float* y, int32_t d_out,
+                      float* act, int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
+                      int32_t zero0_row_floats, float* zero1, const int32_t* zero1_rows_dev,
+                      int32_t zero1_row_floats, void* stream);
+/* Backward of the aggregation (nn.py:167, 171-174 re-associated):
+ * dz = dh[r] * (act[r] > 0);  g[r, d_out:] = dz;  g[col_e, :d_out] += val_e dz.
+ * g (n_src x 2*d_out) must be zero for rows [0, n_src) on entry. */
+int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                        const int32_t* n_dst_dev, int32_t n_dst_max, const float* dh, int32_t lddh,
+                        const float* act, int32_t ldact, int32_t d_out, float* g, void* stream);
+/* dW (2*d_in x d_out) = [h^T g_top ; h^T g_bot] over m = *m_dev rows and, if
+ * dh != NULL, dh (m x d_in, ld lddh) = g [W_top | W_bot]^T (nn.py:168-174). */
+int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
+                          int32_t d_in, const float* W, int32_t d_out, const float* g, float* dW,
+                          float* dh, int32_t lddh, void* scratch, void* stream);
+/* The last layer in one launch: agg = block_apply(h) for the *n_dst_dev target
+ * rows (sequential triplet order, nn.py:79-89), logits = [agg | h_dst] W,
+ * summed softmax-CE (loss_acc += loss; nonfinite |= 1 on NaN/Inf, nn.py:141-156),
+ * dlogits -> dW (2*d x n_classes, deterministic fixed-order reduction) and,
+ * if dh != NULL, dh += block_apply_t(dt[:, :d]) + self half (nn.py:167-174;
+ * dh must be zero for rows [0, n_src) on entry).  With loss_ring != NULL the
+ * batch loss is then moved to loss_ring[(key_dev[2]/world) % ring_len] and
+ * loss_acc reset (mq_step_commit fused).  scratch: mq_sage_head_scratch_bytes,
+ * zero-filled ONCE before first use (it holds a self-resetting grid barrier). */
+int64_t mq_sage_head_scratch_bytes(int32_t n_dst_max, int32_t d, int32_t n_classes);
+int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                 const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh, int32_t d,
+                 const float* W, int32_t n_classes, const int32_t* labels, float* dW, float* dh,
+                 int32_t lddh, double* loss_acc, const uint32_t* key_dev, int32_t world,
+                 double* loss_ring, int32_t ring_len, int32_t* nonfinite, void* scratch,
+                 void* stream);
+
 /* batch_loss (nn.py:141-156): summed max-shifted softmax-CE over n rows;
  * dlogits = softmax - onehot; loss_out[0] += loss (f64);  nonfinite[0] |= 1
  * when any dlogit is NaN/Inf (FloatingPointError, nn.py:74-76). */
@@ -205,7 +255,9 @@ int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_
  * runtime.py:115-116).  step_dev is incremented on device; bias[2*(t-1)],
  * bias[2*(t-1)+1] hold float32(1 - 0.9**t), float32(1 - 0.999**t) for
  * t = 1..bias_len; lr is float32(learning_rate).  nonfinite[0] |= 1 on a
- * non-finite weight. */
+ * non-finite weight.  step_dev points at TWO int32: [0] the update count t,
+ * [1] an arrival counter that must be 0 at rest (the launch's last CTA
+ * publishes t+1 and resets it, so the bump costs no extra launch). */
 int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
             double grad_scale, int64_t n, int32_t* step_dev, const float* bias,
             int32_t bias_len, float lr, int32_t* nonfinite, void* stream);
@@ -223,6 +275,12 @@ int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, do
  * replica average of sync_models (sum over replicas in f64, then / n). */
 int mq_f32_to_f64(const float* in32, double* out64, int64_t n, void* stream);
 int mq_f64_to_f32(const double* in64, double divisor, float* out32, int64_t n, void* stream);
+
+/* Dense-transform backend of the fused step: 1 (default) = tcgen05 3xTF32
+ * (fp32-accurate split-precision on the 5th-gen tensor cores), 0 = fp32 FFMA
+ * split-K on the CUDA cores.  Process-wide; for tests and A/B measurement. */
+int mq_set_gemm_backend(int32_t backend);
+int mq_get_gemm_backend(void);
 
 /* ------------------------------------------------------------- utilities */
 /* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */

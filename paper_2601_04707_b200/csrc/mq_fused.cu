@@ -1,0 +1,728 @@
+// The fused SAGE training step: transform-first hidden layers and a one-launch
+// head (aggregate + transform + softmax-CE + backward of the last layer).
+//
+// Reference: mqpipe/nn.py:116-180 (sage_forward, batch_loss, backward).  The
+// reference evaluates every layer aggregate-first,
+//     z = [A h | h_dst] W,          W = [W_top ; W_bot]  (2 d_in x d_out),
+// which for the Reddit-shaped input layer means a 602-wide SpMM over every
+// sampled edge.  A hidden layer here is evaluated transform-first (the same
+// linear map, re-associated):
+//     Y = h [W_top | W_bot]          (n_src x 2 d_out; one dense GEMM over the
+//                                     sampled rows, h read once)
+//     z[r] = sum_e val_e Y_top[col_e] + Y_bot[r]
+// and its backward never needs the wide aggregate either:
+//     dz = dh_out * (z > 0)
+//     G  = [A^T dz | dz (dst rows, zero below)]     (n_src x 2 d_out)
+//     dW = h^T G  -> rows [0, d_in) = W_top grad, [d_in, 2 d_in) = W_bot grad
+//     dh = G [W_top | W_bot]^T                      (only for layers above 0)
+// so the aggregation runs at d_out = 64 instead of d_in = 602.  The result is
+// the reference's up to fp32 re-association (DESIGN.md §5 tolerances).
+//
+// The last layer (hop 0, the seeds' block) stays aggregate-first and is ONE
+// kernel: each CTA owns R target rows, aggregates them (sequential fp32 in
+// triplet order = np.add.at), applies W (smem-resident), runs the summed
+// softmax-CE (nn.py:141-156), back-propagates dt = dl W^T straight into dh
+// with vector atomics (block_apply_t + the self half, nn.py:171-174), writes
+// its dW partial, and after a grid barrier the CTAs reduce the partials in a
+// fixed order (deterministic dW).  CTA 0 then commits the batch loss to the
+// epoch's loss ring.
+#include <climits>
+
+#include "mq_gemm.cuh"
+
+namespace mq {
+
+// tcgen05 3xTF32 path (mq_tc.cu)
+int tc_backend();
+bool tc_supported(int n_out);
+int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d_in, const float* W,
+                 int d_out, float* y, float* part, cudaStream_t s);
+int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
+                   int d_out, const float* g, float* dW, float* part, cudaStream_t s);
+int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out);
+
+
+// ------------------------------------------------------------ GEMM loaders
+// B(k, j) of Y = h [W_top | W_bot]: k < d_in, j < 2N
+struct BLoadWSplit {
+  const float* W;
+  int d_in;
+  int N;
+  __device__ float4 load4(int k, int j) const {
+    if (k >= d_in) return make_float4(0.f, 0.f, 0.f, 0.f);
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j + t;
+      v[t] = jj < N ? __ldg(W + (int64_t)k * N + jj)
+                    : (jj < 2 * N ? __ldg(W + (int64_t)(d_in + k) * N + (jj - N)) : 0.f);
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+struct BLoadWSplitVec {  // N % 4 == 0 and W 16-byte aligned
+  const float* W;
+  int d_in;
+  int N;
+  __device__ float4 load4(int k, int j) const {
+    if (k >= d_in || j >= 2 * N) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* p = j < N ? W + (int64_t)k * N + j : W + (int64_t)(d_in + k) * N + (j - N);
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+};
+// A(o, r) = h[r, o] (dW = h^T G): o contiguous
+struct ALoadT {
+  static constexpr bool kKContig = false;
+  const float* h;
+  int ld;
+  __device__ float4 load4m(int o, int r) const {
+    return __ldg(reinterpret_cast<const float4*>(h + (int64_t)r * ld + o));
+  }
+};
+// B(k, j) of dh = G [W_top | W_bot]^T: k < 2N, j < d_in
+struct BLoadWSplitT {
+  const float* W;
+  int d_in;
+  int N;
+  __device__ float4 load4(int k, int j) const {
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int jj = j + t;
+      float x = 0.f;
+      if (jj < d_in && k < 2 * N)
+        x = k < N ? __ldg(W + (int64_t)jj * N + k) : __ldg(W + (int64_t)(d_in + jj) * N + (k - N));
+      v[t] = x;
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+// ------------------------------------------------------------ aggregate
+struct ZeroRange {
+  float* p;
+  const int32_t* rows_dev;
+  int row_floats;
+};
+
+__device__ __forceinline__ void zero_range(ZeroRange z, int64_t tid, int64_t nthreads) {
+  if (z.p == nullptr) return;
+  const int64_t n = (int64_t)(*z.rows_dev) * z.row_floats;
+  if ((z.row_floats & 3) == 0 && ((uintptr_t)z.p & 15) == 0) {
+    float4* p4 = reinterpret_cast<float4*>(z.p);
+    const float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = tid; i < n / 4; i += nthreads) p4[i] = zz;
+  } else {
+    for (int64_t i = tid; i < n; i += nthreads) z.p[i] = 0.f;
+  }
+}
+
+constexpr int kAggThreads = 256;
+
+// Row aggregation: sum over the edges [e0, e1) of val_e * h[col_e, c .. c+1]
+// (lanes own a float2 column pair).  With kExact the products are rounded
+// separately and added sequentially in edge order — np.add.at's evaluation
+// order (nn.py:88) — otherwise fused multiply-adds.  The row's gathers are
+// issued U at a time, so a row costs about ceil(nnz / U) L2 round trips
+// instead of nnz dependent ones.
+template <bool kExact>
+__device__ __forceinline__ float2 row_agg2(const int32_t* __restrict__ cols,
+                                           const float* __restrict__ vals, int e0, int e1,
+                                           const float* __restrict__ h, int ldh, int c,
+                                           bool active) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int eb = e0; eb < e1; eb += 32) {
+    const int me = eb + lane;
+    int32_t my_col = 0;
+    float my_val = 0.f;
+    if (me < e1) {
+      my_col = __ldg(&cols[me]);
+      my_val = __ldg(&vals[me]);
+    }
+    const int m = min(32, e1 - eb);
+    for (int t0 = 0; t0 < m; t0 += U) {
+      float2 x[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int32_t col = __shfl_sync(0xffffffffu, my_col, t & 31);
+        v[u] = __shfl_sync(0xffffffffu, my_val, t & 31);
+        x[u] = (active && t < m)
+                   ? __ldg(reinterpret_cast<const float2*>(h + (int64_t)col * ldh + c))
+                   : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (t0 + u < m) {
+          if (kExact) {
+            acc.x = __fadd_rn(acc.x, __fmul_rn(v[u], x[u].x));
+            acc.y = __fadd_rn(acc.y, __fmul_rn(v[u], x[u].y));
+          } else {
+            acc.x = fmaf(v[u], x[u].x, acc.x);
+            acc.y = fmaf(v[u], x[u].y, acc.y);
+          }
+        }
+      }
+    }
+  }
+  return acc;
+}
+
+// scalar-column variant (odd widths / pitches)
+template <bool kExact>
+__device__ __forceinline__ float row_agg1(const int32_t* __restrict__ cols,
+                                          const float* __restrict__ vals, int e0, int e1,
+                                          const float* __restrict__ h, int ldh, int c,
+                                          bool active) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int eb = e0; eb < e1; eb += 32) {
+    const int me = eb + lane;
+    int32_t my_col = 0;
+    float my_val = 0.f;
+    if (me < e1) {
+      my_col = __ldg(&cols[me]);
+      my_val = __ldg(&vals[me]);
+    }
+    const int m = min(32, e1 - eb);
+    for (int t0 = 0; t0 < m; t0 += U) {
+      float x[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int32_t col = __shfl_sync(0xffffffffu, my_col, t & 31);
+        v[u] = __shfl_sync(0xffffffffu, my_val, t & 31);
+        x[u] = (active && t < m) ? __ldg(h + (int64_t)col * ldh + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u < m) acc = kExact ? __fadd_rn(acc, __fmul_rn(v[u], x[u])) : fmaf(v[u], x[u], acc);
+    }
+  }
+  return acc;
+}
+
+// act[r, j] = relu(sum_e val_e Y[col_e, j] + Y[r, N + j]) for r < n_dst; pad
+// columns [N, ldact) are written as zeros.  Then zero the requested ranges.
+__global__ void __launch_bounds__(kAggThreads) sage_aggregate_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
+    const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
+    const float* __restrict__ y, int N, float* __restrict__ act, int ldact, ZeroRange z0,
+    ZeroRange z1) {
+  const int lane = threadIdx.x & 31;
+  const int warps = kAggThreads / 32;
+  const int n = *n_dst_dev;
+  const int ldy = 2 * N;
+  const bool vec2 = (N & 1) == 0 && (ldact & 1) == 0 && (((uintptr_t)y | (uintptr_t)act) & 7) == 0;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
+    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    const float* yb = y + (int64_t)r * ldy + N;
+    float* out = act + (int64_t)r * ldact;
+    if (vec2) {
+      for (int cb = 0; cb < ldact; cb += 64) {
+        const int c = cb + 2 * lane;
+        const float2 acc = row_agg2<false>(cols, vals, e0, e1, y, ldy, c, c < N);
+        if (c < N) {
+          const float2 b = __ldg(reinterpret_cast<const float2*>(yb + c));
+          const float zx = acc.x + b.x, zy = acc.y + b.y;
+          *reinterpret_cast<float2*>(out + c) = make_float2(zx > 0.f ? zx : 0.f, zy > 0.f ? zy : 0.f);
+        } else if (c < ldact) {
+          *reinterpret_cast<float2*>(out + c) = make_float2(0.f, 0.f);
+        }
+      }
+    } else {
+      for (int cb = 0; cb < ldact; cb += 32) {
+        const int c = cb + lane;
+        const float acc = row_agg1<false>(cols, vals, e0, e1, y, ldy, c, c < N);
+        if (c < N) {
+          const float z = acc + __ldg(yb + c);
+          out[c] = z > 0.f ? z : 0.f;
+        } else if (c < ldact) {
+          out[c] = 0.f;
+        }
+      }
+    }
+  }
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  zero_range(z0, tid, nth);
+  zero_range(z1, tid, nth);
+}
+
+// ------------------------------------------------------------ scatter bwd
+// dz = dh[r] * (act[r] > 0);  G[r, N:2N] = dz;  G[col_e, 0:N] += val_e dz
+// (G zeroed beforehand for rows [0, n_src)).
+__global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
+    const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
+    const float* __restrict__ dh, int lddh, const float* __restrict__ act, int ldact, int N,
+    float* __restrict__ G) {
+  const int lane = threadIdx.x & 31;
+  const int warps = kAggThreads / 32;
+  const int n = *n_dst_dev;
+  const int ldg = 2 * N;
+  const bool vec2 = (N & 1) == 0 && (lddh & 1) == 0 && (ldact & 1) == 0 &&
+                    (((uintptr_t)dh | (uintptr_t)act | (uintptr_t)G) & 7) == 0;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
+    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    if (vec2) {
+      const int n2 = N / 2;
+      for (int c = lane; c < n2; c += 32) {
+        const float2 g = *reinterpret_cast<const float2*>(dh + (int64_t)r * lddh + 2 * c);
+        const float2 a = *reinterpret_cast<const float2*>(act + (int64_t)r * ldact + 2 * c);
+        const float2 dz = make_float2(a.x > 0.f ? g.x : 0.f, a.y > 0.f ? g.y : 0.f);
+        *reinterpret_cast<float2*>(G + (int64_t)r * ldg + N + 2 * c) = dz;
+        for (int e = e0; e < e1; ++e) {
+          const int32_t col = __ldg(&cols[e]);
+          const float val = __ldg(&vals[e]);
+          atomicAdd(reinterpret_cast<float2*>(G + (int64_t)col * ldg + 2 * c),
+                    make_float2(val * dz.x, val * dz.y));
+        }
+      }
+    } else {
+      for (int c = lane; c < N; c += 32) {
+        const float g = dh[(int64_t)r * lddh + c];
+        const float dz = act[(int64_t)r * ldact + c] > 0.f ? g : 0.f;
+        G[(int64_t)r * ldg + N + c] = dz;
+        for (int e = e0; e < e1; ++e)
+          atomicAdd(G + (int64_t)__ldg(&cols[e]) * ldg + c, __ldg(&vals[e]) * dz);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ head
+__device__ __forceinline__ void grid_barrier(int32_t* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile int32_t* vgen = bar + 1;
+    const int gen = *vgen;
+    __threadfence();
+    if (atomicAdd(&bar[0], 1) == (int)gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(&bar[1], 1);
+    } else {
+      while (*vgen == gen) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct HeadArgs {
+  const int32_t* row_ptr;
+  const int32_t* cols;
+  const float* vals;
+  const int32_t* n_dst_dev;
+  const float* h;
+  int ldh;
+  int d;
+  const float* W;
+  int C;
+  int Cp;  // smem row stride of W (odd: conflict-free column walks)
+  const int32_t* labels;
+  float* dW;
+  float* dh;
+  int lddh;
+  float* part;
+  int32_t* bar;
+  double* loss_acc;
+  const uint32_t* key;
+  int world;
+  double* ring;
+  int ring_len;
+  int32_t* nonfinite;
+  int R;
+};
+
+constexpr int kHeadThreads = 256;
+constexpr int kHeadRowQuant = 16;  // R is a multiple of this (phase-2 row groups)
+
+__global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp, R = a.R;
+  float* Ws = smem;                 // [d2p][Cp]  (rows >= d2 zero)
+  float* both = Ws + d2p * Cp;      // [R][d2p]   = [agg | h_dst | 0 pad]
+  float* dl = both + R * d2p;       // [R][C]     logits, then dlogits
+  __shared__ double s_loss[kHeadThreads / 32];
+  __shared__ int s_bad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int warps = kHeadThreads / 32;
+  const int n = *a.n_dst_dev;
+  const int r0 = blockIdx.x * R;
+  if (tid == 0) s_bad = 0;
+  for (int i = tid; i < d2p * C; i += kHeadThreads) {
+    const int k = i / C, c = i % C;
+    Ws[k * Cp + c] = k < d2 ? __ldg(a.W + i) : 0.f;
+  }
+
+  // 1. both = [agg | h_dst] (agg bit-exact: sequential triplet order)
+  const bool vec2 = (d & 1) == 0 && (a.ldh & 1) == 0 && ((uintptr_t)a.h & 7) == 0;
+  for (int i = warp; i < R; i += warps) {
+    const int r = r0 + i;
+    float* brow = both + i * d2p;
+    if (r >= n) {
+      for (int c = lane; c < d2p; c += 32) brow[c] = 0.f;
+      continue;
+    }
+    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+    const float* self = a.h + (int64_t)r * a.ldh;
+    if (vec2) {
+      for (int cb = 0; cb < d; cb += 64) {
+        const int c = cb + 2 * lane;
+        const float2 acc = row_agg2<true>(a.cols, a.vals, e0, e1, a.h, a.ldh, c, c < d);
+        if (c < d) {
+          brow[c] = acc.x;
+          brow[c + 1] = acc.y;
+          const float2 hv = __ldg(reinterpret_cast<const float2*>(self + c));
+          brow[d + c] = hv.x;
+          brow[d + c + 1] = hv.y;
+        }
+      }
+    } else {
+      for (int cb = 0; cb < d; cb += 32) {
+        const int c = cb + lane;
+        const float acc = row_agg1<true>(a.cols, a.vals, e0, e1, a.h, a.ldh, c, c < d);
+        if (c < d) {
+          brow[c] = acc;
+          brow[d + c] = __ldg(self + c);
+        }
+      }
+    }
+    for (int c = d2 + lane; c < d2p; c += 32) brow[c] = 0.f;
+  }
+  __syncthreads();
+
+  // 2. logits = both W: thread (row group g of 4 rows, class c), float4 over k
+  {
+    const int g = tid >> 6, cl = tid & 63;
+    for (int c = cl; c < C; c += 64) {
+      for (int ib = 4 * g; ib < R; ib += kHeadRowQuant) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int k = 0; k < d2p; k += 4) {
+          const float w0 = Ws[(k + 0) * Cp + c], w1 = Ws[(k + 1) * Cp + c];
+          const float w2 = Ws[(k + 2) * Cp + c], w3 = Ws[(k + 3) * Cp + c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 b = *reinterpret_cast<const float4*>(both + (ib + q) * d2p + k);
+            acc[q] = fmaf(b.x, w0, acc[q]);
+            acc[q] = fmaf(b.y, w1, acc[q]);
+            acc[q] = fmaf(b.z, w2, acc[q]);
+            acc[q] = fmaf(b.w, w3, acc[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dl[(ib + q) * C + c] = acc[q];
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot
+  double wloss = 0.0;
+  int bad = 0;
+  for (int i = warp; i < R; i += warps) {
+    const int r = r0 + i;
+    float* x = dl + i * C;
+    if (r >= n) {
+      for (int c = lane; c < C; c += 32) x[c] = 0.f;
+      continue;
+    }
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = fmaxf(m, x[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32) s += expf(x[c] - m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float logd = logf(s);
+    const int lab = a.labels[r];
+    for (int c = lane; c < C; c += 32) {
+      const float sh = x[c] - m;
+      float p = expf(sh) / s;
+      if (c == lab) {
+        p -= 1.f;
+        wloss += -(double)(sh - logd);
+      }
+      x[c] = p;
+      bad |= !isfinite(p);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wloss += __shfl_xor_sync(0xffffffffu, wloss, o);
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (lane == 0) {
+    s_loss[warp] = wloss;
+    if (bad) s_bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < warps; ++w) t += s_loss[w];
+    if (t != 0.0) atomicAdd(a.loss_acc, t);
+    if (s_bad) atomicOr(a.nonfinite, 1);
+  }
+
+  // 4. dt = dl W^T -> dh: the self half to the dst row, the top half scattered
+  //    over the row's edges (dh was zeroed for rows [0, n_src))
+  if (a.dh != nullptr) {
+    for (int i = warp; i < R; i += warps) {
+      const int r = r0 + i;
+      if (r >= n) continue;
+      const float* x = dl + i * C;
+      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
+      for (int kb = 0; kb < d; kb += 32) {
+        const int k = kb + lane;
+        if (k >= d) continue;
+        float top = 0.f, bot = 0.f;
+        const float* wt = Ws + k * Cp;
+        const float* wb = Ws + (d + k) * Cp;
+        for (int c = 0; c < C; ++c) {
+          const float xc = x[c];
+          top = fmaf(xc, wt[c], top);
+          bot = fmaf(xc, wb[c], bot);
+        }
+        atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
+        for (int e = e0; e < e1; ++e)
+          atomicAdd(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + k, __ldg(&a.vals[e]) * top);
+      }
+    }
+  }
+
+  // 5. this CTA's dW partial = both^T dl: thread (k group, class c), 8 k per pass
+  {
+    float* part = a.part + (int64_t)blockIdx.x * d2 * C;
+    const int g = tid >> 6, cl = tid & 63;
+    for (int c = cl; c < C; c += 64) {
+      for (int k0 = 8 * g; k0 < d2p; k0 += 32) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+        for (int i = 0; i < R; ++i) {
+          const float v = dl[i * C + c];
+          const float4 b0 = *reinterpret_cast<const float4*>(both + i * d2p + k0);
+          const float4 b1 = k0 + 4 < d2p ? *reinterpret_cast<const float4*>(both + i * d2p + k0 + 4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          acc[0] = fmaf(b0.x, v, acc[0]);
+          acc[1] = fmaf(b0.y, v, acc[1]);
+          acc[2] = fmaf(b0.z, v, acc[2]);
+          acc[3] = fmaf(b0.w, v, acc[3]);
+          acc[4] = fmaf(b1.x, v, acc[4]);
+          acc[5] = fmaf(b1.y, v, acc[5]);
+          acc[6] = fmaf(b1.z, v, acc[6]);
+          acc[7] = fmaf(b1.w, v, acc[7]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (k0 + q < d2) part[(k0 + q) * C + c] = acc[q];
+      }
+    }
+  }
+
+  // 6. fixed-order reduction of the partials after a grid barrier
+  grid_barrier(a.bar);
+  const int total = d2 * C;
+  for (int o = blockIdx.x * kHeadThreads + tid; o < total; o += gridDim.x * kHeadThreads)
+    a.dW[o] = fixed_order_sum(a.part + o, total, (int)gridDim.x);
+  if (blockIdx.x == 0 && tid == 0 && a.ring != nullptr) {
+    const int k = (int)((a.key[2] / (uint32_t)a.world) % (uint32_t)a.ring_len);
+    volatile double* la = a.loss_acc;
+    a.ring[k] = *la;
+    *la = 0.0;
+  }
+}
+
+inline int head_rows(int n_dst_max) {
+  int R = kHeadRowQuant;
+  while ((n_dst_max + R - 1) / R > 128) R += kHeadRowQuant;
+  return R;
+}
+
+inline int64_t head_smem_bytes(int R, int d, int C) {
+  const int Cp = C | 1, d2p = (2 * d + 3) & ~3;
+  return (int64_t)(d2p * Cp + R * d2p + R * C) * (int64_t)sizeof(float);
+}
+
+}  // namespace mq
+
+using namespace mq;
+
+extern "C" {
+
+int64_t mq_sage_fused_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out) {
+  const int64_t K4 = pitch_of(d_in);
+  int64_t a = splitk_part_floats(m_max, 2 * d_out);  // transform
+  int64_t b = splitk_part_floats(K4, 2 * d_out);     // dW
+  int64_t c = splitk_part_floats(m_max, d_in);       // dh
+  int64_t mx = a > b ? a : b;
+  mx = mx > c ? mx : c;
+  const int64_t t = tc_scratch_floats(m_max, d_in, d_out);
+  mx = mx > t ? mx : t;
+  return mx * (int64_t)sizeof(float);
+}
+
+int mq_sage_transform(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, float* y, void* scratch,
+                      void* stream) {
+  MQ_CHECK_ARG(h && m_dev && W && y && scratch, "mq_sage_transform: null pointer");
+  MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldh >= d_in && ldh % 4 == 0 && (uintptr_t)h % 16 == 0,
+               "mq_sage_transform: h needs a 16-byte-aligned pitch (multiple of 4) >= d_in");
+  if (m_max <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  Dims dims{m_dev, 0, nullptr, d_in, 2 * d_out};
+  float* part = reinterpret_cast<float*>(scratch);
+  if (tc_backend() == 1 && tc_supported(2 * d_out))
+    return tc_transform(h, ldh, m_dev, m_max, d_in, W, d_out, y, part, s);
+  EpiStore epi{y, 2 * d_out};
+  if (d_out % 4 == 0 && (uintptr_t)W % 16 == 0)
+    return run_gemm(ALoadRow{h, ldh}, BLoadWSplitVec{W, d_in, d_out}, epi, dims, m_max, d_in,
+                    kMaxSplits, part, s, K_SAGE_TRANSFORM, K_SAGE_TRANSFORM_REDUCE);
+  return run_gemm(ALoadRow{h, ldh}, BLoadWSplit{W, d_in, d_out}, epi, dims, m_max, d_in, kMaxSplits,
+                  part, s, K_SAGE_TRANSFORM, K_SAGE_TRANSFORM_REDUCE);
+}
+
+int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                      const int32_t* n_dst_dev, int32_t n_dst_max, const float* y, int32_t d_out,
+                      float* act, int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
+                      int32_t zero0_row_floats, float* zero1, const int32_t* zero1_rows_dev,
+                      int32_t zero1_row_floats, void* stream) {
+  MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && y && act, "mq_sage_aggregate: null pointer");
+  MQ_CHECK_ARG(d_out >= 1 && ldact >= d_out, "mq_sage_aggregate: bad dims");
+  MQ_CHECK_ARG((!zero0 || zero0_rows_dev) && (!zero1 || zero1_rows_dev),
+               "mq_sage_aggregate: zero range without a row count");
+  cudaStream_t s = as_stream(stream);
+  const int warps = kAggThreads / 32;
+  int blocks = ceil_div(n_dst_max < 1 ? 1 : n_dst_max, warps);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  {
+    ProfScope ps(K_SAGE_AGG, s);
+    sage_aggregate_kernel<<<blocks, kAggThreads, 0, s>>>(
+        row_ptr, cols, vals, n_dst_dev, y, d_out, act, ldact,
+        ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
+        ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
+  }
+  MQ_LAUNCH_CHECK("sage_aggregate");
+  return MQ_OK;
+}
+
+int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                        const int32_t* n_dst_dev, int32_t n_dst_max, const float* dh, int32_t lddh,
+                        const float* act, int32_t ldact, int32_t d_out, float* g, void* stream) {
+  MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && dh && act && g,
+               "mq_sage_scatter_bwd: null pointer");
+  MQ_CHECK_ARG(d_out >= 1 && lddh >= d_out && ldact >= d_out, "mq_sage_scatter_bwd: bad dims");
+  if (n_dst_max <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  const int warps = kAggThreads / 32;
+  int blocks = ceil_div(n_dst_max, warps);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  {
+    ProfScope ps(K_SAGE_SCATTER, s);
+    sage_scatter_bwd_kernel<<<blocks, kAggThreads, 0, s>>>(row_ptr, cols, vals, n_dst_dev, dh, lddh,
+                                                           act, ldact, d_out, g);
+  }
+  MQ_LAUNCH_CHECK("sage_scatter_bwd");
+  return MQ_OK;
+}
+
+int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
+                          int32_t d_in, const float* W, int32_t d_out, const float* g, float* dW,
+                          float* dh, int32_t lddh, void* scratch, void* stream) {
+  MQ_CHECK_ARG(h && m_dev && W && g && dW && scratch, "mq_sage_transform_bwd: null pointer");
+  MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldh >= d_in && ldh % 4 == 0 && (uintptr_t)h % 16 == 0 &&
+                   (!dh || lddh >= d_in),
+               "mq_sage_transform_bwd: bad dims / alignment");
+  cudaStream_t s = as_stream(stream);
+  float* part = reinterpret_cast<float*>(scratch);
+  if (tc_backend() == 1 && tc_supported(2 * d_out)) {
+    int rc = tc_weight_grad(h, ldh, m_dev, m_max, d_in, d_out, g, dW, part, s);
+    if (rc) return rc;
+  } else {
+    Dims dims{nullptr, pitch_of(d_in), m_dev, 0, 2 * d_out};
+    int rc = run_gemm(ALoadT{h, ldh}, BLoadRow{g, 2 * d_out, 2 * d_out}, EpiDWSplit{dW, d_in, d_out},
+                      dims, pitch_of(d_in), m_max, kMaxSplits, part, s, K_SAGE_DW,
+                      K_SAGE_DW_REDUCE);
+    if (rc) return rc;
+  }
+  if (dh != nullptr && m_max > 0) {
+    Dims dims{m_dev, 0, nullptr, 2 * d_out, d_in};
+    int rc = run_gemm(ALoadRow{g, 2 * d_out}, BLoadWSplitT{W, d_in, d_out}, EpiStore{dh, lddh}, dims,
+                      m_max, 2 * d_out, (2 * d_out + GBK - 1) / GBK, part, s, K_SAGE_DH,
+                      K_SAGE_DH_REDUCE);
+    if (rc) return rc;
+  }
+  return MQ_OK;
+}
+
+int64_t mq_sage_head_scratch_bytes(int32_t n_dst_max, int32_t d, int32_t n_classes) {
+  const int R = head_rows(n_dst_max < 1 ? 1 : n_dst_max);
+  const int64_t G = (n_dst_max + R - 1) / R;
+  return 256 + G * 2 * d * (int64_t)n_classes * (int64_t)sizeof(float);
+}
+
+int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
+                 const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh, int32_t d,
+                 const float* W, int32_t n_classes, const int32_t* labels, float* dW, float* dh,
+                 int32_t lddh, double* loss_acc, const uint32_t* key_dev, int32_t world,
+                 double* loss_ring, int32_t ring_len, int32_t* nonfinite, void* scratch,
+                 void* stream) {
+  MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && h && W && labels && dW && loss_acc &&
+                   nonfinite && scratch,
+               "mq_sage_head: null pointer");
+  MQ_CHECK_ARG(d >= 1 && n_classes >= 1 && ldh >= d && (!dh || lddh >= d),
+               "mq_sage_head: bad dims");
+  MQ_CHECK_ARG(!loss_ring || (key_dev && ring_len > 0 && world >= 1), "mq_sage_head: bad ring");
+  if (n_dst_max <= 0) return MQ_OK;
+  const int R = head_rows(n_dst_max);
+  const int G = ceil_div(n_dst_max, R);
+  const int64_t smem = head_smem_bytes(R, d, n_classes);
+  MQ_CHECK_ARG(smem <= 220 * 1024, "mq_sage_head: d=%d, classes=%d need %lld B of shared memory", d,
+               n_classes, (long long)smem);
+  cudaStream_t s = as_stream(stream);
+  static thread_local int64_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    MQ_CUDA(cudaFuncSetAttribute(sage_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    configured = smem;
+  }
+  HeadArgs a;
+  a.row_ptr = row_ptr;
+  a.cols = cols;
+  a.vals = vals;
+  a.n_dst_dev = n_dst_dev;
+  a.h = h;
+  a.ldh = ldh;
+  a.d = d;
+  a.W = W;
+  a.C = n_classes;
+  a.Cp = n_classes | 1;
+  a.labels = labels;
+  a.dW = dW;
+  a.dh = dh;
+  a.lddh = lddh;
+  a.bar = reinterpret_cast<int32_t*>(scratch);
+  a.part = reinterpret_cast<float*>(reinterpret_cast<char*>(scratch) + 256);
+  a.loss_acc = loss_acc;
+  a.key = key_dev;
+  a.world = world;
+  a.ring = loss_ring;
+  a.ring_len = ring_len;
+  a.nonfinite = nonfinite;
+  a.R = R;
+  {
+    ProfScope ps(K_SAGE_HEAD, s);
+    sage_head_kernel<<<G, kHeadThreads, smem, s>>>(a);
+  }
+  MQ_LAUNCH_CHECK("sage_head");
+  return MQ_OK;
+}
+
+}  // extern "C"

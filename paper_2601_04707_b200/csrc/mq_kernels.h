@@ -32,7 +32,16 @@
   X(K_SGD, "sgd")                                 \
   X(K_STEP_BUMP, "step_bump")                     \
   X(K_CONVERT, "convert")                         \
-  X(K_BATCH_SETUP, "batch_setup")
+  X(K_BATCH_SETUP, "batch_setup")                \
+  X(K_SAGE_TRANSFORM, "sage_transform")           \
+  X(K_SAGE_TRANSFORM_REDUCE, "sage_transform_reduce") \
+  X(K_SAGE_AGG, "sage_aggregate")                 \
+  X(K_SAGE_HEAD, "sage_head")                     \
+  X(K_SAGE_SCATTER, "sage_scatter_bwd")           \
+  X(K_SAGE_DW, "sage_dw")                         \
+  X(K_SAGE_DW_REDUCE, "sage_dw_reduce")           \
+  X(K_SAGE_DH, "sage_dh")                         \
+  X(K_SAGE_DH_REDUCE, "sage_dh_reduce")
 
 namespace mq {
 enum KernelId {

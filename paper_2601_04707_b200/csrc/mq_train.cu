@@ -59,8 +59,6 @@ __global__ void softmax_ce_kernel(const float* __restrict__ logits, int ld,
   }
 }
 
-__global__ void step_bump_kernel(int32_t* step) { *step += 1; }
-
 __global__ void step_commit_kernel(double* loss_acc, const uint32_t* key, int world, double* ring,
                                    int ring_len) {
   int k = (int)((key[2] / (uint32_t)world) % (uint32_t)ring_len);
@@ -70,6 +68,20 @@ __global__ void step_commit_kernel(double* loss_acc, const uint32_t* key, int wo
 
 // grad32, or the f64 window sum: * scale, or (scale == 0) / the all-reduced
 // contributor count packed at g64[n] by mq_pack_grads
+// step[0] = update count, step[1] = arrival counter (0 at rest): every CTA
+// reads step[0] on entry; the last CTA to arrive publishes t and resets the
+// counter, so the bump is fused into the optimizer launch.
+__device__ __forceinline__ void step_arrive(int32_t* step, int t) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&step[1], 1) == (int)gridDim.x - 1) {
+      step[0] = t;
+      step[1] = 0;
+    }
+  }
+}
+
 __device__ __forceinline__ float load_grad(const float* g32, const double* g64, double scale,
                                            double count, int64_t i) {
   if (g32) return g32[i];
@@ -82,12 +94,13 @@ __device__ __forceinline__ double grad_count(const double* g64, double scale, in
 
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
                             const float* __restrict__ g32, const double* __restrict__ g64,
-                            double scale, int64_t n, const int32_t* __restrict__ step,
+                            double scale, int64_t n, int32_t* __restrict__ step,
                             const float* __restrict__ bias, int bias_len, float lr,
                             int32_t* __restrict__ nonfinite) {
-  const int t = *step;
+  const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
   if (t < 1 || t > bias_len) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
+    step_arrive(step, t);
     return;
   }
   const float bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
@@ -112,11 +125,13 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
     bad |= !finite_f(wi);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+  step_arrive(step, t);
 }
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
                            const double* __restrict__ g64, double scale, int64_t n, float lr,
-                           int32_t* __restrict__ nonfinite) {
+                           int32_t* __restrict__ step, int32_t* __restrict__ nonfinite) {
+  const int t = step[0] + 1;
   const double count = grad_count(g64, scale, n);
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -126,6 +141,7 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
     bad |= !finite_f(wi);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+  step_arrive(step, t);
 }
 
 __global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
@@ -185,12 +201,6 @@ int mq_adam(float* w, float* m, float* v, const float* grad32, const double* gra
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_adam: exactly one gradient source");
   cudaStream_t s = as_stream(stream);
   {
-    ProfScope ps(K_STEP_BUMP, s);
-    step_bump_kernel<<<1, 1, 0, s>>>(step_dev);
-  }
-  MQ_LAUNCH_CHECK("step_bump");
-  if (n <= 0) return MQ_OK;
-  {
     ProfScope ps(K_ADAM, s);
     adam_kernel<<<elem_blocks(n), 256, 0, s>>>(w, m, v, grad32, grad64, grad_scale, n, step_dev,
                                                bias, bias_len, lr, nonfinite);
@@ -205,14 +215,9 @@ int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scal
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_sgd: exactly one gradient source");
   cudaStream_t s = as_stream(stream);
   {
-    ProfScope ps(K_STEP_BUMP, s);
-    step_bump_kernel<<<1, 1, 0, s>>>(step_dev);
-  }
-  MQ_LAUNCH_CHECK("step_bump");
-  if (n <= 0) return MQ_OK;
-  {
     ProfScope ps(K_SGD, s);
-    sgd_kernel<<<elem_blocks(n), 256, 0, s>>>(w, grad32, grad64, grad_scale, n, lr, nonfinite);
+    sgd_kernel<<<elem_blocks(n), 256, 0, s>>>(w, grad32, grad64, grad_scale, n, lr, step_dev,
+                                              nonfinite);
   }
   MQ_LAUNCH_CHECK("sgd");
   return MQ_OK;

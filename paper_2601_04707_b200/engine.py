@@ -142,7 +142,8 @@ class DeviceModel:
                 self.view(self.flat_m, i).copy_(_t(m[i], device))
             if v is not None:
                 self.view(self.flat_v, i).copy_(_t(v[i], device))
-        self.step_dev = torch.tensor([step_count], dtype=torch.int32, device=device)
+        # [update count t, optimizer arrival counter] (mqgnn.h mq_adam)
+        self.step_dev = torch.tensor([step_count, 0], dtype=torch.int32, device=device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=device)
         self.bias_len = 0
         self.bias = None
@@ -313,6 +314,94 @@ class TrainWorkspace:
                          ptr(model.step_dev), model.lr32, ptr(model.nonfinite), stream)
         else:
             raise ValueError(f"unknown optimizer {optimizer!r}")
+
+
+class FusedTrainWorkspace:
+    """Buffers of the fused SAGE step (csrc/mq_fused.cu).
+
+    Layers 0..L-2 run transform-first (Y = h [W_top | W_bot], then a
+    d_out-wide aggregation); layer L-1 (the seeds' block) is the one-launch
+    head (aggregate + transform + softmax-CE + its backward + deterministic
+    dW).  Per layer l (hop h = L-1-l):
+      Y[l], G[l]   (n_src_h x 2 d_{l+1})   transform output / its gradient
+      act[l+1]     (n_dst_h x ld_{l+1})    relu output = next layer's input
+      dh[l]        (n_src_h x ld_l)        gradient w.r.t. layer l's input, l >= 1
+    The scatter targets (G[l], dh[L-1]) are cleared by the forward's
+    aggregation kernels, so the step has no memset nodes."""
+
+    def __init__(self, sw: SampleWorkspace, dims, num_classes: int):
+        g = sw.graph
+        dev = g.device
+        L = len(sw.fanouts)
+        if len(dims) != L + 1:
+            raise ValueError("dims must list input, hidden..., classes")
+        self.sw = sw
+        self.dims = list(dims)
+        self.L = L
+        self.C = num_classes
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.ld_in = [g.pitch] + [round_up(d, 4) for d in self.dims[1:L]]
+        self.Y, self.G, self.act, self.dh = [], [], [None] * (L + 1), [None] * L
+        scr = 1
+        for l in range(L - 1):
+            b = sw.bounds[L - 1 - l]
+            n2 = 2 * self.dims[l + 1]
+            self.Y.append(torch.zeros((max(b.n_src_max, 1), n2), **f32))
+            self.G.append(torch.zeros((max(b.n_src_max, 1), n2), **f32))
+            self.act[l + 1] = torch.zeros((max(b.n_dst_max, 1), self.ld_in[l + 1]), **f32)
+            if l >= 1:
+                self.dh[l] = torch.zeros((max(b.n_src_max, 1), self.ld_in[l]), **f32)
+            scr = max(scr, int(lib().mq_sage_fused_scratch_bytes(b.n_src_max, self.dims[l],
+                                                                  self.dims[l + 1])))
+        if L > 1:
+            b0 = sw.bounds[0]
+            self.dh[L - 1] = torch.zeros((max(b0.n_src_max, 1), self.ld_in[L - 1]), **f32)
+        self.scratch = torch.zeros(scr // 4 + 1, **f32)
+        hb = int(lib().mq_sage_head_scratch_bytes(sw.batch_size, self.dims[L - 1], num_classes))
+        self.head_scratch = torch.zeros(hb // 4 + 1, **f32)  # zeroed once: grid barrier state
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def h_in(self, l, sw):
+        return sw.x0 if l == 0 else self.act[l]
+
+    launch_gather = staticmethod(TrainWorkspace.launch_gather)
+    launch_optimizer = staticmethod(TrainWorkspace.launch_optimizer)
+
+    def launch_train(self, model: DeviceModel, stream, sw, ring=None, ring_len=0, world=1):
+        """Forward, loss and backward of one batch; gradients land in
+        model.flat_g.  With ``ring`` the batch loss is committed to it
+        (mq_step_commit fused into the head); otherwise it accumulates in
+        ``self.loss``."""
+        L, d, ld = self.L, self.dims, self.ld_in
+        lb = lib()
+        for l in range(L - 1):
+            h = L - 1 - l
+            hb, b = sw.hops[h], sw.bounds[h]
+            lb.mq_sage_transform(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts), b.n_src_max, d[l],
+                                 ptr(model.weight(l)), d[l + 1], ptr(self.Y[l]), ptr(self.scratch),
+                                 stream)
+            z1 = (self.dh[L - 1], sw.hops[0].counts, ld[L - 1]) if l == L - 2 else (None, None, 0)
+            lb.mq_sage_aggregate(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals), ptr(sw.n_dst_dev(h)),
+                                 b.n_dst_max, ptr(self.Y[l]), d[l + 1], ptr(self.act[l + 1]),
+                                 ld[l + 1], ptr(self.G[l]), ptr(hb.counts), 2 * d[l + 1],
+                                 ptr(z1[0]), ptr(z1[1]), z1[2], stream)
+        hb0 = sw.hops[0]
+        lb.mq_sage_head(ptr(hb0.row_ptr), ptr(hb0.cols), ptr(hb0.vals), ptr(sw.n_targets),
+                        sw.batch_size, ptr(self.h_in(L - 1, sw)), ld[L - 1], d[L - 1],
+                        ptr(model.weight(L - 1)), self.C, ptr(sw.labels), ptr(model.grad(L - 1)),
+                        ptr(self.dh[L - 1]), ld[L - 1], ptr(self.loss), ptr(sw.key), world,
+                        ptr(ring), ring_len, ptr(model.nonfinite), ptr(self.head_scratch), stream)
+        for l in range(L - 2, -1, -1):
+            h = L - 1 - l
+            hb, b = sw.hops[h], sw.bounds[h]
+            lb.mq_sage_scatter_bwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
+                                   ptr(sw.n_dst_dev(h)), b.n_dst_max, ptr(self.dh[l + 1]),
+                                   ld[l + 1], ptr(self.act[l + 1]), ld[l + 1], d[l + 1],
+                                   ptr(self.G[l]), stream)
+            lb.mq_sage_transform_bwd(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts), b.n_src_max,
+                                     d[l], ptr(model.weight(l)), d[l + 1], ptr(self.G[l]),
+                                     ptr(model.grad(l)), ptr(self.dh[l]), ld[l],
+                                     ptr(self.scratch), stream)
 
 
 def current_stream(device) -> int:

@@ -55,6 +55,7 @@ class PipelineConfig:
     capture_weights: bool = False
     use_graph: bool = True
     pipeline: bool = True   # prep of batch k+1 overlaps training of batch k
+    fused_step: bool = True  # transform-first fused SAGE step (mq_fused.cu)
 
     def validate(self) -> None:
         if self.num_devices < 1:
@@ -151,14 +152,15 @@ def _distributed():
 
 def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
     key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
-           config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline)
+           config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline,
+           config.fused_step)
     r = getattr(replica, "_runner", None)
     if r is None or r[0] != key:
         runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
                             batch_size=config.batch_size, num_train=num_train, cache=cache,
                             optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
                             multi=multi, use_graph=config.use_graph,
-                            pipeline=config.pipeline)
+                            pipeline=config.pipeline, fused=config.fused_step)
         replica._runner = (key, runner)
         return runner, True
     return r[1], False

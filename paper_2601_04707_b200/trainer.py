@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from ._lib import lib, ptr
-from .engine import SampleWorkspace, TrainWorkspace
+from .engine import FusedTrainWorkspace, SampleWorkspace, TrainWorkspace
 
 
 class StepRunner:
@@ -33,7 +33,7 @@ class StepRunner:
     def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
                  multi: bool = False, use_graph: bool = True, pipeline: bool = True,
-                 ring_len: int = 1 << 16):
+                 ring_len: int = 1 << 16, fused: bool = True):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         self.g = g
@@ -54,7 +54,11 @@ class StepRunner:
         dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
         if dims[-1] != g.num_classes:
             raise ValueError("model output width must equal num_classes")
-        self.tw = TrainWorkspace(self.sw, dims, g.num_classes)
+        # fused: transform-first hidden layers + one-launch head (mq_fused.cu);
+        # otherwise the reference-shaped per-op kernels (aggregate-first)
+        self.fused = bool(fused)
+        self.tw = (FusedTrainWorkspace if self.fused else TrainWorkspace)(self.sw, dims,
+                                                                          g.num_classes)
         self.num_train = int(num_train)
         self.batch_size = int(batch_size)
         self.perm = torch.zeros(max(self.num_train, 1), dtype=torch.int32, device=dev)
@@ -117,12 +121,16 @@ class StepRunner:
         self.tw.launch_gather(sw, self.cache, s)
 
     def _enqueue_train(self, sw, s, commit=True):
-        self.tw.launch_forward(self.dm, s, sw)
-        self.tw.launch_loss(self.dm, s, sw)
-        if commit:
-            lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world, ptr(self.loss_ring),
-                                 self.ring_len, s)
-        self.tw.launch_backward(self.dm, s, sw)
+        if self.fused:
+            self.tw.launch_train(self.dm, s, sw, ring=self.loss_ring if commit else None,
+                                 ring_len=self.ring_len, world=self.world)
+        else:
+            self.tw.launch_forward(self.dm, s, sw)
+            self.tw.launch_loss(self.dm, s, sw)
+            if commit:
+                lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world,
+                                     ptr(self.loss_ring), self.ring_len, s)
+            self.tw.launch_backward(self.dm, s, sw)
         if self.grad64 is not None:
             lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(sw.n_targets),
                                 ptr(self.grad64), s)

@@ -1,0 +1,130 @@
+"""GPU: the fused SAGE step (csrc/mq_fused.cu) against the CPU oracle.
+
+The StepRunner's default step evaluates hidden layers transform-first and the
+last layer as one fused head kernel.  Sampling and gather are
+bit-exact, so the oracle (the reference's aggregate-first nn.py restated) sees
+the identical batch; loss and gradients agree up to fp32 re-association:
+loss rel 1e-5, gradients max|a-b| <= 2e-5 * max|b| per layer.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import HostGraph, make_cfg1, make_g2
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2601_04707_b200 as mq  # noqa: E402
+from oracle import nn as onn  # noqa: E402
+from oracle import sampler as osamp  # noqa: E402
+from paper_2601_04707_b200.graph import DeviceGraph  # noqa: E402
+from paper_2601_04707_b200.runtime import epoch_permutation  # noqa: E402
+
+GRAD_RTOL = 2e-5
+
+
+def _normwise(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+
+
+def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
+    """Run `windows` eager fused steps on device (compute only, no optimizer)
+    and compare loss + gradients of each batch with the oracle."""
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, mask) if mask is not None else None
+    L = len(fanouts)
+    C = int(hg.num_classes)
+    state = mq.init_model(hg.feature_dim, hidden, C, num_layers=L, seed=7, learning_rate=0.01)
+    model = onn.init_model(hg.feature_dim, hidden, C, num_layers=L, seed=7, learning_rate=0.01)
+    perm = epoch_permutation(hg.train_mask, seed, 0)
+    runner = mq.StepRunner(g, state, fanouts=fanouts, batch_size=B, num_train=perm.size,
+                           cache=cache, seed=seed, use_graph=False, pipeline=False)
+    assert runner.fused
+    runner.begin_epoch(0, perm)
+    s = runner.stream
+    for j in range(windows):
+        with torch.cuda.stream(s):
+            runner._enqueue_prep(runner.slots[0], s.cuda_stream)
+            runner._enqueue_train(runner.slots[0], s.cuda_stream, commit=False)
+        torch.cuda.synchronize()
+        loss = float(runner.tw.loss.item())
+        runner.tw.loss.zero_()
+        assert int(state.dev.nonfinite.item()) == 0
+        grads = [state.dev.grad(l).cpu().numpy() for l in range(L)]
+        tg = perm[j * B:(j + 1) * B]
+        mb = osamp.build_minibatch(hg.row_offsets, hg.col_indices, hg.features, hg.labels, tg,
+                                   fanouts, seed=seed, epoch=0, batch_id=j, cached_mask=mask)
+        oloss, ograds, _ = onn.loss_and_grads(mb.layers, mb.features, mb.target_labels,
+                                              model.weights)
+        assert abs(loss - oloss) <= 1e-5 * abs(oloss), (j, loss, oloss)
+        for l, (a, b) in enumerate(zip(grads, ograds)):
+            assert a.shape == b.shape
+            err = _normwise(a, b)
+            assert err <= GRAD_RTOL, (j, l, err)
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return make_cfg1()
+
+
+def test_fused_two_layer_cfg1(cfg1):
+    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=3, windows=3)
+
+
+def test_fused_two_layer_cfg1_cached(cfg1):
+    rng = np.random.default_rng(0)
+    mask = np.zeros(cfg1.num_nodes, bool)
+    mask[rng.choice(cfg1.num_nodes, 100, replace=False)] = True
+    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=4, mask=mask, windows=2)
+
+
+def test_fused_three_layer_g2(golden_sampling):
+    hg = make_g2(golden_sampling)
+    _fused_vs_oracle(hg, (6, 4, 3), 32, 200, seed=5, mask=golden_sampling["g2/mask10"], windows=2)
+
+
+def test_fused_one_layer(golden_sampling):
+    hg = make_g2(golden_sampling)
+    _fused_vs_oracle(hg, (7,), 16, 128, seed=6, windows=2)
+
+
+def test_fused_odd_widths():
+    """d_in = 30 (pitch 32, pad columns), hidden 13 (odd: scalar paths), 7 classes."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    src = rng.integers(0, n, 40_000)
+    dst = (src + rng.integers(1, 200, src.size)) % n
+    keys = np.unique(np.concatenate([src * n + dst, dst * n + src]))
+    s, d = keys // n, keys % n
+    ro = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(s, minlength=n), out=ro[1:])
+    feats = rng.standard_normal((n, 30)).astype(np.float32)
+    labels = rng.integers(0, 7, n).astype(np.int32)
+    train = rng.random(n) < 0.5
+    hg = HostGraph(ro, d, feats, labels, 7, train)
+    _fused_vs_oracle(hg, (5, 4, 3), 13, 256, seed=9, windows=2)
+
+
+def test_fused_epoch_matches_unfused(golden_sampling):
+    """A whole graph-captured epoch: fused and per-op step agree to training tolerance."""
+    hg = make_g2(golden_sampling)
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, golden_sampling["g2/mask10"])
+    out = {}
+    for fused in (True, False):
+        cfg = mq.PipelineConfig(num_devices=1, batch_size=64,
+                                sampler=mq.SamplerParams("sage", (4, 3), num_layers=2),
+                                optimizer="adam", seed=5, fused_step=fused)
+        st = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        stats, _ = mq.run_epoch(g, cache, [st], cfg, epoch=0)
+        out[fused] = (np.array([stats.losses[b] for b in sorted(stats.losses)]),
+                      [w.cpu().numpy() for w in st.weights])
+    np.testing.assert_allclose(out[True][0], out[False][0], rtol=1e-4)
+    for a, b in zip(out[True][1], out[False][1]):
+        assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max()

@@ -1,0 +1,97 @@
+"""GPU: the dense SAGE transforms on both backends (tcgen05 3xTF32 and fp32
+FFMA split-K) against an fp64 reference of the same contraction.
+
+mq_sage_transform:     y = h[:, :d_in] [W_top | W_bot]           (nn.py:126-131, re-associated)
+mq_sage_transform_bwd: dW = [h^T g_top ; h^T g_bot], dh = g [W_top | W_bot]^T   (nn.py:168-174)
+Bar: max|a-b| <= 1e-5 * max|b| (fp32-level; one TF32 pass would miss it).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2601_04707_b200._lib import lib, ptr  # noqa: E402
+
+RTOL = 1e-5
+SHAPES = [  # (rows, d_in, d_out)
+    (3262, 602, 64),   # Reddit-shaped layer 0
+    (1, 602, 64),
+    (129, 100, 64),    # products-shaped layer 0
+    (1000, 64, 64),
+    (257, 30, 13),     # odd widths: N = 26 padded to 32 on the tensor core
+    (0, 64, 64),       # empty frontier
+]
+
+
+def _normwise(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if b.size == 0:
+        return 0.0
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+@pytest.fixture(params=[1, 0], ids=["tcgen05", "ffma"])
+def backend(request):
+    old = lib().mq_get_gemm_backend()
+    lib().mq_set_gemm_backend(request.param)
+    yield request.param
+    lib().mq_set_gemm_backend(old)
+
+
+@pytest.mark.parametrize("rows,d_in,d_out", SHAPES)
+def test_transform_fwd_bwd(backend, rows, d_in, d_out):
+    rng = np.random.default_rng(rows + d_in + d_out)
+    ld = (d_in + 3) // 4 * 4
+    m_max = max(rows, 1) + 37  # bound larger than the live count
+    h = np.zeros((m_max, ld), np.float32)
+    h[:rows, :d_in] = rng.standard_normal((rows, d_in))
+    h[:rows, d_in:] = 7.0  # pad columns must not leak into the result
+    W = (rng.standard_normal((2 * d_in, d_out)) / np.sqrt(d_in)).astype(np.float32)
+    g = np.zeros((m_max, 2 * d_out), np.float32)
+    g[:rows] = rng.standard_normal((rows, 2 * d_out))
+    dev = "cuda"
+    th, tW, tg = (torch.from_numpy(x).to(dev) for x in (h, W, g))
+    ty = torch.zeros((m_max, 2 * d_out), dtype=torch.float32, device=dev)
+    tdW = torch.zeros_like(tW)
+    tdh = torch.zeros((m_max, ld), dtype=torch.float32, device=dev)
+    m_dev = torch.tensor([rows], dtype=torch.int32, device=dev)
+    scr = torch.zeros(int(lib().mq_sage_fused_scratch_bytes(m_max, d_in, d_out)) // 4 + 1,
+                      dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    lib().mq_sage_transform(ptr(th), ld, ptr(m_dev), m_max, d_in, ptr(tW), d_out, ptr(ty),
+                            ptr(scr), s)
+    y = ty.cpu().numpy()[:rows]
+    lib().mq_sage_transform_bwd(ptr(th), ld, ptr(m_dev), m_max, d_in, ptr(tW), d_out, ptr(tg),
+                                ptr(tdW), ptr(tdh), ld, ptr(scr), s)
+    torch.cuda.synchronize()
+    h64 = h[:rows, :d_in].astype(np.float64)
+    W64 = W.astype(np.float64)
+    Wcat = np.concatenate([W64[:d_in], W64[d_in:]], axis=1)  # [W_top | W_bot]
+    ref_y = h64 @ Wcat
+    assert _normwise(y, ref_y) <= RTOL
+    g64 = g[:rows].astype(np.float64)
+    ref_dW = np.concatenate([h64.T @ g64[:, :d_out], h64.T @ g64[:, d_out:]], axis=0)
+    assert _normwise(tdW.cpu().numpy(), ref_dW) <= RTOL
+    ref_dh = g64 @ Wcat.T
+    assert _normwise(tdh.cpu().numpy()[:rows, :d_in], ref_dh) <= RTOL
+
+
+def test_tf32_single_pass_would_fail():
+    """Sanity of the bar: rounding the operands to TF32 once breaks 1e-5."""
+    rng = np.random.default_rng(0)
+    h = rng.standard_normal((512, 602)).astype(np.float32)
+    W = rng.standard_normal((602, 128)).astype(np.float32)
+
+    def tf32(x):
+        u = x.view(np.uint32).astype(np.uint64)
+        u = ((u + 0x1000) & 0xFFFFE000).astype(np.uint32)
+        return u.view(np.float32)
+
+    exact = h.astype(np.float64) @ W.astype(np.float64)
+    one_pass = tf32(h).astype(np.float64) @ tf32(W).astype(np.float64)
+    assert _normwise(one_pass, exact) > RTOL
