@@ -24,6 +24,10 @@ SHAPES = [  # (rows, d_in, d_out)
     (1000, 64, 64),
     (257, 30, 13),     # odd widths: N = 26 padded to 32 on the tensor core
     (0, 64, 64),       # empty frontier
+    (1131, 32, 32),    # 3-layer g2 middle layer (36 k blocks -> 18 splits of 2)
+    (1323, 16, 32),
+    (1118, 32, 32),
+    (5000, 64, 64),    # several items per CTA on the forward
 ]
 
 
@@ -95,3 +99,24 @@ def test_tf32_single_pass_would_fail():
     exact = h.astype(np.float64) @ W.astype(np.float64)
     one_pass = tf32(h).astype(np.float64) @ tf32(W).astype(np.float64)
     assert _normwise(one_pass, exact) > RTOL
+
+
+@pytest.mark.parametrize("rows,d_in,d_out", [(1131, 32, 32), (3262, 602, 64)])
+def test_transform_bwd_deterministic(rows, d_in, d_out):
+    """Two runs of the tcgen05 weight gradient give bit-identical results."""
+    rng = np.random.default_rng(5)
+    ld = (d_in + 3) // 4 * 4
+    h = torch.from_numpy(rng.standard_normal((rows, ld)).astype(np.float32)).cuda()
+    W = torch.from_numpy(rng.standard_normal((2 * d_in, d_out)).astype(np.float32)).cuda()
+    g = torch.from_numpy(rng.standard_normal((rows, 2 * d_out)).astype(np.float32)).cuda()
+    m_dev = torch.tensor([rows], dtype=torch.int32, device="cuda")
+    scr = torch.zeros(int(lib().mq_sage_fused_scratch_bytes(rows, d_in, d_out)) // 4 + 1,
+                      dtype=torch.float32, device="cuda")
+    outs = []
+    for _ in range(3):
+        dW = torch.zeros_like(W)
+        lib().mq_sage_transform_bwd(ptr(h), ld, ptr(m_dev), rows, d_in, ptr(W), d_out, ptr(g),
+                                    ptr(dW), None, ld, ptr(scr),
+                                    torch.cuda.current_stream().cuda_stream)
+        outs.append(dW.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
