@@ -40,6 +40,32 @@ extern "C" {
 
 #define MQ_MAX_FANOUT 32
 
+/* Deferred split-K gradient reduction.  A flat gradient
+ * element i in [offset, offset + size) is the fixed-order sum over p <
+ * nparts of part[p * stride + j], with j = i - offset (kind 0) or, for
+ * kind 1, the split-W layout of mq_sage_transform_bwd's partial tiles:
+ * row = j / d_out, col = j % d_out, j' = row < d_in ? row * 2 d_out + col
+ * : (row - d_in) * 2 d_out + d_out + col.  Elements outside every segment
+ * come from the plain f32 gradient.  Passed by value into the optimizer
+ * kernels, so the split-K reduction costs no launch of its own. */
+#define MQ_GRAD_MAX_SEG 8
+typedef struct mq_grad_seg {
+  const float* part;
+  const int32_t* nparts_dev; /* device-side partial count, or NULL: use nparts */
+  int64_t stride;
+  int64_t offset;
+  int64_t size;
+  int32_t nparts;
+  int32_t kind;
+  int32_t d_in;
+  int32_t d_out;
+} mq_grad_seg;
+typedef struct mq_grad_src {
+  int32_t nseg;
+  int32_t pad_;
+  mq_grad_seg seg[MQ_GRAD_MAX_SEG];
+} mq_grad_src;
+
 /* --------------------------------------------------------------- library */
 int mq_version(void);
 const char* mq_last_error(void);
@@ -200,19 +226,30 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
                         const int32_t* n_dst_dev, int32_t n_dst_max, const float* dh, int32_t lddh,
                         const float* act, int32_t ldact, int32_t d_out, float* g, void* stream);
 /* dW (2*d_in x d_out) = [h^T g_top ; h^T g_bot] over m = *m_dev rows and, if
- * dh != NULL, dh (m x d_in, ld lddh) = g [W_top | W_bot]^T (nn.py:168-174). */
+ * dh != NULL, dh (m x d_in, ld lddh) = g [W_top | W_bot]^T (nn.py:168-174).
+ * Deferred weight gradient: when dw_parts != NULL and mq_sage_dw_deferred(d_out)
+ * is 1 (tcgen05 backend), the split-K partial tiles are left in dw_parts
+ * (mq_sage_dw_parts_bytes) with their count in *dw_nparts_dev and dW is not
+ * written; mq_sage_dw_grad_seg describes them for the optimizer. */
+int mq_sage_dw_deferred(int32_t d_out);
+int64_t mq_sage_dw_parts_bytes(int32_t d_in, int32_t d_out);
 int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
                           int32_t d_in, const float* W, int32_t d_out, const float* g, float* dW,
-                          float* dh, int32_t lddh, void* scratch, void* stream);
+                          float* dh, int32_t lddh, void* scratch, float* dw_parts,
+                          int32_t* dw_nparts_dev, void* stream);
+int mq_sage_dw_grad_seg(float* dw_parts, const int32_t* dw_nparts_dev, int32_t d_in, int32_t d_out,
+                        int64_t offset, mq_grad_seg* out);
 /* The last layer in one launch: agg = block_apply(h) for the *n_dst_dev target
  * rows (sequential triplet order, nn.py:79-89), logits = [agg | h_dst] W,
  * summed softmax-CE (loss_acc += loss; nonfinite |= 1 on NaN/Inf, nn.py:141-156),
- * dlogits -> dW (2*d x n_classes, deterministic fixed-order reduction) and,
+ * dlogits -> per-CTA dW partials in scratch (reduced in fixed CTA order into dW
+ * when dW != NULL, else left for the optimizer: mq_sage_head_grad_seg) and,
  * if dh != NULL, dh += block_apply_t(dt[:, :d]) + self half (nn.py:167-174;
  * dh must be zero for rows [0, n_src) on entry).  With loss_ring != NULL the
  * batch loss is then moved to loss_ring[(key_dev[2]/world) % ring_len] and
- * loss_acc reset (mq_step_commit fused).  scratch: mq_sage_head_scratch_bytes,
- * zero-filled ONCE before first use (it holds a self-resetting grid barrier). */
+ * loss_acc reset (mq_step_commit fused) by the last CTA to finish.  scratch:
+ * mq_sage_head_scratch_bytes, zero-filled ONCE before first use (it holds a
+ * self-resetting completion counter). */
 int64_t mq_sage_head_scratch_bytes(int32_t n_dst_max, int32_t d, int32_t n_classes);
 int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                  const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh, int32_t d,
@@ -220,6 +257,8 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                  int32_t lddh, double* loss_acc, const uint32_t* key_dev, int32_t world,
                  double* loss_ring, int32_t ring_len, int32_t* nonfinite, void* scratch,
                  void* stream);
+int mq_sage_head_grad_seg(int32_t n_dst_max, int32_t d, int32_t n_classes, void* scratch,
+                          int64_t offset, mq_grad_seg* out);
 
 /* batch_loss (nn.py:141-156): summed max-shifted softmax-CE over n rows;
  * dlogits = softmax - onehot; loss_out[0] += loss (f64);  nonfinite[0] |= 1
@@ -257,18 +296,26 @@ int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_
  * t = 1..bias_len; lr is float32(learning_rate).  nonfinite[0] |= 1 on a
  * non-finite weight.  step_dev points at TWO int32: [0] the update count t,
  * [1] an arrival counter that must be 0 at rest (the launch's last CTA
- * publishes t+1 and resets it, so the bump costs no extra launch). */
+ * publishes t+1 and resets it, so the bump costs no extra launch).  With
+ * src != NULL (grad32 path) gradients are resolved through the deferred
+ * split-K segments (mq_grad_src). */
 int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
             double grad_scale, int64_t n, int32_t* step_dev, const float* bias,
-            int32_t bias_len, float lr, int32_t* nonfinite, void* stream);
+            int32_t bias_len, float lr, int32_t* nonfinite, const mq_grad_src* src,
+            void* stream);
 /* sgd_step (nn.py:209-215) */
 int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale,
-           int64_t n, int32_t* step_dev, float lr, int32_t* nonfinite, void* stream);
+           int64_t n, int32_t* step_dev, float lr, int32_t* nonfinite,
+           const mq_grad_src* src, void* stream);
 /* out64[i] = (double)grad[i] for i < n and out64[n] = (n_targets_dev[0] > 0):
  * one f64 buffer carries the window's gradient sum and contributor count
  * through a single all-reduce. */
 int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, double* out64,
-                  void* stream);
+                  const mq_grad_src* src, void* stream);
+/* out32[i] = gradient element i resolved through src (materialises the
+ * deferred reduction; tests and the eager API). */
+int mq_grad_reduce(const mq_grad_src* src, const float* grad32, int64_t n, float* out32,
+                   void* stream);
 
 /* RaCoM packing for the NCCL collectives (racom.py:47-57, 118-139):
  * out64[i] = (double)in32[i];  out32[i] = (float)(in64[i] / divisor) — the

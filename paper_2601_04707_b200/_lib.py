@@ -20,6 +20,20 @@ U64 = C.c_uint64
 F32 = C.c_float
 F64 = C.c_double
 
+MQ_GRAD_MAX_SEG = 8
+
+
+class GradSeg(C.Structure):
+    """mq_grad_seg (include/mqgnn.h): one deferred split-K gradient range."""
+    _fields_ = [("part", P), ("nparts_dev", P), ("stride", I64), ("offset", I64), ("size", I64),
+                ("nparts", I32), ("kind", I32), ("d_in", I32), ("d_out", I32)]
+
+
+class GradSrc(C.Structure):
+    """mq_grad_src: up to MQ_GRAD_MAX_SEG segments resolved by the optimizer kernels."""
+    _fields_ = [("nseg", I32), ("pad_", I32), ("seg", GradSeg * MQ_GRAD_MAX_SEG)]
+
+
 # name -> (restype, argtypes); mirrors include/mqgnn.h one to one
 SIGNATURES = {
     "mq_version": (C.c_int, []),
@@ -46,17 +60,22 @@ SIGNATURES = {
                                      P, P]),
     "mq_softmax_ce": (C.c_int, [P, I32, P, P, I32, I32, P, I32, P, P, P]),
     "mq_gather_labels": (C.c_int, [P, P, P, I32, P, P]),
-    "mq_adam": (C.c_int, [P, P, P, P, P, F64, I64, P, P, I32, F32, P, P]),
-    "mq_sgd": (C.c_int, [P, P, P, F64, I64, P, F32, P, P]),
+    "mq_adam": (C.c_int, [P, P, P, P, P, F64, I64, P, P, I32, F32, P, P, P]),
+    "mq_sgd": (C.c_int, [P, P, P, F64, I64, P, F32, P, P, P]),
     "mq_f32_to_f64": (C.c_int, [P, P, I64, P]),
-    "mq_pack_grads": (C.c_int, [P, I64, P, P, P]),
+    "mq_pack_grads": (C.c_int, [P, I64, P, P, P, P]),
+    "mq_grad_reduce": (C.c_int, [P, P, I64, P, P]),
     "mq_f64_to_f32": (C.c_int, [P, F64, P, I64, P]),
     "mq_scan_i32": (C.c_int, [P, P, I32, P, P, P]),
     "mq_sage_fused_scratch_bytes": (I64, [I32, I32, I32]),
     "mq_sage_transform": (C.c_int, [P, I32, P, I32, I32, P, I32, P, P, P]),
     "mq_sage_aggregate": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, P, P, I32, P, P, I32, P]),
     "mq_sage_scatter_bwd": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, I32, P, P]),
-    "mq_sage_transform_bwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, P, P, I32, P, P]),
+    "mq_sage_dw_deferred": (C.c_int, [I32]),
+    "mq_sage_dw_parts_bytes": (I64, [I32, I32]),
+    "mq_sage_transform_bwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, P, P, I32, P, P, P, P]),
+    "mq_sage_dw_grad_seg": (C.c_int, [P, P, I32, I32, I64, P]),
+    "mq_sage_head_grad_seg": (C.c_int, [I32, I32, I32, P, I64, P]),
     "mq_sage_head_scratch_bytes": (I64, [I32, I32, I32]),
     "mq_sage_head": (C.c_int, [P, P, P, P, I32, P, I32, I32, P, I32, P, P, P, I32, P, P, I32, P,
                                I32, P, P, P]),
@@ -72,7 +91,8 @@ SIGNATURES = {
 
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
                if res is C.c_int and name not in ("mq_version", "mq_prof_num_kernels",
-                                                       "mq_get_gemm_backend")}
+                                                       "mq_get_gemm_backend",
+                                                       "mq_sage_dw_deferred")}
 
 
 class MQError(RuntimeError):

@@ -38,7 +38,9 @@ bool tc_supported(int n_out);
 int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d_in, const float* W,
                  int d_out, float* y, float* part, cudaStream_t s);
 int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
-                   int d_out, const float* g, float* dW, float* part, cudaStream_t s);
+                   int d_out, const float* g, float* dW, float* part, int32_t* nparts_out,
+                   cudaStream_t s);
+int64_t tc_dw_part_floats(int64_t d_in, int64_t d_out);
 int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out);
 
 
@@ -295,24 +297,6 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
 }
 
 // ------------------------------------------------------------ head
-__device__ __forceinline__ void grid_barrier(int32_t* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int32_t* vgen = bar + 1;
-    const int gen = *vgen;
-    __threadfence();
-    if (atomicAdd(&bar[0], 1) == (int)gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1);
-    } else {
-      while (*vgen == gen) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 struct HeadArgs {
   const int32_t* row_ptr;
   const int32_t* cols;
@@ -329,7 +313,7 @@ struct HeadArgs {
   float* dh;
   int lddh;
   float* part;
-  int32_t* bar;
+  int32_t* done;
   double* loss_acc;
   const uint32_t* key;
   int world;
@@ -356,9 +340,16 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   const int n = *a.n_dst_dev;
   const int r0 = blockIdx.x * R;
   if (tid == 0) s_bad = 0;
-  for (int i = tid; i < d2p * C; i += kHeadThreads) {
-    const int k = i / C, c = i % C;
-    Ws[k * Cp + c] = k < d2 ? __ldg(a.W + i) : 0.f;
+  if (Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0) {  // same layout: float4 copy
+    const float4* src = reinterpret_cast<const float4*>(a.W);
+    float4* dst = reinterpret_cast<float4*>(Ws);
+    for (int i = tid; i < d2 * C / 4; i += kHeadThreads) dst[i] = __ldg(src + i);
+    for (int i = d2 * C + tid; i < d2p * Cp; i += kHeadThreads) Ws[i] = 0.f;
+  } else {
+    for (int i = tid; i < d2p * C; i += kHeadThreads) {
+      const int k = i / C, c = i % C;
+      Ws[k * Cp + c] = k < d2 ? __ldg(a.W + i) : 0.f;
+    }
   }
 
   // 1. both = [agg | h_dst] (agg bit-exact: sequential triplet order)
@@ -472,27 +463,62 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
 
   // 4. dt = dl W^T -> dh: the self half to the dst row, the top half scattered
-  //    over the row's edges (dh was zeroed for rows [0, n_src))
+  //    over the row's edges (dh was zeroed for rows [0, n_src)).  A lane owns
+  //    4 consecutive k of [top | bot] and issues one v4 reduction per target.
   if (a.dh != nullptr) {
+    const bool v4 = (d & 3) == 0 && (a.lddh & 3) == 0 && ((uintptr_t)a.dh & 15) == 0;
     for (int i = warp; i < R; i += warps) {
       const int r = r0 + i;
       if (r >= n) continue;
       const float* x = dl + i * C;
       const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-      for (int kb = 0; kb < d; kb += 32) {
-        const int k = kb + lane;
-        if (k >= d) continue;
-        float top = 0.f, bot = 0.f;
-        const float* wt = Ws + k * Cp;
-        const float* wb = Ws + (d + k) * Cp;
-        for (int c = 0; c < C; ++c) {
-          const float xc = x[c];
-          top = fmaf(xc, wt[c], top);
-          bot = fmaf(xc, wb[c], bot);
+      if (v4) {
+        for (int kb = 4 * lane; kb < d2; kb += 128) {
+          float acc[4][2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.f;
+          const float* w0 = Ws + kb * Cp;
+          int c = 0;
+          for (; c + 2 <= C; c += 2) {
+            const float x0 = x[c], x1 = x[c + 1];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[q][0] = fmaf(x0, w0[q * Cp + c], acc[q][0]);
+              acc[q][1] = fmaf(x1, w0[q * Cp + c + 1], acc[q][1]);
+            }
+          }
+          if (c < C) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q][0] = fmaf(x[c], w0[q * Cp + c], acc[q][0]);
+          }
+          const float4 dt = make_float4(acc[0][0] + acc[0][1], acc[1][0] + acc[1][1],
+                                        acc[2][0] + acc[2][1], acc[3][0] + acc[3][1]);
+          if (kb >= d) {  // self half -> the dst row (dst ids lead src ids)
+            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)r * a.lddh + (kb - d)), dt);
+          } else {
+            for (int e = e0; e < e1; ++e) {
+              const float v = __ldg(&a.vals[e]);
+              atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + kb),
+                        make_float4(v * dt.x, v * dt.y, v * dt.z, v * dt.w));
+            }
+          }
         }
-        atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
-        for (int e = e0; e < e1; ++e)
-          atomicAdd(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + k, __ldg(&a.vals[e]) * top);
+      } else {
+        for (int kb = 0; kb < d; kb += 32) {
+          const int k = kb + lane;
+          if (k >= d) continue;
+          float top = 0.f, bot = 0.f;
+          const float* wt = Ws + k * Cp;
+          const float* wb = Ws + (d + k) * Cp;
+          for (int c = 0; c < C; ++c) {
+            const float xc = x[c];
+            top = fmaf(xc, wt[c], top);
+            bot = fmaf(xc, wb[c], bot);
+          }
+          atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
+          for (int e = e0; e < e1; ++e)
+            atomicAdd(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + k, __ldg(&a.vals[e]) * top);
+        }
       }
     }
   }
@@ -527,17 +553,30 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     }
   }
 
-  // 6. fixed-order reduction of the partials after a grid barrier
-  grid_barrier(a.bar);
-  const int total = d2 * C;
-  for (int o = blockIdx.x * kHeadThreads + tid; o < total; o += gridDim.x * kHeadThreads)
-    a.dW[o] = fixed_order_sum(a.part + o, total, (int)gridDim.x);
-  if (blockIdx.x == 0 && tid == 0 && a.ring != nullptr) {
-    const int k = (int)((a.key[2] / (uint32_t)a.world) % (uint32_t)a.ring_len);
-    volatile double* la = a.loss_acc;
-    a.ring[k] = *la;
-    *la = 0.0;
+  // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA
+  //    order (mq_grad_src), so no grid-wide barrier is needed here.  The last
+  //    CTA to finish commits the batch loss to the epoch's loss ring.
+  if (a.ring != nullptr) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
+        __threadfence();
+        const int k = (int)((a.key[2] / (uint32_t)a.world) % (uint32_t)a.ring_len);
+        volatile double* la = a.loss_acc;
+        a.ring[k] = *la;
+        *la = 0.0;
+        *a.done = 0;
+      }
+    }
   }
+}
+
+// dW = fixed-order sum of the head's per-CTA partials (materialising API)
+__global__ void head_dw_reduce_kernel(const float* __restrict__ part, int nparts, int total,
+                                      float* __restrict__ dW) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x)
+    dW[o] = fixed_order_sum(part + o, total, nparts);
 }
 
 inline int head_rows(int n_dst_max) {
@@ -633,17 +672,33 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
   return MQ_OK;
 }
 
+int mq_sage_dw_deferred(int32_t d_out) {
+  return (tc_backend() == 1 && tc_supported(2 * d_out)) ? 1 : 0;
+}
+
+int64_t mq_sage_dw_parts_bytes(int32_t d_in, int32_t d_out) {
+  return tc_dw_part_floats(d_in, d_out) * (int64_t)sizeof(float);
+}
+
 int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
                           int32_t d_in, const float* W, int32_t d_out, const float* g, float* dW,
-                          float* dh, int32_t lddh, void* scratch, void* stream) {
-  MQ_CHECK_ARG(h && m_dev && W && g && dW && scratch, "mq_sage_transform_bwd: null pointer");
+                          float* dh, int32_t lddh, void* scratch, float* dw_parts,
+                          int32_t* dw_nparts_dev, void* stream) {
+  MQ_CHECK_ARG(h && m_dev && W && g && scratch, "mq_sage_transform_bwd: null pointer");
+  MQ_CHECK_ARG((dw_parts == nullptr) == (dw_nparts_dev == nullptr),
+               "mq_sage_transform_bwd: dw_parts and dw_nparts_dev go together");
+  MQ_CHECK_ARG(dW || (dw_parts && mq_sage_dw_deferred(d_out)),
+               "mq_sage_transform_bwd: dW is required unless the weight gradient is deferred");
   MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldh >= d_in && ldh % 4 == 0 && (uintptr_t)h % 16 == 0 &&
                    (!dh || lddh >= d_in),
                "mq_sage_transform_bwd: bad dims / alignment");
   cudaStream_t s = as_stream(stream);
   float* part = reinterpret_cast<float*>(scratch);
   if (tc_backend() == 1 && tc_supported(2 * d_out)) {
-    int rc = tc_weight_grad(h, ldh, m_dev, m_max, d_in, d_out, g, dW, part, s);
+    // deferred: the partial tiles stay in dw_parts for the optimizer to reduce
+    int rc = dw_parts ? tc_weight_grad(h, ldh, m_dev, m_max, d_in, d_out, g, nullptr, dw_parts,
+                                       dw_nparts_dev, s)
+                      : tc_weight_grad(h, ldh, m_dev, m_max, d_in, d_out, g, dW, part, nullptr, s);
     if (rc) return rc;
   } else {
     Dims dims{nullptr, pitch_of(d_in), m_dev, 0, 2 * d_out};
@@ -674,8 +729,8 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                  int32_t lddh, double* loss_acc, const uint32_t* key_dev, int32_t world,
                  double* loss_ring, int32_t ring_len, int32_t* nonfinite, void* scratch,
                  void* stream) {
-  MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && h && W && labels && dW && loss_acc &&
-                   nonfinite && scratch,
+  MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && h && W && labels && loss_acc && nonfinite &&
+                   scratch,
                "mq_sage_head: null pointer");
   MQ_CHECK_ARG(d >= 1 && n_classes >= 1 && ldh >= d && (!dh || lddh >= d),
                "mq_sage_head: bad dims");
@@ -708,7 +763,7 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
   a.dW = dW;
   a.dh = dh;
   a.lddh = lddh;
-  a.bar = reinterpret_cast<int32_t*>(scratch);
+  a.done = reinterpret_cast<int32_t*>(scratch);
   a.part = reinterpret_cast<float*>(reinterpret_cast<char*>(scratch) + 256);
   a.loss_acc = loss_acc;
   a.key = key_dev;
@@ -722,6 +777,43 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
     sage_head_kernel<<<G, kHeadThreads, smem, s>>>(a);
   }
   MQ_LAUNCH_CHECK("sage_head");
+  if (dW != nullptr) {
+    const int total = 2 * d * n_classes;
+    ProfScope ps(K_SAGE_DW_REDUCE, s);
+    head_dw_reduce_kernel<<<ceil_div(total, 256), 256, 0, s>>>(a.part, G, total, dW);
+  }
+  MQ_LAUNCH_CHECK("head_dw_reduce");
+  return MQ_OK;
+}
+
+int mq_sage_head_grad_seg(int32_t n_dst_max, int32_t d, int32_t n_classes, void* scratch,
+                          int64_t offset, mq_grad_seg* out) {
+  MQ_CHECK_ARG(scratch && out && n_dst_max >= 1 && d >= 1 && n_classes >= 1,
+               "mq_sage_head_grad_seg: bad arguments");
+  const int R = head_rows(n_dst_max);
+  memset(out, 0, sizeof(*out));
+  out->part = reinterpret_cast<const float*>(reinterpret_cast<char*>(scratch) + 256);
+  out->nparts = ceil_div(n_dst_max, R);
+  out->stride = 2LL * d * n_classes;
+  out->offset = offset;
+  out->size = 2LL * d * n_classes;
+  out->kind = 0;
+  return MQ_OK;
+}
+
+int mq_sage_dw_grad_seg(float* dw_parts, const int32_t* dw_nparts_dev, int32_t d_in, int32_t d_out,
+                        int64_t offset, mq_grad_seg* out) {
+  MQ_CHECK_ARG(dw_parts && dw_nparts_dev && out && d_in >= 1 && d_out >= 1,
+               "mq_sage_dw_grad_seg: bad arguments");
+  memset(out, 0, sizeof(*out));
+  out->part = dw_parts;
+  out->nparts_dev = dw_nparts_dev;
+  out->stride = (int64_t)d_in * 2 * d_out;
+  out->offset = offset;
+  out->size = 2LL * d_in * d_out;
+  out->kind = 1;
+  out->d_in = d_in;
+  out->d_out = d_out;
   return MQ_OK;
 }
 

@@ -306,7 +306,7 @@ struct Smem {
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(Operands op, const int32_t* m_dev, int m_static, const int32_t* k_dev,
-                   int k_static, float* __restrict__ part) {
+                   int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kStages + 1];
@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int Np = op.Np;
   const Work wk = choose_work(M, K, gridDim.x);
   const int items = wk.tiles_m * wk.S;
+  if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
   if ((int)blockIdx.x >= items || M <= 0) return;
 
   const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
@@ -453,7 +454,8 @@ inline int tc_grid(int m_max, int k_max) {
 template <int MODE, class Epi>
 int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
                 const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
-                cudaStream_t s, int kid, int kid_red) {
+                cudaStream_t s, int kid, int kid_red, bool skip_reduce = false,
+                int32_t* nparts_out = nullptr) {
   const int smem = tc::Smem::total(op.Np);
   static thread_local bool configured[2] = {false, false};
   if (!configured[MODE]) {
@@ -465,9 +467,10 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
   {
     ProfScope ps(kid, s);
     tc::tc_gemm_kernel<MODE><<<grid, tc::kThreads, smem, s>>>(op, m_dev, m_static, k_dev, k_static,
-                                                             part);
+                                                             part, nparts_out);
   }
   MQ_LAUNCH_CHECK("tc_gemm");
+  if (skip_reduce) return MQ_OK;
   int64_t mn = (int64_t)(m_max < 1 ? 1 : m_max) * op.N;
   int rb = ceil_div(mn, 256);
   if (rb > kNumSMs * 4) rb = kNumSMs * 4;
@@ -512,11 +515,16 @@ int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d
 }
 
 int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
-                   int d_out, const float* g, float* dW, float* part, cudaStream_t s) {
+                   int d_out, const float* g, float* dW, float* part, int32_t* nparts_out,
+                   cudaStream_t s) {
   tc::Operands op{h, ldh, d_in, nullptr, d_out, g, 2 * d_out, (2 * d_out + 15) / 16 * 16};
+  // dW == NULL: leave the partial tiles (count -> *nparts_out) for the consumer
   return run_tc_gemm<tc::kDw>(op, nullptr, d_in, d_in, rows_dev, 0, rows_max, part,
-                              EpiDWSplit{dW, d_in, d_out}, s, K_SAGE_DW, K_SAGE_DW_REDUCE);
+                              EpiDWSplit{dW, d_in, d_out}, s, K_SAGE_DW, K_SAGE_DW_REDUCE,
+                              dW == nullptr, nparts_out);
 }
+
+int64_t tc_dw_part_floats(int64_t d_in, int64_t d_out) { return tc_part_floats(d_in, 2 * d_out); }
 
 int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out) {
   int64_t a = tc_part_floats(m_max, 2 * d_out);

@@ -82,9 +82,34 @@ __device__ __forceinline__ void step_arrive(int32_t* step, int t) {
   }
 }
 
-__device__ __forceinline__ float load_grad(const float* g32, const double* g64, double scale,
-                                           double count, int64_t i) {
-  if (g32) return g32[i];
+// Gradient element i through the deferred split-K segments (mqgnn.h).
+struct GradSrc {
+  mq_grad_src s;
+  bool on;
+};
+
+__device__ __forceinline__ float grad_at(const GradSrc& src, const float* g32, int64_t i) {
+  if (src.on) {
+    for (int k = 0; k < src.s.nseg; ++k) {
+      const mq_grad_seg& sg = src.s.seg[k];
+      if (i >= sg.offset && i < sg.offset + sg.size) {
+        int64_t j = i - sg.offset;
+        if (sg.kind == 1) {
+          const int64_t row = j / sg.d_out, col = j % sg.d_out;
+          j = row < sg.d_in ? row * 2 * sg.d_out + col
+                            : (row - sg.d_in) * 2 * sg.d_out + sg.d_out + col;
+        }
+        const int np = sg.nparts_dev ? *sg.nparts_dev : sg.nparts;
+        return fixed_order_sum(sg.part + j, sg.stride, np);
+      }
+    }
+  }
+  return g32[i];
+}
+
+__device__ __forceinline__ float load_grad(const GradSrc& src, const float* g32, const double* g64,
+                                           double scale, double count, int64_t i) {
+  if (g32) return grad_at(src, g32, i);
   return scale != 0.0 ? (float)(g64[i] * scale) : (float)(g64[i] / count);
 }
 
@@ -96,7 +121,7 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
                             const float* __restrict__ g32, const double* __restrict__ g64,
                             double scale, int64_t n, int32_t* __restrict__ step,
                             const float* __restrict__ bias, int bias_len, float lr,
-                            int32_t* __restrict__ nonfinite) {
+                            int32_t* __restrict__ nonfinite, GradSrc src) {
   const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
   if (t < 1 || t > bias_len) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
@@ -110,7 +135,7 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float g = load_grad(g32, g64, scale, count, i);
+    const float g = load_grad(src, g32, g64, scale, count, i);
     float mi = __fmul_rn(m[i], b1);                         // m *= beta1
     mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
     float vi = __fmul_rn(v[i], b2);                         // v *= beta2
@@ -130,13 +155,14 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
                            const double* __restrict__ g64, double scale, int64_t n, float lr,
-                           int32_t* __restrict__ step, int32_t* __restrict__ nonfinite) {
+                           int32_t* __restrict__ step, int32_t* __restrict__ nonfinite,
+                           GradSrc src) {
   const int t = step[0] + 1;
   const double count = grad_count(g64, scale, n);
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float wi = __fsub_rn(w[i], __fmul_rn(lr, load_grad(g32, g64, scale, count, i)));
+    const float wi = __fsub_rn(w[i], __fmul_rn(lr, load_grad(src, g32, g64, scale, count, i)));
     w[i] = wi;
     bad |= !finite_f(wi);
   }
@@ -151,10 +177,18 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restric
 }
 
 __global__ void pack_grads_kernel(const float* __restrict__ a, int64_t n,
-                                  const int32_t* __restrict__ n_targets, double* __restrict__ b) {
+                                  const int32_t* __restrict__ n_targets, double* __restrict__ b,
+                                  GradSrc src) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = i < n ? (double)a[i] : (n_targets[0] > 0 ? 1.0 : 0.0);
+    b[i] = i < n ? (double)grad_at(src, a, i) : (n_targets[0] > 0 ? 1.0 : 0.0);
+}
+
+__global__ void grad_reduce_kernel(GradSrc src, const float* __restrict__ a, int64_t n,
+                                   float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = grad_at(src, a, i);
 }
 
 __global__ void f64_to_f32_kernel(const double* __restrict__ a, double divisor,
@@ -162,6 +196,28 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ a, double divisor,
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (float)(a[i] / divisor);
+}
+
+inline GradSrc make_src(const mq_grad_src* src) {
+  GradSrc g;
+  memset(&g, 0, sizeof(g));
+  if (src != nullptr && src->nseg > 0) {
+    g.s = *src;
+    g.on = true;
+  }
+  return g;
+}
+
+inline bool src_ok(const mq_grad_src* src) {
+  if (src == nullptr) return true;
+  if (src->nseg < 0 || src->nseg > MQ_GRAD_MAX_SEG) return false;
+  for (int k = 0; k < src->nseg; ++k) {
+    const mq_grad_seg& sg = src->seg[k];
+    if (!sg.part || sg.size < 0 || sg.offset < 0 || (!sg.nparts_dev && sg.nparts < 0)) return false;
+    if (sg.kind == 1 && (sg.d_in < 1 || sg.d_out < 1 || sg.size != 2LL * sg.d_in * sg.d_out))
+      return false;
+  }
+  return true;
 }
 
 inline int elem_blocks(int64_t n) {
@@ -196,28 +252,30 @@ int mq_softmax_ce(const float* logits, int32_t ld, const int32_t* labels, const 
 
 int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
             double grad_scale, int64_t n, int32_t* step_dev, const float* bias, int32_t bias_len,
-            float lr, int32_t* nonfinite, void* stream) {
+            float lr, int32_t* nonfinite, const mq_grad_src* src, void* stream) {
   MQ_CHECK_ARG(w && m && v && step_dev && bias && nonfinite, "mq_adam: null pointer");
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_adam: exactly one gradient source");
+  MQ_CHECK_ARG(src_ok(src), "mq_adam: bad deferred gradient source");
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_ADAM, s);
     adam_kernel<<<elem_blocks(n), 256, 0, s>>>(w, m, v, grad32, grad64, grad_scale, n, step_dev,
-                                               bias, bias_len, lr, nonfinite);
+                                               bias, bias_len, lr, nonfinite, make_src(src));
   }
   MQ_LAUNCH_CHECK("adam");
   return MQ_OK;
 }
 
 int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale, int64_t n,
-           int32_t* step_dev, float lr, int32_t* nonfinite, void* stream) {
+           int32_t* step_dev, float lr, int32_t* nonfinite, const mq_grad_src* src, void* stream) {
   MQ_CHECK_ARG(w && step_dev && nonfinite, "mq_sgd: null pointer");
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_sgd: exactly one gradient source");
+  MQ_CHECK_ARG(src_ok(src), "mq_sgd: bad deferred gradient source");
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_SGD, s);
     sgd_kernel<<<elem_blocks(n), 256, 0, s>>>(w, grad32, grad64, grad_scale, n, lr, step_dev,
-                                              nonfinite);
+                                              nonfinite, make_src(src));
   }
   MQ_LAUNCH_CHECK("sgd");
   return MQ_OK;
@@ -249,14 +307,29 @@ int mq_f32_to_f64(const float* in32, double* out64, int64_t n, void* stream) {
 }
 
 int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, double* out64,
-                  void* stream) {
+                  const mq_grad_src* src, void* stream) {
   MQ_CHECK_ARG(grad && n_targets_dev && out64, "mq_pack_grads: null pointer");
+  MQ_CHECK_ARG(src_ok(src), "mq_pack_grads: bad gradient source");
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_CONVERT, s);
-    pack_grads_kernel<<<elem_blocks(n + 1), 256, 0, s>>>(grad, n, n_targets_dev, out64);
+    pack_grads_kernel<<<elem_blocks(n + 1), 256, 0, s>>>(grad, n, n_targets_dev, out64,
+                                                         make_src(src));
   }
   MQ_LAUNCH_CHECK("pack_grads");
+  return MQ_OK;
+}
+
+int mq_grad_reduce(const mq_grad_src* src, const float* grad32, int64_t n, float* out32,
+                   void* stream) {
+  MQ_CHECK_ARG(grad32 && out32 && src_ok(src), "mq_grad_reduce: bad arguments");
+  if (n <= 0) return MQ_OK;
+  cudaStream_t s = as_stream(stream);
+  {
+    ProfScope ps(K_CONVERT, s);
+    grad_reduce_kernel<<<elem_blocks(n), 256, 0, s>>>(make_src(src), grad32, n, out32);
+  }
+  MQ_LAUNCH_CHECK("grad_reduce");
   return MQ_OK;
 }
 

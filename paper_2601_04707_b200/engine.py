@@ -15,12 +15,13 @@ Layer l (bottom-up) consumes hop L-1-l.
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-from ._lib import lib, ptr
+from ._lib import GradSrc, lib, ptr
 from .graph import DeviceGraph, round_up
 
 
@@ -302,16 +303,21 @@ class TrainWorkspace:
                 dz, lddz = self.dh[l], self.ld_in[l]
 
     @staticmethod
-    def launch_optimizer(model: DeviceModel, optimizer: str, stream, grad64=None, scale=1.0):
+    def launch_optimizer(model: DeviceModel, optimizer: str, stream, grad64=None, scale=1.0,
+                         src=None):
+        """apply_update (racom.py:81-87): the gradient is model.flat_g resolved
+        through the deferred split-K segments ``src`` (a _lib.GradSrc), or the
+        all-reduced f64 window sum ``grad64``."""
         g32 = None if grad64 is not None else ptr(model.flat_g)
         g64 = ptr(grad64) if grad64 is not None else None
+        psrc = C.byref(src) if (src is not None and grad64 is None) else None
         if optimizer == "adam":
             lib().mq_adam(ptr(model.flat_w), ptr(model.flat_m), ptr(model.flat_v), g32, g64, scale,
                           model.num_params, ptr(model.step_dev), ptr(model.bias), model.bias_len,
-                          model.lr32, ptr(model.nonfinite), stream)
+                          model.lr32, ptr(model.nonfinite), psrc, stream)
         elif optimizer == "sgd":
             lib().mq_sgd(ptr(model.flat_w), g32, g64, scale, model.num_params,
-                         ptr(model.step_dev), model.lr32, ptr(model.nonfinite), stream)
+                         ptr(model.step_dev), model.lr32, ptr(model.nonfinite), psrc, stream)
         else:
             raise ValueError(f"unknown optimizer {optimizer!r}")
 
@@ -358,14 +364,61 @@ class FusedTrainWorkspace:
             self.dh[L - 1] = torch.zeros((max(b0.n_src_max, 1), self.ld_in[L - 1]), **f32)
         self.scratch = torch.zeros(scr // 4 + 1, **f32)
         hb = int(lib().mq_sage_head_scratch_bytes(sw.batch_size, self.dims[L - 1], num_classes))
-        self.head_scratch = torch.zeros(hb // 4 + 1, **f32)  # zeroed once: grid barrier state
+        self.head_scratch = torch.zeros(hb // 4 + 1, **f32)  # zeroed once: completion counter
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        # deferred weight gradients: per-layer split-K partials, reduced by the
+        # optimizer (mq_grad_src) instead of a reduction launch per layer
+        self.dw_parts = [None] * L
+        self.dw_nparts = torch.zeros(max(L, 1), dtype=torch.int32, device=dev)
+        self._src_key = None
+        self._src = None
+
+    def grad_src(self, model: DeviceModel):
+        """The _lib.GradSrc describing where each layer's gradient lives this
+        step (head partials, deferred tcgen05 partials, or model.flat_g)."""
+        key = tuple(int(lib().mq_sage_dw_deferred(self.dims[l + 1])) for l in range(self.L - 1))
+        if key == self._src_key and self._src is not None:
+            return self._src
+        src = GradSrc()
+        segs = []
+        L = self.L
+        seg = GradSrc().seg[0]
+        lib().mq_sage_head_grad_seg(self.sw.batch_size, self.dims[L - 1], self.C,
+                                    ptr(self.head_scratch), model.offsets[L - 1], C.byref(seg))
+        segs.append(seg)
+        for l in range(L - 1):
+            if key[l]:
+                if self.dw_parts[l] is None:
+                    nb = int(lib().mq_sage_dw_parts_bytes(self.dims[l], self.dims[l + 1]))
+                    self.dw_parts[l] = torch.zeros(nb // 4 + 1, dtype=torch.float32,
+                                                   device=self.sw.graph.device)
+                s2 = GradSrc().seg[0]
+                lib().mq_sage_dw_grad_seg(ptr(self.dw_parts[l]), ptr(self.dw_nparts[l:l + 1]),
+                                          self.dims[l], self.dims[l + 1], model.offsets[l],
+                                          C.byref(s2))
+                segs.append(s2)
+        src.nseg = len(segs)
+        for i, sg in enumerate(segs):
+            src.seg[i] = sg
+        self._src_key, self._src = key, src
+        return src
+
+    def materialize_grads(self, model: DeviceModel, stream):
+        """Resolve the deferred gradient into model.flat_g (tests, eager API)."""
+        src = self.grad_src(model)
+        tmp = torch.empty_like(model.flat_g)
+        lib().mq_grad_reduce(C.byref(src), ptr(model.flat_g), model.num_params, ptr(tmp), stream)
+        model.flat_g.copy_(tmp)
 
     def h_in(self, l, sw):
         return sw.x0 if l == 0 else self.act[l]
 
     launch_gather = staticmethod(TrainWorkspace.launch_gather)
-    launch_optimizer = staticmethod(TrainWorkspace.launch_optimizer)
+
+    def launch_optimizer(self, model: DeviceModel, optimizer: str, stream, grad64=None,
+                         scale=1.0):
+        TrainWorkspace.launch_optimizer(model, optimizer, stream, grad64=grad64, scale=scale,
+                                        src=self.grad_src(model))
 
     def launch_train(self, model: DeviceModel, stream, sw, ring=None, ring_len=0, world=1):
         """Forward, loss and backward of one batch; gradients land in
@@ -374,6 +427,7 @@ class FusedTrainWorkspace:
         ``self.loss``."""
         L, d, ld = self.L, self.dims, self.ld_in
         lb = lib()
+        self.grad_src(model)  # allocate the deferred partial buffers before capture
         for l in range(L - 1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
@@ -388,7 +442,7 @@ class FusedTrainWorkspace:
         hb0 = sw.hops[0]
         lb.mq_sage_head(ptr(hb0.row_ptr), ptr(hb0.cols), ptr(hb0.vals), ptr(sw.n_targets),
                         sw.batch_size, ptr(self.h_in(L - 1, sw)), ld[L - 1], d[L - 1],
-                        ptr(model.weight(L - 1)), self.C, ptr(sw.labels), ptr(model.grad(L - 1)),
+                        ptr(model.weight(L - 1)), self.C, ptr(sw.labels), None,
                         ptr(self.dh[L - 1]), ld[L - 1], ptr(self.loss), ptr(sw.key), world,
                         ptr(ring), ring_len, ptr(model.nonfinite), ptr(self.head_scratch), stream)
         for l in range(L - 2, -1, -1):
@@ -398,10 +452,13 @@ class FusedTrainWorkspace:
                                    ptr(sw.n_dst_dev(h)), b.n_dst_max, ptr(self.dh[l + 1]),
                                    ld[l + 1], ptr(self.act[l + 1]), ld[l + 1], d[l + 1],
                                    ptr(self.G[l]), stream)
+            dp = self.dw_parts[l]
             lb.mq_sage_transform_bwd(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts), b.n_src_max,
                                      d[l], ptr(model.weight(l)), d[l + 1], ptr(self.G[l]),
                                      ptr(model.grad(l)), ptr(self.dh[l]), ld[l],
-                                     ptr(self.scratch), stream)
+                                     ptr(self.scratch), ptr(dp),
+                                     ptr(self.dw_nparts[l:l + 1]) if dp is not None else None,
+                                     stream)
 
 
 def current_stream(device) -> int:

@@ -238,7 +238,7 @@ def adam_step(state: ModelState, grads: list) -> ModelState:
     d.ensure_bias(d.host_steps + 1)
     lib().mq_adam(ptr(d.flat_w), ptr(d.flat_m), ptr(d.flat_v), ptr(d.flat_g), None, 1.0,
                   d.num_params, ptr(d.step_dev), ptr(d.bias), d.bias_len, d.lr32,
-                  ptr(d.nonfinite), current_stream(d.device))
+                  ptr(d.nonfinite), None, current_stream(d.device))
     d.host_steps += 1
     _check(state, "adam_step")
     return state
@@ -248,7 +248,7 @@ def sgd_step(state: ModelState, grads: list) -> ModelState:
     _flat_grad(state, grads)
     d = state.dev
     lib().mq_sgd(ptr(d.flat_w), ptr(d.flat_g), None, 1.0, d.num_params, ptr(d.step_dev), d.lr32,
-                 ptr(d.nonfinite), current_stream(d.device))
+                 ptr(d.nonfinite), None, current_stream(d.device))
     d.host_steps += 1
     _check(state, "sgd_step")
     return state

@@ -20,6 +20,8 @@ count] (NCCL in production, gloo / in-process in tests) -> update graph.
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -132,8 +134,9 @@ class StepRunner:
                                      ptr(self.loss_ring), self.ring_len, s)
             self.tw.launch_backward(self.dm, s, sw)
         if self.grad64 is not None:
+            src = self.tw.grad_src(self.dm) if self.fused else None
             lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(sw.n_targets),
-                                ptr(self.grad64), s)
+                                ptr(self.grad64), C.byref(src) if src is not None else None, s)
 
     def _enqueue_update(self, s):
         if self.grad64 is None:

@@ -51,6 +51,7 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
         with torch.cuda.stream(s):
             runner._enqueue_prep(runner.slots[0], s.cuda_stream)
             runner._enqueue_train(runner.slots[0], s.cuda_stream, commit=False)
+            runner.tw.materialize_grads(state.dev, s.cuda_stream)
         torch.cuda.synchronize()
         loss = float(runner.tw.loss.item())
         runner.tw.loss.zero_()

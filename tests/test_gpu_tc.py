@@ -71,7 +71,7 @@ def test_transform_fwd_bwd(backend, rows, d_in, d_out):
                             ptr(scr), s)
     y = ty.cpu().numpy()[:rows]
     lib().mq_sage_transform_bwd(ptr(th), ld, ptr(m_dev), m_max, d_in, ptr(tW), d_out, ptr(tg),
-                                ptr(tdW), ptr(tdh), ld, ptr(scr), s)
+                                ptr(tdW), ptr(tdh), ld, ptr(scr), None, None, s)
     torch.cuda.synchronize()
     h64 = h[:rows, :d_in].astype(np.float64)
     W64 = W.astype(np.float64)
@@ -116,7 +116,7 @@ def test_transform_bwd_deterministic(rows, d_in, d_out):
     for _ in range(3):
         dW = torch.zeros_like(W)
         lib().mq_sage_transform_bwd(ptr(h), ld, ptr(m_dev), rows, d_in, ptr(W), d_out, ptr(g),
-                                    ptr(dW), None, ld, ptr(scr),
+                                    ptr(dW), None, ld, ptr(scr), None, None,
                                     torch.cuda.current_stream().cuda_stream)
         outs.append(dW.cpu())
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
