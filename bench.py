@@ -66,7 +66,8 @@ def parse():
     ap.add_argument("--feature-placement", default="hbm", choices=["hbm", "host"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--profile-steps", type=int, default=20)
+    ap.add_argument("--profile-steps", type=int, default=20,
+                    help="launches per op in the per-kernel graph timing (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
@@ -271,7 +272,6 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     import paper_2601_04707_b200 as mq
     from paper_2601_04707_b200._lib import lib
-    from paper_2601_04707_b200.roofline import step_flops, step_models
     from paper_2601_04707_b200.runtime import epoch_permutation
 
     setup = {}
@@ -349,53 +349,24 @@ def run_ours(args):
     runner.check_finite()
     value = seeds_done[0] / (ms_max / 1e3)
 
-    # -------- per-kernel profile (eager, instrumented, same workload) --------
+    # -------- per-kernel profile: each op replayed in a CUDA graph, warm --------
     per_kernel = {}
     n_kernels = runner.kernels_per_step()
-    if rank == 0:
-        L = lib()
-        L.mq_prof_reset()
-        L.mq_prof_enable(1)
-        bytes_acc: dict = {}
-        flops_acc: dict = {}
-        prof_ev0 = torch.cuda.Event(enable_timing=True)
-        prof_ev1 = torch.cuda.Event(enable_timing=True)
-        dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
-        prof_step_ms = []
-        for _ in range(args.profile_steps):
-            if runner.windows_done >= windows:
-                epoch[0] += 1
-                runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
-            prof_ev0.record(runner.stream)
-            runner.eager_window()
-            prof_ev1.record(runner.stream)
-            c = runner.read_counts()
-            prof_step_ms.append(prof_ev0.elapsed_time(prof_ev1))
-            for name, lst in step_models(c, dims, fanouts, True, runner.dm.num_params,
-                                         g.num_classes).items():
-                bytes_acc[name] = bytes_acc.get(name, 0.0) + sum(lst)
-            for name, f in step_flops(c, dims, fanouts).items():
-                flops_acc[name] = flops_acc.get(name, 0.0) + f
-        L.mq_prof_enable(0)
-        nk = L.mq_prof_num_kernels()
-        tot = np.zeros(nk, dtype=np.float64)
-        cnt = np.zeros(nk, dtype=np.int64)
-        L.mq_prof_read(tot.ctypes.data, cnt.ctypes.data, nk)
-        all_ms = float(tot.sum())
-        for i in range(nk):
-            if cnt[i] == 0:
-                continue
-            name = L.mq_prof_kernel_name(i).decode()
-            b = bytes_acc.get(name)
-            per_kernel[name] = {
-                "ms_per_step": tot[i] / args.profile_steps,
-                "launches_per_step": cnt[i] / args.profile_steps,
-                "share": tot[i] / all_ms,
-                "avg_launch_us": tot[i] / cnt[i] * 1e3,
-                "gbps": (b / (tot[i] / 1e3) / 1e9) if b else None,
-                "bytes_per_launch": (b / cnt[i]) if b else None,
-                "tflops": (flops_acc[name] / (tot[i] / 1e3) / 1e12) if name in flops_acc else None,
+    if rank == 0 and args.profile_steps > 0:
+        from paper_2601_04707_b200.profiling import op_table
+        tab = op_table(runner, reps=args.profile_steps)
+        Q = runner.Q
+        per_step = {nm: rec["us"] * (1.0 / Q if nm.startswith("prep_") else 1.0)
+                    for nm, rec in tab["ops"].items()}
+        tot = sum(per_step.values())
+        for nm, rec in tab["ops"].items():
+            per_kernel[nm] = {
+                "avg_launch_us": rec["us"], "us_per_step": per_step[nm],
+                "share": per_step[nm] / tot, "units": rec.get("units"),
+                "bytes_per_launch": rec.get("bytes"), "gbps": rec.get("gbps"),
+                "flops_per_launch": rec.get("flops"), "tflops": rec.get("tflops"),
             }
+        per_kernel["_counts"] = tab["counts"]
     # ----------------------------- e2e through the host-buffer entry point ---
     e2e = None
     if world == 1:
@@ -435,28 +406,34 @@ def run_ours(args):
 
     if rank == 0:
         hbm, peak_kind = measured_peaks()
-        sample_like = {k: v for k, v in per_kernel.items()}
-        dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms_per_step"]) if per_kernel else None
+        kern = {k: v for k, v in per_kernel.items() if not k.startswith("_")}
+        dom = max(kern.items(), key=lambda kv: kv[1]["us_per_step"]) if kern else None
         traffic = traffic_table()
         roof = None
         if dom:
             name, kd = dom
             achieved = kd["gbps"]
-            t = traffic.get(name)
             roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm,
                     "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
-                    "traffic": t, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                    "traffic": traffic.get(name), "peak_source":
+                        f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                     "algorithmic_bytes_per_launch": kd["bytes_per_launch"],
-                    "avg_launch_us": kd["avg_launch_us"], "share_of_step": kd["share"]}
+                    "avg_launch_us": kd["avg_launch_us"], "share_of_step": kd["share"],
+                    "timing": "CUDA-event time of the op replayed 20x in a CUDA graph "
+                              "(warm, same buffers as the step)"}
+            if kd.get("tflops"):
+                roof["tflops_fp32_equiv"] = kd["tflops"]
         focus = {}
-        for nm in ("sample_hop", "gather", "spmm_fwd", "spmm_bwd_scatter", "linear_fwd",
-                   "linear_bwd_w", "residency_compact"):
-            if nm in sample_like:
-                focus[nm] = {"gbps": sample_like[nm]["gbps"],
-                             "frac_hbm": (sample_like[nm]["gbps"] / hbm
-                                          if sample_like[nm]["gbps"] else None),
-                             "share": sample_like[nm]["share"],
-                             "avg_launch_us": sample_like[nm]["avg_launch_us"]}
+        for nm in ("prep_sample", "prep_relabel", "prep_gather", "sage_aggregate_l0",
+                   "sage_head", "sage_transform_l0", "sage_transform_bwd_l0",
+                   "sage_scatter_bwd_l0", "optimizer"):
+            if nm in kern:
+                k = kern[nm]
+                focus[nm] = {"gbps": k["gbps"], "frac_hbm": (k["gbps"] / hbm if k["gbps"] else None),
+                             "avg_launch_us": k["avg_launch_us"], "share": k["share"],
+                             "units": k["units"]}
+                if k.get("tflops"):
+                    focus[nm]["tflops_fp32_equiv"] = k["tflops"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -474,7 +451,7 @@ def run_ours(args):
             "epoch_ms": ms_max / args.steps * windows, "windows_per_epoch": windows,
             "roofline": roof, "kernels": focus,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": n_kernels * args.steps, "kernels_per_step": n_kernels,
+            "gpu_launches": int(round(n_kernels * args.steps)), "kernels_per_step": n_kernels,
             "wall_s_timed": t_wall, "setup": setup,
         }
         print(json.dumps(line), flush=True)

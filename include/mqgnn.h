@@ -146,6 +146,53 @@ int mq_relabel(const int32_t* dst, const int32_t* n_dst_dev, int32_t n_dst_max,
                float* vals, int32_t* src_ids, int32_t* counts_dev, void* scratch,
                void* stream);
 
+/* ------------------------------------------------ multi-queue preparation
+ * The MQ-GNN batch queue (runtime.py:380-612, pipeline.py:109-167) as ONE
+ * pass of batched kernels over Q device slots: per slot exactly
+ * mq_batch_setup (when cursor != NULL; else the host staged targets /
+ * n_targets / key) -> [mq_sample_hop -> mq_relabel] per hop -> mq_gather +
+ * mq_gather_labels, bit-identical to the single-batch entry points.  Every
+ * per-slot array is given as slot 0's pointer plus a stride (elements) to the
+ * next slot.  dpos / first are node-indexed tables per slot (stride
+ * table_s) holding -1 / INT32_MAX on entry, restored on exit; scratch holds
+ * Q regions of mq_prep_scratch_bytes(max n_dst_max, its fanout) each
+ * (scratch_s bytes apart).  When cursor != NULL, cursor[0] (window) advances
+ * by Q and cursor[1] must be 0 at rest. */
+#define MQ_MAX_HOPS 4
+typedef struct mq_prep_hop {
+  int32_t fanout, n_dst_max, n_src_max, pad_;
+  int32_t* nbr;     int64_t nbr_s;      /* n_dst_max * fanout */
+  int32_t* cnt;     int64_t cnt_s;      /* n_dst_max */
+  int32_t* row_ptr; int64_t row_ptr_s;  /* n_dst_max + 1 */
+  int32_t* rows;    int32_t* cols;  float* vals;  int64_t edge_s;  /* n_dst_max * fanout */
+  int32_t* src_ids; int64_t src_s;      /* n_src_max */
+  int32_t* counts;  int64_t counts_s;   /* [n_src, nnz] */
+} mq_prep_hop;
+typedef struct mq_prep_desc {
+  int32_t nslots, num_hops, batch_size, world, rank, d;
+  const int32_t* perm; int64_t n_perm; int32_t* cursor;
+  int32_t* targets;   int64_t targets_s;
+  int32_t* n_targets; int64_t n_targets_s;
+  uint32_t* key;      int64_t key_s;      /* {seed mod 2^32, epoch, batch} per slot */
+  mq_prep_hop hop[MQ_MAX_HOPS];
+  int32_t* dpos; int32_t* first; int64_t table_s;
+  void* scratch; int64_t scratch_s;
+  const int64_t* row_off; const int32_t* col; const int64_t* hot_arc; const int64_t* hot_off;
+  const float* cache_tbl; int32_t cache_pitch, store_pitch;
+  const int32_t* slot_of; const float* store;
+  float* x0; int64_t x0_s; int32_t x0_pitch;
+  uint32_t stage_mask;  /* 0 = all; else bits MQ_PREP_* select stages (profiling) */
+  unsigned long long* hit_miss;
+  const int32_t* all_labels; int32_t* labels; int64_t labels_s;
+} mq_prep_desc;
+#define MQ_PREP_SETUP 1u
+#define MQ_PREP_SAMPLE 2u
+#define MQ_PREP_RELABEL 4u
+#define MQ_PREP_GATHER 8u
+#define MQ_PREP_LABELS 16u
+int64_t mq_prep_scratch_bytes(int32_t n_dst_max, int32_t fanout);
+int mq_prep_batches(const mq_prep_desc* desc, void* stream);
+
 /* --------------------------------------------------------------- gather
  * gather_features / lookup (cache.py:111-134, runtime.py:127-143):
  *   out[i, :d] = slot_of[id] >= 0 ? cache_tbl[slot_of[id]] : store[id]
@@ -207,16 +254,25 @@ int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t 
  *   W (2*d_in x d_out) as in the reference.  m = *m_dev (<= m_max).
  * scratch for transform / transform_bwd: mq_sage_fused_scratch_bytes. */
 int64_t mq_sage_fused_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out);
+/* Deferred output: when y_parts != NULL (requires mq_sage_y_deferred(d_out)),
+ * the tensor-core split-K partial tiles part[s][m][2 d_out] (s < *y_nparts_dev,
+ * m < *m_dev) are left in y_parts (mq_sage_y_parts_bytes) and y is not
+ * written; mq_sage_aggregate then sums them on the fly. */
+int mq_sage_y_deferred(int32_t d_out);
+int64_t mq_sage_y_parts_bytes(int32_t m_max, int32_t d_out);
 int mq_sage_transform(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
                       int32_t d_in, const float* W, int32_t d_out, float* y, void* scratch,
-                      void* stream);
+                      float* y_parts, int32_t* y_nparts_dev, void* stream);
 /* act[r, :d_out] = relu(sum_e val_e y[col_e, :d_out] + y[r, d_out:2 d_out]) for
  * r < *n_dst_dev (pad columns up to ldact zeroed); then zero the rows
  * [0, *zeroK_rows_dev) x zeroK_row_floats of zero0 / zero1 (either may be NULL)
- * — the backward's scatter targets, cleared here so they cost no launch. */
+ * — the backward's scatter targets, cleared here so they cost no launch.
+ * With y_nparts_dev != NULL, y holds mq_sage_transform's deferred partials
+ * (y_rows_dev = their m) and is reduced in fixed order on the fly. */
 int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                       const int32_t* n_dst_dev, int32_t n_dst_max, const float* y, int32_t d_out,
-                      float* act, int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
+                      const int32_t* y_nparts_dev, const int32_t* y_rows_dev, float* act,
+                      int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
                       int32_t zero0_row_floats, float* zero1, const int32_t* zero1_rows_dev,
                       int32_t zero1_row_floats, void* stream);
 /* Backward of the aggregation (nn.py:167, 171-174 re-associated):
@@ -242,6 +298,8 @@ int mq_sage_dw_grad_seg(float* dw_parts, const int32_t* dw_nparts_dev, int32_t d
 /* The last layer in one launch: agg = block_apply(h) for the *n_dst_dev target
  * rows (sequential triplet order, nn.py:79-89), logits = [agg | h_dst] W,
  * summed softmax-CE (loss_acc += loss; nonfinite |= 1 on NaN/Inf, nn.py:141-156),
+ * Rows must carry <= MQ_MAX_FANOUT triplets (true of every sampled block;
+ * otherwise nonfinite |= 4).
  * dlogits -> per-CTA dW partials in scratch (reduced in fixed CTA order into dW
  * when dW != NULL, else left for the optimizer: mq_sage_head_grad_seg) and,
  * if dh != NULL, dh += block_apply_t(dt[:, :d]) + self half (nn.py:167-174;

@@ -68,8 +68,11 @@ SIGNATURES = {
     "mq_f64_to_f32": (C.c_int, [P, F64, P, I64, P]),
     "mq_scan_i32": (C.c_int, [P, P, I32, P, P, P]),
     "mq_sage_fused_scratch_bytes": (I64, [I32, I32, I32]),
-    "mq_sage_transform": (C.c_int, [P, I32, P, I32, I32, P, I32, P, P, P]),
-    "mq_sage_aggregate": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, P, P, I32, P, P, I32, P]),
+    "mq_sage_y_deferred": (C.c_int, [I32]),
+    "mq_sage_y_parts_bytes": (I64, [I32, I32]),
+    "mq_sage_transform": (C.c_int, [P, I32, P, I32, I32, P, I32, P, P, P, P, P]),
+    "mq_sage_aggregate": (C.c_int, [P, P, P, P, I32, P, I32, P, P, P, I32, P, P, I32, P, P, I32,
+                                    P]),
     "mq_sage_scatter_bwd": (C.c_int, [P, P, P, P, I32, P, I32, P, I32, I32, P, P]),
     "mq_sage_dw_deferred": (C.c_int, [I32]),
     "mq_sage_dw_parts_bytes": (I64, [I32, I32]),
@@ -81,6 +84,8 @@ SIGNATURES = {
                                I32, P, P, P]),
     "mq_set_gemm_backend": (C.c_int, [I32]),
     "mq_get_gemm_backend": (C.c_int, []),
+    "mq_prep_scratch_bytes": (I64, [I32, I32]),
+    "mq_prep_batches": (C.c_int, [P, P]),
     "mq_prof_enable": (C.c_int, [C.c_int]),
     "mq_prof_reset": (C.c_int, []),
     "mq_prof_num_kernels": (C.c_int, []),
@@ -92,7 +97,8 @@ SIGNATURES = {
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
                if res is C.c_int and name not in ("mq_version", "mq_prof_num_kernels",
                                                        "mq_get_gemm_backend",
-                                                       "mq_sage_dw_deferred")}
+                                                       "mq_sage_dw_deferred",
+                                                       "mq_sage_y_deferred")}
 
 
 class MQError(RuntimeError):

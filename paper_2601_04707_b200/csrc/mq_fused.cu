@@ -36,7 +36,8 @@ namespace mq {
 int tc_backend();
 bool tc_supported(int n_out);
 int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d_in, const float* W,
-                 int d_out, float* y, float* part, cudaStream_t s);
+                 int d_out, float* y, float* part, int32_t* nparts_out, cudaStream_t s);
+int64_t tc_y_part_floats(int64_t m_max, int64_t d_out);
 int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
                    int d_out, const float* g, float* dW, float* part, int32_t* nparts_out,
                    cudaStream_t s);
@@ -254,6 +255,98 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_kernel(
   zero_range(z1, tid, nth);
 }
 
+// Same as sage_aggregate_kernel but Y arrives as the split-K partial tiles of
+// the tensor-core transform (part[s][m][2N], s < *nparts, m < *m_dev): the
+// reduction over s happens on the fly in fixed order, so the transform needs
+// no separate reduction pass.  (float2 columns: N even.)
+__global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
+    const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
+    const float* __restrict__ part, const int32_t* __restrict__ nparts_dev,
+    const int32_t* __restrict__ m_dev, int N, float* __restrict__ act, int ldact, ZeroRange z0,
+    ZeroRange z1) {
+  constexpr int U = 4, SU = 4;
+  const int lane = threadIdx.x & 31;
+  const int warps = kAggThreads / 32;
+  const int n = *n_dst_dev;
+  const int S = *nparts_dev;
+  const int ldy = 2 * N;
+  const int64_t stride = (int64_t)(*m_dev) * ldy;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
+    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    float* out = act + (int64_t)r * ldact;
+    for (int cb = 0; cb < ldact; cb += 64) {
+      const int c = cb + 2 * lane;
+      const bool active = c < N;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int eb = e0; eb < e1; eb += 32) {
+        const int me = eb + lane;
+        int32_t my_col = 0;
+        float my_val = 0.f;
+        if (me < e1) {
+          my_col = __ldg(&cols[me]);
+          my_val = __ldg(&vals[me]);
+        }
+        const int m = min(32, e1 - eb);
+        for (int t0 = 0; t0 < m; t0 += U) {
+          int32_t col[U];
+          float val[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            col[u] = __shfl_sync(0xffffffffu, my_col, (t0 + u) & 31);
+            val[u] = __shfl_sync(0xffffffffu, my_val, (t0 + u) & 31);
+          }
+          float2 x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) x[u] = make_float2(0.f, 0.f);
+          for (int s0 = 0; s0 < S; s0 += SU) {
+            float2 ld[SU][U];
+#pragma unroll
+            for (int ss = 0; ss < SU; ++ss)
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                ld[ss][u] = (active && s0 + ss < S && t0 + u < m)
+                                ? __ldcg(reinterpret_cast<const float2*>(
+                                      part + (s0 + ss) * stride + (int64_t)col[u] * ldy + c))
+                                : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int ss = 0; ss < SU; ++ss)
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                x[u].x += ld[ss][u].x;
+                x[u].y += ld[ss][u].y;
+              }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (t0 + u < m) {
+              acc.x = fmaf(val[u], x[u].x, acc.x);
+              acc.y = fmaf(val[u], x[u].y, acc.y);
+            }
+          }
+        }
+      }
+      if (active) {
+        float2 b = make_float2(0.f, 0.f);
+        for (int s = 0; s < S; ++s) {
+          const float2 p = __ldcg(reinterpret_cast<const float2*>(part + s * stride +
+                                                                  (int64_t)r * ldy + N + c));
+          b.x += p.x;
+          b.y += p.y;
+        }
+        const float zx = acc.x + b.x, zy = acc.y + b.y;
+        *reinterpret_cast<float2*>(out + c) = make_float2(zx > 0.f ? zx : 0.f, zy > 0.f ? zy : 0.f);
+      } else if (c < ldact) {
+        *reinterpret_cast<float2*>(out + c) = make_float2(0.f, 0.f);
+      }
+    }
+  }
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  zero_range(z0, tid, nth);
+  zero_range(z1, tid, nth);
+}
+
 // ------------------------------------------------------------ scatter bwd
 // dz = dh[r] * (act[r] > 0);  G[r, N:2N] = dz;  G[col_e, 0:N] += val_e dz
 // (G zeroed beforehand for rows [0, n_src)).
@@ -323,23 +416,51 @@ struct HeadArgs {
   int R;
 };
 
-constexpr int kHeadThreads = 256;
-constexpr int kHeadRowQuant = 16;  // R is a multiple of this (phase-2 row groups)
+constexpr int kHeadRows = 16;              // target rows per CTA: one warp per row
+constexpr int kHeadThreads = 32 * kHeadRows;
+constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp, R = a.R;
+  constexpr int R = kHeadRows;
+  const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp;
   float* Ws = smem;                 // [d2p][Cp]  (rows >= d2 zero)
   float* both = Ws + d2p * Cp;      // [R][d2p]   = [agg | h_dst | 0 pad]
   float* dl = both + R * d2p;       // [R][C]     logits, then dlogits
-  __shared__ double s_loss[kHeadThreads / 32];
+  float* WsT = dl + R * C;          // [C][d2p]   W^T for dt = dl W^T (k contiguous)
+  __shared__ int32_t s_col[R][kHeadMaxEdges];
+  __shared__ float s_val[R][kHeadMaxEdges];
+  __shared__ int s_ne[R];
+  __shared__ double s_loss[R];
   __shared__ int s_bad;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int warps = kHeadThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // warp <-> row
   const int n = *a.n_dst_dev;
-  const int r0 = blockIdx.x * R;
+  const int r = blockIdx.x * R + warp;
+  const bool live = r < n;
   if (tid == 0) s_bad = 0;
+  // this row's edges and label first: their latency overlaps the W copy
+  int e0 = 0, ne = 0, lab = -1;
+  if (live) {
+    e0 = a.row_ptr[r];
+    ne = a.row_ptr[r + 1] - e0;
+    if (lane == 0) lab = a.labels[r];
+    if (ne > kHeadMaxEdges) {  // not a sampled block (rows carry <= fanout triplets)
+      if (lane == 0) atomicOr(a.nonfinite, 4);
+      ne = kHeadMaxEdges;
+    }
+  }
+  if (lane < ne) {
+    s_col[warp][lane] = __ldg(&a.cols[e0 + lane]);
+    s_val[warp][lane] = __ldg(&a.vals[e0 + lane]);
+  }
+  if (lane == 0) s_ne[warp] = ne;
+  if (a.dh != nullptr) {  // transposed copy for phase 4 (conflict-free float4 rows)
+    for (int i = tid; i < C * d2p; i += kHeadThreads) {
+      const int c = i / d2p, k = i % d2p;
+      WsT[i] = k < d2 ? __ldg(a.W + (int64_t)k * C + c) : 0.f;
+    }
+  }
   if (Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0) {  // same layout: float4 copy
     const float4* src = reinterpret_cast<const float4*>(a.W);
     float4* dst = reinterpret_cast<float4*>(Ws);
@@ -352,204 +473,220 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     }
   }
 
-  // 1. both = [agg | h_dst] (agg bit-exact: sequential triplet order)
-  const bool vec2 = (d & 1) == 0 && (a.ldh & 1) == 0 && ((uintptr_t)a.h & 7) == 0;
-  for (int i = warp; i < R; i += warps) {
-    const int r = r0 + i;
-    float* brow = both + i * d2p;
-    if (r >= n) {
+  // 1. both[row] = [agg | h_dst]: agg bit-exact (sequential triplet order,
+  //    nn.py:79-89); the row's gathers issued together
+  {
+    float* brow = both + warp * d2p;
+    if (!live) {
       for (int c = lane; c < d2p; c += 32) brow[c] = 0.f;
-      continue;
-    }
-    const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-    const float* self = a.h + (int64_t)r * a.ldh;
-    if (vec2) {
-      for (int cb = 0; cb < d; cb += 64) {
-        const int c = cb + 2 * lane;
-        const float2 acc = row_agg2<true>(a.cols, a.vals, e0, e1, a.h, a.ldh, c, c < d);
-        if (c < d) {
-          brow[c] = acc.x;
-          brow[c + 1] = acc.y;
-          const float2 hv = __ldg(reinterpret_cast<const float2*>(self + c));
-          brow[d + c] = hv.x;
-          brow[d + c + 1] = hv.y;
-        }
-      }
     } else {
-      for (int cb = 0; cb < d; cb += 32) {
-        const int c = cb + lane;
-        const float acc = row_agg1<true>(a.cols, a.vals, e0, e1, a.h, a.ldh, c, c < d);
-        if (c < d) {
-          brow[c] = acc;
-          brow[d + c] = __ldg(self + c);
+      __syncwarp();
+      const float* self = a.h + (int64_t)r * a.ldh;
+      const bool vec2 = (d & 1) == 0 && (a.ldh & 1) == 0 && ((uintptr_t)a.h & 7) == 0;
+      if (vec2) {
+        for (int cb = 0; cb < d; cb += 64) {
+          const int c = cb + 2 * lane;
+          float2 acc = make_float2(0.f, 0.f);
+          for (int e0b = 0; e0b < ne; e0b += 8) {
+            float2 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              x[u] = (c < d && e0b + u < ne)
+                         ? __ldg(reinterpret_cast<const float2*>(
+                               a.h + (int64_t)s_col[warp][e0b + u] * a.ldh + c))
+                         : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (e0b + u < ne) {
+                const float v = s_val[warp][e0b + u];
+                acc.x = __fadd_rn(acc.x, __fmul_rn(v, x[u].x));
+                acc.y = __fadd_rn(acc.y, __fmul_rn(v, x[u].y));
+              }
+            }
+          }
+          if (c < d) {
+            const float2 hv = __ldg(reinterpret_cast<const float2*>(self + c));
+            brow[c] = acc.x;
+            brow[c + 1] = acc.y;
+            brow[d + c] = hv.x;
+            brow[d + c + 1] = hv.y;
+          }
+        }
+      } else {
+        for (int cb = 0; cb < d; cb += 32) {
+          const int c = cb + lane;
+          float acc = 0.f;
+          for (int e = 0; e < ne; ++e)
+            if (c < d)
+              acc = __fadd_rn(acc, __fmul_rn(s_val[warp][e],
+                                             __ldg(a.h + (int64_t)s_col[warp][e] * a.ldh + c)));
+          if (c < d) {
+            brow[c] = acc;
+            brow[d + c] = __ldg(self + c);
+          }
         }
       }
+      for (int c = d2 + lane; c < d2p; c += 32) brow[c] = 0.f;
     }
-    for (int c = d2 + lane; c < d2p; c += 32) brow[c] = 0.f;
   }
   __syncthreads();
 
-  // 2. logits = both W: thread (row group g of 4 rows, class c), float4 over k
-  {
-    const int g = tid >> 6, cl = tid & 63;
-    for (int c = cl; c < C; c += 64) {
-      for (int ib = 4 * g; ib < R; ib += kHeadRowQuant) {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int k = 0; k < d2p; k += 4) {
-          const float w0 = Ws[(k + 0) * Cp + c], w1 = Ws[(k + 1) * Cp + c];
-          const float w2 = Ws[(k + 2) * Cp + c], w3 = Ws[(k + 3) * Cp + c];
+  // 2. logits = both W: thread (4-row quad, class), float4 over k
+  for (int item = tid; item < (R / 4) * C; item += kHeadThreads) {
+    const int ib = 4 * (item / C), c = item % C;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < d2p; k += 4) {
+      const float w0 = Ws[(k + 0) * Cp + c], w1 = Ws[(k + 1) * Cp + c];
+      const float w2 = Ws[(k + 2) * Cp + c], w3 = Ws[(k + 3) * Cp + c];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 b = *reinterpret_cast<const float4*>(both + (ib + q) * d2p + k);
-            acc[q] = fmaf(b.x, w0, acc[q]);
-            acc[q] = fmaf(b.y, w1, acc[q]);
-            acc[q] = fmaf(b.z, w2, acc[q]);
-            acc[q] = fmaf(b.w, w3, acc[q]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dl[(ib + q) * C + c] = acc[q];
+      for (int q = 0; q < 4; ++q) {
+        const float4 b = *reinterpret_cast<const float4*>(both + (ib + q) * d2p + k);
+        acc[q] = fmaf(b.x, w0, acc[q]);
+        acc[q] = fmaf(b.y, w1, acc[q]);
+        acc[q] = fmaf(b.z, w2, acc[q]);
+        acc[q] = fmaf(b.w, w3, acc[q]);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dl[(ib + q) * C + c] = acc[q];
   }
   __syncthreads();
 
   // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot
-  double wloss = 0.0;
-  int bad = 0;
-  for (int i = warp; i < R; i += warps) {
-    const int r = r0 + i;
-    float* x = dl + i * C;
-    if (r >= n) {
+  {
+    float* x = dl + warp * C;
+    double wloss = 0.0;
+    int bad = 0;
+    if (!live) {
       for (int c = lane; c < C; c += 32) x[c] = 0.f;
-      continue;
-    }
-    float m = -INFINITY;
-    for (int c = lane; c < C; c += 32) m = fmaxf(m, x[c]);
+    } else {
+      lab = __shfl_sync(0xffffffffu, lab, 0);
+      float m = -INFINITY;
+      for (int c = lane; c < C; c += 32) m = fmaxf(m, x[c]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float s = 0.f;
-    for (int c = lane; c < C; c += 32) s += expf(x[c] - m);
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float s = 0.f;
+      for (int c = lane; c < C; c += 32) s += expf(x[c] - m);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float logd = logf(s);
-    const int lab = a.labels[r];
-    for (int c = lane; c < C; c += 32) {
-      const float sh = x[c] - m;
-      float p = expf(sh) / s;
-      if (c == lab) {
-        p -= 1.f;
-        wloss += -(double)(sh - logd);
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const float logd = logf(s);
+      for (int c = lane; c < C; c += 32) {
+        const float sh = x[c] - m;
+        float p = expf(sh) / s;
+        if (c == lab) {
+          p -= 1.f;
+          wloss += -(double)(sh - logd);
+        }
+        x[c] = p;
+        bad |= !isfinite(p);
       }
-      x[c] = p;
-      bad |= !isfinite(p);
     }
-  }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    wloss += __shfl_xor_sync(0xffffffffu, wloss, o);
-    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    for (int o = 16; o; o >>= 1) {
+      wloss += __shfl_xor_sync(0xffffffffu, wloss, o);
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+      s_loss[warp] = wloss;
+      if (bad) s_bad = 1;
+    }
+    __syncwarp();
   }
-  if (lane == 0) {
-    s_loss[warp] = wloss;
-    if (bad) s_bad = 1;
+
+  // 4. dt = dl W^T -> dh: self half to the dst row, top half scattered over the
+  //    row's edges (dh zeroed for rows [0, n_src) beforehand).  A lane owns 4
+  //    consecutive k of [top | bot]; one v4 reduction per target row.
+  if (a.dh != nullptr && live) {
+    const float* x = dl + warp * C;
+    const bool v4 = (d & 3) == 0 && (a.lddh & 3) == 0 && ((uintptr_t)a.dh & 15) == 0;
+    if (v4) {
+      for (int kb = 4 * lane; kb < d2; kb += 128) {
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+        int c = 0;
+        for (; c + 2 <= C; c += 2) {
+          const float x0 = x[c], x1 = x[c + 1];
+          const float4 w0 = *reinterpret_cast<const float4*>(WsT + c * d2p + kb);
+          const float4 w1 = *reinterpret_cast<const float4*>(WsT + (c + 1) * d2p + kb);
+          a0.x = fmaf(x0, w0.x, a0.x);
+          a0.y = fmaf(x0, w0.y, a0.y);
+          a0.z = fmaf(x0, w0.z, a0.z);
+          a0.w = fmaf(x0, w0.w, a0.w);
+          a1.x = fmaf(x1, w1.x, a1.x);
+          a1.y = fmaf(x1, w1.y, a1.y);
+          a1.z = fmaf(x1, w1.z, a1.z);
+          a1.w = fmaf(x1, w1.w, a1.w);
+        }
+        if (c < C) {
+          const float x0 = x[c];
+          const float4 w0 = *reinterpret_cast<const float4*>(WsT + c * d2p + kb);
+          a0.x = fmaf(x0, w0.x, a0.x);
+          a0.y = fmaf(x0, w0.y, a0.y);
+          a0.z = fmaf(x0, w0.z, a0.z);
+          a0.w = fmaf(x0, w0.w, a0.w);
+        }
+        const float4 dt = make_float4(a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w);
+        if (kb >= d) {
+          atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)r * a.lddh + (kb - d)), dt);
+        } else {
+          for (int e = 0; e < ne; ++e) {
+            const float v = s_val[warp][e];
+            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)s_col[warp][e] * a.lddh + kb),
+                      make_float4(v * dt.x, v * dt.y, v * dt.z, v * dt.w));
+          }
+        }
+      }
+    } else {
+      for (int kb = 0; kb < d; kb += 32) {
+        const int k = kb + lane;
+        if (k >= d) continue;
+        float top = 0.f, bot = 0.f;
+        const float* wt = Ws + k * Cp;
+        const float* wb = Ws + (d + k) * Cp;
+        for (int c = 0; c < C; ++c) {
+          top = fmaf(x[c], wt[c], top);
+          bot = fmaf(x[c], wb[c], bot);
+        }
+        atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
+        for (int e = 0; e < ne; ++e)
+          atomicAdd(a.dh + (int64_t)s_col[warp][e] * a.lddh + k, s_val[warp][e] * top);
+      }
+    }
   }
   __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int w = 0; w < warps; ++w) t += s_loss[w];
+    for (int w = 0; w < R; ++w) t += s_loss[w];
     if (t != 0.0) atomicAdd(a.loss_acc, t);
     if (s_bad) atomicOr(a.nonfinite, 1);
   }
 
-  // 4. dt = dl W^T -> dh: the self half to the dst row, the top half scattered
-  //    over the row's edges (dh was zeroed for rows [0, n_src)).  A lane owns
-  //    4 consecutive k of [top | bot] and issues one v4 reduction per target.
-  if (a.dh != nullptr) {
-    const bool v4 = (d & 3) == 0 && (a.lddh & 3) == 0 && ((uintptr_t)a.dh & 15) == 0;
-    for (int i = warp; i < R; i += warps) {
-      const int r = r0 + i;
-      if (r >= n) continue;
-      const float* x = dl + i * C;
-      const int e0 = a.row_ptr[r], e1 = a.row_ptr[r + 1];
-      if (v4) {
-        for (int kb = 4 * lane; kb < d2; kb += 128) {
-          float acc[4][2];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.f;
-          const float* w0 = Ws + kb * Cp;
-          int c = 0;
-          for (; c + 2 <= C; c += 2) {
-            const float x0 = x[c], x1 = x[c + 1];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              acc[q][0] = fmaf(x0, w0[q * Cp + c], acc[q][0]);
-              acc[q][1] = fmaf(x1, w0[q * Cp + c + 1], acc[q][1]);
-            }
-          }
-          if (c < C) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q][0] = fmaf(x[c], w0[q * Cp + c], acc[q][0]);
-          }
-          const float4 dt = make_float4(acc[0][0] + acc[0][1], acc[1][0] + acc[1][1],
-                                        acc[2][0] + acc[2][1], acc[3][0] + acc[3][1]);
-          if (kb >= d) {  // self half -> the dst row (dst ids lead src ids)
-            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)r * a.lddh + (kb - d)), dt);
-          } else {
-            for (int e = e0; e < e1; ++e) {
-              const float v = __ldg(&a.vals[e]);
-              atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + kb),
-                        make_float4(v * dt.x, v * dt.y, v * dt.z, v * dt.w));
-            }
-          }
-        }
-      } else {
-        for (int kb = 0; kb < d; kb += 32) {
-          const int k = kb + lane;
-          if (k >= d) continue;
-          float top = 0.f, bot = 0.f;
-          const float* wt = Ws + k * Cp;
-          const float* wb = Ws + (d + k) * Cp;
-          for (int c = 0; c < C; ++c) {
-            const float xc = x[c];
-            top = fmaf(xc, wt[c], top);
-            bot = fmaf(xc, wb[c], bot);
-          }
-          atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
-          for (int e = e0; e < e1; ++e)
-            atomicAdd(a.dh + (int64_t)__ldg(&a.cols[e]) * a.lddh + k, __ldg(&a.vals[e]) * top);
-        }
-      }
-    }
-  }
-
-  // 5. this CTA's dW partial = both^T dl: thread (k group, class c), 8 k per pass
+  // 5. this CTA's dW partial = both^T dl: thread (k octet, class), 8 k per item
   {
     float* part = a.part + (int64_t)blockIdx.x * d2 * C;
-    const int g = tid >> 6, cl = tid & 63;
-    for (int c = cl; c < C; c += 64) {
-      for (int k0 = 8 * g; k0 < d2p; k0 += 32) {
-        float acc[8];
+    const int n8 = (d2p + 7) / 8;
+    for (int item = tid; item < n8 * C; item += kHeadThreads) {
+      const int k0 = 8 * (item / C), c = item % C;
+      float acc[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-        for (int i = 0; i < R; ++i) {
-          const float v = dl[i * C + c];
-          const float4 b0 = *reinterpret_cast<const float4*>(both + i * d2p + k0);
-          const float4 b1 = k0 + 4 < d2p ? *reinterpret_cast<const float4*>(both + i * d2p + k0 + 4)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-          acc[0] = fmaf(b0.x, v, acc[0]);
-          acc[1] = fmaf(b0.y, v, acc[1]);
-          acc[2] = fmaf(b0.z, v, acc[2]);
-          acc[3] = fmaf(b0.w, v, acc[3]);
-          acc[4] = fmaf(b1.x, v, acc[4]);
-          acc[5] = fmaf(b1.y, v, acc[5]);
-          acc[6] = fmaf(b1.z, v, acc[6]);
-          acc[7] = fmaf(b1.w, v, acc[7]);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (k0 + q < d2) part[(k0 + q) * C + c] = acc[q];
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+#pragma unroll 4
+      for (int i = 0; i < R; ++i) {
+        const float v = dl[i * C + c];
+        const float4 b0 = *reinterpret_cast<const float4*>(both + i * d2p + k0);
+        const float4 b1 = k0 + 4 < d2p ? *reinterpret_cast<const float4*>(both + i * d2p + k0 + 4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc[0] = fmaf(b0.x, v, acc[0]);
+        acc[1] = fmaf(b0.y, v, acc[1]);
+        acc[2] = fmaf(b0.z, v, acc[2]);
+        acc[3] = fmaf(b0.w, v, acc[3]);
+        acc[4] = fmaf(b1.x, v, acc[4]);
+        acc[5] = fmaf(b1.y, v, acc[5]);
+        acc[6] = fmaf(b1.z, v, acc[6]);
+        acc[7] = fmaf(b1.w, v, acc[7]);
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q < d2) part[(k0 + q) * C + c] = acc[q];
     }
   }
 
@@ -579,15 +716,12 @@ __global__ void head_dw_reduce_kernel(const float* __restrict__ part, int nparts
     dW[o] = fixed_order_sum(part + o, total, nparts);
 }
 
-inline int head_rows(int n_dst_max) {
-  int R = kHeadRowQuant;
-  while ((n_dst_max + R - 1) / R > 128) R += kHeadRowQuant;
-  return R;
-}
+inline int head_rows(int) { return kHeadRows; }
 
 inline int64_t head_smem_bytes(int R, int d, int C) {
   const int Cp = C | 1, d2p = (2 * d + 3) & ~3;
-  return (int64_t)(d2p * Cp + R * d2p + R * C) * (int64_t)sizeof(float);
+  // W, both, dl, W^T (+ the static edge stash)
+  return (int64_t)(d2p * Cp + R * d2p + R * C + C * d2p) * (int64_t)sizeof(float);
 }
 
 }  // namespace mq
@@ -608,18 +742,32 @@ int64_t mq_sage_fused_scratch_bytes(int32_t m_max, int32_t d_in, int32_t d_out) 
   return mx * (int64_t)sizeof(float);
 }
 
+int mq_sage_y_deferred(int32_t d_out) {
+  return (tc_backend() == 1 && tc_supported(2 * d_out) && (d_out % 2) == 0) ? 1 : 0;
+}
+
+int64_t mq_sage_y_parts_bytes(int32_t m_max, int32_t d_out) {
+  return tc_y_part_floats(m_max, d_out) * (int64_t)sizeof(float);
+}
+
 int mq_sage_transform(const float* h, int32_t ldh, const int32_t* m_dev, int32_t m_max,
                       int32_t d_in, const float* W, int32_t d_out, float* y, void* scratch,
-                      void* stream) {
-  MQ_CHECK_ARG(h && m_dev && W && y && scratch, "mq_sage_transform: null pointer");
+                      float* y_parts, int32_t* y_nparts_dev, void* stream) {
+  MQ_CHECK_ARG(h && m_dev && W && scratch && (y || y_parts), "mq_sage_transform: null pointer");
+  MQ_CHECK_ARG((y_parts == nullptr) == (y_nparts_dev == nullptr),
+               "mq_sage_transform: y_parts and y_nparts_dev go together");
+  MQ_CHECK_ARG(!y_parts || mq_sage_y_deferred(d_out),
+               "mq_sage_transform: deferred partials need the tcgen05 backend and even d_out");
   MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldh >= d_in && ldh % 4 == 0 && (uintptr_t)h % 16 == 0,
                "mq_sage_transform: h needs a 16-byte-aligned pitch (multiple of 4) >= d_in");
   if (m_max <= 0) return MQ_OK;
   cudaStream_t s = as_stream(stream);
   Dims dims{m_dev, 0, nullptr, d_in, 2 * d_out};
   float* part = reinterpret_cast<float*>(scratch);
+  if (y_parts != nullptr)  // deferred: the aggregation sums the partial tiles
+    return tc_transform(h, ldh, m_dev, m_max, d_in, W, d_out, nullptr, y_parts, y_nparts_dev, s);
   if (tc_backend() == 1 && tc_supported(2 * d_out))
-    return tc_transform(h, ldh, m_dev, m_max, d_in, W, d_out, y, part, s);
+    return tc_transform(h, ldh, m_dev, m_max, d_in, W, d_out, y, part, nullptr, s);
   EpiStore epi{y, 2 * d_out};
   if (d_out % 4 == 0 && (uintptr_t)W % 16 == 0)
     return run_gemm(ALoadRow{h, ldh}, BLoadWSplitVec{W, d_in, d_out}, epi, dims, m_max, d_in,
@@ -630,7 +778,8 @@ int mq_sage_transform(const float* h, int32_t ldh, const int32_t* m_dev, int32_t
 
 int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                       const int32_t* n_dst_dev, int32_t n_dst_max, const float* y, int32_t d_out,
-                      float* act, int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
+                      const int32_t* y_nparts_dev, const int32_t* y_rows_dev, float* act,
+                      int32_t ldact, float* zero0, const int32_t* zero0_rows_dev,
                       int32_t zero0_row_floats, float* zero1, const int32_t* zero1_rows_dev,
                       int32_t zero1_row_floats, void* stream) {
   MQ_CHECK_ARG(row_ptr && cols && vals && n_dst_dev && y && act, "mq_sage_aggregate: null pointer");
@@ -641,12 +790,21 @@ int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* 
   const int warps = kAggThreads / 32;
   int blocks = ceil_div(n_dst_max < 1 ? 1 : n_dst_max, warps);
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  MQ_CHECK_ARG(!y_nparts_dev || (y_rows_dev && d_out % 2 == 0 && ldact % 2 == 0 &&
+                                  ((uintptr_t)y & 7) == 0 && ((uintptr_t)act & 7) == 0),
+               "mq_sage_aggregate: partial input needs y_rows_dev and even, aligned widths");
   {
     ProfScope ps(K_SAGE_AGG, s);
-    sage_aggregate_kernel<<<blocks, kAggThreads, 0, s>>>(
-        row_ptr, cols, vals, n_dst_dev, y, d_out, act, ldact,
-        ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
-        ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
+    if (y_nparts_dev)
+      sage_aggregate_parts_kernel<<<blocks, kAggThreads, 0, s>>>(
+          row_ptr, cols, vals, n_dst_dev, y, y_nparts_dev, y_rows_dev, d_out, act, ldact,
+          ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
+          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
+    else
+      sage_aggregate_kernel<<<blocks, kAggThreads, 0, s>>>(
+          row_ptr, cols, vals, n_dst_dev, y, d_out, act, ldact,
+          ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
+          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
   }
   MQ_LAUNCH_CHECK("sage_aggregate");
   return MQ_OK;

@@ -1,0 +1,458 @@
+// Multi-queue batch preparation: sample -> relabel -> gather for Q batches in
+// ONE pass (one launch per stage for all Q batches).
+//
+// MQ-GNN keeps a queue of prepared mini-batches ahead of the trainer
+// (runtime.py:380-612, BoundedQueue pipeline.py:109-167).  Here the queue is a
+// group of Q device slots filled by one pass of batched kernels: blockIdx.y
+// selects the slot, so each stage's latency (dependent CSR loads, look-back
+// scans) is paid once per Q batches instead of once per batch, and each
+// launch has Q times the parallelism.
+//
+// Per slot the semantics are exactly the single-batch entry points':
+// mq_batch_setup (runtime.py:95-124), mq_sample_hop (samplers.py:159-200),
+// mq_relabel (samplers.py:155-156, 186-200), mq_gather (cache.py:123-134,
+// runtime.py:127-143) and mq_gather_labels (samplers.py:532) — bit-identical
+// blocks, ids and features for the same (seed, epoch, batch) key.
+#include <climits>
+
+#include "mq_common.cuh"
+#include "mq_scan.cuh"
+
+namespace mq {
+namespace prep {
+
+template <class T>
+struct QP {
+  T* p;
+  int64_t s;  // elements between consecutive slots
+  __host__ __device__ __forceinline__ T* at(int q) const { return p + (int64_t)q * s; }
+};
+
+template <class T>
+inline QP<T> qp(T* p, int64_t s) {
+  return QP<T>{p, s};
+}
+
+// ------------------------------------------------------------ batch setup
+// slot q <- window cursor[0] + q: batch j = window*world + rank (round-robin
+// deal, runtime.py:111-113), targets = perm[j*B, min(n_perm, (j+1)*B)).  The
+// last block to finish advances the cursor by Q (cursor[1] = arrival count).
+__global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm, int B, int world,
+                               int rank, int32_t* __restrict__ cursor, QP<int32_t> targets,
+                               QP<int32_t> n_targets, QP<uint32_t> key) {
+  const int q = blockIdx.y;
+  __shared__ int64_t s_begin;
+  __shared__ int s_len;
+  if (threadIdx.x == 0) {
+    const int64_t window = (int64_t)cursor[0] + q;
+    const int64_t j = window * world + rank;
+    const int64_t b = j * B;
+    int64_t len = n_perm - b;
+    len = len < 0 ? 0 : (len > B ? B : len);
+    s_begin = b;
+    s_len = (int)len;
+    n_targets.at(q)[0] = (int32_t)len;
+    key.at(q)[2] = (uint32_t)j;
+  }
+  __syncthreads();
+  int32_t* t = targets.at(q);
+  for (int i = threadIdx.x; i < s_len; i += blockDim.x) t[i] = __ldg(&perm[s_begin + i]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&cursor[1], 1) == (int)gridDim.y - 1) {
+      cursor[0] += (int)gridDim.y;
+      cursor[1] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------ sample
+// One thread per dst row (node_wise_block, SAGE arm).  Every case is O(fanout)
+// through the per-epoch residency index; the row's gathers are issued from
+// register arrays so a row costs ~4 dependent round trips
+// (dst -> offsets -> hot arcs -> columns), not 2*fanout.
+template <int MAXK>
+__global__ void __launch_bounds__(64) sample_q_kernel(
+    const int64_t* __restrict__ row_off, const int32_t* __restrict__ col,
+    const int64_t* __restrict__ hot_arc, const int64_t* __restrict__ hot_off, QP<const int32_t> dst,
+    QP<const int32_t> n_dst, QP<const uint32_t> key, int fanout, uint32_t hop, QP<int32_t> nbr,
+    QP<int32_t> cnt) {
+  const int q = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= *n_dst.at(q)) return;
+  const uint32_t* k = key.at(q);
+  const int32_t v = dst.at(q)[r];
+  const int64_t beg = row_off[v];
+  const int n = (int)(row_off[v + 1] - beg);
+  int64_t hb = 0;
+  int nh = 0;
+  if (hot_off != nullptr) {
+    hb = hot_off[v];
+    nh = (int)(hot_off[v + 1] - hb);
+  }
+  int32_t* out = nbr.at(q) + (int64_t)r * fanout;
+  int32_t x[MAXK];
+  if (n <= fanout) {  // samplers.py:164-167: every neighbour, CSR order
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i) x[i] = i < n ? __ldg(&col[beg + i]) : 0;
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i)
+      if (i < n) out[i] = x[i];
+    cnt.at(q)[r] = n;
+    return;
+  }
+  RowStream rs(k[0], k[1], k[2], hop, (uint32_t)r);
+  int pos[MAXK];
+  if (hot_off != nullptr && nh >= fanout) {  // samplers.py:171-172: choice(hot, f)
+    fisher_yates<MAXK, int>(rs, nh, fanout, pos);
+    int64_t arc[MAXK];
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) arc[j] = j < fanout ? __ldg(&hot_arc[hb + pos[j]]) : 0;
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) x[j] = j < fanout ? __ldg(&col[arc[j]]) : 0;
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j)
+      if (j < fanout) out[j] = x[j];
+  } else if (hot_off != nullptr) {  // samplers.py:173-175: hot ++ choice(cold, f - |hot|)
+    int64_t ha[MAXK];
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i) ha[i] = i < nh ? __ldg(&hot_arc[hb + i]) : 0;
+    const int k2 = fanout - nh;
+    fisher_yates<MAXK, int>(rs, n - nh, k2, pos);
+    int64_t ca[MAXK];
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) {
+      // cold rank -> row position: skip every hot position h_i with h_i - i <= rank
+      const int rr = j < k2 ? pos[j] : 0;
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < MAXK; ++i) c += (i < nh && (int)(ha[i] - beg) - i <= rr) ? 1 : 0;
+      ca[j] = beg + rr + c;
+    }
+    int32_t y[MAXK];
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i) x[i] = i < nh ? __ldg(&col[ha[i]]) : 0;
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) y[j] = j < k2 ? __ldg(&col[ca[j]]) : 0;
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i)
+      if (i < nh) out[i] = x[i];
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j)
+      if (j < k2) out[nh + j] = y[j];
+  } else {  // samplers.py:176-177: choice(nbrs, f)
+    fisher_yates<MAXK, int>(rs, n, fanout, pos);
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j) x[j] = j < fanout ? __ldg(&col[beg + pos[j]]) : 0;
+#pragma unroll
+    for (int j = 0; j < MAXK; ++j)
+      if (j < fanout) out[j] = x[j];
+  }
+  cnt.at(q)[r] = fanout;
+}
+
+// ------------------------------------------------------------ relabel
+struct QLoadCnt {
+  QP<const int32_t> cnt;
+  QP<const int32_t> n_dst;
+  __device__ int64_t size() const { return *n_dst.at(blockIdx.y); }
+  __device__ int64_t operator()(int64_t i) const { return cnt.at(blockIdx.y)[i]; }
+};
+struct QStoreRowPtr {
+  QP<int32_t> row_ptr;
+  QP<int32_t> counts;  // counts[1] = nnz
+  __device__ void operator()(int64_t i, int64_t excl, int64_t) const {
+    row_ptr.at(blockIdx.y)[i] = (int32_t)excl;
+  }
+  __device__ void total(int64_t n, int64_t t) const {
+    row_ptr.at(blockIdx.y)[n] = (int32_t)t;
+    counts.at(blockIdx.y)[1] = (int32_t)t;
+  }
+};
+
+__global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP<int32_t> dpos,
+                              QP<int32_t> src_ids) {
+  const int q = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_dst.at(q)) return;
+  const int32_t v = dst.at(q)[i];
+  src_ids.at(q)[i] = v;
+  atomicMax(&dpos.at(q)[v], i);
+}
+
+__global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
+                               QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
+                               QP<const int32_t> dpos, QP<int32_t> first) {
+  const int q = blockIdx.y;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = (int)(s / fanout), i = (int)(s % fanout);
+  if (r >= *n_dst.at(q) || i >= cnt.at(q)[r]) return;
+  const int32_t u = nbr.at(q)[s];
+  if (dpos.at(q)[u] < 0) atomicMin(&first.at(q)[u], row_ptr.at(q)[r] + i);
+}
+
+struct QLoadFirstFlag {
+  QP<const int32_t> nbr, cnt, row_ptr, n_dst, dpos, first;
+  int fanout;
+  __device__ int64_t size() const { return (int64_t)(*n_dst.at(blockIdx.y)) * fanout; }
+  __device__ int64_t operator()(int64_t s) const {
+    const int q = blockIdx.y;
+    const int r = (int)(s / fanout), i = (int)(s % fanout);
+    if (i >= cnt.at(q)[r]) return 0;
+    const int32_t u = nbr.at(q)[s];
+    return (dpos.at(q)[u] < 0 && first.at(q)[u] == row_ptr.at(q)[r] + i) ? 1 : 0;
+  }
+};
+struct QStoreLabel {
+  QP<const int32_t> nbr, n_dst;
+  QP<int32_t> dpos, src_ids, counts;
+  __device__ void operator()(int64_t s, int64_t excl, int64_t val) const {
+    if (!val) return;
+    const int q = blockIdx.y;
+    const int32_t u = nbr.at(q)[s];
+    const int32_t lab = *n_dst.at(q) + (int32_t)excl;
+    src_ids.at(q)[lab] = u;
+    dpos.at(q)[u] = lab;
+  }
+  __device__ void total(int64_t, int64_t t) const {
+    const int q = blockIdx.y;
+    counts.at(q)[0] = *n_dst.at(q) + (int32_t)t;
+  }
+};
+
+__global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
+                              QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
+                              QP<const int32_t> dpos, QP<int32_t> rows, QP<int32_t> cols,
+                              QP<float> vals) {
+  const int q = blockIdx.y;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = (int)(s / fanout), i = (int)(s % fanout);
+  if (r >= *n_dst.at(q)) return;
+  const int c = cnt.at(q)[r];
+  if (i >= c) return;
+  const int e = row_ptr.at(q)[r] + i;
+  rows.at(q)[e] = r;
+  cols.at(q)[e] = dpos.at(q)[nbr.at(q)[s]];
+  vals.at(q)[e] = (float)(1.0 / (double)c);  // float32(1.0 / s), samplers.py:200 + nn.py:85
+}
+
+__global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> counts,
+                               QP<const int32_t> n_dst, QP<int32_t> dpos, QP<int32_t> first) {
+  const int q = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= counts.at(q)[0]) return;
+  const int32_t u = src_ids.at(q)[j];
+  dpos.at(q)[u] = -1;
+  if (j >= *n_dst.at(q)) first.at(q)[u] = INT_MAX;
+}
+
+// ------------------------------------------------------------ gather
+constexpr int kGatherThreads = 256;
+
+__global__ void __launch_bounds__(kGatherThreads) gather_q_kernel(
+    const float* __restrict__ cache_tbl, int cache_pitch, const int32_t* __restrict__ slot_of,
+    const float* __restrict__ store, int store_pitch, QP<const int32_t> ids, QP<const int32_t> n_dev,
+    int d4, QP<float> out, int out_pitch, unsigned long long* __restrict__ hit_miss) {
+  __shared__ unsigned int s_hits, s_miss;
+  if (threadIdx.x == 0) {
+    s_hits = 0;
+    s_miss = 0;
+  }
+  __syncthreads();
+  const int q = blockIdx.y;
+  const int n = *n_dev.at(q);
+  const int32_t* idq = ids.at(q);
+  float* outq = out.at(q);
+  const int lane = threadIdx.x & 31;
+  const int warps = kGatherThreads / 32;
+  int64_t row = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+  const int64_t stride = (int64_t)gridDim.x * warps;
+  unsigned int hits = 0, miss = 0;
+  for (; row < n; row += stride) {
+    const int32_t id = idq[row];
+    const float4* src;
+    const int32_t slot = slot_of ? slot_of[id] : -1;
+    if (slot >= 0) {
+      src = reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch);
+      ++hits;
+    } else {
+      src = reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
+      ++miss;
+    }
+    float4* dst = reinterpret_cast<float4*>(outq + row * out_pitch);
+    int c = lane;
+    for (; c + 96 < d4; c += 128) {
+      const float4 a = src[c], b = src[c + 32], e = src[c + 64], f = src[c + 96];
+      dst[c] = a;
+      dst[c + 32] = b;
+      dst[c + 64] = e;
+      dst[c + 96] = f;
+    }
+    for (; c < d4; c += 32) dst[c] = src[c];
+  }
+  if (slot_of != nullptr && lane == 0) {
+    atomicAdd(&s_hits, hits);
+    atomicAdd(&s_miss, miss);
+  }
+  __syncthreads();
+  if (slot_of != nullptr && threadIdx.x == 0 && (s_hits | s_miss)) {
+    atomicAdd(&hit_miss[0], (unsigned long long)s_hits);
+    atomicAdd(&hit_miss[1], (unsigned long long)s_miss);
+  }
+}
+
+__global__ void labels_q_kernel(const int32_t* __restrict__ all_labels, QP<const int32_t> ids,
+                                QP<const int32_t> n_dev, QP<int32_t> out) {
+  const int q = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *n_dev.at(q)) out.at(q)[i] = all_labels[ids.at(q)[i]];
+}
+
+template <class T>
+inline QP<const T> cq(T* p, int64_t s) {
+  return QP<const T>{p, s};
+}
+
+}  // namespace prep
+}  // namespace mq
+
+using namespace mq;
+using namespace mq::prep;
+
+extern "C" {
+
+int64_t mq_prep_scratch_bytes(int32_t n_dst_max, int32_t fanout) {
+  const int64_t slots = (int64_t)(n_dst_max < 1 ? 1 : n_dst_max) * (fanout < 1 ? 1 : fanout);
+  // 256-byte aligned per-slot region of the scan ticket/status words
+  return (scan_scratch_bytes(slots) + 255) / 256 * 256;
+}
+
+int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
+  MQ_CHECK_ARG(pd != nullptr, "mq_prep_batches: null descriptor");
+  const mq_prep_desc& d = *pd;
+  const int Q = d.nslots;
+  MQ_CHECK_ARG(Q >= 1 && Q <= 65535, "mq_prep_batches: nslots %d out of range", Q);
+  MQ_CHECK_ARG(d.num_hops >= 1 && d.num_hops <= MQ_MAX_HOPS, "mq_prep_batches: num_hops %d",
+               d.num_hops);
+  MQ_CHECK_ARG(d.row_off && d.col && d.targets && d.n_targets && d.key && d.dpos && d.first &&
+                   d.scratch && d.store && d.x0 && d.all_labels && d.labels,
+               "mq_prep_batches: null pointer");
+  MQ_CHECK_ARG((d.hot_arc == nullptr) == (d.hot_off == nullptr),
+               "mq_prep_batches: hot_arc / hot_off must both be set or both NULL");
+  MQ_CHECK_ARG(!d.slot_of || (d.cache_tbl && d.hit_miss), "mq_prep_batches: cache without table");
+  const int dv4 = (d.d + 3) / 4;
+  MQ_CHECK_ARG(d.d >= 1 && d.store_pitch % 4 == 0 && d.x0_pitch % 4 == 0 &&
+                   d.store_pitch >= 4 * dv4 && d.x0_pitch >= 4 * dv4 &&
+                   (!d.slot_of || (d.cache_pitch % 4 == 0 && d.cache_pitch >= 4 * dv4)),
+               "mq_prep_batches: feature pitches must be multiples of 4 covering d");
+  cudaStream_t s = as_stream(stream);
+  const uint32_t mask = d.stage_mask ? d.stage_mask : 0xFFFFFFFFu;
+
+  // 1. device batch plan (skipped when the host staged targets/keys)
+  if (d.cursor != nullptr && (mask & MQ_PREP_SETUP)) {
+    MQ_CHECK_ARG(d.perm && d.batch_size >= 1 && d.world >= 1 && d.rank >= 0 && d.rank < d.world,
+                 "mq_prep_batches: bad batch plan");
+    {
+      ProfScope ps(K_BATCH_SETUP, s);
+      setup_q_kernel<<<dim3(1, Q), 256, 0, s>>>(d.perm, d.n_perm, d.batch_size, d.world, d.rank,
+                                                d.cursor, qp(d.targets, d.targets_s),
+                                                qp(d.n_targets, d.n_targets_s),
+                                                qp(d.key, d.key_s));
+    }
+    MQ_LAUNCH_CHECK("prep setup");
+  }
+
+  // 2. hops: sample + relabel (samplers.py:213-226 hop chain)
+  for (int h = 0; h < d.num_hops; ++h) {
+    const mq_prep_hop& hp = d.hop[h];
+    MQ_CHECK_ARG(hp.fanout >= 1 && hp.fanout <= MQ_MAX_FANOUT && hp.n_dst_max >= 1,
+                 "mq_prep_batches: hop %d bad fanout / bound", h);
+    MQ_CHECK_ARG(hp.nbr && hp.cnt && hp.row_ptr && hp.rows && hp.cols && hp.vals && hp.src_ids &&
+                     hp.counts,
+                 "mq_prep_batches: hop %d null buffer", h);
+    const int32_t* dst = h == 0 ? d.targets : d.hop[h - 1].src_ids;
+    const int64_t dst_s = h == 0 ? d.targets_s : d.hop[h - 1].src_s;
+    const int32_t* nd = h == 0 ? d.n_targets : d.hop[h - 1].counts;  // counts[0] = n_src
+    const int64_t nd_s = h == 0 ? d.n_targets_s : d.hop[h - 1].counts_s;
+    const int f = hp.fanout;
+    const int64_t slots = (int64_t)hp.n_dst_max * f;
+    if (mask & MQ_PREP_SAMPLE) {
+      ProfScope ps(K_SAMPLE, s);
+      const dim3 grid(ceil_div(hp.n_dst_max, 64), Q);
+      if (f <= 16)
+        sample_q_kernel<16><<<grid, 64, 0, s>>>(
+            d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
+            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s));
+      else
+        sample_q_kernel<MQ_MAX_FANOUT><<<grid, 64, 0, s>>>(
+            d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
+            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s));
+    }
+    MQ_LAUNCH_CHECK("prep sample");
+    if (!(mask & MQ_PREP_RELABEL)) continue;
+    int rc = launch_scan_q(QLoadCnt{cq(hp.cnt, hp.cnt_s), cq(nd, nd_s)},
+                           QStoreRowPtr{qp(hp.row_ptr, hp.row_ptr_s), qp(hp.counts, hp.counts_s)},
+                           hp.n_dst_max, Q, d.scratch, d.scratch_s, s, K_SCAN);
+    if (rc) return rc;
+    {
+      ProfScope ps(K_RELABEL_MARK, s);
+      mark_q_kernel<<<dim3(ceil_div(hp.n_dst_max, 256), Q), 256, 0, s>>>(
+          cq(dst, dst_s), cq(nd, nd_s), qp(d.dpos, d.table_s), qp(hp.src_ids, hp.src_s));
+    }
+    MQ_LAUNCH_CHECK("prep mark");
+    {
+      ProfScope ps(K_RELABEL_FIRST, s);
+      first_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
+          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s), cq(nd, nd_s), f,
+          cq(d.dpos, d.table_s), qp(d.first, d.table_s));
+    }
+    MQ_LAUNCH_CHECK("prep first");
+    rc = launch_scan_q(
+        QLoadFirstFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s),
+                       cq(nd, nd_s), cq(d.dpos, d.table_s), cq(d.first, d.table_s), f},
+        QStoreLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.dpos, d.table_s),
+                    qp(hp.src_ids, hp.src_s), qp(hp.counts, hp.counts_s)},
+        slots, Q, d.scratch, d.scratch_s, s, K_RELABEL_FLAG);
+    if (rc) return rc;
+    {
+      ProfScope ps(K_RELABEL_COLS, s);
+      cols_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
+          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s), cq(nd, nd_s), f,
+          cq(d.dpos, d.table_s), qp(hp.rows, hp.edge_s), qp(hp.cols, hp.edge_s),
+          qp(hp.vals, hp.edge_s));
+    }
+    MQ_LAUNCH_CHECK("prep cols");
+    {
+      ProfScope ps(K_RELABEL_CLEAN, s);
+      clean_q_kernel<<<dim3(ceil_div(slots + hp.n_dst_max, 256), Q), 256, 0, s>>>(
+          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), cq(nd, nd_s),
+          qp(d.dpos, d.table_s), qp(d.first, d.table_s));
+    }
+    MQ_LAUNCH_CHECK("prep clean");
+  }
+
+  // 3. transfer stage: gather the input rows of every slot + target labels
+  const mq_prep_hop& last = d.hop[d.num_hops - 1];
+  if (mask & MQ_PREP_GATHER) {
+    ProfScope ps(K_GATHER, s);
+    const int warps = kGatherThreads / 32;
+    int blocks = ceil_div(last.n_src_max, warps);
+    const int cap = ceil_div(kNumSMs * 16, Q);
+    if (blocks > cap) blocks = cap;
+    gather_q_kernel<<<dim3(blocks, Q), kGatherThreads, 0, s>>>(
+        d.cache_tbl, d.cache_pitch, d.slot_of, d.store, d.store_pitch, cq(last.src_ids, last.src_s),
+        cq(last.counts, last.counts_s), dv4, qp(d.x0, d.x0_s), d.x0_pitch, d.hit_miss);
+  }
+  MQ_LAUNCH_CHECK("prep gather");
+  if (mask & MQ_PREP_LABELS) {
+    ProfScope ps(K_LABELS, s);
+    labels_q_kernel<<<dim3(ceil_div(d.batch_size, 256), Q), 256, 0, s>>>(
+        d.all_labels, cq(d.targets, d.targets_s), cq(d.n_targets, d.n_targets_s),
+        qp(d.labels, d.labels_s));
+  }
+  MQ_LAUNCH_CHECK("prep labels");
+  return MQ_OK;
+}
+
+}  // extern "C"

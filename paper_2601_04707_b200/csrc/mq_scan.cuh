@@ -42,7 +42,7 @@ inline int64_t scan_scratch_bytes(int64_t n_max) {
 // Store: __device__ void operator()(int64_t i, int64_t excl, int64_t val) const;
 //        __device__ void total(int64_t n, int64_t t) const
 template <class Load, class Store>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(Load load, Store store, void* scratch) {
+__device__ __forceinline__ void scan_tile(const Load& load, const Store& store, void* scratch) {
   unsigned int* ticket = reinterpret_cast<unsigned int*>(scratch);
   unsigned long long* status = reinterpret_cast<unsigned long long*>((char*)scratch + 16);
   __shared__ int s_tile;
@@ -121,6 +121,19 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Load load, Store sto
 }
 
 template <class Load, class Store>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(Load load, Store store, void* scratch) {
+  scan_tile(load, store, scratch);
+}
+
+// Q independent scans in one launch: blockIdx.y selects the slot (the Load /
+// Store functors read it too) and its private ticket/status region.
+template <class Load, class Store>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_q_kernel(Load load, Store store, void* scratch, int64_t scratch_stride) {
+  scan_tile(load, store, reinterpret_cast<char*>(scratch) + (int64_t)blockIdx.y * scratch_stride);
+}
+
+template <class Load, class Store>
 int launch_scan(const Load& load, const Store& store, int64_t n_max, void* scratch,
                 cudaStream_t s, int kid = K_SCAN) {
   MQ_CUDA(cudaMemsetAsync(scratch, 0, scan_scratch_bytes(n_max), s));
@@ -149,5 +162,20 @@ struct StoreOffsets {
   __device__ void operator()(int64_t i, int64_t excl, int64_t) const { out[i] = (OutT)excl; }
   __device__ void total(int64_t n, int64_t t) const { out[n] = (OutT)t; }
 };
+
+template <class Load, class Store>
+int launch_scan_q(const Load& load, const Store& store, int64_t n_max, int nslots, void* scratch,
+                  int64_t scratch_stride, cudaStream_t s, int kid) {
+  MQ_CUDA(cudaMemsetAsync(scratch, 0, (size_t)scratch_stride * nslots, s));
+  int tiles = (int)scan_tiles(n_max);
+  if (tiles < 1) tiles = 1;
+  {
+    ProfScope ps(kid, s);
+    scan_q_kernel<Load, Store><<<dim3(tiles, nslots), kScanThreads, 0, s>>>(load, store, scratch,
+                                                                           scratch_stride);
+  }
+  MQ_LAUNCH_CHECK("scan_q");
+  return MQ_OK;
+}
 
 }  // namespace mq

@@ -251,46 +251,58 @@ __device__ __forceinline__ void store_a(uint8_t* hi, uint8_t* lo, int tid, const
   }
 }
 
-// B block: (k0..k0+31) x (n 0..Np): 8 k4 x Np/4 n4 blocks of 4x4
+// B block: (k0..k0+31) x (n 0..Np): 8 k4 x Np/4 n4 blocks of 4x4, at most
+// kMaxN/128 = 2 blocks per thread, register double-buffered like A
+constexpr int kBPerThread = (8 * (kMaxN / 4) + kThreads - 1) / kThreads;
+
 template <int MODE>
-__device__ __forceinline__ void stage_b(const Operands& op, int K, int k0, uint8_t* hi, uint8_t* lo,
-                                        int tid) {
-  const int n4s = op.Np / 4;
-  for (int c = tid; c < 8 * n4s; c += kThreads) {
-    const int n4 = c % n4s, k4 = c / n4s;
-    const int n = 4 * n4;
-    float4 r[4];
+__device__ __forceinline__ float4 load_b4(const Operands& op, int K, int k, int n) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (k >= K || n >= op.N) return v;
+  if (MODE == kFwd) {
+    if (k >= op.d_in) return v;
+    const int h = op.n_half;
+    if ((h & 3) == 0)
+      return n < h ? __ldg(reinterpret_cast<const float4*>(op.w + (int64_t)k * h + n))
+                   : __ldg(reinterpret_cast<const float4*>(op.w + (int64_t)(op.d_in + k) * h +
+                                                           (n - h)));
+    float t4[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + 4 * k4 + u;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k < K && n < op.N) {
-        if (MODE == kFwd) {
-          if (k < op.d_in) {
-            const int h = op.n_half;
-            if ((h & 3) == 0) {
-              v = n < h ? __ldg(reinterpret_cast<const float4*>(op.w + (int64_t)k * h + n))
-                        : __ldg(reinterpret_cast<const float4*>(op.w + (int64_t)(op.d_in + k) * h +
-                                                                (n - h)));
-            } else {
-              float t4[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int nn = n + e;
-                t4[e] = nn < h ? __ldg(op.w + (int64_t)k * h + nn)
-                               : (nn < op.N ? __ldg(op.w + (int64_t)(op.d_in + k) * h + (nn - h))
-                                            : 0.f);
-              }
-              v = make_float4(t4[0], t4[1], t4[2], t4[3]);
-            }
-          }
-        } else {
-          v = ld_row4(op.g + (int64_t)k * op.N, n, op.N, (op.N & 3) == 0);
-        }
-      }
-      r[u] = v;
+    for (int e = 0; e < 4; ++e) {
+      const int nn = n + e;
+      t4[e] = nn < h ? __ldg(op.w + (int64_t)k * h + nn)
+                     : (nn < op.N ? __ldg(op.w + (int64_t)(op.d_in + k) * h + (nn - h)) : 0.f);
     }
-    st_transposed(hi, lo, (uint32_t)(k4 * (op.Np * 16) + n * 16), r);
+    return make_float4(t4[0], t4[1], t4[2], t4[3]);
+  }
+  return ld_row4(op.g + (int64_t)k * op.N, n, op.N, (op.N & 3) == 0);
+}
+
+template <int MODE>
+__device__ __forceinline__ void load_b(const Operands& op, int K, int k0, int tid,
+                                       float4 (&rb)[kBPerThread][4]) {
+  const int n4s = op.Np / 4;
+#pragma unroll
+  for (int i = 0; i < kBPerThread; ++i) {
+    const int c = tid + i * kThreads;
+    const int n4 = c % n4s, k4 = c / n4s;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      rb[i][u] = c < 8 * n4s ? load_b4<MODE>(op, K, k0 + 4 * k4 + u, 4 * n4)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__device__ __forceinline__ void store_b(const Operands& op, uint8_t* hi, uint8_t* lo, int tid,
+                                        const float4 (&rb)[kBPerThread][4]) {
+  const int n4s = op.Np / 4;
+#pragma unroll
+  for (int i = 0; i < kBPerThread; ++i) {
+    const int c = tid + i * kThreads;
+    if (c < 8 * n4s) {
+      const int n4 = c % n4s, k4 = c / n4s;
+      st_transposed(hi, lo, (uint32_t)(k4 * (op.Np * 16) + 4 * n4 * 16), rb[i]);
+    }
   }
 }
 
@@ -353,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       continue;
     }
     float4 ra[4];
+    float4 rb[kBPerThread][4];
     load_a<MODE>(op, M, K, m0, kb0 * BK, tid, ra);
+    load_b<MODE>(op, K, kb0 * BK, tid, rb);
     for (int kb = kb0; kb < kb1; ++kb, ++it) {
       const int stage = it % kStages;
       uint8_t* st = smem + stage * stage_bytes;
@@ -361,12 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it >= (uint32_t)kStages) mbar_wait(&bars[stage], ((it / kStages) - 1) & 1);
       // ---- stage A and B (split hi/lo)
       store_a<MODE>(st, st + Smem::kA, tid, ra);
-      stage_b<MODE>(op, K, kb * BK, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid);
+      store_b(op, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid, rb);
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
       // prefetch the next A block while the tensor core works on this one
-      if (kb + 1 < kb1) load_a<MODE>(op, M, K, m0, (kb + 1) * BK, tid, ra);
+      if (kb + 1 < kb1) {
+        load_a<MODE>(op, M, K, m0, (kb + 1) * BK, tid, ra);
+        load_b<MODE>(op, K, (kb + 1) * BK, tid, rb);
+      }
       if (tid == 0) {
         tc_fence_after();
         const uint32_t a_hi = smem_base + stage * stage_bytes;
@@ -507,12 +524,15 @@ bool tc_supported(int n_out) {
 }
 
 int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d_in, const float* W,
-                 int d_out, float* y, float* part, cudaStream_t s) {
+                 int d_out, float* y, float* part, int32_t* nparts_out, cudaStream_t s) {
   tc::Operands op{h, ldh, d_in, W, d_out, nullptr, 2 * d_out, (2 * d_out + 15) / 16 * 16};
+  // y == NULL: leave the partial tiles (count -> *nparts_out) for the aggregation
   return run_tc_gemm<tc::kFwd>(op, m_dev, 0, m_max, nullptr, d_in, d_in, part,
                                EpiStore{y, 2 * d_out}, s, K_SAGE_TRANSFORM,
-                               K_SAGE_TRANSFORM_REDUCE);
+                               K_SAGE_TRANSFORM_REDUCE, y == nullptr, nparts_out);
 }
+
+int64_t tc_y_part_floats(int64_t m_max, int64_t d_out) { return tc_part_floats(m_max, 2 * d_out); }
 
 int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
                    int d_out, const float* g, float* dW, float* part, int32_t* nparts_out,

@@ -352,7 +352,10 @@ class FusedTrainWorkspace:
         for l in range(L - 1):
             b = sw.bounds[L - 1 - l]
             n2 = 2 * self.dims[l + 1]
-            self.Y.append(torch.zeros((max(b.n_src_max, 1), n2), **f32))
+            # Y, or (tensor-core backend) its deferred split-K partial tiles
+            ny = max(b.n_src_max, 1) * n2
+            ny = max(ny, int(lib().mq_sage_y_parts_bytes(b.n_src_max, self.dims[l + 1])) // 4)
+            self.Y.append(torch.zeros(ny, **f32))
             self.G.append(torch.zeros((max(b.n_src_max, 1), n2), **f32))
             self.act[l + 1] = torch.zeros((max(b.n_dst_max, 1), self.ld_in[l + 1]), **f32)
             if l >= 1:
@@ -370,6 +373,7 @@ class FusedTrainWorkspace:
         # optimizer (mq_grad_src) instead of a reduction launch per layer
         self.dw_parts = [None] * L
         self.dw_nparts = torch.zeros(max(L, 1), dtype=torch.int32, device=dev)
+        self.y_nparts = torch.zeros(max(L, 1), dtype=torch.int32, device=dev)
         self._src_key = None
         self._src = None
 
@@ -422,43 +426,67 @@ class FusedTrainWorkspace:
 
     def launch_train(self, model: DeviceModel, stream, sw, ring=None, ring_len=0, world=1):
         """Forward, loss and backward of one batch; gradients land in
-        model.flat_g.  With ``ring`` the batch loss is committed to it
-        (mq_step_commit fused into the head); otherwise it accumulates in
-        ``self.loss``."""
+        model.flat_g (or its deferred partials, grad_src).  With ``ring`` the
+        batch loss is committed to it (mq_step_commit fused into the head);
+        otherwise it accumulates in ``self.loss``."""
+        for _, op in self.train_ops(model, sw, ring, ring_len, world):
+            op(stream)
+
+    def train_ops(self, model: DeviceModel, sw, ring=None, ring_len=0, world=1):
+        """The step as an ordered list of (kernel family, fn(stream)) — one C-ABI
+        call each, so a profiler can time every launch in isolation."""
         L, d, ld = self.L, self.dims, self.ld_in
         lb = lib()
         self.grad_src(model)  # allocate the deferred partial buffers before capture
+        ops = []
         for l in range(L - 1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
-            lb.mq_sage_transform(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts), b.n_src_max, d[l],
-                                 ptr(model.weight(l)), d[l + 1], ptr(self.Y[l]), ptr(self.scratch),
-                                 stream)
+            # tensor-core backend: Y stays as split-K partials, summed by the aggregation
+            yn = self.y_nparts[l:l + 1] if lb.mq_sage_y_deferred(d[l + 1]) else None
+            ops.append((f"sage_transform_l{l}", lambda s, l=l, hb=hb, b=b, yn=yn:
+                        lb.mq_sage_transform(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts),
+                                             b.n_src_max, d[l], ptr(model.weight(l)), d[l + 1],
+                                             None if yn is not None else ptr(self.Y[l]),
+                                             ptr(self.scratch),
+                                             ptr(self.Y[l]) if yn is not None else None,
+                                             ptr(yn), s)))
             z1 = (self.dh[L - 1], sw.hops[0].counts, ld[L - 1]) if l == L - 2 else (None, None, 0)
-            lb.mq_sage_aggregate(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals), ptr(sw.n_dst_dev(h)),
-                                 b.n_dst_max, ptr(self.Y[l]), d[l + 1], ptr(self.act[l + 1]),
-                                 ld[l + 1], ptr(self.G[l]), ptr(hb.counts), 2 * d[l + 1],
-                                 ptr(z1[0]), ptr(z1[1]), z1[2], stream)
+            ops.append((f"sage_aggregate_l{l}", lambda s, l=l, h=h, hb=hb, b=b, yn=yn, z1=z1:
+                        lb.mq_sage_aggregate(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
+                                             ptr(sw.n_dst_dev(h)), b.n_dst_max, ptr(self.Y[l]),
+                                             d[l + 1], ptr(yn),
+                                             ptr(hb.counts) if yn is not None else None,
+                                             ptr(self.act[l + 1]), ld[l + 1], ptr(self.G[l]),
+                                             ptr(hb.counts), 2 * d[l + 1], ptr(z1[0]),
+                                             ptr(z1[1]), z1[2], s)))
         hb0 = sw.hops[0]
-        lb.mq_sage_head(ptr(hb0.row_ptr), ptr(hb0.cols), ptr(hb0.vals), ptr(sw.n_targets),
-                        sw.batch_size, ptr(self.h_in(L - 1, sw)), ld[L - 1], d[L - 1],
-                        ptr(model.weight(L - 1)), self.C, ptr(sw.labels), None,
-                        ptr(self.dh[L - 1]), ld[L - 1], ptr(self.loss), ptr(sw.key), world,
-                        ptr(ring), ring_len, ptr(model.nonfinite), ptr(self.head_scratch), stream)
+        ops.append(("sage_head", lambda s:
+                    lb.mq_sage_head(ptr(hb0.row_ptr), ptr(hb0.cols), ptr(hb0.vals),
+                                    ptr(sw.n_targets), sw.batch_size, ptr(self.h_in(L - 1, sw)),
+                                    ld[L - 1], d[L - 1], ptr(model.weight(L - 1)), self.C,
+                                    ptr(sw.labels), None, ptr(self.dh[L - 1]), ld[L - 1],
+                                    ptr(self.loss), ptr(sw.key), world, ptr(ring), ring_len,
+                                    ptr(model.nonfinite), ptr(self.head_scratch), s)))
         for l in range(L - 2, -1, -1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
-            lb.mq_sage_scatter_bwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
-                                   ptr(sw.n_dst_dev(h)), b.n_dst_max, ptr(self.dh[l + 1]),
-                                   ld[l + 1], ptr(self.act[l + 1]), ld[l + 1], d[l + 1],
-                                   ptr(self.G[l]), stream)
+            ops.append((f"sage_scatter_bwd_l{l}", lambda s, l=l, h=h, hb=hb, b=b:
+                        lb.mq_sage_scatter_bwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
+                                               ptr(sw.n_dst_dev(h)), b.n_dst_max,
+                                               ptr(self.dh[l + 1]), ld[l + 1],
+                                               ptr(self.act[l + 1]), ld[l + 1], d[l + 1],
+                                               ptr(self.G[l]), s)))
             dp = self.dw_parts[l]
-            lb.mq_sage_transform_bwd(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts), b.n_src_max,
-                                     d[l], ptr(model.weight(l)), d[l + 1], ptr(self.G[l]),
-                                     ptr(model.grad(l)), ptr(self.dh[l]), ld[l],
-                                     ptr(self.scratch), ptr(dp),
-                                     ptr(self.dw_nparts[l:l + 1]) if dp is not None else None,
-                                     stream)
+            ops.append((f"sage_transform_bwd_l{l}", lambda s, l=l, hb=hb, b=b, dp=dp:
+                        lb.mq_sage_transform_bwd(ptr(self.h_in(l, sw)), ld[l], ptr(hb.counts),
+                                                 b.n_src_max, d[l], ptr(model.weight(l)),
+                                                 d[l + 1], ptr(self.G[l]), ptr(model.grad(l)),
+                                                 ptr(self.dh[l]), ld[l], ptr(self.scratch),
+                                                 ptr(dp),
+                                                 ptr(self.dw_nparts[l:l + 1])
+                                                 if dp is not None else None, s)))
+        return ops
 
 
 def current_stream(device) -> int:

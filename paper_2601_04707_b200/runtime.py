@@ -153,14 +153,15 @@ def _distributed():
 def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
     key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
            config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline,
-           config.fused_step)
+           config.fused_step, config.queue_capacity)
     r = getattr(replica, "_runner", None)
     if r is None or r[0] != key:
         runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
                             batch_size=config.batch_size, num_train=num_train, cache=cache,
                             optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
                             multi=multi, use_graph=config.use_graph,
-                            pipeline=config.pipeline, fused=config.fused_step)
+                            pipeline=config.pipeline, fused=config.fused_step,
+                            queue_depth=config.queue_capacity)
         replica._runner = (key, runner)
         return runner, True
     return r[1], False

@@ -1,21 +1,22 @@
 """One replica's per-iteration hot path as captured, pipelined CUDA graphs.
 
-A step = batch setup (device-side plan), L hops of sample + relabel, feature
-gather ("prep": the reference's sample + transfer stages, samplers.py:502-540
-and runtime.py:127-143) followed by SAGE forward, summed softmax-CE,
-backward and the optimizer ("train": nn.py:116-206 and the RaCoM window
-apply, runtime.py:167-195).
+A window = one batch of SAGE forward, summed softmax-CE, backward and the
+optimizer ("train": nn.py:116-206 and the RaCoM window apply,
+runtime.py:167-195) on a slot that was prepared earlier by the device batch
+queue (prep.PrepGroup: batch plan, L hops of sample + relabel, feature gather
+— the reference's sample + transfer stages, samplers.py:502-540,
+runtime.py:127-143).
 
 The multi-queue pipeline of MQ-GNN (sample -> transfer -> compute -> update,
-runtime.py:380-612) is expressed with two CUDA streams inside ONE graph per
-step: the prep of batch k+1 runs on the prep stream into the other of two
-double-buffered slots while batch k trains on the train stream; the graph
-joins both branches, so the host launches one graph per window and never
-synchronises.  Queue depth is the slot count (2).
+runtime.py:380-612) is two CUDA streams and two slot groups of depth Q: while
+the train stream works through group i one window at a time, the prep stream
+fills group 1-i with the next Q batches in ONE batched pass
+(mq_prep_batches).  Cross-stream order is carried by CUDA events recorded
+between graph launches, so the host never synchronises.
 
-Multi-replica (RaCoM) steps split the graph around the gradient exchange:
-[prep k+1 || train k + pack] -> f64 all-reduce of [grads | contributor
-count] (NCCL in production, gloo / in-process in tests) -> update graph.
+Multi-replica (RaCoM) windows split the train graph around the gradient
+exchange: [train + pack] -> f64 all-reduce of [grads | contributor count]
+(NCCL in production, gloo / in-process in tests) -> update graph.
 """
 
 from __future__ import annotations
@@ -26,7 +27,10 @@ import numpy as np
 import torch
 
 from ._lib import lib, ptr
-from .engine import FusedTrainWorkspace, SampleWorkspace, TrainWorkspace
+from .engine import FusedTrainWorkspace, TrainWorkspace
+from .prep import PrepGroup, PrepShared
+
+DEFAULT_QUEUE_DEPTH = 4
 
 
 class StepRunner:
@@ -35,9 +39,12 @@ class StepRunner:
     def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
                  multi: bool = False, use_graph: bool = True, pipeline: bool = True,
-                 ring_len: int = 1 << 16, fused: bool = True):
+                 ring_len: int = 1 << 16, fused: bool = True, queue_depth: int | None = None):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
+        Q = DEFAULT_QUEUE_DEPTH if queue_depth is None else int(queue_depth)
+        if Q < 1:
+            raise ValueError("queue depth must be at least 1")
         self.g = g
         self.model = model
         self.dm = model.dev
@@ -48,10 +55,13 @@ class StepRunner:
         self.multi = bool(multi)
         self.use_graph = use_graph
         self.pipeline = bool(pipeline)
+        self.Q = Q
         dev = g.device
         self.device = dev
-        self.slots = [SampleWorkspace(g, fanouts, batch_size)
-                      for _ in range(2 if self.pipeline else 1)]
+        self.shared = PrepShared(g, fanouts, batch_size, Q)
+        self.groups = [PrepGroup(g, fanouts, batch_size, Q, self.shared)
+                       for _ in range(2 if self.pipeline else 1)]
+        self.slots = [s for grp in self.groups for s in grp.slots]
         self.sw = self.slots[0]
         dims = [g.feature_dim] + [int(w.shape[1]) for w in model.weights]
         if dims[-1] != g.num_classes:
@@ -64,63 +74,66 @@ class StepRunner:
         self.num_train = int(num_train)
         self.batch_size = int(batch_size)
         self.perm = torch.zeros(max(self.num_train, 1), dtype=torch.int32, device=dev)
-        self.cursor = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cursor = torch.zeros(2, dtype=torch.int32, device=dev)  # [window, arrivals]
         self.ring_len = int(ring_len)
         self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
         self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
                        if self.multi else None)
         self.stream = torch.cuda.Stream(device=dev)       # train stream
         self.prep_stream = torch.cuda.Stream(device=dev)  # sample + transfer stream
+        self.ev_prep = [torch.cuda.Event() for _ in self.groups]
+        self.ev_train = [torch.cuda.Event() for _ in self.groups]
+        self._desc = {}
+        self._hphases = None
         self.graphs = {}
         self.launches_per_phase = {}
         self.windows_done = 0
         self.epoch = 0
         self._primed = False
+        self._last = (0, 0)
 
     # ---------------------------------------------------------------- epochs
     def begin_epoch(self, epoch: int, perm: np.ndarray):
         """Upload this epoch's shuffled train ids (plan_epoch, runtime.py:95-117)
-        and, when pipelined, prepare batch 0 (the pipeline prologue)."""
+        and, when pipelined, prepare the first slot group (the prologue)."""
         perm = np.asarray(perm)
         if perm.size != self.num_train:
             raise ValueError("permutation length changed; build a new StepRunner")
-        # stream-ordered and host-asynchronous: pinned staging + non_blocking
-        # copies, so an epoch boundary does not drain the step pipeline
         staged = torch.from_numpy(perm.astype(np.int32)).pin_memory()
-        key = torch.from_numpy(np.array([self.seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF, 0],
-                                        dtype=np.uint32).view(np.int32)).pin_memory()
+        # an in-flight prep pass may still read perm / cursor
+        self.stream.wait_stream(self.prep_stream)
         with torch.cuda.stream(self.stream):
             self.perm.copy_(staged, non_blocking=True)
             self.cursor.zero_()
-            for sw in self.slots:
-                sw.key.copy_(key, non_blocking=True)
+            for grp in self.groups:
+                grp.set_key(self.seed, epoch)
         self.epoch = epoch
         self.windows_done = 0
         n_windows = -(-self.num_train // (self.batch_size * self.world))
         self.dm.ensure_bias(self.dm.host_steps + n_windows + 8)
         self._primed = False
-        if self.pipeline and self.graphs:
+        if self.pipeline and (self.graphs or not self.use_graph):
             self._prologue()
 
     def _prologue(self):
-        with torch.cuda.stream(self.stream):
-            if self.use_graph:
-                self.graphs["prologue"].replay()
-            else:
-                self._enqueue_prep(self.slots[0], self.stream.cuda_stream)
+        self.prep_stream.wait_stream(self.stream)
+        self._run("prep0", self.prep_stream)
+        self.ev_prep[0].record(self.prep_stream)
         self._primed = True
 
     # --------------------------------------------------------------- enqueue
-    def _enqueue_setup(self, sw, s):
-        lib().mq_batch_setup(ptr(self.perm), self.num_train, self.batch_size, self.world,
-                             self.rank, ptr(self.cursor), ptr(sw.targets), ptr(sw.n_targets),
-                             ptr(sw.key), s)
+    def _prep_desc(self, gi: int, host: bool):
+        key = (gi, host)
+        if key not in self._desc:
+            self._desc[key] = self.groups[gi].desc(self.cache, self.perm,
+                                                   None if host else self.cursor,
+                                                   self.world, self.rank)
+        return self._desc[key]
 
     def _enqueue_prep(self, sw, s, setup=True):
-        if setup:
-            self._enqueue_setup(sw, s)
-        sw.launch(self.cache, s, key_on_device=True)
-        self.tw.launch_gather(sw, self.cache, s)
+        """One batched prep pass filling the whole group that holds slot ``sw``."""
+        gi = next(i for i, grp in enumerate(self.groups) if sw in grp.slots)
+        self.groups[gi].launch(self._prep_desc(gi, not setup), s)
 
     def _enqueue_train(self, sw, s, commit=True):
         if self.fused:
@@ -144,39 +157,18 @@ class StepRunner:
         else:  # scale 0: divide by the all-reduced contributor count (expected[k])
             self.tw.launch_optimizer(self.dm, self.optimizer, s, grad64=self.grad64, scale=0.0)
 
-    def _fork_join(self, s_train, prep_fn, train_fn):
-        """prep_fn on the prep stream in parallel with train_fn on s_train."""
-        cur = torch.cuda.current_stream(self.device)
-        self.prep_stream.wait_stream(cur)
-        with torch.cuda.stream(self.prep_stream):
-            prep_fn(self.prep_stream.cuda_stream)
-        train_fn(s_train)
-        cur.wait_stream(self.prep_stream)
-
     def _phases(self):
         """name -> fn(stream) for every graph this runner captures."""
         ph = {}
-        if not self.pipeline:
-            sw = self.slots[0]
-
-            def full(s):
-                self._enqueue_prep(sw, s)
-                self._enqueue_train(sw, s)
-                if not self.multi:
-                    self._enqueue_update(s)
-            ph["step0" if not self.multi else "compute0"] = full
-        else:
-            ph["prologue"] = lambda s: self._enqueue_prep(self.slots[0], s)
-            for i in (0, 1):
-                cur, nxt = self.slots[i], self.slots[1 - i]
-
-                def step(s, cur=cur, nxt=nxt):
-                    def train(st):
-                        self._enqueue_train(cur, st)
-                        if not self.multi:
-                            self._enqueue_update(st)
-                    self._fork_join(s, lambda sp: self._enqueue_prep(nxt, sp), train)
-                ph[("step" if not self.multi else "compute") + str(i)] = step
+        for gi, grp in enumerate(self.groups):
+            ph[f"prep{gi}"] = (lambda s, gi=gi: self.groups[gi].launch(self._prep_desc(gi, False),
+                                                                       s))
+            for q, sw in enumerate(grp.slots):
+                def train(s, sw=sw):
+                    self._enqueue_train(sw, s)
+                    if not self.multi:
+                        self._enqueue_update(s)
+                ph[f"train{gi}_{q}"] = train
         if self.multi:
             ph["update"] = self._enqueue_update
         return ph
@@ -189,12 +181,12 @@ class StepRunner:
             ts.append(self.cache.hit_miss)
         return ts
 
-    def _warm(self):
-        """Run every phase once eagerly (module loading, first-touch) and
-        restore all mutable state afterwards."""
+    def _warm(self, phases):
+        """Run phases once eagerly (module loading, first-touch) and restore
+        all mutable state afterwards."""
         snap = [t.clone() for t in self._state_tensors()]
         with torch.cuda.stream(self.stream):
-            for fn in self._phases().values():
+            for fn in phases.values():
                 fn(self.stream.cuda_stream)
         torch.cuda.synchronize(self.device)
         for t, v in zip(self._state_tensors(), snap):
@@ -203,13 +195,8 @@ class StepRunner:
         self.dm.nonfinite.zero_()
         torch.cuda.synchronize(self.device)
 
-    def capture(self):
-        """Eager warm-up (state restored), then capture each phase as a graph."""
-        if self.graphs:
-            return
-        self._warm()
-        self.launches_per_phase = {}
-        for name, fn in self._phases().items():
+    def _capture(self, phases):
+        for name, fn in phases.items():
             graph = torch.cuda.CUDAGraph()
             before = lib().mq_launch_count()
             with torch.cuda.graph(graph, stream=self.stream):
@@ -217,16 +204,32 @@ class StepRunner:
             self.launches_per_phase[name] = int(lib().mq_launch_count() - before)
             self.graphs[name] = graph
         torch.cuda.synchronize(self.device)
+
+    def capture(self):
+        """Eager warm-up (state restored), then capture each phase as a graph."""
+        if self.graphs:
+            return
+        phases = self._phases()
+        self._warm(phases)
+        self._capture(phases)
         if self.pipeline and not self._primed:
             self._prologue()
 
-    def kernels_per_step(self) -> int:
-        """libmqgnn kernel launches in one steady-state step (counted while the
-        step's graphs were captured)."""
+    def kernels_per_step(self) -> float:
+        """libmqgnn kernel launches per steady-state window (counted while the
+        graphs were captured): the train graph plus 1/Q of a prep pass."""
         ph = self.launches_per_phase
+        n = ph.get("train0_0", 0) + ph.get("prep0", 0) / self.Q
         if self.multi:
-            return ph.get("compute0", 0) + ph.get("update", 0)
-        return ph.get("step0", 0)
+            n += ph.get("update", 0)
+        return n
+
+    def _run(self, name, stream):
+        with torch.cuda.stream(stream):
+            if self.use_graph:
+                self.graphs[name].replay()
+            else:
+                self._phases()[name](stream.cuda_stream)
 
     def eager_window(self):
         """One window enqueued eagerly (not from the graphs) — used by the bench
@@ -240,24 +243,33 @@ class StepRunner:
         finally:
             self.use_graph = g
 
-    def _replay(self, name):
-        with torch.cuda.stream(self.stream):
-            if self.use_graph:
-                self.graphs[name].replay()
-            else:
-                self._phases()[name](self.stream.cuda_stream)
-
     # RaCoM protocol (racom.WindowDriver): compute -> exchange grad64 -> apply.
-    # A lone replica's compute already contains its update ("step" graph).
+    # A lone replica's train graph already contains its update.
     def compute_window(self):
-        if self.pipeline and not self._primed:
-            self._prologue()
-        i = self.windows_done % 2 if self.pipeline else 0
-        self._replay(("compute" if self.multi else "step") + str(i))
+        k, Q = self.windows_done, self.Q
+        q = k % Q
+        if self.pipeline:
+            if not self._primed:
+                self._prologue()
+            gi = (k // Q) % 2
+            if q == 0:  # the next group fills the other half while this one trains
+                nxt = 1 - gi
+                self.prep_stream.wait_event(self.ev_train[nxt])
+                self._run(f"prep{nxt}", self.prep_stream)
+                self.ev_prep[nxt].record(self.prep_stream)
+                self.stream.wait_event(self.ev_prep[gi])
+        else:
+            gi = 0
+            if q == 0:
+                self._run("prep0", self.stream)
+        self._run(f"train{gi}_{q}", self.stream)
+        if self.pipeline and q == Q - 1:
+            self.ev_train[gi].record(self.stream)
+        self._last = (gi, q)
 
     def apply_window(self):
         if self.multi:
-            self._replay("update")
+            self._run("update", self.stream)
         self.dm.host_steps += 1
         self.windows_done += 1
 
@@ -294,10 +306,14 @@ class StepRunner:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
 
     def read_counts(self, slot: int | None = None) -> dict:
-        """Device counts of a slot's batch: targets and (n_dst, n_src, nnz) per hop."""
+        """Device counts of a slot's batch: targets and (n_dst, n_src, nnz) per hop
+        (default: the slot trained last)."""
         torch.cuda.synchronize(self.device)
-        sw = self.slots[slot if slot is not None else
-                        ((self.windows_done - 1) % 2 if self.pipeline else 0)]
+        if slot is None:
+            gi, q = self._last
+            sw = self.groups[gi].slots[q]
+        else:
+            sw = self.slots[slot]
         c = torch.cat([sw.n_targets] + [hb.counts for hb in sw.hops]).cpu().tolist()
         hops, nd = [], c[0]
         for h in range(len(sw.hops)):
@@ -321,108 +337,116 @@ class StepRunner:
 
     # ------------------------------------------------- host-input (e2e) path
     def capture_host_input(self):
-        """Graphs whose prep reads targets staged by the host (no device plan):
-        slot i trains while the other slot's host-staged batch is prepared."""
-        if "host0" in self.graphs:
+        """Graphs whose prep reads targets staged by the host (no device plan)
+        and whose train step leaves the batch loss for a per-step read-back."""
+        if self._hphases is not None:
             return
         if self.multi:
             raise NotImplementedError("host-input steps are single-replica")
-        self._stage = [torch.zeros(4, dtype=torch.int32, pin_memory=True) for _ in self.slots]
-        self._loss_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        Q = self.Q
+        # a ring of pinned staging rows: a row set is reused only after the copies
+        # that read it (4 groups earlier) have executed, so the host never waits
+        # on the group that is about to train
+        self._stage = [torch.zeros((Q, 4), dtype=torch.int32, pin_memory=True) for _ in range(4)]
+        self._stage_ev = [torch.cuda.Event() for _ in range(4)]
+        self._stage_i = 0
+        self._loss_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
+        self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
         phases = {}
-        if not self.pipeline:
-            sw = self.slots[0]
+        for gi, grp in enumerate(self.groups):
+            phases[f"hprep{gi}"] = (lambda s, gi=gi: self.groups[gi].launch(
+                self._prep_desc(gi, True), s))
+            for q, sw in enumerate(grp.slots):
+                def htrain(s, sw=sw):
+                    self._enqueue_train(sw, s, commit=False)
+                    self._enqueue_update(s)
+                phases[f"htrain{gi}_{q}"] = htrain
+        if self.use_graph:
+            self._warm(phases)
+            self._capture(phases)
+        self._hphases = phases
 
-            def host0(s):
-                self._enqueue_prep(sw, s, setup=False)
-                self._enqueue_train(sw, s, commit=False)
-                self._enqueue_update(s)
-            phases["host0"] = host0
-        else:
-            phases["hostpro"] = lambda s: self._enqueue_prep(self.slots[0], s, setup=False)
-            for i in (0, 1):
-                cur, nxt = self.slots[i], self.slots[1 - i]
+    def _hrun(self, name, stream):
+        with torch.cuda.stream(stream):
+            if self.use_graph:
+                self.graphs[name].replay()
+            else:
+                self._hphases[name](stream.cuda_stream)
 
-                def hstep(s, cur=cur, nxt=nxt):
-                    def train(st):
-                        self._enqueue_train(cur, st, commit=False)
-                        self._enqueue_update(st)
-                    self._fork_join(s, lambda sp: self._enqueue_prep(nxt, sp, setup=False), train)
-                phases[f"host{i}"] = hstep
-        snap = [t.clone() for t in self._state_tensors()]
-        with torch.cuda.stream(self.stream):
-            for fn in phases.values():
-                fn(self.stream.cuda_stream)
-        torch.cuda.synchronize(self.device)
-        for t, v in zip(self._state_tensors(), snap):
-            t.copy_(v)
-        self.tw.loss.zero_()
-        torch.cuda.synchronize(self.device)
-        for name, fn in phases.items():
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=self.stream):
-                fn(torch.cuda.current_stream().cuda_stream)
-            self.graphs[name] = graph
-        torch.cuda.synchronize(self.device)
-
-    def _stage_batch(self, slot: int, targets_pinned: torch.Tensor, batch_id: int):
-        sw = self.slots[slot]
-        n = int(targets_pinned.numel())
-        st = self._stage[slot]
-        st.numpy().view(np.uint32)[:] = (n, self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF,
-                                        batch_id & 0xFFFFFFFF)
-        sw.targets[:n].copy_(targets_pinned, non_blocking=True)
-        sw.n_targets.copy_(st[0:1], non_blocking=True)
-        sw.key.copy_(st[1:4], non_blocking=True)
+    def _stage_group(self, gi: int, group, stream):
+        """H2D: every slot's targets and {n, seed, epoch, batch} (empty slots: n = 0)."""
+        grp = self.groups[gi]
+        si = self._stage_i
+        self._stage_i = (si + 1) % len(self._stage)
+        st = self._stage[si]
+        self._stage_ev[si].synchronize()
+        sv = st.numpy().view(np.uint32)
+        for q in range(self.Q):
+            if q < len(group):
+                bid, t = group[q]
+                sv[q] = (int(t.numel()), self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF,
+                         bid & 0xFFFFFFFF)
+            else:
+                sv[q] = (0, self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF, 0)
+        with torch.cuda.stream(stream):
+            for q, (bid, t) in enumerate(group):
+                grp.targets[q, :t.numel()].copy_(t, non_blocking=True)
+            grp.n_targets.copy_(st[:, 0:1], non_blocking=True)
+            grp.key.copy_(st[:, 1:4], non_blocking=True)
+        self._stage_ev[si].record(stream)
 
     def run_host_batches(self, batches):
         """Public host-buffer entry point (one replica): for each pinned int32
         target batch (batch_id, targets) the step H2D-copies its inputs, trains,
-        and D2H-reads its summed loss.  With pipelining, batch k+1 is staged and
-        prepared while batch k trains; every batch still gets its own H2D copy
-        and its own loss read-back.  Yields (batch_id, loss)."""
+        and D2H-reads its summed loss.  Batches are prepared Q at a time (the
+        device queue); group j+1 is staged and prepared while group j trains.
+        Every batch still gets its own H2D copy and its own loss read-back,
+        one step behind the launch.  Yields (batch_id, loss)."""
         batches = list(batches)
         if not batches:
             return
-        with torch.cuda.stream(self.stream):
-            if not self.pipeline:
-                for bid, t in batches:
-                    self._stage_batch(0, t, bid)
-                    self.graphs["host0"].replay()
-                    self._loss_host.copy_(self.tw.loss, non_blocking=True)
+        self.capture_host_input()
+        Q = self.Q
+        chunks = [batches[i:i + Q] for i in range(0, len(batches), Q)]
+        prep_s = self.prep_stream if self.pipeline else self.stream
+        ngroups = len(self.groups)
+
+        def stage_and_prep(j):
+            gi = j % ngroups
+            prep_s.wait_event(self.ev_train[gi])
+            self._stage_group(gi, chunks[j], prep_s)
+            self._hrun(f"hprep{gi}", prep_s)
+            self.ev_prep[gi].record(prep_s)
+
+        stage_and_prep(0)
+        pending = None
+        nstep = 0
+        for j, chunk in enumerate(chunks):
+            gi = j % ngroups
+            if j + 1 < len(chunks) and self.pipeline:
+                stage_and_prep(j + 1)
+            elif j > 0 and not self.pipeline:
+                stage_and_prep(j)
+            self.stream.wait_event(self.ev_prep[gi])
+            for q, (bid, _) in enumerate(chunk):
+                slot = nstep % 2
+                self._hrun(f"htrain{gi}_{q}", self.stream)
+                with torch.cuda.stream(self.stream):
+                    self._loss_host[slot:slot + 1].copy_(self.tw.loss, non_blocking=True)
                     self.tw.loss.zero_()
-                    self.stream.synchronize()
-                    self.dm.host_steps += 1
-                    yield bid, float(self._loss_host[0])
-                return
-            # the host runs one step ahead: step k's loss is read back (its own
-            # D2H + event wait) right after step k+1 has been launched
-            if not hasattr(self, "_loss_ring_host"):
-                self._loss_ring_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
-                self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
-            self._stage_batch(0, batches[0][1], batches[0][0])
-            self.graphs["hostpro"].replay()
-            pending = None
-            for k, (bid, t) in enumerate(batches):
-                cur, nxt = k % 2, 1 - (k % 2)
-                if k + 1 < len(batches):
-                    self._stage_batch(nxt, batches[k + 1][1], batches[k + 1][0])
-                else:  # nothing left to prepare: an empty batch keeps the graph fixed
-                    self.slots[nxt].n_targets.zero_()
-                self.graphs[f"host{cur}"].replay()
-                self._loss_ring_host[cur:cur + 1].copy_(self.tw.loss, non_blocking=True)
-                self.tw.loss.zero_()
-                self._loss_ev[cur].record(self.stream)
+                self._loss_ev[slot].record(self.stream)
                 self.dm.host_steps += 1
+                nstep += 1
                 if pending is not None:
                     pbid, pslot = pending
                     self._loss_ev[pslot].synchronize()
-                    yield pbid, float(self._loss_ring_host[pslot])
-                pending = (bid, cur)
-            pbid, pslot = pending
-            self._loss_ev[pslot].synchronize()
-            yield pbid, float(self._loss_ring_host[pslot])
+                    yield pbid, float(self._loss_host[pslot])
+                pending = (bid, slot)
+            self.ev_train[gi].record(self.stream)
+        pbid, pslot = pending
+        self._loss_ev[pslot].synchronize()
+        yield pbid, float(self._loss_host[pslot])
 
     def step_from_host(self, targets_pinned: torch.Tensor, batch_id: int) -> float:
-        """Single synchronous step from one host batch (no cross-step overlap)."""
+        """Single synchronous step from one host batch."""
         return next(iter(self.run_host_batches([(batch_id, targets_pinned)])))[1]

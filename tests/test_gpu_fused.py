@@ -48,9 +48,12 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
     runner.begin_epoch(0, perm)
     s = runner.stream
     for j in range(windows):
+        q = j % runner.Q  # one batched prep pass fills Q slots
+        sw = runner.groups[0].slots[q]
         with torch.cuda.stream(s):
-            runner._enqueue_prep(runner.slots[0], s.cuda_stream)
-            runner._enqueue_train(runner.slots[0], s.cuda_stream, commit=False)
+            if q == 0:
+                runner._enqueue_prep(sw, s.cuda_stream)
+            runner._enqueue_train(sw, s.cuda_stream, commit=False)
             runner.tw.materialize_grads(state.dev, s.cuda_stream)
         torch.cuda.synchronize()
         loss = float(runner.tw.loss.item())
@@ -69,6 +72,7 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
         # bar stays rounding-level (the flip itself is legitimate fp32 noise).
         for l in range(L - 1):
             ours = runner.tw.act[l + 1][:cache["pre"][l].shape[0], :cache["pre"][l].shape[1]]
+            # (act is shared by all slots and was last written by slot q's step)
             cache["pre"][l] = ours.cpu().numpy()
         ograds = onn.backward(mb.layers, model.weights, cache, dlogits)
         for l, (a, b) in enumerate(zip(grads, ograds)):
@@ -137,3 +141,14 @@ def test_fused_epoch_matches_unfused(golden_sampling):
     np.testing.assert_allclose(out[True][0], out[False][0], rtol=1e-4)
     for a, b in zip(out[True][1], out[False][1]):
         assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max()
+
+
+def test_fused_ffma_backend(cfg1):
+    """The fp32 CUDA-core backend of the dense transforms (no deferred partials)."""
+    from paper_2601_04707_b200._lib import lib
+    old = lib().mq_get_gemm_backend()
+    lib().mq_set_gemm_backend(0)
+    try:
+        _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=8, windows=2)
+    finally:
+        lib().mq_set_gemm_backend(old)

@@ -68,7 +68,7 @@ def test_transform_fwd_bwd(backend, rows, d_in, d_out):
                       dtype=torch.float32, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     lib().mq_sage_transform(ptr(th), ld, ptr(m_dev), m_max, d_in, ptr(tW), d_out, ptr(ty),
-                            ptr(scr), s)
+                            ptr(scr), None, None, s)
     y = ty.cpu().numpy()[:rows]
     lib().mq_sage_transform_bwd(ptr(th), ld, ptr(m_dev), m_max, d_in, ptr(tW), d_out, ptr(tg),
                                 ptr(tdW), ptr(tdh), ld, ptr(scr), None, None, s)
