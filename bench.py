@@ -303,22 +303,27 @@ def run_ours(args):
     plan_sizes = np.minimum(args.batch, np.maximum(
         0, n_train - np.arange(windows * world) * args.batch))
 
-    def one_window():
-        if runner.windows_done >= windows:
-            epoch[0] += 1
-            runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
-        k = runner.windows_done
-        for r in range(world):
-            seeds_done[0] += int(plan_sizes[k * world + r])
-        if world == 1:
-            runner.step()
-        else:
-            runner.compute_window()
-            driver._reduce([runner.grad64])
-            runner.apply_window()
+    def run_windows(n):
+        """n windows; a single replica issues whole slot groups as one graph each."""
+        left = n
+        while left > 0:
+            if runner.windows_done >= windows:
+                epoch[0] += 1
+                runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
+            k = runner.windows_done
+            if world == 1:
+                done = runner.steps(left, windows)
+            else:
+                runner.compute_window()
+                driver._reduce([runner.grad64])
+                runner.apply_window()
+                done = 1
+            for kk in range(k, k + done):
+                for r in range(world):
+                    seeds_done[0] += int(plan_sizes[kk * world + r])
+            left -= done
 
-    for _ in range(args.warmup):
-        one_window()
+    run_windows(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -333,8 +338,7 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(runner.stream)
     t_wall = time.perf_counter()
-    for _ in range(args.steps):
-        one_window()
+    run_windows(args.steps)
     ev1.record(runner.stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall

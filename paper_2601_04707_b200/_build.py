@@ -17,10 +17,10 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OUT = PKG / "libmqgnn.so"
+OUT = Path(os.environ.get("MQ_BUILD_OUT", PKG / "libmqgnn.so"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr"] + os.environ.get("MQ_EXTRA_NVCC_FLAGS", "").split()
 
 
 def nvcc() -> str:
@@ -44,7 +44,7 @@ def _stale(out: Path, deps) -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     srcs = sources()
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
-    objdir = ROOT / "build" / "obj"
+    objdir = ROOT / "build" / ("obj" + os.environ.get("MQ_BUILD_TAG", ""))
     objdir.mkdir(parents=True, exist_ok=True)
     exe = nvcc()
 

@@ -328,11 +328,18 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
       }
       if (active) {
         float2 b = make_float2(0.f, 0.f);
-        for (int s = 0; s < S; ++s) {
-          const float2 p = __ldcg(reinterpret_cast<const float2*>(part + s * stride +
-                                                                  (int64_t)r * ldy + N + c));
-          b.x += p.x;
-          b.y += p.y;
+        for (int s0 = 0; s0 < S; s0 += 8) {
+          float2 p[8];
+#pragma unroll
+          for (int ss = 0; ss < 8; ++ss)
+            p[ss] = s0 + ss < S ? __ldcg(reinterpret_cast<const float2*>(
+                                      part + (s0 + ss) * stride + (int64_t)r * ldy + N + c))
+                                : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int ss = 0; ss < 8; ++ss) {
+            b.x += p[ss].x;
+            b.y += p[ss].y;
+          }
         }
         const float zx = acc.x + b.x, zy = acc.y + b.y;
         *reinterpret_cast<float2*>(out + c) = make_float2(zx > 0.f ? zx : 0.f, zy > 0.f ? zy : 0.f);
@@ -365,16 +372,32 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
     const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
     if (vec2) {
       const int n2 = N / 2;
-      for (int c = lane; c < n2; c += 32) {
-        const float2 g = *reinterpret_cast<const float2*>(dh + (int64_t)r * lddh + 2 * c);
-        const float2 a = *reinterpret_cast<const float2*>(act + (int64_t)r * ldact + 2 * c);
-        const float2 dz = make_float2(a.x > 0.f ? g.x : 0.f, a.y > 0.f ? g.y : 0.f);
-        *reinterpret_cast<float2*>(G + (int64_t)r * ldg + N + 2 * c) = dz;
-        for (int e = e0; e < e1; ++e) {
-          const int32_t col = __ldg(&cols[e]);
-          const float val = __ldg(&vals[e]);
-          atomicAdd(reinterpret_cast<float2*>(G + (int64_t)col * ldg + 2 * c),
-                    make_float2(val * dz.x, val * dz.y));
+      for (int cb = 0; cb < n2; cb += 32) {
+        const int c = cb + lane;
+        const bool active = c < n2;
+        float2 dz = make_float2(0.f, 0.f);
+        if (active) {
+          const float2 g = *reinterpret_cast<const float2*>(dh + (int64_t)r * lddh + 2 * c);
+          const float2 a = *reinterpret_cast<const float2*>(act + (int64_t)r * ldact + 2 * c);
+          dz = make_float2(a.x > 0.f ? g.x : 0.f, a.y > 0.f ? g.y : 0.f);
+          *reinterpret_cast<float2*>(G + (int64_t)r * ldg + N + 2 * c) = dz;
+        }
+        for (int eb = e0; eb < e1; eb += 32) {
+          const int me = eb + lane;
+          int32_t my_col = 0;
+          float my_val = 0.f;
+          if (me < e1) {
+            my_col = __ldg(&cols[me]);
+            my_val = __ldg(&vals[me]);
+          }
+          const int m = min(32, e1 - eb);
+          for (int t = 0; t < m; ++t) {
+            const int32_t col = __shfl_sync(0xffffffffu, my_col, t);
+            const float val = __shfl_sync(0xffffffffu, my_val, t);
+            if (active)
+              atomicAdd(reinterpret_cast<float2*>(G + (int64_t)col * ldg + 2 * c),
+                        make_float2(val * dz.x, val * dz.y));
+          }
         }
       }
     } else {
@@ -416,7 +439,7 @@ struct HeadArgs {
   int R;
 };
 
-constexpr int kHeadRows = 16;              // target rows per CTA: one warp per row
+constexpr int kHeadRows = 8;               // target rows per CTA: one warp per row
 constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
@@ -455,12 +478,6 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     s_val[warp][lane] = __ldg(&a.vals[e0 + lane]);
   }
   if (lane == 0) s_ne[warp] = ne;
-  if (a.dh != nullptr) {  // transposed copy for phase 4 (conflict-free float4 rows)
-    for (int i = tid; i < C * d2p; i += kHeadThreads) {
-      const int c = i / d2p, k = i % d2p;
-      WsT[i] = k < d2 ? __ldg(a.W + (int64_t)k * C + c) : 0.f;
-    }
-  }
   if (Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0) {  // same layout: float4 copy
     const float4* src = reinterpret_cast<const float4*>(a.W);
     float4* dst = reinterpret_cast<float4*>(Ws);
@@ -531,8 +548,19 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
   __syncthreads();
 
-  // 2. logits = both W: thread (4-row quad, class), float4 over k
-  for (int item = tid; item < (R / 4) * C; item += kHeadThreads) {
+  // 2. logits = both W: thread (4-row quad, class), float4 over k.  The
+  //    threads without a logits item build W^T (smem -> smem) for phase 4.
+  const int n_items = (R / 4) * C;
+  if (a.dh != nullptr && n_items >= kHeadThreads && tid == 0) {
+    for (int i = 0; i < C * d2p; ++i) WsT[i] = Ws[(i % d2p) * Cp + i / d2p];
+  }
+  if (a.dh != nullptr && tid >= n_items) {
+    for (int i = tid - n_items; i < C * d2p; i += kHeadThreads - n_items) {
+      const int c = i / d2p, k = i % d2p;
+      WsT[i] = Ws[k * Cp + c];
+    }
+  }
+  for (int item = tid; item < n_items; item += kHeadThreads) {
     const int ib = 4 * (item / C), c = item % C;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int k = 0; k < d2p; k += 4) {
@@ -901,7 +929,7 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                n_classes, (long long)smem);
   cudaStream_t s = as_stream(stream);
   static thread_local int64_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > configured) {  // (static smem counts against the 48 KB default too)
     MQ_CUDA(cudaFuncSetAttribute(sage_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     configured = smem;

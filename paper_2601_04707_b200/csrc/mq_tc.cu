@@ -138,6 +138,20 @@ __device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
   lo.w = tf32_rn(v.w - hi.w);
 }
 
+// ---- optional per-phase timeline of CTA 0 (build with -DMQ_TC_TRACE)
+#ifdef MQ_TC_TRACE
+__device__ unsigned long long g_tc_trace[32];
+__device__ __forceinline__ void trace(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && i < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tc_trace[i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
+
 // ------------------------------------------------------------ work split
 struct Work {
   int tiles_m, S, kb_per;  // m tiles, k splits, k blocks per split
@@ -333,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
   if ((int)blockIdx.x >= items || M <= 0) return;
 
+  trace(0);
   const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(&s_tmem, tmem_cols);
   if (tid == 0) {
@@ -346,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stage_bytes = Smem::stage_bytes(Np);
   const uint32_t smem_base = smem_u32(smem);
   const uint32_t idesc = instr_desc(Np, false, false);
+  trace(1);
 
   uint32_t it = 0;  // global k-block counter (stage/phase bookkeeping)
   uint32_t acc_phase = 0;
@@ -368,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 rb[kBPerThread][4];
     load_a<MODE>(op, M, K, m0, kb0 * BK, tid, ra);
     load_b<MODE>(op, K, kb0 * BK, tid, rb);
+    trace(2);
     for (int kb = kb0; kb < kb1; ++kb, ++it) {
       const int stage = it % kStages;
       uint8_t* st = smem + stage * stage_bytes;
@@ -379,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
+      trace(3 + 2 * (kb - kb0));
       // prefetch the next A block while the tensor core works on this one
       if (kb + 1 < kb1) {
         load_a<MODE>(op, M, K, m0, (kb + 1) * BK, tid, ra);
@@ -405,12 +423,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bars[stage]);
       }
+      trace(4 + 2 * (kb - kb0));
     }
     // ---- accumulator ready -> partial tile
     if (tid == 0) mma_commit(&bars[kStages]);
     mbar_wait(&bars[kStages], acc_phase & 1);
     ++acc_phase;
     tc_fence_after();
+    trace(20);
     if (warp < 4) {
       const int m = warp * 32 + lane;
       const int gm = m0 + m;
@@ -433,11 +453,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    trace(21);
   }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols);
   }
+  trace(22);
 }
 
 // fixed-order split reduction + layer epilogue (same decomposition as the GEMM)
@@ -563,5 +585,12 @@ int mq_set_gemm_backend(int32_t backend) {
 }
 
 int mq_get_gemm_backend(void) { return g_gemm_backend; }
+
+#ifdef MQ_TC_TRACE
+int mq_debug_tc_trace(unsigned long long* out) {
+  MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_trace, sizeof(unsigned long long) * 32));
+  return MQ_OK;
+}
+#endif
 
 }  // extern "C"

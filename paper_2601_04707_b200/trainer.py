@@ -206,12 +206,27 @@ class StepRunner:
         torch.cuda.synchronize(self.device)
 
     def capture(self):
-        """Eager warm-up (state restored), then capture each phase as a graph."""
+        """Eager warm-up (state restored), then capture each phase as a graph,
+        plus (single replica, pipelined) one graph per slot group that runs
+        all Q windows of the group while the other group is prepared."""
         if self.graphs:
             return
         phases = self._phases()
         self._warm(phases)
         self._capture(phases)
+        if self.pipeline and not self.multi:
+            for gi in range(2):
+                def group(s, gi=gi):
+                    cur = torch.cuda.current_stream(self.device)
+                    self.prep_stream.wait_stream(cur)
+                    with torch.cuda.stream(self.prep_stream):
+                        self.groups[1 - gi].launch(self._prep_desc(1 - gi, False),
+                                                   self.prep_stream.cuda_stream)
+                    for q in range(self.Q):
+                        ph = phases[f"train{gi}_{q}"]
+                        ph(cur.cuda_stream)
+                    cur.wait_stream(self.prep_stream)
+                self._capture({f"group{gi}": group})
         if self.pipeline and not self._primed:
             self._prologue()
 
@@ -279,6 +294,41 @@ class StepRunner:
             raise RuntimeError("multi-replica runners need the exchange: use racom.WindowDriver")
         self.compute_window()
         self.apply_window()
+
+    def steps(self, n: int, epoch_windows: int | None = None) -> int:
+        """Up to n windows of this epoch (async).  Whole slot groups run as ONE
+        graph launch each (prep of the next group forked inside it), the
+        rest window by window.  Returns the number of windows issued."""
+        if self.multi:
+            raise RuntimeError("multi-replica runners need the exchange: use racom.WindowDriver")
+        if epoch_windows is None:
+            epoch_windows = -(-self.num_train // (self.batch_size * self.world))
+        n = min(n, epoch_windows - self.windows_done)
+        done = 0
+        Q = self.Q
+        while done < n:
+            k = self.windows_done
+            if (self.use_graph and self.pipeline and "group0" in self.graphs and k % Q == 0
+                    and n - done >= Q):
+                if not self._primed:
+                    self._prologue()
+                gi = (k // Q) % 2
+                with torch.cuda.stream(self.stream):
+                    # the group graph joins its own prep branch; prep(1-gi)
+                    # overwrites the other half, whose last trains preceded it
+                    self.stream.wait_event(self.ev_prep[gi])
+                    self.graphs[f"group{gi}"].replay()
+                self.ev_train[gi].record(self.stream)
+                self.ev_prep[1 - gi].record(self.stream)
+                self._last = (gi, Q - 1)
+                self.dm.host_steps += Q
+                self.windows_done += Q
+                done += Q
+            else:
+                self.compute_window()
+                self.apply_window()
+                done += 1
+        return done
 
     def state64(self) -> torch.Tensor:
         from .racom import _pack_state

@@ -152,3 +152,31 @@ def test_fused_ffma_backend(cfg1):
         _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=8, windows=2)
     finally:
         lib().mq_set_gemm_backend(old)
+
+
+def test_group_graphs_match_window_graphs(golden_sampling):
+    """steps(n) (one graph per slot group, prep forked inside) trains like n
+    single-window graph launches; the epoch tail runs window by window."""
+    hg = make_g2(golden_sampling)
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, golden_sampling["g2/mask10"])
+    perm = epoch_permutation(hg.train_mask, 5, 0)
+    B = 64
+    n_win = -(-perm.size // B)
+    outs = []
+    for grouped in (False, True):
+        st = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        r = mq.StepRunner(g, st, fanouts=(4, 3), batch_size=B, num_train=perm.size, cache=cache,
+                          seed=5, queue_depth=3)
+        r.begin_epoch(0, perm)
+        r.capture()
+        if grouped:
+            assert r.steps(n_win) == n_win
+        else:
+            for _ in range(n_win):
+                r.step()
+        r.check_finite()
+        outs.append((r.losses(n_win), [w.cpu().numpy() for w in st.weights]))
+    np.testing.assert_allclose(outs[1][0], outs[0][0], rtol=1e-5)
+    for a, b in zip(outs[1][1], outs[0][1]):
+        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
