@@ -386,6 +386,68 @@ int mq_f64_to_f32(const double* in64, double divisor, float* out32, int64_t n, v
  * split-K on the CUDA cores.  Process-wide; for tests and A/B measurement. */
 int mq_set_gemm_backend(int32_t backend);
 int mq_get_gemm_backend(void);
+/* Programmatic dependent launch for the step's kernel chains (default on):
+ * kernel k+1 is scheduled while kernel k runs and waits on the device for
+ * k's completion (griddepcontrol), hiding the launch gap.  Process-wide; for
+ * A/B measurement.  Takes effect for launches (and graph captures) made
+ * after the call. */
+int mq_set_pdl(int32_t on);
+int mq_get_pdl(void);
+
+/* ------------------------------------------------ full-graph evaluation
+ * The per-epoch evaluate() of the reference driver (bench.py:82-87) over
+ * nn.full_forward's sage arm (nn.py:218-250) and nn.accuracy (nn.py:253-256).
+ * A layer is  Y = h [W_top | W_bot]  (mq_full_transform: n x 2 d_out, tcgen05
+ * 3xTF32, `part` holds mq_full_transform_part_floats floats) followed by
+ *   out[v] = relu?( f32(1/deg v) * sum_{arcs v->u, CSR order} Y_top[u] + Y_bot[v] )
+ * (mq_full_aggregate; row_off/col = the loop-stripped CSR, deg 0 -> 0 * ...;
+ * pad columns [n_out, ldo) are zeroed; scratch: mq_full_agg_scratch_bytes).
+ * The segment sums are deterministic (no atomics).  mq_accuracy adds to
+ * *correct_dev the number of ids whose first-max logit column equals the
+ * label. */
+int64_t mq_full_transform_part_floats(int64_t n_nodes, int32_t d_out);
+int mq_full_transform(const float* h, int32_t ldh, int64_t n_nodes, int32_t d_in, const float* W,
+                      int32_t d_out, float* y, float* part, void* stream);
+int64_t mq_full_agg_scratch_bytes(int64_t n_arcs, int32_t n_out);
+int mq_full_aggregate(const int64_t* row_off, const int32_t* col, int64_t n_nodes, int64_t n_arcs,
+                      const float* y, int32_t ldy, int32_t n_out, int32_t relu, float* out,
+                      int32_t ldo, void* scratch, void* stream);
+int mq_accuracy(const float* logits, int32_t ld, int32_t n_classes, const int32_t* labels,
+                const int32_t* ids, int64_t n_ids, unsigned long long* correct_dev,
+                void* stream);
+
+/* ------------------------------------------------- per-epoch cache refresh
+ * GNS residency on the device (cache.py:41-108, samplers.py:113-135).
+ * mq_in_degrees: deg[v] = #arcs u->v of the stored CSR (graph.py in_degrees);
+ *   col is the loop-stripped column array, `loops` (nullable) the per-row count
+ *   of stripped self loops, which count toward their own row's in-degree.
+ * mq_degree_probs: probs = deg / total (cache_probs_degree; total = stored
+ *   arcs; total 0 -> uniform).
+ * mq_walk_probs: cache_probs_walk — p0 = 1/|train| on train nodes, `steps`
+ *   rounds of p <- D A p + p with D = min(fanout, deg)/deg, the per-row flow
+ *   summed sequentially in CSR order (stored loops at their sorted position),
+ *   then p / sum(p) with NumPy's pairwise summation; *bad_dev = 1 if the total
+ *   is not positive.  scratch: mq_walk_scratch_bytes(n).  train_mask: u8 [n].
+ * mq_refresh_select: refresh_cache's resident set as chosen[v] in {0,1}:
+ *   take = min(budget, #positive) nodes by the exponential keys u^(1/w), u the
+ *   refresh contract's random(#positive) (oracle/philox.py), largest first,
+ *   ties to the lower id; then a WOR Fisher-Yates choice of budget - take ids
+ *   from the rest (ascending).  counts_dev[0] = #positive, [1] = take.
+ *   scratch: mq_refresh_scratch_bytes(n).  No host synchronisation. */
+int mq_in_degrees(const int32_t* col, int64_t n_nodes, int64_t n_arcs, const int32_t* loops,
+                  int64_t* deg, void* stream);
+int mq_degree_probs(const int64_t* deg, int64_t n_nodes, int64_t total, double* probs,
+                    void* stream);
+int64_t mq_walk_scratch_bytes(int64_t n_nodes);
+int mq_walk_probs(const int64_t* row_off, const int32_t* col, int64_t n_nodes, const int32_t* loops,
+                  const int64_t* deg, const uint8_t* train_mask, int64_t n_train, int32_t fanout,
+                  int32_t steps, double* probs, int32_t* bad_dev, void* scratch, void* stream);
+int64_t mq_refresh_scratch_bytes(int64_t n_nodes);
+int mq_refresh_select(const double* probs, int64_t n_nodes, int64_t budget, uint64_t seed,
+                      uint64_t epoch, uint8_t* chosen, int64_t* counts_dev, void* scratch,
+                      void* stream);
+/* host restatement of the refresh contract's random(n) (tests) */
+int mq_refresh_uniforms_host(uint64_t seed, uint64_t epoch, int64_t n, double* out);
 
 /* ------------------------------------------------------------- utilities */
 /* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */

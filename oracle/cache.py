@@ -4,6 +4,8 @@
 * ``gather_features`` — ``mqpipe/cache.py:123-134``
 * ``degree_probs``    — ``mqpipe/cache.py:41-48``
 * ``walk_probs``      — ``mqpipe/cache.py:51-76``
+* ``weighted_sample_without_replacement`` — ``mqpipe/samplers.py:113-135``
+* ``refresh_cache_ids`` — ``mqpipe/cache.py:79-108`` (resident ids)
 """
 
 from __future__ import annotations
@@ -60,3 +62,35 @@ def walk_probs(row_offsets, col_indices, train_mask, fanout, steps):
     if total <= 0:
         raise ValueError("walk produced no probability mass")
     return p / total
+
+
+def weighted_sample_without_replacement(weights, k, rng):
+    """Exponential keys u^(1/w), descending, ties to the lower index
+    (samplers.py:113-135)."""
+    w = np.asarray(weights, dtype=np.float64)
+    positive = np.flatnonzero(w > 0)
+    if k > positive.size:
+        raise ValueError(f"k={k} exceeds {positive.size} positive weights")
+    if k == 0:
+        return np.empty(0, dtype=np.int64)
+    u = rng.random(positive.size)
+    keys = u ** (1.0 / w[positive])
+    order = np.lexsort((positive, -keys))
+    return positive[order[:k]].astype(np.int64)
+
+
+def refresh_cache_ids(num_nodes, probs, fraction, rng):
+    """Resident ids of refresh_cache (cache.py:79-108): ceil(f*|V|) drawn WOR
+    by probs, shortfall filled uniformly from the zero-probability rest."""
+    if not (0.0 < fraction <= 1.0):
+        raise ValueError("fraction must lie in (0, 1]")
+    probs = np.asarray(probs, dtype=np.float64)
+    budget = int(np.ceil(fraction * num_nodes))
+    positive = int(np.count_nonzero(probs > 0))
+    take = min(budget, positive)
+    chosen = weighted_sample_without_replacement(probs, take, rng)
+    if take < budget:
+        rest = np.setdiff1d(np.arange(num_nodes), chosen, assume_unique=False)
+        extra = rng.choice(rest, size=budget - take, replace=False)
+        chosen = np.concatenate([chosen, extra])
+    return np.sort(chosen.astype(np.int64))

@@ -11,6 +11,7 @@ Follows ``mqpipe/nn.py`` of the reference:
 * ``adam_step``    — ``nn.py:191-206`` (beta 0.9/0.999, eps 1e-8; NumPy-2
   weak-scalar f32 arithmetic)
 * ``sgd_step``     — ``nn.py:209-215``
+* ``full_forward`` — ``nn.py:218-250`` (sage arm), ``accuracy`` — ``nn.py:253-256``
 
 Blocks are any objects with ``rows, cols, values, num_dst, dst_in_src``.
 """
@@ -159,3 +160,32 @@ def sgd_step(model, grads):
         w -= model.learning_rate * g.astype(w.dtype)
         _check_finite("sgd_step", w)
     return model
+
+
+def full_forward(row_offsets, col_indices, features, weights):
+    """Whole-graph SAGE forward (nn.py:218-250, sage arm): mean over the
+    out-neighbours with stored self loops dropped (nn.py:236-238), concat the
+    node's own embedding, ReLU except after the last layer."""
+    n = row_offsets.size - 1
+    h = features.astype(np.float32)
+    last = len(weights) - 1
+    src_all = np.repeat(np.arange(n), np.diff(row_offsets))
+    keep = col_indices != src_all
+    src, dst = src_all[keep], col_indices[keep]
+    counts = np.bincount(src, minlength=n).astype(np.float32)
+    inv = np.where(counts > 0, 1.0 / np.maximum(counts, 1), 0.0)
+    for l, w in enumerate(weights):
+        agg = np.zeros_like(h)
+        np.add.at(agg, src, h[dst])
+        agg *= inv[:, None]
+        z = np.concatenate([agg, h], axis=1) @ w
+        h = np.maximum(z, 0) if l < last else z
+    _check_finite("full_forward", h)
+    return h
+
+
+def accuracy(logits, labels):
+    """nn.py:253-256 (first-max argmax)."""
+    if logits.shape[0] == 0:
+        return 0.0
+    return float((logits.argmax(axis=1) == np.asarray(labels)).mean())

@@ -117,3 +117,45 @@ class RowStream:
         a = np.asarray(a)
         x = draws(*self.key, count=size)
         return a[fisher_yates_positions(x, a.size, size)]
+
+
+# ---------------------------------------------------------------------------
+# Injected draws of the per-epoch cache refresh (refresh_cache, cache.py:79-108;
+# weighted_sample_without_replacement, samplers.py:113-135).  Two reserved row
+# streams of the (seed, epoch) key, disjoint from every sampling stream
+# (batch ids < 2^32 - 1):
+#   random(n)[i] = ((x_{4i} >> 5) * 2^26 + (x_{4i+1} >> 6)) * 2^-53
+#                  of stream (batch 0xFFFFFFFF, hop 0xFFFFFFFE, row 0)
+#                  (NumPy's 53-bit double from two 32-bit words);
+#   choice(a, k)  = partial Fisher-Yates of stream (batch 0xFFFFFFFF,
+#                  hop 0xFFFFFFFF, row 0), the sampling contract's selection.
+REFRESH_BATCH = 0xFFFFFFFF
+REFRESH_HOP_RANDOM = 0xFFFFFFFE
+REFRESH_HOP_CHOICE = 0xFFFFFFFF
+
+
+def refresh_uniforms(seed: int, epoch: int, n: int) -> np.ndarray:
+    """random(n) of the refresh contract: f64 uniforms in [0, 1)."""
+    if n <= 0:
+        return np.empty(0, dtype=np.float64)
+    x = draws(seed, epoch, REFRESH_BATCH, REFRESH_HOP_RANDOM, 0, 4 * n).reshape(n, 4)
+    a = (x[:, 0] >> np.uint32(5)).astype(np.float64)
+    b = (x[:, 1] >> np.uint32(6)).astype(np.float64)
+    return (a * 67108864.0 + b) / 9007199254740992.0
+
+
+class RefreshRng:
+    """Duck-typed ``rng`` for refresh_cache: ``random`` and WOR ``choice``."""
+
+    def __init__(self, seed: int, epoch: int):
+        self.seed, self.epoch = int(seed), int(epoch)
+
+    def random(self, n):
+        return refresh_uniforms(self.seed, self.epoch, int(n))
+
+    def choice(self, a, size, replace=False):
+        if replace:
+            raise ValueError("the injected-draw contract is WOR only")
+        a = np.asarray(a)
+        x = draws(self.seed, self.epoch, REFRESH_BATCH, REFRESH_HOP_CHOICE, 0, int(size))
+        return a[fisher_yates_positions(x, a.size, int(size))]

@@ -6,11 +6,13 @@ Compute runs in hand-written CUDA kernels reached through the C-ABI library
 """
 
 from .graph import DeviceGraph
-from .cache import (DeviceCache, cache_probs_degree, gather_features, lookup, refresh_cache,
+from .cache import (DeviceCache, RefreshStream, cache_probs_degree, cache_probs_walk,
+                    gather_features, lookup, refresh_cache, refresh_mask,
                     weighted_sample_without_replacement)
 from .samplers import (Block, MiniBatch, PhiloxStream, SamplerParams, SamplingError,
                        build_minibatch, node_wise_block, sample_node_wise)
-from .nn import (ModelState, accuracy, adam_step, backward, batch_loss, forward, init_model,
+from .nn import (ModelState, accuracy, adam_step, backward, batch_loss, evaluate, forward,
+                 full_forward, init_model,
                  loss_and_grads, sage_forward, sgd_step)
 from .racom import (DistExchange, LocalExchange, WindowDriver, apply_update, compute_sync_period,
                     staleness_cost, sync_models)

@@ -84,6 +84,20 @@ SIGNATURES = {
                                I32, P, P, P]),
     "mq_set_gemm_backend": (C.c_int, [I32]),
     "mq_get_gemm_backend": (C.c_int, []),
+    "mq_set_pdl": (C.c_int, [I32]),
+    "mq_get_pdl": (C.c_int, []),
+    "mq_full_transform_part_floats": (I64, [I64, I32]),
+    "mq_full_transform": (C.c_int, [P, I32, I64, I32, P, I32, P, P, P]),
+    "mq_full_agg_scratch_bytes": (I64, [I64, I32]),
+    "mq_full_aggregate": (C.c_int, [P, P, I64, I64, P, I32, I32, I32, P, I32, P, P]),
+    "mq_accuracy": (C.c_int, [P, I32, I32, P, P, I64, P, P]),
+    "mq_in_degrees": (C.c_int, [P, I64, I64, P, P, P]),
+    "mq_degree_probs": (C.c_int, [P, I64, I64, P, P]),
+    "mq_walk_scratch_bytes": (I64, [I64]),
+    "mq_walk_probs": (C.c_int, [P, P, I64, P, P, P, I64, I32, I32, P, P, P, P]),
+    "mq_refresh_scratch_bytes": (I64, [I64]),
+    "mq_refresh_select": (C.c_int, [P, I64, I64, U64, U64, P, P, P, P]),
+    "mq_refresh_uniforms_host": (C.c_int, [U64, U64, I64, P]),
     "mq_prep_scratch_bytes": (I64, [I32, I32]),
     "mq_prep_batches": (C.c_int, [P, P]),
     "mq_prof_enable": (C.c_int, [C.c_int]),
@@ -96,7 +110,7 @@ SIGNATURES = {
 
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
                if res is C.c_int and name not in ("mq_version", "mq_prof_num_kernels",
-                                                       "mq_get_gemm_backend",
+                                                       "mq_get_gemm_backend", "mq_get_pdl",
                                                        "mq_sage_dw_deferred",
                                                        "mq_sage_y_deferred")}
 

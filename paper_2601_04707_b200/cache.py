@@ -5,9 +5,9 @@ Reference: ``mqpipe/cache.py`` —
   * ``CacheState`` (``cache.py:20-38``): sorted ``cached_ids``, bool
     ``cached_mask``, ``cached_features`` copy, locked hit/miss counters;
   * ``lookup`` / ``gather_features`` (``cache.py:111-134``);
-  * ``refresh_cache`` (``cache.py:79-108``) — per-epoch residency, host side
-    here (it runs once per epoch, off the per-iteration path; SURVEY §8f f1
-    moves it on device next).
+  * ``cache_probs_degree`` / ``cache_probs_walk`` / ``refresh_cache``
+    (``cache.py:41-108``) — per-epoch residency, on the device
+    (mq_refresh.cu) under the refresh injected-draw contract.
 
 Per-epoch device structures built from the mask:
   * ``bits``      uint32 [ceil(n/32)] residency bitmap;
@@ -105,17 +105,78 @@ def _pack_bits(mask: torch.Tensor) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------- per-epoch
-def cache_probs_degree(g: DeviceGraph) -> np.ndarray:
-    """In-degree importance (cache.py:41-48)."""
-    deg = g.in_degrees().double().cpu().numpy()
-    total = deg.sum()
-    if total == 0:
-        return np.full(g.num_nodes, 1.0 / g.num_nodes)
-    return deg / total
+class RefreshStream:
+    """Key of the per-epoch refresh's injected draws (oracle/philox.py
+    RefreshRng): ``random(n)`` and the shortfall ``choice`` come from reserved
+    Philox row streams of (seed, epoch), so the device refresh reproduces the
+    reference's refresh_cache driven by the same draws."""
+
+    def __init__(self, seed: int, epoch: int = 0):
+        self.seed, self.epoch = int(seed), int(epoch)
+
+    def uniforms(self, n) -> np.ndarray:
+        """random(n) of the contract (the library's host restatement; tests)."""
+        out = np.empty(int(n), dtype=np.float64)
+        lib().mq_refresh_uniforms_host(self.seed, self.epoch, int(n),
+                                       out.ctypes.data if n else None)
+        return out
+
+
+def _stream(g):
+    return torch.cuda.current_stream(g.device).cuda_stream
+
+
+def cache_probs_degree(g: DeviceGraph) -> torch.Tensor:
+    """In-degree importance (cache.py:41-48) as a device f64 tensor."""
+    deg = g.in_degrees()
+    probs = torch.empty(max(g.num_nodes, 1), dtype=torch.float64, device=g.device)
+    lib().mq_degree_probs(ptr(deg), g.num_nodes, g.num_edges, ptr(probs), _stream(g))
+    return probs[:g.num_nodes]
+
+
+def cache_probs_walk(g: DeviceGraph, fanout: int, steps: int) -> torch.Tensor:
+    """Sampling-reachability walk p <- D A p + p from the training set
+    (cache.py:51-76), bit-exact, as a device f64 tensor."""
+    train = np.asarray(g.train_mask, dtype=bool)
+    n_train = int(train.sum())
+    if n_train == 0:
+        raise ValueError("walk probabilities need a nonempty training set")
+    dev = g.device
+    deg = g.in_degrees()
+    tm = torch.as_tensor(train.astype(np.uint8)).to(dev)
+    probs = torch.empty(g.num_nodes, dtype=torch.float64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    scr = torch.empty(int(lib().mq_walk_scratch_bytes(g.num_nodes)), dtype=torch.uint8, device=dev)
+    lib().mq_walk_probs(ptr(g.row_off), ptr(g.col), g.num_nodes, ptr(g.loops), ptr(deg), ptr(tm),
+                        n_train, int(fanout), int(steps), ptr(probs), ptr(bad), ptr(scr),
+                        _stream(g))
+    if int(bad.item()):
+        raise ValueError("walk produced no probability mass")
+    return probs
+
+
+def refresh_mask(g: DeviceGraph, probs: torch.Tensor, fraction: float,
+                 key: RefreshStream) -> torch.Tensor:
+    """Device resident set of refresh_cache (cache.py:79-108) as a bool mask."""
+    if not (0.0 < fraction <= 1.0):
+        raise ValueError("fraction must lie in (0, 1]")
+    n = g.num_nodes
+    dev = g.device
+    probs = torch.as_tensor(probs, dtype=torch.float64).to(dev).contiguous()
+    if probs.shape != (n,):
+        raise ValueError("probs must have one entry per node")
+    budget = int(math.ceil(fraction * n))
+    chosen = torch.empty(n, dtype=torch.uint8, device=dev)
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    scr = torch.empty(int(lib().mq_refresh_scratch_bytes(n)), dtype=torch.uint8, device=dev)
+    lib().mq_refresh_select(ptr(probs), n, budget, key.seed, key.epoch, ptr(chosen), ptr(counts),
+                            ptr(scr), _stream(g))
+    return chosen.view(torch.bool)
 
 
 def weighted_sample_without_replacement(weights, k: int, rng) -> np.ndarray:
-    """Exponential-key WOR draw (samplers.py:113-135)."""
+    """Exponential-key WOR draw (samplers.py:113-135), host form for a
+    caller-supplied generator (the device refresh does not use it)."""
     w = np.asarray(weights, dtype=np.float64)
     if np.any(w < 0) or not np.all(np.isfinite(w)):
         raise ValueError("weights must be finite and nonnegative")
@@ -131,9 +192,18 @@ def weighted_sample_without_replacement(weights, k: int, rng) -> np.ndarray:
 
 
 def refresh_cache(g: DeviceGraph, probs, fraction: float, rng) -> DeviceCache:
-    """ceil(fraction * |V|) residents drawn WOR by probs (cache.py:79-108)."""
+    """ceil(fraction * |V|) residents drawn WOR by probs (cache.py:79-108).
+
+    With a :class:`RefreshStream` key (the injected-draw contract) the whole
+    selection runs on the device (mq_refresh_select).  Any other ``rng``
+    (e.g. a NumPy Generator, whose draw stream a GPU cannot replay) is
+    honoured on the host, as the reference does."""
+    if isinstance(rng, RefreshStream):
+        return DeviceCache(g, refresh_mask(g, probs, fraction, rng), fraction)
     if not (0.0 < fraction <= 1.0):
         raise ValueError("fraction must lie in (0, 1]")
+    if isinstance(probs, torch.Tensor):
+        probs = probs.detach().cpu().numpy()
     probs = np.asarray(probs, dtype=np.float64)
     if probs.shape != (g.num_nodes,):
         raise ValueError("probs must have one entry per node")

@@ -32,6 +32,8 @@ static std::vector<cudaEvent_t> g_free_events;
 static double g_total_ms[K_COUNT];
 static int64_t g_launches[K_COUNT];
 static std::atomic<int64_t> g_launch_count{0};
+static std::atomic<bool> g_pdl_on{true};
+bool pdl_enabled() { return g_pdl_on.load(std::memory_order_relaxed); }
 
 static cudaEvent_t take_event() {
   if (!g_free_events.empty()) {
@@ -130,5 +132,12 @@ int mq_prof_read(double* total_ms, int64_t* launches, int32_t n) {
 }
 
 int64_t mq_launch_count(void) { return mq::g_launch_count.load(); }
+
+int mq_set_pdl(int32_t on) {
+  mq::g_pdl_on.store(on != 0);
+  return MQ_OK;
+}
+
+int mq_get_pdl(void) { return mq::g_pdl_on.load() ? 1 : 0; }
 
 }  // extern "C"

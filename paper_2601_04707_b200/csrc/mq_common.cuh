@@ -6,6 +6,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <utility>
+
 #include "../../include/mqgnn.h"
 #include "mq_kernels.h"
 
@@ -62,6 +64,42 @@ struct ProfScope {
   ProfScope(int kernel_id, cudaStream_t stream);
   ~ProfScope();
 };
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Kernels of the step's dependent chains
+// are launched with programmatic stream serialisation, so kernel k+1 is
+// scheduled while kernel k still runs and blocks in griddepcontrol.wait until
+// k has completed and its writes are visible.  Every PDL-launched kernel
+// calls MQ_PDL_ENTRY() first, unconditionally (a grid that exits without
+// waiting would let its successor overtake the grid before it).  Without the
+// launch attribute both instructions are no-ops.
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#define MQ_PDL_ENTRY() \
+  do {                 \
+    ::mq::pdl_wait();  \
+    ::mq::pdl_trigger(); \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Random123 constants), shared host/device so that host and GPU

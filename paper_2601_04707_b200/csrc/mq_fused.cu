@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_kernel(
     const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
     const float* __restrict__ y, int N, float* __restrict__ act, int ldact, ZeroRange z0,
     ZeroRange z1) {
+  MQ_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
   const int n = *n_dst_dev;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
     const float* __restrict__ part, const int32_t* __restrict__ nparts_dev,
     const int32_t* __restrict__ m_dev, int N, float* __restrict__ act, int ldact, ZeroRange z0,
     ZeroRange z1) {
+  MQ_PDL_ENTRY();
   constexpr int U = 4, SU = 4;
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
     const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
     const float* __restrict__ dh, int lddh, const float* __restrict__ act, int ldact, int N,
     float* __restrict__ G) {
+  MQ_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
   const int n = *n_dst_dev;
@@ -444,6 +447,7 @@ constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
+  MQ_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   constexpr int R = kHeadRows;
   const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp;
@@ -740,6 +744,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
 // dW = fixed-order sum of the head's per-CTA partials (materialising API)
 __global__ void head_dw_reduce_kernel(const float* __restrict__ part, int nparts, int total,
                                       float* __restrict__ dW) {
+  MQ_PDL_ENTRY();
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x)
     dW[o] = fixed_order_sum(part + o, total, nparts);
 }
@@ -824,15 +829,15 @@ int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* 
   {
     ProfScope ps(K_SAGE_AGG, s);
     if (y_nparts_dev)
-      sage_aggregate_parts_kernel<<<blocks, kAggThreads, 0, s>>>(
+      MQ_CUDA(launch_k(sage_aggregate_parts_kernel, dim3(blocks), dim3(kAggThreads), 0, s, 
           row_ptr, cols, vals, n_dst_dev, y, y_nparts_dev, y_rows_dev, d_out, act, ldact,
           ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
-          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
+          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats}));
     else
-      sage_aggregate_kernel<<<blocks, kAggThreads, 0, s>>>(
+      MQ_CUDA(launch_k(sage_aggregate_kernel, dim3(blocks), dim3(kAggThreads), 0, s, 
           row_ptr, cols, vals, n_dst_dev, y, d_out, act, ldact,
           ZeroRange{zero0, zero0_rows_dev, zero0_row_floats},
-          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats});
+          ZeroRange{zero1, zero1_rows_dev, zero1_row_floats}));
   }
   MQ_LAUNCH_CHECK("sage_aggregate");
   return MQ_OK;
@@ -851,8 +856,8 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
   {
     ProfScope ps(K_SAGE_SCATTER, s);
-    sage_scatter_bwd_kernel<<<blocks, kAggThreads, 0, s>>>(row_ptr, cols, vals, n_dst_dev, dh, lddh,
-                                                           act, ldact, d_out, g);
+    MQ_CUDA(launch_k(sage_scatter_bwd_kernel, dim3(blocks), dim3(kAggThreads), 0, s, row_ptr, cols, vals, n_dst_dev, dh, lddh,
+                                                           act, ldact, d_out, g));
   }
   MQ_LAUNCH_CHECK("sage_scatter_bwd");
   return MQ_OK;
@@ -960,13 +965,13 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
   a.R = R;
   {
     ProfScope ps(K_SAGE_HEAD, s);
-    sage_head_kernel<<<G, kHeadThreads, smem, s>>>(a);
+    MQ_CUDA(launch_k(sage_head_kernel, dim3(G), dim3(kHeadThreads), smem, s, a));
   }
   MQ_LAUNCH_CHECK("sage_head");
   if (dW != nullptr) {
     const int total = 2 * d * n_classes;
     ProfScope ps(K_SAGE_DW_REDUCE, s);
-    head_dw_reduce_kernel<<<ceil_div(total, 256), 256, 0, s>>>(a.part, G, total, dW);
+    MQ_CUDA(launch_k(head_dw_reduce_kernel, dim3(ceil_div(total, 256)), dim3(256), 0, s, a.part, G, total, dW));
   }
   MQ_LAUNCH_CHECK("head_dw_reduce");
   return MQ_OK;

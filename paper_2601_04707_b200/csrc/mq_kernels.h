@@ -41,7 +41,16 @@
   X(K_SAGE_DW, "sage_dw")                         \
   X(K_SAGE_DW_REDUCE, "sage_dw_reduce")           \
   X(K_SAGE_DH, "sage_dh")                         \
-  X(K_SAGE_DH_REDUCE, "sage_dh_reduce")
+  X(K_SAGE_DH_REDUCE, "sage_dh_reduce")         \
+  X(K_FULL_TRANSFORM, "full_transform")         \
+  X(K_FULL_TRANSFORM_REDUCE, "full_transform_reduce") \
+  X(K_FULL_AGG, "full_aggregate")               \
+  X(K_FULL_AGG_FIXUP, "full_aggregate_fixup")   \
+  X(K_ACCURACY, "accuracy")                     \
+  X(K_REFRESH_DEGREE, "refresh_degree")         \
+  X(K_REFRESH_PROBS, "refresh_probs")           \
+  X(K_REFRESH_WALK, "refresh_walk")             \
+  X(K_REFRESH_SELECT, "refresh_select")
 
 namespace mq {
 enum KernelId {

@@ -333,6 +333,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(Operands op, const int32_t* m_dev, int m_static, const int32_t* k_dev,
                    int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out) {
+  MQ_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kStages + 1];
@@ -466,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <class Epi>
 __global__ void tc_reduce_kernel(const float* __restrict__ part, const int32_t* m_dev, int m_static,
                                  const int32_t* k_dev, int k_static, int N, int grid_gemm, Epi epi) {
+  MQ_PDL_ENTRY();
   const int M = m_dev ? *m_dev : m_static;
   const int K = k_dev ? *k_dev : k_static;
   const Work wk = choose_work(M, K, grid_gemm);
@@ -505,8 +507,8 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
   const int grid = tc_grid(m_max, k_max);
   {
     ProfScope ps(kid, s);
-    tc::tc_gemm_kernel<MODE><<<grid, tc::kThreads, smem, s>>>(op, m_dev, m_static, k_dev, k_static,
-                                                             part, nparts_out);
+    MQ_CUDA(launch_k(tc::tc_gemm_kernel<MODE>, dim3(grid), dim3(tc::kThreads), smem, s, op, m_dev, m_static, k_dev, k_static,
+                                                             part, nparts_out));
   }
   MQ_LAUNCH_CHECK("tc_gemm");
   if (skip_reduce) return MQ_OK;
@@ -515,8 +517,8 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
   if (rb > kNumSMs * 4) rb = kNumSMs * 4;
   {
     ProfScope ps(kid_red, s);
-    tc::tc_reduce_kernel<Epi><<<rb, 256, 0, s>>>(part, m_dev, m_static, k_dev, k_static, op.N, grid,
-                                                 epi);
+    MQ_CUDA(launch_k(tc::tc_reduce_kernel<Epi>, dim3(rb), dim3(256), 0, s, part, m_dev, m_static, k_dev, k_static, op.N, grid,
+                                                 epi));
   }
   MQ_LAUNCH_CHECK("tc_reduce");
   return MQ_OK;
@@ -555,6 +557,15 @@ int tc_transform(const float* h, int ldh, const int32_t* m_dev, int m_max, int d
 }
 
 int64_t tc_y_part_floats(int64_t m_max, int64_t d_out) { return tc_part_floats(m_max, 2 * d_out); }
+
+// Y = h [W_top | W_bot] over a host-known row count (full-graph evaluation)
+int tc_transform_rows(const float* h, int ldh, int64_t n, int d_in, const float* W, int d_out,
+                      float* y, float* part, cudaStream_t s) {
+  tc::Operands op{h, ldh, d_in, W, d_out, nullptr, 2 * d_out, (2 * d_out + 15) / 16 * 16};
+  return run_tc_gemm<tc::kFwd>(op, nullptr, (int)n, (int)n, nullptr, d_in, d_in, part,
+                               EpiStore{y, 2 * d_out}, s, K_FULL_TRANSFORM,
+                               K_FULL_TRANSFORM_REDUCE);
+}
 
 int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_max, int d_in,
                    int d_out, const float* g, float* dW, float* part, int32_t* nparts_out,

@@ -61,6 +61,7 @@ __global__ void softmax_ce_kernel(const float* __restrict__ logits, int ld,
 
 __global__ void step_commit_kernel(double* loss_acc, const uint32_t* key, int world, double* ring,
                                    int ring_len) {
+  MQ_PDL_ENTRY();
   int k = (int)((key[2] / (uint32_t)world) % (uint32_t)ring_len);
   ring[k] = loss_acc[0];
   loss_acc[0] = 0.0;
@@ -122,6 +123,7 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
                             double scale, int64_t n, int32_t* __restrict__ step,
                             const float* __restrict__ bias, int bias_len, float lr,
                             int32_t* __restrict__ nonfinite, GradSrc src) {
+  MQ_PDL_ENTRY();
   const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
   if (t < 1 || t > bias_len) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
@@ -157,6 +159,7 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
                            const double* __restrict__ g64, double scale, int64_t n, float lr,
                            int32_t* __restrict__ step, int32_t* __restrict__ nonfinite,
                            GradSrc src) {
+  MQ_PDL_ENTRY();
   const int t = step[0] + 1;
   const double count = grad_count(g64, scale, n);
   int bad = 0;
@@ -179,6 +182,7 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ a, double* __restric
 __global__ void pack_grads_kernel(const float* __restrict__ a, int64_t n,
                                   const int32_t* __restrict__ n_targets, double* __restrict__ b,
                                   GradSrc src) {
+  MQ_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
        i += (int64_t)gridDim.x * blockDim.x)
     b[i] = i < n ? (double)grad_at(src, a, i) : (n_targets[0] > 0 ? 1.0 : 0.0);
@@ -259,8 +263,8 @@ int mq_adam(float* w, float* m, float* v, const float* grad32, const double* gra
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_ADAM, s);
-    adam_kernel<<<elem_blocks(n), 256, 0, s>>>(w, m, v, grad32, grad64, grad_scale, n, step_dev,
-                                               bias, bias_len, lr, nonfinite, make_src(src));
+    MQ_CUDA(launch_k(adam_kernel, dim3(elem_blocks(n)), dim3(256), 0, s, w, m, v, grad32, grad64, grad_scale, n, step_dev,
+                                               bias, bias_len, lr, nonfinite, make_src(src)));
   }
   MQ_LAUNCH_CHECK("adam");
   return MQ_OK;
@@ -274,8 +278,8 @@ int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scal
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_SGD, s);
-    sgd_kernel<<<elem_blocks(n), 256, 0, s>>>(w, grad32, grad64, grad_scale, n, lr, step_dev,
-                                              nonfinite, make_src(src));
+    MQ_CUDA(launch_k(sgd_kernel, dim3(elem_blocks(n)), dim3(256), 0, s, w, grad32, grad64, grad_scale, n, lr, step_dev,
+                                              nonfinite, make_src(src)));
   }
   MQ_LAUNCH_CHECK("sgd");
   return MQ_OK;
@@ -288,7 +292,7 @@ int mq_step_commit(double* loss_acc, const uint32_t* key_dev, int32_t world, dou
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_STEP_BUMP, s);
-    step_commit_kernel<<<1, 1, 0, s>>>(loss_acc, key_dev, world, loss_ring, ring_len);
+    MQ_CUDA(launch_k(step_commit_kernel, dim3(1), dim3(1), 0, s, loss_acc, key_dev, world, loss_ring, ring_len));
   }
   MQ_LAUNCH_CHECK("step_commit");
   return MQ_OK;
@@ -313,8 +317,8 @@ int mq_pack_grads(const float* grad, int64_t n, const int32_t* n_targets_dev, do
   cudaStream_t s = as_stream(stream);
   {
     ProfScope ps(K_CONVERT, s);
-    pack_grads_kernel<<<elem_blocks(n + 1), 256, 0, s>>>(grad, n, n_targets_dev, out64,
-                                                         make_src(src));
+    MQ_CUDA(launch_k(pack_grads_kernel, dim3(elem_blocks(n + 1)), dim3(256), 0, s, grad, n, n_targets_dev, out64,
+                                                         make_src(src)));
   }
   MQ_LAUNCH_CHECK("pack_grads");
   return MQ_OK;

@@ -81,6 +81,10 @@ class DeviceGraph:
             self.col = out_col[:max(kept, 1)].clone() if kept != e else out_col
             self.num_arcs = kept
             self.self_loops = e - kept
+            # stripped loops per row: they still count toward in-degrees and
+            # the cache walk's flow (cache.py:41-76 use the stored CSR)
+            self.loops = (((row_off[1:] - row_off[:-1]) - (out_off[1:] - out_off[:-1]))
+                          .to(torch.int32) if self.self_loops else None)
             del row_off, col, scratch
             self.labels = _as_tensor(g.labels, torch.int32, dev)
             self.feature_placement = feature_placement
@@ -107,10 +111,12 @@ class DeviceGraph:
 
     def in_degrees(self) -> torch.Tensor:
         """In-degree counts of the stored CSR (graph.py:47-49), self loops
-        included, as the reference's cache_probs_degree uses them."""
-        src = self.source
-        col = _as_tensor(src.col_indices, torch.int64, self.device)
-        return torch.bincount(col, minlength=self.num_nodes)
+        included, as the reference's cache_probs_degree uses them (int64,
+        computed on the device by mq_in_degrees)."""
+        deg = torch.empty(max(self.num_nodes, 1), dtype=torch.int64, device=self.device)
+        lib().mq_in_degrees(ptr(self.col), self.num_nodes, self.num_arcs, ptr(self.loops),
+                            ptr(deg), torch.cuda.current_stream(self.device).cuda_stream)
+        return deg[:self.num_nodes]
 
 
 def _host(a):

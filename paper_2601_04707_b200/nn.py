@@ -260,3 +260,85 @@ def accuracy(logits, labels) -> float:
         return 0.0
     lab = torch.as_tensor(labels, device=logits.device)
     return float((logits.argmax(dim=1) == lab.long()).float().mean().item())
+
+
+# ------------------------------------------------------- full-graph evaluation
+class _EvalWorkspace:
+    """Per-(graph, layer widths) buffers of full_forward, reused across epochs."""
+
+    def __init__(self, g, dims):
+        dev = g.device
+        n = max(g.num_nodes, 1)
+        self.dims = tuple(dims)
+        self.y, self.part, self.out, self.scratch = [], [], [], []
+        for l in range(len(dims) - 1):
+            d_out = dims[l + 1]
+            last = l == len(dims) - 2
+            self.y.append(torch.empty((n, 2 * d_out), dtype=torch.float32, device=dev))
+            self.part.append(torch.empty(int(lib().mq_full_transform_part_floats(n, d_out)),
+                                         dtype=torch.float32, device=dev))
+            self.out.append(torch.empty((n, d_out if last else round_up(d_out, 4)),
+                                        dtype=torch.float32, device=dev))
+            self.scratch.append(torch.empty(
+                int(lib().mq_full_agg_scratch_bytes(g.num_arcs, d_out)), dtype=torch.uint8,
+                device=dev))
+        # the transform scratch is only live inside one layer: share the largest
+        big = max(self.part, key=lambda t: t.numel())
+        self.part = [big] * len(self.part)
+        self.correct = torch.zeros(1, dtype=torch.int64, device=dev)
+
+
+def _eval_ws(g, dims):
+    ws = getattr(g, "_eval_ws", None)
+    if ws is None or ws.dims != tuple(dims):
+        ws = _EvalWorkspace(g, dims)
+        g._eval_ws = ws
+    return ws
+
+
+def full_forward(g, state: ModelState) -> torch.Tensor:
+    """Exact whole-graph forward pass (nn.py:218-250, sage arm) on the device.
+
+    Per layer: Y = h [W_top | W_bot] (tcgen05 3xTF32 GEMM over every node),
+    then z[v] = f32(1/deg v) * sum_{v->u} Y_top[u] + Y_bot[v] over the
+    loop-stripped CSR (nn.py:236-243), ReLU except after the last layer.
+    Returns logits [n, num_classes] (fp32 re-association of the reference;
+    DESIGN.md §5 tolerance)."""
+    if state.arch != "sage":
+        raise ValueError("full_forward implements the sage arch")
+    dev = g.device
+    stream = current_stream(dev)
+    dims = [g.feature_dim] + [int(w.shape[1]) for w in state.weights]
+    if int(state.weights[0].shape[0]) != 2 * g.feature_dim:
+        raise ValueError("model input width does not match the graph's features")
+    ws = _eval_ws(g, dims)
+    n = g.num_nodes
+    h, ldh = g.features, g.pitch
+    L = len(state.weights)
+    for l, W in enumerate(state.weights):
+        d_in, d_out = dims[l], dims[l + 1]
+        lib().mq_full_transform(ptr(h), ldh, n, d_in, ptr(W), d_out, ptr(ws.y[l]),
+                                ptr(ws.part[l]), stream)
+        out = ws.out[l]
+        lib().mq_full_aggregate(ptr(g.row_off), ptr(g.col), n, g.num_arcs, ptr(ws.y[l]),
+                                2 * d_out, d_out, 0 if l == L - 1 else 1, ptr(out),
+                                int(out.shape[1]), ptr(ws.scratch[l]), stream)
+        h, ldh = out, int(out.shape[1])
+    logits = ws.out[-1][:n]
+    _finite_or_raise("full_forward", logits)
+    return logits
+
+
+def evaluate(g, state: ModelState, mask) -> float:
+    """Accuracy of full_forward over the nodes selected by ``mask``
+    (the reference driver's evaluate, bench.py:82-87)."""
+    idx = np.flatnonzero(np.asarray(mask))
+    if idx.size == 0:
+        return 0.0
+    logits = full_forward(g, state)
+    ws = g._eval_ws
+    ids = torch.as_tensor(idx.astype(np.int32)).to(g.device, non_blocking=False)
+    ws.correct.zero_()
+    lib().mq_accuracy(ptr(logits), int(logits.stride(0)), int(logits.shape[1]), ptr(g.labels),
+                      ptr(ids), int(ids.numel()), ptr(ws.correct), current_stream(g.device))
+    return int(ws.correct.item()) / idx.size

@@ -1,0 +1,79 @@
+#!/usr/bin/env python
+"""Per-epoch work around the hot path on one B200: GNS cache refresh
+(degree / walk probabilities + the WOR residency draw, mq_refresh.cu) and
+full-graph evaluation (full_forward + accuracy, mq_eval.cu), CUDA-event
+timed after a warm-up, on a bench shape.  Prints one JSON line.
+
+    python scripts/epoch_timing.py [--shape reddit|products|cfg1] [--reps 3]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="reddit")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--fraction", type=float, default=0.01)
+    ap.add_argument("--hidden", type=int, default=64)
+    args = ap.parse_args()
+    import torch
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200 import synth
+
+    dev = "cuda:0"
+    t0 = time.perf_counter()
+    sg, fanouts = synth.generate_shape(args.shape, seed=0, device=dev)
+    g = mq.DeviceGraph.from_csr(sg, device=dev)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    state = mq.init_model(g.feature_dim, args.hidden, g.num_classes, num_layers=len(fanouts),
+                          seed=0, device=dev)
+    s = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()  # warm
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        out = None
+        for _ in range(args.reps):
+            out = fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.reps, out
+
+    res = {"shape": args.shape, "nodes": g.num_nodes, "arcs": g.num_edges,
+           "feature_dim": g.feature_dim, "classes": g.num_classes, "setup_s": setup_s}
+    res["degree_probs_ms"], probs = timed(lambda: mq.cache_probs_degree(g))
+    res["walk_probs_ms"], wprobs = timed(lambda: mq.cache_probs_walk(g, fanouts[0], len(fanouts)))
+    key = mq.RefreshStream(0, 1)
+    res["refresh_select_ms"], mask = timed(lambda: mq.refresh_mask(g, probs, args.fraction, key))
+    res["resident"] = int(mask.sum().item())
+    res["cache_build_ms"], _ = timed(lambda: mq.DeviceCache(g, mask, args.fraction))
+    res["full_forward_ms"], logits = timed(lambda: mq.full_forward(g, state))
+    val = g.val_mask
+    res["evaluate_ms"], acc = timed(lambda: mq.evaluate(g, state, val))
+    res["val_acc_init"] = acc
+    # algorithmic bytes of the full-graph aggregation (per layer: col + Y_top
+    # row per arc, Y_bot + out per node) for the achieved-GB/s figure
+    E, n = g.num_arcs, g.num_nodes
+    dims = [g.feature_dim] + [int(w.shape[1]) for w in state.weights]
+    agg_bytes = sum(4 * E + 4 * dims[l + 1] * (E + 2 * n) for l in range(len(dims) - 1))
+    gemm_bytes = sum(4 * n * (dims[l] + 2 * dims[l + 1]) for l in range(len(dims) - 1))
+    res["full_forward_alg_bytes"] = agg_bytes + gemm_bytes
+    res["full_forward_gbps"] = res["full_forward_alg_bytes"] / (res["full_forward_ms"] * 1e-3) / 1e9
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

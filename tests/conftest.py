@@ -119,3 +119,26 @@ def batch_prefixes(golden):
         if k.endswith("/digest"):
             out.append(k[:-len("/digest")])
     return sorted(out)
+
+
+@pytest.fixture(scope="session")
+def golden_epoch():
+    return load_golden("epoch.npz")
+
+
+def epoch_graph(golden, name):
+    """G2 / g8 of epoch.npz as a HostGraph with its split masks."""
+    g = HostGraph(golden[f"{name}/row_offsets"], golden[f"{name}/col_indices"],
+                  golden[f"{name}/features"], golden[f"{name}/labels"],
+                  int(golden[f"{name}/labels"].max()) + 1, golden[f"{name}/train_mask"])
+    g.val_mask = np.asarray(golden[f"{name}/val_mask"], bool)
+    g.test_mask = np.asarray(golden[f"{name}/test_mask"], bool)
+    return g
+
+
+def eval_cases(golden):
+    return sorted({k.split("/")[1] for k in golden if k.startswith("eval/")})
+
+
+def refresh_cases(golden):
+    return sorted({k.split("/")[2] for k in golden if k.startswith("refresh/case/")})

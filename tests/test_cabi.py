@@ -77,3 +77,18 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     from paper_2601_04707_b200 import _lib
     with pytest.raises(_lib.MQError, match="no CPU fallback"):
         _lib._Lib(tmp_path / "nope.so")
+
+
+@pytest.mark.parametrize("seed,epoch,n", [(3, 1, 1000), (2**40 + 7, 9, 77), (0, 0, 1)])
+def test_host_refresh_uniforms_match_oracle(L, seed, epoch, n):
+    from oracle.philox import refresh_uniforms
+    out = np.zeros(n, dtype=np.float64)
+    L.mq_refresh_uniforms_host(seed, epoch, n, out.ctypes.data)
+    assert np.array_equal(out, refresh_uniforms(seed, epoch, n))
+
+
+def test_eval_and_refresh_scratch_queries(L):
+    assert L.mq_full_agg_scratch_bytes(10**8, 64) >= 2 * (10**8 // 1024) * 64 * 4
+    assert L.mq_full_transform_part_floats(232965, 64) >= 232965 * 128
+    assert L.mq_walk_scratch_bytes(10**6) >= 3 * 8 * 10**6
+    assert L.mq_refresh_scratch_bytes(10**6) >= 12 * 10**6
