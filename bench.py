@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--queue-depth", type=int, default=None,
                     help="batches per batched prep pass (MQ-GNN queue depth Q)")
     ap.add_argument("--no-pdl", action="store_true", help="disable programmatic dependent launch")
+    ap.add_argument("--layer0", default="auto", choices=["auto", "tf", "af"],
+                    help="input layer transform-first / aggregate-first")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="prep and train on one stream (no multi-queue overlap)")
     return ap.parse_args()
@@ -307,7 +309,7 @@ def run_ours(args):
     runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=args.batch, num_train=n_train,
                            cache=cache, optimizer="adam", seed=args.seed, world=world, rank=rank,
                            multi=world > 1, queue_depth=args.queue_depth,
-                           pipeline=not args.no_pipeline)
+                           pipeline=not args.no_pipeline, layer0=args.layer0)
     exchange = mq.DistExchange() if world > 1 else None
     driver = mq.WindowDriver([runner], exchange, sync_period=1)
     t0 = time.perf_counter()
@@ -495,10 +497,14 @@ def run_ours(args):
                        "parallelism": f"dp{world} (RaCoM sync P=1)" if world > 1 else "dp1",
                        "l2": "inputs larger than L2 (CSR+features ~1.1 GB), no flush",
                        "cuda_graph": True, "queue_depth": runner.Q,
-                       "pdl": bool(lib().mq_get_pdl()), "pipeline": runner.pipeline},
+                       "pdl": bool(lib().mq_get_pdl()), "pipeline": runner.pipeline,
+                       "layer0": "aggregate-first" if getattr(runner.tw, "af0", False)
+                                 else "transform-first"},
             "epoch_ms": ms_max / args.steps * windows, "windows_per_epoch": windows,
             "roofline": roof, "kernels": focus,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "per_epoch": epoch_extra,
+            "cache": {"mode": cache_mode, "fraction": args.cache_fraction,
+                      "resident": cache.size, "hit_rate": cache.hit_rate()},
             "gpu_launches": int(round(n_kernels * args.steps)), "kernels_per_step": n_kernels,
             "wall_s_timed": t_wall, "setup": setup,
         }

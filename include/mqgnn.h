@@ -394,6 +394,26 @@ int mq_get_gemm_backend(void);
 int mq_set_pdl(int32_t on);
 int mq_get_pdl(void);
 
+/* Aggregate-first input layer of the fused step (the reference's own
+ * association, nn.py:126-131 and 167-170), chosen when the input width is
+ * narrow (d_in <= 2 d_out): the layer reads `agg` = block_apply(h)
+ * (mq_spmm_fwd, bit-exact) and needs no input gradient.
+ *   mq_sage_linear_af:      act = relu([agg | h[:m]] W), W (2 d_in x d_out), tcgen05
+ *                           3xTF32; `part` holds mq_sage_af_parts_bytes bytes.
+ *   mq_sage_linear_af_bwd:  dW partials [S][2 d_in][d_out] of
+ *                           [agg | h]^T (dh * (act > 0)) over *rows_dev rows,
+ *                           S -> *dw_nparts_dev (reduced by the optimizer, a
+ *                           kind-0 mq_grad_seg).  d_in % 4 == 0. */
+int64_t mq_sage_af_parts_bytes(int32_t m_max, int32_t d_out);
+int64_t mq_sage_af_dw_parts_bytes(int32_t d_in, int32_t d_out);
+int mq_sage_linear_af(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                      const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                      int32_t d_out, float* act, int32_t ldact, float* part, void* stream);
+int mq_sage_linear_af_bwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                          const int32_t* rows_dev, int32_t rows_max, int32_t d_in, const float* dh,
+                          int32_t lddh, const float* act, int32_t ldact, int32_t d_out,
+                          float* dw_parts, int32_t* dw_nparts_dev, void* stream);
+
 /* ------------------------------------------------ full-graph evaluation
  * The per-epoch evaluate() of the reference driver (bench.py:82-87) over
  * nn.full_forward's sage arm (nn.py:218-250) and nn.accuracy (nn.py:253-256).
@@ -450,6 +470,11 @@ int mq_refresh_select(const double* probs, int64_t n_nodes, int64_t budget, uint
 int mq_refresh_uniforms_host(uint64_t seed, uint64_t epoch, int64_t n, double* out);
 
 /* ------------------------------------------------------------- utilities */
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): the step's
+ * pinned-host result read-back as a node of a captured graph. */
+int mq_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* cudaMemsetAsync (a scatter target's clear inside a captured step). */
+int mq_memset_async(void* dst, int32_t value, int64_t bytes, void* stream);
 /* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */
 int mq_scan_i32(const int32_t* in, const int32_t* n_dev, int32_t n_max, int32_t* out,
                 void* scratch, void* stream);

@@ -85,7 +85,14 @@ SIGNATURES = {
     "mq_set_gemm_backend": (C.c_int, [I32]),
     "mq_get_gemm_backend": (C.c_int, []),
     "mq_set_pdl": (C.c_int, [I32]),
+    "mq_memcpy_async": (C.c_int, [P, P, I64, P]),
+    "mq_memset_async": (C.c_int, [P, I32, I64, P]),
     "mq_get_pdl": (C.c_int, []),
+    "mq_sage_af_parts_bytes": (I64, [I32, I32]),
+    "mq_sage_af_dw_parts_bytes": (I64, [I32, I32]),
+    "mq_sage_linear_af": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, P, P]),
+    "mq_sage_linear_af_bwd": (C.c_int, [P, I32, P, I32, P, I32, I32, P, I32, P, I32, I32, P, P,
+                                        P]),
     "mq_full_transform_part_floats": (I64, [I64, I32]),
     "mq_full_transform": (C.c_int, [P, I32, I64, I32, P, I32, P, P, P]),
     "mq_full_agg_scratch_bytes": (I64, [I64, I32]),

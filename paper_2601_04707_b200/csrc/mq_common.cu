@@ -133,6 +133,18 @@ int mq_prof_read(double* total_ms, int64_t* launches, int32_t n) {
 
 int64_t mq_launch_count(void) { return mq::g_launch_count.load(); }
 
+int mq_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  MQ_CHECK_ARG(bytes >= 0 && (bytes == 0 || (dst && src)), "mq_memcpy_async: bad arguments");
+  if (bytes) MQ_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, mq::as_stream(stream)));
+  return MQ_OK;
+}
+
+int mq_memset_async(void* dst, int32_t value, int64_t bytes, void* stream) {
+  MQ_CHECK_ARG(bytes >= 0 && (bytes == 0 || dst), "mq_memset_async: bad arguments");
+  if (bytes) MQ_CUDA(cudaMemsetAsync(dst, value, (size_t)bytes, mq::as_stream(stream)));
+  return MQ_OK;
+}
+
 int mq_set_pdl(int32_t on) {
   mq::g_pdl_on.store(on != 0);
   return MQ_OK;

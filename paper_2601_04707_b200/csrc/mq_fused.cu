@@ -43,6 +43,15 @@ int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_ma
                    cudaStream_t s);
 int64_t tc_dw_part_floats(int64_t d_in, int64_t d_out);
 int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out);
+int tc_linear_af(const float* agg, int ldagg, const float* h, int ldh, const int32_t* m_dev,
+                 int m_max, int d_in, const float* W, int d_out, float* act, int ldact,
+                 float* part, cudaStream_t s);
+int64_t tc_af_part_floats(int64_t m_max, int64_t d_out);
+int tc_linear_af_bwd(const float* agg, int ldagg, const float* h, int ldh,
+                     const int32_t* rows_dev, int rows_max, int d_in, const float* dh, int lddh,
+                     const float* act, int ldact, int d_out, float* part, int32_t* nparts_out,
+                     cudaStream_t s);
+int64_t tc_af_dw_part_floats(int64_t d_in, int64_t d_out);
 
 
 // ------------------------------------------------------------ GEMM loaders
@@ -865,6 +874,41 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
 
 int mq_sage_dw_deferred(int32_t d_out) {
   return (tc_backend() == 1 && tc_supported(2 * d_out)) ? 1 : 0;
+}
+
+int64_t mq_sage_af_parts_bytes(int32_t m_max, int32_t d_out) {
+  return tc_af_part_floats(m_max, d_out) * (int64_t)sizeof(float);
+}
+
+int64_t mq_sage_af_dw_parts_bytes(int32_t d_in, int32_t d_out) {
+  return tc_af_dw_part_floats(d_in, d_out) * (int64_t)sizeof(float);
+}
+
+int mq_sage_linear_af(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                      const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                      int32_t d_out, float* act, int32_t ldact, float* part, void* stream) {
+  MQ_CHECK_ARG(agg && h && m_dev && W && act && part, "mq_sage_linear_af: null pointer");
+  MQ_CHECK_ARG(d_in >= 4 && d_in % 4 == 0 && d_out >= 1 && d_out <= 256 && ldagg >= d_in &&
+                   ldh >= d_in && ldagg % 4 == 0 && ldh % 4 == 0 && ldact >= d_out &&
+                   ((uintptr_t)agg | (uintptr_t)h) % 16 == 0,
+               "mq_sage_linear_af: bad dims / alignment (d_in % 4 == 0, d_out <= 256)");
+  if (m_max <= 0) return MQ_OK;
+  return tc_linear_af(agg, ldagg, h, ldh, m_dev, m_max, d_in, W, d_out, act, ldact, part,
+                      as_stream(stream));
+}
+
+int mq_sage_linear_af_bwd(const float* agg, int32_t ldagg, const float* h, int32_t ldh,
+                          const int32_t* rows_dev, int32_t rows_max, int32_t d_in, const float* dh,
+                          int32_t lddh, const float* act, int32_t ldact, int32_t d_out,
+                          float* dw_parts, int32_t* dw_nparts_dev, void* stream) {
+  MQ_CHECK_ARG(agg && h && rows_dev && dh && act && dw_parts && dw_nparts_dev,
+               "mq_sage_linear_af_bwd: null pointer");
+  MQ_CHECK_ARG(d_in >= 4 && d_in % 4 == 0 && d_out >= 1 && d_out <= 256 && ldagg % 4 == 0 &&
+                   ldh % 4 == 0 && lddh >= d_out && ldact >= d_out &&
+                   ((uintptr_t)agg | (uintptr_t)h) % 16 == 0,
+               "mq_sage_linear_af_bwd: bad dims / alignment");
+  return tc_linear_af_bwd(agg, ldagg, h, ldh, rows_dev, rows_max, d_in, dh, lddh, act, ldact,
+                          d_out, dw_parts, dw_nparts_dev, as_stream(stream));
 }
 
 int64_t mq_sage_dw_parts_bytes(int32_t d_in, int32_t d_out) {

@@ -50,7 +50,10 @@
   X(K_REFRESH_DEGREE, "refresh_degree")         \
   X(K_REFRESH_PROBS, "refresh_probs")           \
   X(K_REFRESH_WALK, "refresh_walk")             \
-  X(K_REFRESH_SELECT, "refresh_select")
+  X(K_REFRESH_SELECT, "refresh_select")         \
+  X(K_SAGE_AF, "sage_linear_af")                \
+  X(K_SAGE_AF_REDUCE, "sage_linear_af_reduce")  \
+  X(K_SAGE_AF_DW, "sage_linear_af_dw")
 
 namespace mq {
 enum KernelId {

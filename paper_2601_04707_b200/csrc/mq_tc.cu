@@ -30,10 +30,11 @@ namespace tc {
 
 constexpr int BM = 128;        // UMMA M (TMEM lanes)
 constexpr int BK = 32;         // k block per stage (4 MMAs of K = 8)
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;           // staging / epilogue warps 0-7
+constexpr int kBlock = kThreads + 32;    // + warp 8: TMEM owner and MMA issuer
 constexpr int kStages = 2;
 constexpr int kMaxN = 256;
-constexpr int kMaxSplitsTc = 32;
+constexpr int kMaxSplitsTc = 148;  // = SMs: a one-tile DW (d_in <= 128) still fills the GPU
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -148,8 +149,12 @@ __device__ __forceinline__ void trace(int i) {
     g_tc_trace[i] = t;
   }
 }
+__device__ __forceinline__ void ktrace(bool on, uint32_t it, int p) {
+  if (on && it < 3) trace(3 + 8 * (int)it + p);
+}
 #else
 __device__ __forceinline__ void trace(int) {}
+__device__ __forceinline__ void ktrace(bool, uint32_t, int) {}
 #endif
 
 // ------------------------------------------------------------ work split
@@ -179,18 +184,35 @@ __host__ __device__ inline Work choose_work(int M, int K, int grid) {
 // so row-major-in-k sources are transposed in registers, 4x4 at a time).
 // FWD: A = X rows (already K-major), B(n, k) = [W_top | W_bot][k][n].
 // DW:  A(m, k) = X[k][m] (m = feature), B(n, k) = G[k][n]   (k = sampled row).
-enum Mode { kFwd = 0, kDw = 1 };
+// Aggregate-first layer (mq_sage_linear_af, the reference's own association,
+// nn.py:126-131 / 167-170) — used for the input layer when d_in is narrow:
+//   FCAT: Z (M x N) = [agg | h] (M x 2 d_in) . W (2 d_in x N)   M = dst rows
+//   DCAT: P (2 d_in x N) = [agg | h]^T . (dh * (act > 0))      K = dst rows
+enum Mode { kFwd = 0, kDw = 1, kFwdCat = 2, kDwCat = 3 };
 
 struct Operands {
-  const float* x;  // X (rows x ldx)
+  const float* x;  // X (rows x ldx)                      CAT: agg
   int ldx;
   int d_in;        // valid X columns
-  const float* w;  // FWD: W (2 d_in x n_half)
+  const float* w;  // FWD: W (2 d_in x n_half)            FCAT: W (2 d_in x N)
   int n_half;      // FWD: d_out
-  const float* g;  // DW: G (rows x N)
-  int N;           // output columns (2 d_out)
+  const float* g;  // DW: G (rows x N)                    DCAT: dh (rows x ldg)
+  int N;           // output columns (2 d_out; CAT: d_out)
   int Np;          // padded to a multiple of 16 (UMMA N)
+  const float* x2 = nullptr;  // CAT: h (second K / M half)
+  int ldx2 = 0;
+  int ldg = 0;                // DCAT: dh pitch
+  const float* act = nullptr; // DCAT: relu output (mask), pitch ldact
+  int ldact = 0;
 };
+
+// CAT operand A: four consecutive columns c of row r of [agg | h] (d_in % 4 == 0)
+__device__ __forceinline__ float4 ld_cat4(const Operands& op, int64_t r, int c) {
+  if (c < op.d_in) return __ldg(reinterpret_cast<const float4*>(op.x + r * op.ldx + c));
+  if (c < 2 * op.d_in)
+    return __ldg(reinterpret_cast<const float4*>(op.x2 + r * op.ldx2 + (c - op.d_in)));
+  return make_float4(0.f, 0.f, 0.f, 0.f);
+}
 
 // four consecutive columns [c, c+4) of a row, zero beyond `valid`
 __device__ __forceinline__ float4 ld_row4(const float* p, int c, int valid, bool vec_ok) {
@@ -209,15 +231,18 @@ template <int MODE>
 __device__ __forceinline__ void load_a(const Operands& op, int M, int K, int m0, int k0, int tid,
                                        float4 (&ra)[4]) {
   const int lane = tid & 31, w = tid >> 5;
-  if (MODE == kFwd) {
+  if (MODE == kFwd || MODE == kFwdCat) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int q = w + 8 * i;
       const int m = (q >> 1) * 8 + (lane & 7);
       const int k = k0 + ((q & 1) * 4 + (lane >> 3)) * 4;
       const int gm = m0 + m;
-      ra[i] = (gm < M && k < K) ? ld_row4(op.x + (int64_t)gm * op.ldx, k, op.d_in, true)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE == kFwd)
+        ra[i] = (gm < M && k < K) ? ld_row4(op.x + (int64_t)gm * op.ldx, k, op.d_in, true)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      else
+        ra[i] = (gm < M && k < K) ? ld_cat4(op, gm, k) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else {
     const int gm = m0 + 4 * lane;
@@ -225,8 +250,11 @@ __device__ __forceinline__ void load_a(const Operands& op, int M, int K, int m0,
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int k = kr + r;
-      ra[r] = (k < K && gm < op.d_in) ? ld_row4(op.x + (int64_t)k * op.ldx, gm, op.d_in, true)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE == kDw)
+        ra[r] = (k < K && gm < op.d_in) ? ld_row4(op.x + (int64_t)k * op.ldx, gm, op.d_in, true)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      else
+        ra[r] = (k < K && gm < 2 * op.d_in) ? ld_cat4(op, k, gm) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
 }
@@ -240,18 +268,28 @@ __device__ __forceinline__ void st_split(uint8_t* hi_base, uint8_t* lo_base, uin
 
 // store a 4x4 block given as 4 rows (k = 0..3) x 4 columns (row index c = 0..3)
 // as 4 K-major chunks: chunk c = (rows[0][c], rows[1][c], rows[2][c], rows[3][c])
+// at off0 + 16 c.  Neighbouring threads' blocks are 64 B apart, so the four
+// stores go out in a thread-dependent rotation (`rot`): the 8 lanes of a
+// store phase then hit 8 distinct 16-byte bank groups (no bank conflicts).
+__device__ __forceinline__ float4 col4(const float4 (&r)[4], int c) {
+  return c == 0 ? make_float4(r[0].x, r[1].x, r[2].x, r[3].x)
+       : c == 1 ? make_float4(r[0].y, r[1].y, r[2].y, r[3].y)
+       : c == 2 ? make_float4(r[0].z, r[1].z, r[2].z, r[3].z)
+                : make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
+}
 __device__ __forceinline__ void st_transposed(uint8_t* hi_base, uint8_t* lo_base, uint32_t off0,
-                                              const float4 (&r)[4]) {
-  st_split(hi_base, lo_base, off0 + 0, make_float4(r[0].x, r[1].x, r[2].x, r[3].x));
-  st_split(hi_base, lo_base, off0 + 16, make_float4(r[0].y, r[1].y, r[2].y, r[3].y));
-  st_split(hi_base, lo_base, off0 + 32, make_float4(r[0].z, r[1].z, r[2].z, r[3].z));
-  st_split(hi_base, lo_base, off0 + 48, make_float4(r[0].w, r[1].w, r[2].w, r[3].w));
+                                              const float4 (&r)[4], int rot) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = (j + rot) & 3;
+    st_split(hi_base, lo_base, off0 + 16 * c, col4(r, c));
+  }
 }
 
 template <int MODE>
 __device__ __forceinline__ void store_a(uint8_t* hi, uint8_t* lo, int tid, const float4 (&ra)[4]) {
   const int lane = tid & 31, w = tid >> 5;
-  if (MODE == kFwd) {
+  if (MODE == kFwd || MODE == kFwdCat) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int q = w + 8 * i;
@@ -261,7 +299,7 @@ __device__ __forceinline__ void store_a(uint8_t* hi, uint8_t* lo, int tid, const
     }
   } else {
     // rows m = 4 lane .. +3 (features), k chunk k4 = w
-    st_transposed(hi, lo, (uint32_t)(w * (BM * 16) + (4 * lane) * 16), ra);
+    st_transposed(hi, lo, (uint32_t)(w * (BM * 16) + (4 * lane) * 16), ra, lane >> 1);
   }
 }
 
@@ -273,6 +311,16 @@ template <int MODE>
 __device__ __forceinline__ float4 load_b4(const Operands& op, int K, int k, int n) {
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (k >= K || n >= op.N) return v;
+  if (MODE == kFwdCat) {  // W (2 d_in x N), row k
+    if (k >= 2 * op.d_in) return v;
+    return ld_row4(op.w + (int64_t)k * op.N, n, op.N, (op.N & 3) == 0);
+  }
+  if (MODE == kDwCat) {  // dz = dh * (act > 0), row k
+    const float4 g = ld_row4(op.g + (int64_t)k * op.ldg, n, op.N, (op.N & 3) == 0);
+    const float4 a = ld_row4(op.act + (int64_t)k * op.ldact, n, op.N, (op.N & 3) == 0);
+    return make_float4(a.x > 0.f ? g.x : 0.f, a.y > 0.f ? g.y : 0.f, a.z > 0.f ? g.z : 0.f,
+                       a.w > 0.f ? g.w : 0.f);
+  }
   if (MODE == kFwd) {
     if (k >= op.d_in) return v;
     const int h = op.n_half;
@@ -315,7 +363,7 @@ __device__ __forceinline__ void store_b(const Operands& op, uint8_t* hi, uint8_t
     const int c = tid + i * kThreads;
     if (c < 8 * n4s) {
       const int n4 = c % n4s, k4 = c / n4s;
-      st_transposed(hi, lo, (uint32_t)(k4 * (op.Np * 16) + 4 * n4 * 16), rb[i]);
+      st_transposed(hi, lo, (uint32_t)(k4 * (op.Np * 16) + 4 * n4 * 16), rb[i], n4 >> 1);
     }
   }
 }
@@ -328,11 +376,159 @@ struct Smem {
   __host__ __device__ static int total(int Np) { return kStages * stage_bytes(Np) + 1024; }
 };
 
-// ------------------------------------------------------------ kernel
+// ------------------------------------------------------------ async staging
+// Deep prefetch for the vectorisable shapes: each thread's A / B chunks of a
+// k block land by cp.async (16 B, zero-filled past the valid columns) in a
+// THREAD-PRIVATE slot of an R-deep raw ring, so R - 1 k blocks are in flight
+// per CTA (the register path holds one) and no barrier is needed between a
+// chunk's arrival and its hi/lo split: the thread that loaded it converts it.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_dyn(int n) {  // wait_group needs an immediate
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+  }
+}
+constexpr int kMaxRaw = 6;  // raw ring depth cap (wait_group <= 4)
+
+__host__ __device__ inline int raw_chunks(int mode, int Np) {
+  const int nb = (Np + 127) / 128;  // B chunk groups per thread (kBPerThread in use)
+  return 4 + 4 * nb + (mode == kDwCat ? 4 * nb : 0);
+}
+__host__ __device__ inline int raw_bytes(int mode, int Np) { return raw_chunks(mode, Np) * kThreads * 16; }
+
+__device__ __forceinline__ int vbytes(int valid_cols) {  // 4-float chunk, `valid_cols` valid
+  return valid_cols <= 0 ? 0 : (valid_cols >= 4 ? 16 : 4 * valid_cols);
+}
+
+// cat source of columns [c, c+4) of row r of [x | x2] (d_in % 4 == 0)
+__device__ __forceinline__ const float* cat_src(const Operands& op, int64_t r, int c, int& bytes) {
+  if (c < op.d_in) {
+    bytes = 16;
+    return op.x + r * op.ldx + c;
+  }
+  if (c < 2 * op.d_in) {
+    bytes = 16;
+    return op.x2 + r * op.ldx2 + (c - op.d_in);
+  }
+  bytes = 0;
+  return op.x;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ void issue_async(const Operands& op, int M, int K, int m0, int k0,
+                                            int tid, uint32_t slot) {
+  const int lane = tid & 31, w = tid >> 5;
+  auto dst = [&](int j) { return slot + (uint32_t)((j * kThreads + tid) * 16); };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float* src = op.x;
+    int bytes = 0;
+    if (MODE == kFwd || MODE == kFwdCat) {
+      const int q = w + 8 * i;
+      const int gm = m0 + (q >> 1) * 8 + (lane & 7);
+      const int k = k0 + ((q & 1) * 4 + (lane >> 3)) * 4;
+      if (gm < M && k < K) {
+        if (MODE == kFwd) {
+          src = op.x + (int64_t)gm * op.ldx + k;
+          bytes = vbytes(op.d_in - k);
+        } else {
+          src = cat_src(op, gm, k, bytes);
+        }
+      }
+    } else {
+      const int gm = m0 + 4 * lane;
+      const int k = k0 + 4 * w + i;
+      if (k < K) {
+        if (MODE == kDw) {
+          src = op.x + (int64_t)k * op.ldx + gm;
+          bytes = vbytes(op.d_in - gm);
+        } else {
+          src = cat_src(op, k, gm, bytes);
+        }
+      }
+    }
+    cp_async16(dst(i), bytes ? src : op.x, bytes);
+  }
+  const int n4s = op.Np / 4;
+  const int nb = (op.Np + 127) / 128;
+  for (int i = 0; i < nb; ++i) {
+    const int c = tid + i * kThreads;
+    const int n4 = c % n4s, k4 = c / n4s;
+    const int n = 4 * n4;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 4 * k4 + u;
+      const float* src = op.x;
+      const float* msk = op.x;
+      int bytes = 0;
+      if (c < 8 * n4s && k < K && n < op.N) {
+        if (MODE == kFwd) {
+          if (k < op.d_in) {
+            const int h = op.n_half;
+            src = n < h ? op.w + (int64_t)k * h + n : op.w + (int64_t)(op.d_in + k) * h + (n - h);
+            bytes = vbytes(op.N - n);
+          }
+        } else if (MODE == kFwdCat) {
+          if (k < 2 * op.d_in) {
+            src = op.w + (int64_t)k * op.N + n;
+            bytes = vbytes(op.N - n);
+          }
+        } else if (MODE == kDw) {
+          src = op.g + (int64_t)k * op.N + n;
+          bytes = vbytes(op.N - n);
+        } else {
+          src = op.g + (int64_t)k * op.ldg + n;
+          msk = op.act + (int64_t)k * op.ldact + n;
+          bytes = vbytes(op.N - n);
+        }
+      }
+      cp_async16(dst(4 + 4 * i + u), bytes ? src : op.x, bytes);
+      if (MODE == kDwCat) cp_async16(dst(4 + 4 * nb + 4 * i + u), bytes ? msk : op.x, bytes);
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void read_raw(const Operands& op, const uint8_t* slot, int tid,
+                                         float4 (&ra)[4], float4 (&rb)[kBPerThread][4]) {
+  auto at = [&](int j) {
+    return *reinterpret_cast<const float4*>(slot + (size_t)(j * kThreads + tid) * 16);
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ra[i] = at(i);
+  const int nb = (op.Np + 127) / 128;
+#pragma unroll
+  for (int i = 0; i < kBPerThread; ++i)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i < nb) {
+        float4 g = at(4 + 4 * i + u);
+        if (MODE == kDwCat) {
+          const float4 a = at(4 + 4 * nb + 4 * i + u);
+          g = make_float4(a.x > 0.f ? g.x : 0.f, a.y > 0.f ? g.y : 0.f, a.z > 0.f ? g.z : 0.f,
+                          a.w > 0.f ? g.w : 0.f);
+        }
+        rb[i][u] = g;
+      } else {
+        rb[i][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+}
+
+// ------------------------------------------------------------ kernel
+template <int MODE, bool ASYNC>
+__global__ void __launch_bounds__(kBlock, 1)
     tc_gemm_kernel(Operands op, const int32_t* m_dev, int m_static, const int32_t* k_dev,
-                   int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out) {
+                   int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out,
+                   int R) {
   MQ_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -349,8 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((int)blockIdx.x >= items || M <= 0) return;
 
   trace(0);
+  const bool worker = warp < kThreads / 32;
+  const bool issuer = tid == kThreads;  // warp 8, lane 0
   const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
-  if (warp == 0) tmem_alloc(&s_tmem, tmem_cols);
+  if (!worker) tmem_alloc(&s_tmem, tmem_cols);
   if (tid == 0) {
     for (int i = 0; i <= kStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -366,44 +564,102 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   uint32_t it = 0;  // global k-block counter (stage/phase bookkeeping)
   uint32_t acc_phase = 0;
+  const int nkb_total = (K + BK - 1) / BK;
+  float4 ra[4];
+  float4 rb[kBPerThread][4];
+  bool have = false;  // ra/rb already hold this item's first k block
+  // async ring: the load cursor runs R - 1 k blocks ahead of the MMAs, across items
+  uint8_t* raw = smem + kStages * stage_bytes;
+  const uint32_t raw_base = smem_u32(raw);
+  const int rbytes = raw_bytes(MODE, Np);
+  int l_item = blockIdx.x, l_kb = 0, l_kb1 = 0;
+  auto l_begin = [&]() {
+    while (l_item < items) {
+      l_kb = (l_item % wk.S) * wk.kb_per;
+      l_kb1 = min(nkb_total, l_kb + wk.kb_per);
+      if (l_kb < l_kb1) return;
+      l_item += gridDim.x;
+    }
+  };
+  auto l_issue = [&](uint32_t seq) {  // the cursor's k block into slot seq % R, then advance
+    if (l_item < items) {
+      issue_async<MODE>(op, M, K, (l_item / wk.S) * BM, l_kb * BK, tid,
+                        raw_base + (uint32_t)((seq % (uint32_t)R) * rbytes));
+      if (++l_kb >= l_kb1) {
+        l_item += gridDim.x;
+        l_begin();
+      }
+    }
+    cp_commit();
+  };
+  if (ASYNC && worker) {
+    l_begin();
+    for (int r = 0; r < R - 1; ++r) l_issue((uint32_t)r);
+  }
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int s = item % wk.S;
     const int tile = item / wk.S;
     const int m0 = tile * BM;
     const int kb0 = s * wk.kb_per;
-    const int nkb_total = (K + BK - 1) / BK;
     const int kb1 = min(nkb_total, kb0 + wk.kb_per);
 
     if (kb0 >= kb1) {  // no rows to reduce over (K == 0): the partial is zero
-      if (warp < 4 && m0 + warp * 32 + lane < M) {
+      if (warp < 4 && m0 + warp * 32 + lane < M) {  // (all threads skip alike)
         float* out = part + ((int64_t)s * M + m0 + warp * 32 + lane) * op.N;
         for (int c = 0; c < op.N; ++c) out[c] = 0.f;
       }
+      have = false;
       continue;
     }
-    float4 ra[4];
-    float4 rb[kBPerThread][4];
-    load_a<MODE>(op, M, K, m0, kb0 * BK, tid, ra);
-    load_b<MODE>(op, K, kb0 * BK, tid, rb);
-    trace(2);
+    if (!ASYNC && !have && worker) {
+      load_a<MODE>(op, M, K, m0, kb0 * BK, tid, ra);
+      load_b<MODE>(op, K, kb0 * BK, tid, rb);
+    }
+    have = false;
+    const bool first_item = item == (int)blockIdx.x;
+    if (first_item) trace(2);
     for (int kb = kb0; kb < kb1; ++kb, ++it) {
       const int stage = it % kStages;
       uint8_t* st = smem + stage * stage_bytes;
-      // the MMAs that last read this stage must have completed
-      if (it >= (uint32_t)kStages) mbar_wait(&bars[stage], ((it / kStages) - 1) & 1);
-      // ---- stage A and B (split hi/lo)
-      store_a<MODE>(st, st + Smem::kA, tid, ra);
-      store_b(op, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid, rb);
+      ktrace(first_item, it, 0);
+      if (worker) {
+        if (ASYNC) {  // this k block's chunks have landed (this thread's own copies)
+          cp_wait_dyn(R - 2);
+          ktrace(first_item, it, 1);
+          read_raw<MODE>(op, raw + (size_t)(it % (uint32_t)R) * rbytes, tid, ra, rb);
+          l_issue(it + (uint32_t)R - 1);
+          ktrace(first_item, it, 2);
+        }
+        // the MMAs that last read this stage must have completed
+        if (it >= (uint32_t)kStages) mbar_wait(&bars[stage], ((it / kStages) - 1) & 1);
+        ktrace(first_item, it, 3);
+        // ---- stage A and B (split hi/lo)
+        store_a<MODE>(st, st + Smem::kA, tid, ra);
+        ktrace(first_item, it, 4);
+        store_b(op, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid, rb);
+        ktrace(first_item, it, 5);
+      }
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
-      trace(3 + 2 * (kb - kb0));
-      // prefetch the next A block while the tensor core works on this one
-      if (kb + 1 < kb1) {
+      ktrace(first_item, it, 6);
+      // prefetch the next A block while the tensor core works on this one;
+      // after the last block, the next item's first block, so its load
+      // latency hides behind this item's accumulator drain
+      if (ASYNC || !worker) {
+      } else if (kb + 1 < kb1) {
         load_a<MODE>(op, M, K, m0, (kb + 1) * BK, tid, ra);
         load_b<MODE>(op, K, (kb + 1) * BK, tid, rb);
+      } else if (item + (int)gridDim.x < items) {
+        const int nitem = item + (int)gridDim.x;
+        const int nkb0 = (nitem % wk.S) * wk.kb_per;
+        if (nkb0 < nkb_total) {
+          load_a<MODE>(op, M, K, (nitem / wk.S) * BM, nkb0 * BK, tid, ra);
+          load_b<MODE>(op, K, nkb0 * BK, tid, rb);
+          have = true;
+        }
       }
-      if (tid == 0) {
+      if (issuer) {  // off the staging warps' critical path
         tc_fence_after();
         const uint32_t a_hi = smem_base + stage * stage_bytes;
         const uint32_t a_lo = a_hi + Smem::kA;
@@ -424,43 +680,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bars[stage]);
       }
-      trace(4 + 2 * (kb - kb0));
+      ktrace(first_item, it, 7);
     }
-    // ---- accumulator ready -> partial tile
-    if (tid == 0) mma_commit(&bars[kStages]);
+    // ---- accumulator ready -> partial tile (all 8 staging warps: warp w
+    // drains TMEM lanes 32 (w % 4).. and every other 32-column block)
+    if (issuer) mma_commit(&bars[kStages]);
     mbar_wait(&bars[kStages], acc_phase & 1);
     ++acc_phase;
     tc_fence_after();
-    trace(20);
-    if (warp < 4) {
-      const int m = warp * 32 + lane;
-      const int gm = m0 + m;
-      float* out = part + ((int64_t)s * M + gm) * op.N;
-      for (int cb = 0; cb < Np; cb += 32) {
+    if (first_item) trace(27);
+    if (worker) {
+      // TMEM -> smem tile [BM][Np + 4] (the stage buffers are idle: this
+      // item's MMAs have completed) -> coalesced row stores: a warp writes
+      // whole rows instead of 32 rows x 16 B per instruction
+      float* tile = reinterpret_cast<float*>(smem);
+      const int ldt = (Np + 31) / 32 * 32 + 4;  // whole 32-column TMEM loads fit
+      const int m = (warp & 3) * 32 + lane;
+      for (int cb = 32 * (warp >> 2); cb < Np; cb += 64) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)cb, v);
-        if (gm < M) {
-          if ((op.N & 3) == 0 && cb + 32 <= op.N) {
+        tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)cb, v);
 #pragma unroll
-            for (int u = 0; u < 32; u += 4)
-              *reinterpret_cast<float4*>(out + cb + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
-          } else {
-#pragma unroll
-            for (int u = 0; u < 32; ++u)
-              if (cb + u < op.N) out[cb + u] = v[u];
-          }
+        for (int u = 0; u < 32; u += 4)
+          *reinterpret_cast<float4*>(tile + m * ldt + cb + u) =
+              make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kThreads));  // staging warps only
+      const int rows = min(BM, M - m0);
+      if ((op.N & 3) == 0) {
+        const int n4 = op.N / 4;
+        for (int e = tid; e < rows * n4; e += kThreads) {
+          const int r = e / n4, c = 4 * (e % n4);
+          *reinterpret_cast<float4*>(part + ((int64_t)s * M + m0 + r) * op.N + c) =
+              *reinterpret_cast<const float4*>(tile + r * ldt + c);
+        }
+      } else {
+        for (int e = tid; e < rows * op.N; e += kThreads) {
+          const int r = e / op.N, c = e % op.N;
+          part[((int64_t)s * M + m0 + r) * op.N + c] = tile[r * ldt + c];
         }
       }
     }
     tc_fence_before();
     __syncthreads();
-    trace(21);
+    if (first_item) trace(28);
   }
-  if (warp == 0) {
+  if (ASYNC && worker) cp_wait_dyn(0);
+  if (!worker) {
     tc_fence_after();
     tmem_dealloc(tmem, tmem_cols);
   }
-  trace(22);
+  trace(29);
 }
 
 // fixed-order split reduction + layer epilogue (same decomposition as the GEMM)
@@ -492,23 +761,52 @@ inline int tc_grid(int m_max, int k_max) {
   return (int)(cap < kNumSMs ? cap : kNumSMs);
 }
 
+inline bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// the cp.async ring needs every operand row chunk 16-byte aligned
+template <int MODE>
+bool tc_async_ok(const tc::Operands& op) {
+  if (!al16(op.x) || (op.ldx & 3)) return false;
+  if (MODE == tc::kFwd) return al16(op.w) && (op.n_half & 3) == 0;
+  if (MODE == tc::kDw) return al16(op.g) && (op.N & 3) == 0;
+  if (MODE == tc::kFwdCat)
+    return al16(op.x2) && (op.ldx2 & 3) == 0 && (op.d_in & 3) == 0 && al16(op.w) && (op.N & 3) == 0;
+  return al16(op.x2) && (op.ldx2 & 3) == 0 && (op.d_in & 3) == 0 && al16(op.g) &&
+         (op.ldg & 3) == 0 && al16(op.act) && (op.ldact & 3) == 0 && (op.N & 3) == 0;
+}
+
+constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the static barriers
+
 template <int MODE, class Epi>
 int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
                 const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
                 cudaStream_t s, int kid, int kid_red, bool skip_reduce = false,
                 int32_t* nparts_out = nullptr) {
-  const int smem = tc::Smem::total(op.Np);
-  static thread_local bool configured[2] = {false, false};
-  if (!configured[MODE]) {
-    MQ_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 tc::Smem::total(tc::kMaxN)));
-    configured[MODE] = true;
+  static thread_local bool configured[4][2] = {};
+  const int base = tc::Smem::total(op.Np);
+  int R = (kSmemBudget - base) / tc::raw_bytes(MODE, op.Np);
+  if (R > tc::kMaxRaw) R = tc::kMaxRaw;
+  const bool async = R >= 2 && tc_async_ok<MODE>(op);
+  const int smem = async ? base + R * tc::raw_bytes(MODE, op.Np) : base;
+  if (!configured[MODE][async]) {
+    if (async)
+      MQ_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<MODE, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    else
+      MQ_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<MODE, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   tc::Smem::total(tc::kMaxN)));
+    configured[MODE][async] = true;
   }
   const int grid = tc_grid(m_max, k_max);
   {
     ProfScope ps(kid, s);
-    MQ_CUDA(launch_k(tc::tc_gemm_kernel<MODE>, dim3(grid), dim3(tc::kThreads), smem, s, op, m_dev, m_static, k_dev, k_static,
-                                                             part, nparts_out));
+    if (async)
+      MQ_CUDA(launch_k(tc::tc_gemm_kernel<MODE, true>, dim3(grid), dim3(tc::kBlock), smem, s, op,
+                       m_dev, m_static, k_dev, k_static, part, nparts_out, R));
+    else
+      MQ_CUDA(launch_k(tc::tc_gemm_kernel<MODE, false>, dim3(grid), dim3(tc::kBlock), smem, s,
+                       op, m_dev, m_static, k_dev, k_static, part, nparts_out, 0));
   }
   MQ_LAUNCH_CHECK("tc_gemm");
   if (skip_reduce) return MQ_OK;
@@ -578,6 +876,38 @@ int tc_weight_grad(const float* h, int ldh, const int32_t* rows_dev, int rows_ma
 }
 
 int64_t tc_dw_part_floats(int64_t d_in, int64_t d_out) { return tc_part_floats(d_in, 2 * d_out); }
+
+// aggregate-first input layer: act = relu([agg | h] W) over the live dst rows
+int tc_linear_af(const float* agg, int ldagg, const float* h, int ldh, const int32_t* m_dev,
+                 int m_max, int d_in, const float* W, int d_out, float* act, int ldact,
+                 float* part, cudaStream_t s) {
+  tc::Operands op{agg, ldagg, d_in, W, d_out, nullptr, d_out, (d_out + 15) / 16 * 16};
+  op.x2 = h;
+  op.ldx2 = ldh;
+  return run_tc_gemm<tc::kFwdCat>(op, m_dev, 0, m_max, nullptr, 2 * d_in, 2 * d_in, part,
+                                  EpiLinearFwd{nullptr, 0, act, ldact}, s, K_SAGE_AF,
+                                  K_SAGE_AF_REDUCE);
+}
+
+int64_t tc_af_part_floats(int64_t m_max, int64_t d_out) { return tc_part_floats(m_max, d_out); }
+
+// its weight gradient as deferred split-K partials [S][2 d_in][d_out]
+int tc_linear_af_bwd(const float* agg, int ldagg, const float* h, int ldh,
+                     const int32_t* rows_dev, int rows_max, int d_in, const float* dh, int lddh,
+                     const float* act, int ldact, int d_out, float* part, int32_t* nparts_out,
+                     cudaStream_t s) {
+  tc::Operands op{agg, ldagg, d_in, nullptr, d_out, dh, d_out, (d_out + 15) / 16 * 16};
+  op.x2 = h;
+  op.ldx2 = ldh;
+  op.ldg = lddh;
+  op.act = act;
+  op.ldact = ldact;
+  return run_tc_gemm<tc::kDwCat>(op, nullptr, 2 * d_in, 2 * d_in, rows_dev, 0, rows_max, part,
+                                 EpiStore{nullptr, 0}, s, K_SAGE_AF_DW, K_SAGE_AF_DW, true,
+                                 nparts_out);
+}
+
+int64_t tc_af_dw_part_floats(int64_t d_in, int64_t d_out) { return tc_part_floats(2 * d_in, d_out); }
 
 int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out) {
   int64_t a = tc_part_floats(m_max, 2 * d_out);

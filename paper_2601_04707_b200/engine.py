@@ -333,9 +333,17 @@ class FusedTrainWorkspace:
       act[l+1]     (n_dst_h x ld_{l+1})    relu output = next layer's input
       dh[l]        (n_src_h x ld_l)        gradient w.r.t. layer l's input, l >= 1
     The scatter targets (G[l], dh[L-1]) are cleared by the forward's
-    aggregation kernels, so the step has no memset nodes."""
+    aggregation kernels, so the step has no memset nodes.
 
-    def __init__(self, sw: SampleWorkspace, dims, num_classes: int):
+    The input layer may instead run aggregate-first (``layer0="af"``; "auto"
+    picks it when d_in <= 2 d_out and d_in % 4 == 0): agg0 = block_apply(x0)
+    (mq_spmm_fwd, bit-exact), act1 = relu([agg0 | x0] W0) and its weight
+    gradient [agg0 | x0]^T (dh1 * mask) on the tensor cores.  For narrow
+    inputs (products-shaped 100-d) this reads n_dst rows instead of
+    transforming every n_src row, and layer 0 needs no scatter (the input
+    has no gradient)."""
+
+    def __init__(self, sw: SampleWorkspace, dims, num_classes: int, layer0: str = "auto"):
         g = sw.graph
         dev = g.device
         L = len(sw.fanouts)
@@ -347,11 +355,28 @@ class FusedTrainWorkspace:
         self.C = num_classes
         f32 = dict(dtype=torch.float32, device=dev)
         self.ld_in = [g.pitch] + [round_up(d, 4) for d in self.dims[1:L]]
+        if layer0 not in ("auto", "tf", "af"):
+            raise ValueError(f"layer0 must be auto, tf or af, not {layer0!r}")
+        af_ok = (L >= 2 and self.dims[0] % 4 == 0 and self.dims[1] <= 256
+                 and lib().mq_get_gemm_backend() == 1)
+        if layer0 == "af" and not af_ok:
+            raise ValueError("aggregate-first layer 0 needs d_in % 4 == 0, d_out <= 256, L >= 2 "
+                             "and the tensor-core backend")
+        self.af0 = af_ok and (layer0 == "af" or
+                              (layer0 == "auto" and self.dims[0] <= 2 * self.dims[1]))
         self.Y, self.G, self.act, self.dh = [], [], [None] * (L + 1), [None] * L
         scr = 1
         for l in range(L - 1):
             b = sw.bounds[L - 1 - l]
             n2 = 2 * self.dims[l + 1]
+            if l == 0 and self.af0:
+                self.Y.append(None)
+                self.G.append(None)
+                self.agg0 = torch.zeros((max(b.n_dst_max, 1), self.ld_in[0]), **f32)
+                self.af_part = torch.zeros(
+                    int(lib().mq_sage_af_parts_bytes(b.n_dst_max, self.dims[1])) // 4 + 1, **f32)
+                self.act[1] = torch.zeros((max(b.n_dst_max, 1), self.ld_in[1]), **f32)
+                continue
             # Y, or (tensor-core backend) its deferred split-K partial tiles
             ny = max(b.n_src_max, 1) * n2
             ny = max(ny, int(lib().mq_sage_y_parts_bytes(b.n_src_max, self.dims[l + 1])) // 4)
@@ -380,7 +405,8 @@ class FusedTrainWorkspace:
     def grad_src(self, model: DeviceModel):
         """The _lib.GradSrc describing where each layer's gradient lives this
         step (head partials, deferred tcgen05 partials, or model.flat_g)."""
-        key = tuple(int(lib().mq_sage_dw_deferred(self.dims[l + 1])) for l in range(self.L - 1))
+        key = tuple(int(self.af0 and l == 0 or lib().mq_sage_dw_deferred(self.dims[l + 1]))
+                    for l in range(self.L - 1))
         if key == self._src_key and self._src is not None:
             return self._src
         src = GradSrc()
@@ -391,7 +417,24 @@ class FusedTrainWorkspace:
                                     ptr(self.head_scratch), model.offsets[L - 1], C.byref(seg))
         segs.append(seg)
         for l in range(L - 1):
-            if key[l]:
+            if l == 0 and self.af0:
+                d0, d1 = self.dims[0], self.dims[1]
+                if self.dw_parts[0] is None:
+                    nb = int(lib().mq_sage_af_dw_parts_bytes(d0, d1))
+                    self.dw_parts[0] = torch.zeros(nb // 4 + 1, dtype=torch.float32,
+                                                   device=self.sw.graph.device)
+                s2 = GradSrc().seg[0]
+                s2.part = ptr(self.dw_parts[0])
+                s2.nparts_dev = ptr(self.dw_nparts[0:1])
+                s2.stride = 2 * d0 * d1
+                s2.offset = model.offsets[0]
+                s2.size = 2 * d0 * d1
+                s2.nparts = 0
+                s2.kind = 0
+                s2.d_in = d0
+                s2.d_out = d1
+                segs.append(s2)
+            elif key[l]:
                 if self.dw_parts[l] is None:
                     nb = int(lib().mq_sage_dw_parts_bytes(self.dims[l], self.dims[l + 1]))
                     self.dw_parts[l] = torch.zeros(nb // 4 + 1, dtype=torch.float32,
@@ -442,6 +485,20 @@ class FusedTrainWorkspace:
         for l in range(L - 1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
+            if l == 0 and self.af0:
+                ops.append(("sage_spmm_l0", lambda s, h=h, hb=hb, b=b:
+                            lb.mq_spmm_fwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
+                                           ptr(sw.n_dst_dev(h)), b.n_dst_max, ptr(sw.x0), ld[0],
+                                           d[0], ptr(self.agg0), ld[0], s)))
+                ops.append(("sage_linear_af_l0", lambda s, h=h, b=b:
+                            lb.mq_sage_linear_af(ptr(self.agg0), ld[0], ptr(sw.x0), ld[0],
+                                                 ptr(sw.n_dst_dev(h)), b.n_dst_max, d[0],
+                                                 ptr(model.weight(0)), d[1], ptr(self.act[1]),
+                                                 ld[1], ptr(self.af_part), s)))
+                if L == 2:  # the head scatters into dh[1]; TF's aggregation clears it
+                    ops.append(("sage_zero_dh", lambda s: lb.mq_memset_async(
+                        ptr(self.dh[L - 1]), 0, self.dh[L - 1].numel() * 4, s)))
+                continue
             # tensor-core backend: Y stays as split-K partials, summed by the aggregation
             yn = self.y_nparts[l:l + 1] if lb.mq_sage_y_deferred(d[l + 1]) else None
             ops.append((f"sage_transform_l{l}", lambda s, l=l, hb=hb, b=b, yn=yn:
@@ -471,6 +528,14 @@ class FusedTrainWorkspace:
         for l in range(L - 2, -1, -1):
             h = L - 1 - l
             hb, b = sw.hops[h], sw.bounds[h]
+            if l == 0 and self.af0:
+                ops.append(("sage_linear_af_bwd_l0", lambda s, h=h, b=b:
+                            lb.mq_sage_linear_af_bwd(ptr(self.agg0), ld[0], ptr(sw.x0), ld[0],
+                                                     ptr(sw.n_dst_dev(h)), b.n_dst_max, d[0],
+                                                     ptr(self.dh[1]), ld[1], ptr(self.act[1]),
+                                                     ld[1], d[1], ptr(self.dw_parts[0]),
+                                                     ptr(self.dw_nparts[0:1]), s)))
+                continue
             ops.append((f"sage_scatter_bwd_l{l}", lambda s, l=l, h=h, hb=hb, b=b:
                         lb.mq_sage_scatter_bwd(ptr(hb.row_ptr), ptr(hb.cols), ptr(hb.vals),
                                                ptr(sw.n_dst_dev(h)), b.n_dst_max,
@@ -491,3 +556,27 @@ class FusedTrainWorkspace:
 
 def current_stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+class capture_graph:
+    """torch.cuda.graph with Python's cyclic GC paused: a CUDAGraph of an
+    earlier runner collected mid-capture would destroy its graph exec inside
+    the capture and invalidate it (cudaErrorStreamCaptureInvalidated)."""
+
+    def __init__(self, graph, stream):
+        self._ctx = torch.cuda.graph(graph, stream=stream)
+
+    def __enter__(self):
+        import gc
+        gc.collect()
+        self._was = gc.isenabled()
+        gc.disable()
+        return self._ctx.__enter__()
+
+    def __exit__(self, *exc):
+        import gc
+        try:
+            return self._ctx.__exit__(*exc)
+        finally:
+            if self._was:
+                gc.enable()

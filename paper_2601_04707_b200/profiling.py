@@ -15,12 +15,13 @@ from __future__ import annotations
 
 import torch
 
+from .engine import capture_graph
 from .prep import PREP_GATHER, PREP_RELABEL, PREP_SAMPLE
 
 
 def _time(fn, stream, reps: int, iters: int) -> float:
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
+    with capture_graph(g, stream):
         for _ in range(reps):
             fn(torch.cuda.current_stream().cuda_stream)
     with torch.cuda.stream(stream):

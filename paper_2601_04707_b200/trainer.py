@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from ._lib import lib, ptr
-from .engine import FusedTrainWorkspace, TrainWorkspace
+from .engine import FusedTrainWorkspace, TrainWorkspace, capture_graph
 from .prep import PrepGroup, PrepShared
 
 DEFAULT_QUEUE_DEPTH = 4
@@ -39,7 +39,8 @@ class StepRunner:
     def __init__(self, g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
                  multi: bool = False, use_graph: bool = True, pipeline: bool = True,
-                 ring_len: int = 1 << 16, fused: bool = True, queue_depth: int | None = None):
+                 ring_len: int = 1 << 16, fused: bool = True, queue_depth: int | None = None,
+                 layer0: str = "auto"):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         Q = DEFAULT_QUEUE_DEPTH if queue_depth is None else int(queue_depth)
@@ -69,8 +70,10 @@ class StepRunner:
         # fused: transform-first hidden layers + one-launch head (mq_fused.cu);
         # otherwise the reference-shaped per-op kernels (aggregate-first)
         self.fused = bool(fused)
-        self.tw = (FusedTrainWorkspace if self.fused else TrainWorkspace)(self.sw, dims,
-                                                                          g.num_classes)
+        if self.fused:
+            self.tw = FusedTrainWorkspace(self.sw, dims, g.num_classes, layer0=layer0)
+        else:
+            self.tw = TrainWorkspace(self.sw, dims, g.num_classes)
         self.num_train = int(num_train)
         self.batch_size = int(batch_size)
         self.perm = torch.zeros(max(self.num_train, 1), dtype=torch.int32, device=dev)
@@ -199,7 +202,7 @@ class StepRunner:
         for name, fn in phases.items():
             graph = torch.cuda.CUDAGraph()
             before = lib().mq_launch_count()
-            with torch.cuda.graph(graph, stream=self.stream):
+            with capture_graph(graph, self.stream):
                 fn(torch.cuda.current_stream().cuda_stream)
             self.launches_per_phase[name] = int(lib().mq_launch_count() - before)
             self.graphs[name] = graph
@@ -402,6 +405,10 @@ class StepRunner:
         self._stage_i = 0
         self._loss_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
         self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
+        # one pinned loss row per window of each slot group: the group graphs
+        # copy every window's loss out (D2H) as a node of the graph
+        self._loss_grp = torch.zeros((len(self.groups), Q), dtype=torch.float64, pin_memory=True)
+        self._grp_ev = [torch.cuda.Event() for _ in self.groups]
         phases = {}
         for gi, grp in enumerate(self.groups):
             phases[f"hprep{gi}"] = (lambda s, gi=gi: self.groups[gi].launch(
@@ -414,6 +421,16 @@ class StepRunner:
         if self.use_graph:
             self._warm(phases)
             self._capture(phases)
+            groups = {}
+            for gi, grp in enumerate(self.groups):
+                def hgroup(s, gi=gi):
+                    for q in range(Q):
+                        phases[f"htrain{gi}_{q}"](s)
+                        lib().mq_memcpy_async(self._loss_grp[gi, q:q + 1].data_ptr(),
+                                              ptr(self.tw.loss), 8, s)
+                        self.tw.loss.zero_()
+                groups[f"hgroup{gi}"] = hgroup
+            self._capture(groups)
         self._hphases = phases
 
     def _hrun(self, name, stream):
@@ -450,8 +467,10 @@ class StepRunner:
         target batch (batch_id, targets) the step H2D-copies its inputs, trains,
         and D2H-reads its summed loss.  Batches are prepared Q at a time (the
         device queue); group j+1 is staged and prepared while group j trains.
-        Every batch still gets its own H2D copy and its own loss read-back,
-        one step behind the launch.  Yields (batch_id, loss)."""
+        A full group of Q windows runs as one graph whose nodes include each
+        window's loss D2H copy; the host reads group j's losses after group
+        j+1 is enqueued, so the GPU never idles on the host.  Yields
+        (batch_id, loss) in order."""
         batches = list(batches)
         if not batches:
             return
@@ -469,8 +488,23 @@ class StepRunner:
             self.ev_prep[gi].record(prep_s)
 
         stage_and_prep(0)
-        pending = None
+        pending = []   # (kind, payload) of enqueued work whose losses are unread
         nstep = 0
+
+        def drain(keep):
+            while len(pending) > keep:
+                kind, pay = pending.pop(0)
+                if kind == "group":
+                    gi, ids = pay
+                    self._grp_ev[gi].synchronize()
+                    vals = self._loss_grp[gi].tolist()
+                    for q, bid in enumerate(ids):
+                        yield bid, float(vals[q])
+                else:
+                    bid, slot = pay
+                    self._loss_ev[slot].synchronize()
+                    yield bid, float(self._loss_host[slot])
+
         for j, chunk in enumerate(chunks):
             gi = j % ngroups
             if j + 1 < len(chunks) and self.pipeline:
@@ -478,24 +512,31 @@ class StepRunner:
             elif j > 0 and not self.pipeline:
                 stage_and_prep(j)
             self.stream.wait_event(self.ev_prep[gi])
-            for q, (bid, _) in enumerate(chunk):
-                slot = nstep % 2
-                self._hrun(f"htrain{gi}_{q}", self.stream)
+            if self.use_graph and len(chunk) == Q and f"hgroup{gi}" in self.graphs:
+                # the group's previous losses must have been read before overwrite
+                yield from drain(0 if any(k == "group" and p[0] == gi for k, p in pending) else 1)
                 with torch.cuda.stream(self.stream):
-                    self._loss_host[slot:slot + 1].copy_(self.tw.loss, non_blocking=True)
-                    self.tw.loss.zero_()
-                self._loss_ev[slot].record(self.stream)
-                self.dm.host_steps += 1
-                nstep += 1
-                if pending is not None:
-                    pbid, pslot = pending
-                    self._loss_ev[pslot].synchronize()
-                    yield pbid, float(self._loss_host[pslot])
-                pending = (bid, slot)
+                    self.graphs[f"hgroup{gi}"].replay()
+                self._grp_ev[gi].record(self.stream)
+                self.dm.host_steps += Q
+                nstep += Q
+                pending.append(("group", (gi, [bid for bid, _ in chunk])))
+            else:
+                for q, (bid, _) in enumerate(chunk):
+                    slot = nstep % 2
+                    yield from drain(0 if any(k == "one" and p[1] == slot for k, p in pending)
+                                     else 1)
+                    self._hrun(f"htrain{gi}_{q}", self.stream)
+                    with torch.cuda.stream(self.stream):
+                        self._loss_host[slot:slot + 1].copy_(self.tw.loss, non_blocking=True)
+                        self.tw.loss.zero_()
+                    self._loss_ev[slot].record(self.stream)
+                    self.dm.host_steps += 1
+                    nstep += 1
+                    pending.append(("one", (bid, slot)))
             self.ev_train[gi].record(self.stream)
-        pbid, pslot = pending
-        self._loss_ev[pslot].synchronize()
-        yield pbid, float(self._loss_host[pslot])
+            yield from drain(1)
+        yield from drain(0)
 
     def step_from_host(self, targets_pinned: torch.Tensor, batch_id: int) -> float:
         """Single synchronous step from one host batch."""

@@ -13,8 +13,7 @@ args = bench.parse()
 dev = torch.device("cuda", 0)
 sg, fanouts, _ = bench.build_inputs(args, "cuda:0")
 g = mq.DeviceGraph.from_csr(sg, device=dev)
-mask = bench.cache_mask_from(sg, args.cache_fraction, args.seed)
-cache = mq.DeviceCache(g, mask, args.cache_fraction)
+cache = mq.refresh_cache(g, mq.cache_probs_degree(g), args.cache_fraction, mq.RefreshStream(args.seed, 0))
 model = mq.init_model(g.feature_dim, args.hidden, g.num_classes, num_layers=len(fanouts), seed=0,
                       learning_rate=1e-3, device=dev)
 n_train = int(g.train_mask.sum())

@@ -32,7 +32,7 @@ def _normwise(got, ref):
     return np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
 
 
-def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
+def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1, layer0="auto"):
     """Run `windows` eager fused steps on device (compute only, no optimizer)
     and compare loss + gradients of each batch with the oracle."""
     g = DeviceGraph.from_csr(hg)
@@ -43,8 +43,11 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1):
     model = onn.init_model(hg.feature_dim, hidden, C, num_layers=L, seed=7, learning_rate=0.01)
     perm = epoch_permutation(hg.train_mask, seed, 0)
     runner = mq.StepRunner(g, state, fanouts=fanouts, batch_size=B, num_train=perm.size,
-                           cache=cache, seed=seed, use_graph=False, pipeline=False)
+                           cache=cache, seed=seed, use_graph=False, pipeline=False,
+                           layer0=layer0)
     assert runner.fused
+    if layer0 != "auto":
+        assert runner.tw.af0 == (layer0 == "af")
     runner.begin_epoch(0, perm)
     s = runner.stream
     for j in range(windows):
@@ -86,20 +89,44 @@ def cfg1():
     return make_cfg1()
 
 
-def test_fused_two_layer_cfg1(cfg1):
-    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=3, windows=3)
+LAYER0 = ["tf", "af"]  # input layer transform-first / aggregate-first (engine.py)
 
 
-def test_fused_two_layer_cfg1_cached(cfg1):
+@pytest.mark.parametrize("layer0", LAYER0)
+def test_fused_two_layer_cfg1(cfg1, layer0):
+    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=3, windows=3, layer0=layer0)
+
+
+@pytest.mark.parametrize("layer0", LAYER0)
+def test_fused_two_layer_cfg1_cached(cfg1, layer0):
     rng = np.random.default_rng(0)
     mask = np.zeros(cfg1.num_nodes, bool)
     mask[rng.choice(cfg1.num_nodes, 100, replace=False)] = True
-    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=4, mask=mask, windows=2)
+    _fused_vs_oracle(cfg1, (10, 5), 64, 1024, seed=4, mask=mask, windows=2, layer0=layer0)
 
 
-def test_fused_three_layer_g2(golden_sampling):
+@pytest.mark.parametrize("layer0", LAYER0)
+def test_fused_three_layer_g2(golden_sampling, layer0):
     hg = make_g2(golden_sampling)
-    _fused_vs_oracle(hg, (6, 4, 3), 32, 200, seed=5, mask=golden_sampling["g2/mask10"], windows=4)
+    _fused_vs_oracle(hg, (6, 4, 3), 32, 200, seed=5, mask=golden_sampling["g2/mask10"], windows=4,
+                     layer0=layer0)
+
+
+def test_fused_af_products_like_widths():
+    """aggregate-first input layer at a products-like width ratio (100-d in,
+    64 hidden, 3 layers, big fanouts) on a random graph."""
+    rng = np.random.default_rng(21)
+    n = 6000
+    src = rng.integers(0, n, 120_000)
+    dst = (src + rng.integers(1, 2000, src.size)) % n
+    keys = np.unique(np.concatenate([src * n + dst, dst * n + src]))
+    s, d = keys // n, keys % n
+    ro = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(s, minlength=n), out=ro[1:])
+    feats = rng.standard_normal((n, 100)).astype(np.float32)
+    labels = rng.integers(0, 47, n).astype(np.int32)
+    hg = HostGraph(ro, d, feats, labels, 47, rng.random(n) < 0.3)
+    _fused_vs_oracle(hg, (15, 10, 5), 64, 512, seed=12, windows=2, layer0="af")
 
 
 def test_fused_one_layer(golden_sampling):

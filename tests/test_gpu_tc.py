@@ -28,6 +28,8 @@ SHAPES = [  # (rows, d_in, d_out)
     (1323, 16, 32),
     (1118, 32, 32),
     (5000, 64, 64),    # several items per CTA on the forward
+    (700, 16, 8),      # N = 16: the narrowest UMMA tile (one 32-column TMEM load)
+    (40000, 100, 64),  # many items per CTA: the async ring crosses item boundaries
 ]
 
 
@@ -120,3 +122,37 @@ def test_transform_bwd_deterministic(rows, d_in, d_out):
                                     torch.cuda.current_stream().cuda_stream)
         outs.append(dW.cpu())
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("rows,d_in,d_out", [(2604, 100, 64), (777, 16, 16), (97, 64, 8),
+                                             (30000, 100, 64), (0, 16, 16)])
+def test_aggregate_first_layer(rows, d_in, d_out):
+    """mq_sage_linear_af (act = relu([agg | h] W)) and mq_sage_linear_af_bwd
+    (dW = [agg | h]^T (dh * (act > 0))) against fp64."""
+    rng = np.random.default_rng(rows + d_in)
+    dev = "cuda"
+    agg = rng.standard_normal((max(rows, 1), d_in)).astype(np.float32)
+    h = rng.standard_normal((max(rows, 1), d_in)).astype(np.float32)
+    W = (rng.standard_normal((2 * d_in, d_out)) / np.sqrt(d_in)).astype(np.float32)
+    dh = rng.standard_normal((max(rows, 1), d_out)).astype(np.float32)
+    t = lambda a: torch.as_tensor(a, device=dev)
+    ag, hh, Wt, dht = t(agg), t(h), t(W), t(dh)
+    act = torch.zeros((max(rows, 1), d_out), device=dev)
+    m = torch.tensor([rows], dtype=torch.int32, device=dev)
+    part = torch.zeros(int(lib().mq_sage_af_parts_bytes(max(rows, 1), d_out)) // 4 + 1, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    lib().mq_sage_linear_af(ptr(ag), d_in, ptr(hh), d_in, ptr(m), max(rows, 1), d_in, ptr(Wt),
+                            d_out, ptr(act), d_out, ptr(part), s)
+    z = np.concatenate([agg, h], 1).astype(np.float64)[:rows] @ W.astype(np.float64)
+    ref_act = np.maximum(z, 0)
+    got = act.cpu().numpy()[:rows]
+    assert _normwise(got, ref_act) <= RTOL
+    dwp = torch.zeros(int(lib().mq_sage_af_dw_parts_bytes(d_in, d_out)) // 4 + 1, device=dev)
+    nparts = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib().mq_sage_linear_af_bwd(ptr(ag), d_in, ptr(hh), d_in, ptr(m), max(rows, 1), d_in, ptr(dht),
+                                d_out, ptr(act), d_out, d_out, ptr(dwp), ptr(nparts), s)
+    S = int(nparts.item())
+    dw = dwp[:S * 2 * d_in * d_out].view(S, 2 * d_in, d_out).sum(0).cpu().numpy()
+    dz = dh[:rows].astype(np.float64) * (got > 0)
+    ref_dw = np.concatenate([agg, h], 1).astype(np.float64)[:rows].T @ dz
+    assert _normwise(dw, ref_dw) <= 2 * RTOL
