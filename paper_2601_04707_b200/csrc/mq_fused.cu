@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     }
   }
 
+
   // 1. both[row] = [agg | h_dst]: agg bit-exact (sequential triplet order,
   //    nn.py:79-89); the row's gathers issued together
   {
@@ -561,18 +562,8 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
   __syncthreads();
 
-  // 2. logits = both W: thread (4-row quad, class), float4 over k.  The
-  //    threads without a logits item build W^T (smem -> smem) for phase 4.
+  // 2. logits = both W: thread (4-row quad, class), float4 over k.
   const int n_items = (R / 4) * C;
-  if (a.dh != nullptr && n_items >= kHeadThreads && tid == 0) {
-    for (int i = 0; i < C * d2p; ++i) WsT[i] = Ws[(i % d2p) * Cp + i / d2p];
-  }
-  if (a.dh != nullptr && tid >= n_items) {
-    for (int i = tid - n_items; i < C * d2p; i += kHeadThreads - n_items) {
-      const int c = i / d2p, k = i % d2p;
-      WsT[i] = Ws[k * Cp + c];
-    }
-  }
   for (int item = tid; item < n_items; item += kHeadThreads) {
     const int ib = 4 * (item / C), c = item % C;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -590,6 +581,11 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) dl[(ib + q) * C + c] = acc[q];
+  }
+  // W^T (smem -> smem, conflict-free: Cp is odd) for dt = dl W^T in phase 4;
+  // the threads without a logits item start on it at once
+  if (a.dh != nullptr) {
+    for (int i = tid; i < C * d2p; i += kHeadThreads) WsT[i] = Ws[(i % d2p) * Cp + i / d2p];
   }
   __syncthreads();
 

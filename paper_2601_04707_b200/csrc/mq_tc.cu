@@ -432,9 +432,13 @@ __device__ __forceinline__ void issue_async(const Operands& op, int M, int K, in
     const float* src = op.x;
     int bytes = 0;
     if (MODE == kFwd || MODE == kFwdCat) {
-      const int q = w + 8 * i;
-      const int gm = m0 + (q >> 1) * 8 + (lane & 7);
-      const int k = k0 + ((q & 1) * 4 + (lane >> 3)) * 4;
+      // coalesced: 8 consecutive lanes fetch one row's 32 k (128 B); the
+      // chunk lands at the XOR-swizzled slot [row][k4 ^ (row & 7)], so both
+      // this write and the converter's column-wise read are conflict-free
+      const int g = i * kThreads + tid;
+      const int row = g >> 3, k4 = g & 7;
+      const int gm = m0 + row;
+      const int k = k0 + 4 * k4;
       if (gm < M && k < K) {
         if (MODE == kFwd) {
           src = op.x + (int64_t)gm * op.ldx + k;
@@ -443,6 +447,8 @@ __device__ __forceinline__ void issue_async(const Operands& op, int M, int K, in
           src = cat_src(op, gm, k, bytes);
         }
       }
+      cp_async16(slot + (uint32_t)((row * 8 + (k4 ^ (row & 7))) * 16), bytes ? src : op.x, bytes);
+      continue;
     } else {
       const int gm = m0 + 4 * lane;
       const int k = k0 + 4 * w + i;
@@ -502,8 +508,19 @@ __device__ __forceinline__ void read_raw(const Operands& op, const uint8_t* slot
   auto at = [&](int j) {
     return *reinterpret_cast<const float4*>(slot + (size_t)(j * kThreads + tid) * 16);
   };
+  if (MODE == kFwd || MODE == kFwdCat) {  // the shared, swizzled A tile (see issue_async)
+    const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) ra[i] = at(i);
+    for (int i = 0; i < 4; ++i) {
+      const int q = w + 8 * i;
+      const int m = (q >> 1) * 8 + (lane & 7);
+      const int k4 = (q & 1) * 4 + (lane >> 3);
+      ra[i] = *reinterpret_cast<const float4*>(slot + (size_t)(m * 8 + (k4 ^ (m & 7))) * 16);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ra[i] = at(i);
+  }
   const int nb = (op.Np + 127) / 128;
 #pragma unroll
   for (int i = 0; i < kBPerThread; ++i)
@@ -623,8 +640,10 @@ __global__ void __launch_bounds__(kBlock, 1)
       uint8_t* st = smem + stage * stage_bytes;
       ktrace(first_item, it, 0);
       if (worker) {
-        if (ASYNC) {  // this k block's chunks have landed (this thread's own copies)
+        if (ASYNC) {  // this k block's chunks have landed
           cp_wait_dyn(R - 2);
+          // the forward A tile is shared between the staging threads
+          if (MODE == kFwd || MODE == kFwdCat) asm volatile("bar.sync 2, %0;" ::"n"(kThreads));
           ktrace(first_item, it, 1);
           read_raw<MODE>(op, raw + (size_t)(it % (uint32_t)R) * rbytes, tid, ra, rb);
           l_issue(it + (uint32_t)R - 1);

@@ -89,8 +89,13 @@ class DeviceGraph:
             self.labels = _as_tensor(g.labels, torch.int32, dev)
             self.feature_placement = feature_placement
             if feature_placement == "hbm":
-                table = torch.zeros((n, self.pitch), dtype=torch.float32, device=dev)
-                table[:, :self.feature_dim] = _as_tensor(feats, torch.float32, dev)
+                if (isinstance(feats, torch.Tensor) and feats.device == dev
+                        and feats.dtype == torch.float32 and feats.is_contiguous()
+                        and self.feature_dim == self.pitch):
+                    table = feats  # already a pitched device table: share it (57 GB at papers)
+                else:
+                    table = torch.zeros((n, self.pitch), dtype=torch.float32, device=dev)
+                    table[:, :self.feature_dim] = _as_tensor(feats, torch.float32, dev)
             else:
                 table = torch.zeros((n, self.pitch), dtype=torch.float32, pin_memory=True)
                 table[:, :self.feature_dim] = _as_tensor(feats, torch.float32, "cpu")

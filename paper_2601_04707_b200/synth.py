@@ -30,6 +30,10 @@ SHAPES = {
     # configs[2..3]: ogbn-products-shaped
     "products": dict(num_nodes=2_449_029, num_arcs=62_000_000, feature_dim=100, num_classes=47,
                      fanouts=(15, 10, 5), train=0.08),
+    # configs[4]: ogbn-papers100M-shaped (1.1% training nodes, as the OGB split);
+    # CSR (7.3 GB) + features (57 GB) fit one B200's 180 GB HBM
+    "papers": dict(num_nodes=111_059_956, num_arcs=1_600_000_000, feature_dim=128,
+                   num_classes=172, fanouts=(15, 10, 5), train=0.011),
 }
 
 
@@ -168,7 +172,10 @@ def generate_torch(num_nodes, num_arcs, feature_dim, num_classes, *, train=0.66,
     del counts
     feats = torch.randn((n, feature_dim), generator=gen, device=device, dtype=torch.float32)
     proj = torch.randn((feature_dim, num_classes), generator=gen, device=device)
-    labels = torch.argmax(feats @ proj, dim=1).to(torch.int32)
+    labels = torch.empty(n, dtype=torch.int32, device=device)
+    for lo in range(0, n, 1 << 23):  # chunked: [n x C] logits would be 76 GB at papers
+        hi = min(n, lo + (1 << 23))
+        labels[lo:hi] = torch.argmax(feats[lo:hi] @ proj, dim=1).to(torch.int32)
     tr, va, te = split_masks(n, ratios_for(train), seed + 4)
     return SynthGraph(n, row_offsets, col, feats, labels, num_classes, tr, va, te)
 
