@@ -52,6 +52,8 @@ int tc_linear_af_bwd(const float* agg, int ldagg, const float* h, int ldh,
                      const float* act, int ldact, int d_out, float* part, int32_t* nparts_out,
                      cudaStream_t s);
 int64_t tc_af_dw_part_floats(int64_t d_in, int64_t d_out);
+int tc_dx(const float* g, const int32_t* m_dev, int m_max, int d_in, int d_out, const float* W,
+          float* dh, int lddh, float* part, cudaStream_t s);
 
 
 // ------------------------------------------------------------ GEMM loaders
@@ -938,7 +940,11 @@ int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int
                       K_SAGE_DW_REDUCE);
     if (rc) return rc;
   }
-  if (dh != nullptr && m_max > 0) {
+  if (dh != nullptr && m_max > 0 && tc_backend() == 1 && d_in <= 256 && (2 * d_out) % 4 == 0 &&
+      ((uintptr_t)g & 15) == 0) {
+    int rc = tc_dx(g, m_dev, m_max, d_in, d_out, W, dh, lddh, part, s);
+    if (rc) return rc;
+  } else if (dh != nullptr && m_max > 0) {
     Dims dims{m_dev, 0, nullptr, 2 * d_out, d_in};
     int rc = run_gemm(ALoadRow{g, 2 * d_out}, BLoadWSplitT{W, d_in, d_out}, EpiStore{dh, lddh}, dims,
                       m_max, 2 * d_out, (2 * d_out + GBK - 1) / GBK, part, s, K_SAGE_DH,

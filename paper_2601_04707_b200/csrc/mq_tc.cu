@@ -188,7 +188,13 @@ __host__ __device__ inline Work choose_work(int M, int K, int grid) {
 // nn.py:126-131 / 167-170) — used for the input layer when d_in is narrow:
 //   FCAT: Z (M x N) = [agg | h] (M x 2 d_in) . W (2 d_in x N)   M = dst rows
 //   DCAT: P (2 d_in x N) = [agg | h]^T . (dh * (act > 0))      K = dst rows
-enum Mode { kFwd = 0, kDw = 1, kFwdCat = 2, kDwCat = 3 };
+//   DX:   dh (M x d_in) = G (M x 2 d_out) . [W_top | W_bot]^T  (nn.py:171-174,
+//         the input gradient of a transform-first hidden layer; B is K-major
+//         straight from W's rows)
+enum Mode { kFwd = 0, kDw = 1, kFwdCat = 2, kDwCat = 3, kDx = 4 };
+__host__ __device__ constexpr bool rowA(int mode) {  // A = rows of a row-major matrix (K-major)
+  return mode == kFwd || mode == kFwdCat || mode == kDx;
+}
 
 struct Operands {
   const float* x;  // X (rows x ldx)                      CAT: agg
@@ -204,7 +210,16 @@ struct Operands {
   int ldg = 0;                // DCAT: dh pitch
   const float* act = nullptr; // DCAT: relu output (mask), pitch ldact
   int ldact = 0;
+  int wd_in = 0, wd_out = 0;  // DX: W is (2 wd_in x wd_out); N = wd_in, K = 2 wd_out
+  float* out = nullptr;       // when the device picks S = 1: write the tile here directly
+  int ldo = 0;
 };
+
+// DX operand B(n, k..k+3): row n of W_top (k < wd_out) or W_bot, K-major
+__device__ __forceinline__ const float* dx_src(const Operands& op, int n, int k) {
+  return k < op.wd_out ? op.w + (int64_t)n * op.wd_out + k
+                       : op.w + (int64_t)(op.wd_in + n) * op.wd_out + (k - op.wd_out);
+}
 
 // CAT operand A: four consecutive columns c of row r of [agg | h] (d_in % 4 == 0)
 __device__ __forceinline__ float4 ld_cat4(const Operands& op, int64_t r, int c) {
@@ -231,14 +246,14 @@ template <int MODE>
 __device__ __forceinline__ void load_a(const Operands& op, int M, int K, int m0, int k0, int tid,
                                        float4 (&ra)[4]) {
   const int lane = tid & 31, w = tid >> 5;
-  if (MODE == kFwd || MODE == kFwdCat) {
+  if (rowA(MODE)) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int q = w + 8 * i;
       const int m = (q >> 1) * 8 + (lane & 7);
       const int k = k0 + ((q & 1) * 4 + (lane >> 3)) * 4;
       const int gm = m0 + m;
-      if (MODE == kFwd)
+      if (MODE != kFwdCat)
         ra[i] = (gm < M && k < K) ? ld_row4(op.x + (int64_t)gm * op.ldx, k, op.d_in, true)
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
       else
@@ -289,7 +304,7 @@ __device__ __forceinline__ void st_transposed(uint8_t* hi_base, uint8_t* lo_base
 template <int MODE>
 __device__ __forceinline__ void store_a(uint8_t* hi, uint8_t* lo, int tid, const float4 (&ra)[4]) {
   const int lane = tid & 31, w = tid >> 5;
-  if (MODE == kFwd || MODE == kFwdCat) {
+  if (rowA(MODE)) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int q = w + 8 * i;
@@ -340,9 +355,32 @@ __device__ __forceinline__ float4 load_b4(const Operands& op, int K, int k, int 
   return ld_row4(op.g + (int64_t)k * op.N, n, op.N, (op.N & 3) == 0);
 }
 
+// DX B chunk j of a thread: g = j * kThreads + tid, n = g % Np, k4 = g / Np
+// (consecutive lanes -> consecutive n: conflict-free K-major smem stores)
 template <int MODE>
 __device__ __forceinline__ void load_b(const Operands& op, int K, int k0, int tid,
                                        float4 (&rb)[kBPerThread][4]) {
+  if (MODE == kDx) {
+#pragma unroll
+    for (int j = 0; j < 4 * kBPerThread; ++j) {
+      const int g = j * kThreads + tid;
+      const int n = g % op.Np, k = k0 + 4 * (g / op.Np);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g < 8 * op.Np && n < op.N && k < K) {
+        const float* p = dx_src(op, n, k);
+        if ((op.wd_out & 3) == 0) {
+          v = __ldg(reinterpret_cast<const float4*>(p));
+        } else {
+          float t[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t[e] = k + e < K ? __ldg(dx_src(op, n, k + e)) : 0.f;
+          v = make_float4(t[0], t[1], t[2], t[3]);
+        }
+      }
+      rb[j >> 2][j & 3] = v;
+    }
+    return;
+  }
   const int n4s = op.Np / 4;
 #pragma unroll
   for (int i = 0; i < kBPerThread; ++i) {
@@ -355,8 +393,18 @@ __device__ __forceinline__ void load_b(const Operands& op, int K, int k0, int ti
   }
 }
 
+template <int MODE>
 __device__ __forceinline__ void store_b(const Operands& op, uint8_t* hi, uint8_t* lo, int tid,
                                         const float4 (&rb)[kBPerThread][4]) {
+  if (MODE == kDx) {
+#pragma unroll
+    for (int j = 0; j < 4 * kBPerThread; ++j) {
+      const int g = j * kThreads + tid;
+      if (g < 8 * op.Np)
+        st_split(hi, lo, (uint32_t)((g / op.Np) * (op.Np * 16) + (g % op.Np) * 16), rb[j >> 2][j & 3]);
+    }
+    return;
+  }
   const int n4s = op.Np / 4;
 #pragma unroll
   for (int i = 0; i < kBPerThread; ++i) {
@@ -431,7 +479,7 @@ __device__ __forceinline__ void issue_async(const Operands& op, int M, int K, in
   for (int i = 0; i < 4; ++i) {
     const float* src = op.x;
     int bytes = 0;
-    if (MODE == kFwd || MODE == kFwdCat) {
+    if (rowA(MODE)) {
       // coalesced: 8 consecutive lanes fetch one row's 32 k (128 B); the
       // chunk lands at the XOR-swizzled slot [row][k4 ^ (row & 7)], so both
       // this write and the converter's column-wise read are conflict-free
@@ -440,7 +488,7 @@ __device__ __forceinline__ void issue_async(const Operands& op, int M, int K, in
       const int gm = m0 + row;
       const int k = k0 + 4 * k4;
       if (gm < M && k < K) {
-        if (MODE == kFwd) {
+        if (MODE != kFwdCat) {
           src = op.x + (int64_t)gm * op.ldx + k;
           bytes = vbytes(op.d_in - k);
         } else {
@@ -465,6 +513,15 @@ __device__ __forceinline__ void issue_async(const Operands& op, int M, int K, in
   }
   const int n4s = op.Np / 4;
   const int nb = (op.Np + 127) / 128;
+  if (MODE == kDx) {
+    for (int j = 0; j < 4 * nb; ++j) {
+      const int g = j * kThreads + tid;
+      const int n = g % op.Np, k = k0 + 4 * (g / op.Np);
+      const bool ok = g < 8 * op.Np && n < op.N && k < K;
+      cp_async16(dst(4 + j), ok ? dx_src(op, n, k) : op.x, ok ? 16 : 0);
+    }
+    return;
+  }
   for (int i = 0; i < nb; ++i) {
     const int c = tid + i * kThreads;
     const int n4 = c % n4s, k4 = c / n4s;
@@ -508,7 +565,7 @@ __device__ __forceinline__ void read_raw(const Operands& op, const uint8_t* slot
   auto at = [&](int j) {
     return *reinterpret_cast<const float4*>(slot + (size_t)(j * kThreads + tid) * 16);
   };
-  if (MODE == kFwd || MODE == kFwdCat) {  // the shared, swizzled A tile (see issue_async)
+  if (rowA(MODE)) {  // the shared, swizzled A tile (see issue_async)
     const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -643,7 +700,7 @@ __global__ void __launch_bounds__(kBlock, 1)
         if (ASYNC) {  // this k block's chunks have landed
           cp_wait_dyn(R - 2);
           // the forward A tile is shared between the staging threads
-          if (MODE == kFwd || MODE == kFwdCat) asm volatile("bar.sync 2, %0;" ::"n"(kThreads));
+          if (rowA(MODE)) asm volatile("bar.sync 2, %0;" ::"n"(kThreads));
           ktrace(first_item, it, 1);
           read_raw<MODE>(op, raw + (size_t)(it % (uint32_t)R) * rbytes, tid, ra, rb);
           l_issue(it + (uint32_t)R - 1);
@@ -655,7 +712,7 @@ __global__ void __launch_bounds__(kBlock, 1)
         // ---- stage A and B (split hi/lo)
         store_a<MODE>(st, st + Smem::kA, tid, ra);
         ktrace(first_item, it, 4);
-        store_b(op, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid, rb);
+        store_b<MODE>(op, st + 2 * Smem::kA, st + 2 * Smem::kA + Smem::b_bytes(Np), tid, rb);
         ktrace(first_item, it, 5);
       }
       fence_async_smem();
@@ -725,17 +782,20 @@ __global__ void __launch_bounds__(kBlock, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kThreads));  // staging warps only
       const int rows = min(BM, M - m0);
-      if ((op.N & 3) == 0) {
+      // a single split is already the result: straight to op.out when given
+      float* dst = (wk.S == 1 && op.out) ? op.out : part + (int64_t)s * M * op.N;
+      const int ldd = (wk.S == 1 && op.out) ? op.ldo : op.N;
+      if ((op.N & 3) == 0 && (ldd & 3) == 0 && ((uintptr_t)dst & 15) == 0) {
         const int n4 = op.N / 4;
         for (int e = tid; e < rows * n4; e += kThreads) {
           const int r = e / n4, c = 4 * (e % n4);
-          *reinterpret_cast<float4*>(part + ((int64_t)s * M + m0 + r) * op.N + c) =
+          *reinterpret_cast<float4*>(dst + (int64_t)(m0 + r) * ldd + c) =
               *reinterpret_cast<const float4*>(tile + r * ldt + c);
         }
       } else {
         for (int e = tid; e < rows * op.N; e += kThreads) {
           const int r = e / op.N, c = e % op.N;
-          part[((int64_t)s * M + m0 + r) * op.N + c] = tile[r * ldt + c];
+          dst[(int64_t)(m0 + r) * ldd + c] = tile[r * ldt + c];
         }
       }
     }
@@ -754,11 +814,13 @@ __global__ void __launch_bounds__(kBlock, 1)
 // fixed-order split reduction + layer epilogue (same decomposition as the GEMM)
 template <class Epi>
 __global__ void tc_reduce_kernel(const float* __restrict__ part, const int32_t* m_dev, int m_static,
-                                 const int32_t* k_dev, int k_static, int N, int grid_gemm, Epi epi) {
+                                 const int32_t* k_dev, int k_static, int N, int grid_gemm, Epi epi,
+                                 bool direct) {
   MQ_PDL_ENTRY();
   const int M = m_dev ? *m_dev : m_static;
   const int K = k_dev ? *k_dev : k_static;
   const Work wk = choose_work(M, K, grid_gemm);
+  if (direct && wk.S == 1) return;  // the GEMM wrote the result (op.out)
   const int64_t total = (int64_t)M * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -788,6 +850,7 @@ bool tc_async_ok(const tc::Operands& op) {
   if (!al16(op.x) || (op.ldx & 3)) return false;
   if (MODE == tc::kFwd) return al16(op.w) && (op.n_half & 3) == 0;
   if (MODE == tc::kDw) return al16(op.g) && (op.N & 3) == 0;
+  if (MODE == tc::kDx) return al16(op.w) && (op.wd_out & 3) == 0;
   if (MODE == tc::kFwdCat)
     return al16(op.x2) && (op.ldx2 & 3) == 0 && (op.d_in & 3) == 0 && al16(op.w) && (op.N & 3) == 0;
   return al16(op.x2) && (op.ldx2 & 3) == 0 && (op.d_in & 3) == 0 && al16(op.g) &&
@@ -801,7 +864,7 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
                 const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
                 cudaStream_t s, int kid, int kid_red, bool skip_reduce = false,
                 int32_t* nparts_out = nullptr) {
-  static thread_local bool configured[4][2] = {};
+  static thread_local bool configured[5][2] = {};
   const int base = tc::Smem::total(op.Np);
   int R = (kSmemBudget - base) / tc::raw_bytes(MODE, op.Np);
   if (R > tc::kMaxRaw) R = tc::kMaxRaw;
@@ -835,7 +898,7 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
   {
     ProfScope ps(kid_red, s);
     MQ_CUDA(launch_k(tc::tc_reduce_kernel<Epi>, dim3(rb), dim3(256), 0, s, part, m_dev, m_static, k_dev, k_static, op.N, grid,
-                                                 epi));
+                                                 epi, op.out != nullptr));
   }
   MQ_LAUNCH_CHECK("tc_reduce");
   return MQ_OK;
@@ -928,10 +991,25 @@ int tc_linear_af_bwd(const float* agg, int ldagg, const float* h, int ldh,
 
 int64_t tc_af_dw_part_floats(int64_t d_in, int64_t d_out) { return tc_part_floats(2 * d_in, d_out); }
 
+// input gradient of a transform-first layer: dh = G [W_top | W_bot]^T over the
+// live rows; a single split writes dh directly (no reduction pass)
+int tc_dx(const float* g, const int32_t* m_dev, int m_max, int d_in, int d_out, const float* W,
+          float* dh, int lddh, float* part, cudaStream_t s) {
+  tc::Operands op{g, 2 * d_out, 2 * d_out, W, 0, nullptr, d_in, (d_in + 15) / 16 * 16};
+  op.wd_in = d_in;
+  op.wd_out = d_out;
+  op.out = dh;
+  op.ldo = lddh;
+  return run_tc_gemm<tc::kDx>(op, m_dev, 0, m_max, nullptr, 2 * d_out, 2 * d_out, part,
+                              EpiStore{dh, lddh}, s, K_SAGE_DH, K_SAGE_DH_REDUCE);
+}
+
 int64_t tc_scratch_floats(int64_t m_max, int64_t d_in, int64_t d_out) {
   int64_t a = tc_part_floats(m_max, 2 * d_out);
   int64_t b = tc_part_floats(d_in, 2 * d_out);
-  return a > b ? a : b;
+  int64_t c = tc_part_floats(m_max, d_in);  // dh (tc_dx)
+  a = a > b ? a : b;
+  return a > c ? a : c;
 }
 
 }  // namespace mq
