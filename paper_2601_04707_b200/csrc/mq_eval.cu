@@ -272,6 +272,9 @@ int mq_full_aggregate(const int64_t* row_off, const int32_t* col, int64_t n_node
 }
 
 int64_t mq_full_transform_part_floats(int64_t n_nodes, int32_t d_out) {
+  // with at least one 128-row tile per SM the device picks a single split and
+  // the GEMM writes y directly: no partial buffer
+  if ((n_nodes + 127) / 128 >= kNumSMs) return 1;
   return tc_y_part_floats(n_nodes, d_out);
 }
 

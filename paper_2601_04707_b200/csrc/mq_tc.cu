@@ -149,12 +149,21 @@ __device__ __forceinline__ void trace(int i) {
     g_tc_trace[i] = t;
   }
 }
+__device__ unsigned long long g_tc_cta[256][2];
+__device__ __forceinline__ void cta_mark(int i) {
+  if (threadIdx.x == 0 && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tc_cta[blockIdx.x][i] = t;
+  }
+}
 __device__ __forceinline__ void ktrace(bool on, uint32_t it, int p) {
   if (on && it < 3) trace(3 + 8 * (int)it + p);
 }
 #else
 __device__ __forceinline__ void trace(int) {}
 __device__ __forceinline__ void ktrace(bool, uint32_t, int) {}
+__device__ __forceinline__ void cta_mark(int) {}
 #endif
 
 // ------------------------------------------------------------ work split
@@ -213,6 +222,7 @@ struct Operands {
   int wd_in = 0, wd_out = 0;  // DX: W is (2 wd_in x wd_out); N = wd_in, K = 2 wd_out
   float* out = nullptr;       // when the device picks S = 1: write the tile here directly
   int ldo = 0;
+  int relu = 0;               // ... through max(., 0) (the FCAT layer's activation)
 };
 
 // DX operand B(n, k..k+3): row n of W_top (k < wd_out) or W_bot, K-major
@@ -619,6 +629,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   if ((int)blockIdx.x >= items || M <= 0) return;
 
   trace(0);
+  cta_mark(0);
   const bool worker = warp < kThreads / 32;
   const bool issuer = tid == kThreads;  // warp 8, lane 0
   const uint32_t tmem_cols = Np <= 32 ? 32 : Np <= 64 ? 64 : Np <= 128 ? 128 : 256;
@@ -785,17 +796,20 @@ __global__ void __launch_bounds__(kBlock, 1)
       // a single split is already the result: straight to op.out when given
       float* dst = (wk.S == 1 && op.out) ? op.out : part + (int64_t)s * M * op.N;
       const int ldd = (wk.S == 1 && op.out) ? op.ldo : op.N;
+      const bool relu = wk.S == 1 && op.out && op.relu;
       if ((op.N & 3) == 0 && (ldd & 3) == 0 && ((uintptr_t)dst & 15) == 0) {
         const int n4 = op.N / 4;
         for (int e = tid; e < rows * n4; e += kThreads) {
           const int r = e / n4, c = 4 * (e % n4);
-          *reinterpret_cast<float4*>(dst + (int64_t)(m0 + r) * ldd + c) =
-              *reinterpret_cast<const float4*>(tile + r * ldt + c);
+          float4 v = *reinterpret_cast<const float4*>(tile + r * ldt + c);
+          if (relu) v = make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+          *reinterpret_cast<float4*>(dst + (int64_t)(m0 + r) * ldd + c) = v;
         }
       } else {
         for (int e = tid; e < rows * op.N; e += kThreads) {
           const int r = e / op.N, c = e % op.N;
-          dst[(int64_t)(m0 + r) * ldd + c] = tile[r * ldt + c];
+          const float v = tile[r * ldt + c];
+          dst[(int64_t)(m0 + r) * ldd + c] = relu ? fmaxf(v, 0.f) : v;
         }
       }
     }
@@ -809,6 +823,7 @@ __global__ void __launch_bounds__(kBlock, 1)
     tmem_dealloc(tmem, tmem_cols);
   }
   trace(29);
+  cta_mark(1);
 }
 
 // fixed-order split reduction + layer epilogue (same decomposition as the GEMM)
@@ -822,11 +837,9 @@ __global__ void tc_reduce_kernel(const float* __restrict__ part, const int32_t* 
   const Work wk = choose_work(M, K, grid_gemm);
   if (direct && wk.S == 1) return;  // the GEMM wrote the result (op.out)
   const int64_t total = (int64_t)M * N;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / N), j = (int)(e % N);
-    epi(i, j, fixed_order_sum(part + e, total, wk.S));
-  }
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < M; i += gridDim.x * wpb)  // warp per row
+    for (int j = lane; j < N; j += 32) epi(i, j, fixed_order_sum(part + (int64_t)i * N + j, total, wk.S));
 }
 
 }  // namespace tc
@@ -942,6 +955,8 @@ int64_t tc_y_part_floats(int64_t m_max, int64_t d_out) { return tc_part_floats(m
 int tc_transform_rows(const float* h, int ldh, int64_t n, int d_in, const float* W, int d_out,
                       float* y, float* part, cudaStream_t s) {
   tc::Operands op{h, ldh, d_in, W, d_out, nullptr, 2 * d_out, (2 * d_out + 15) / 16 * 16};
+  op.out = y;
+  op.ldo = 2 * d_out;
   return run_tc_gemm<tc::kFwd>(op, nullptr, (int)n, (int)n, nullptr, d_in, d_in, part,
                                EpiStore{y, 2 * d_out}, s, K_FULL_TRANSFORM,
                                K_FULL_TRANSFORM_REDUCE);
@@ -966,6 +981,9 @@ int tc_linear_af(const float* agg, int ldagg, const float* h, int ldh, const int
   tc::Operands op{agg, ldagg, d_in, W, d_out, nullptr, d_out, (d_out + 15) / 16 * 16};
   op.x2 = h;
   op.ldx2 = ldh;
+  op.out = act;
+  op.ldo = ldact;
+  op.relu = 1;
   return run_tc_gemm<tc::kFwdCat>(op, m_dev, 0, m_max, nullptr, 2 * d_in, 2 * d_in, part,
                                   EpiLinearFwd{nullptr, 0, act, ldact}, s, K_SAGE_AF,
                                   K_SAGE_AF_REDUCE);
@@ -1025,6 +1043,11 @@ int mq_set_gemm_backend(int32_t backend) {
 int mq_get_gemm_backend(void) { return g_gemm_backend; }
 
 #ifdef MQ_TC_TRACE
+int mq_debug_tc_cta(unsigned long long* out) {
+  MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_cta, sizeof(unsigned long long) * 512));
+  return MQ_OK;
+}
+
 int mq_debug_tc_trace(unsigned long long* out) {
   MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_trace, sizeof(unsigned long long) * 32));
   return MQ_OK;
