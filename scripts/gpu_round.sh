@@ -11,4 +11,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 MQ_BENCH_KERNELS=1 timeout 600 python bench.py > $OUT/bench.jsonl 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 30 --warmup 3 --no-cpu-baseline --profile-steps 2 --e2e-steps 10 > $OUT/ncu_bench.log 2>&1; echo "ncu exit $?" >> $OUT/ncu_bench.log
-tail -3 $OUT/*.log $OUT/bench.err
+for f in $OUT/*.log $OUT/bench.err; do echo "== $f"; tail -n 3 $f; done
