@@ -346,6 +346,8 @@ def run_ours(args):
     windows = -(-n_train // (args.batch * world))
     if args.no_pdl:
         lib().mq_set_pdl(0)
+    if os.environ.get("MQ_TC_GRID_CAP"):
+        lib().mq_set_tc_grid_cap(int(os.environ["MQ_TC_GRID_CAP"]))
     runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=args.batch, num_train=n_train,
                            cache=cache, optimizer="adam", seed=args.seed, world=world, rank=rank,
                            multi=world > 1, queue_depth=args.queue_depth,

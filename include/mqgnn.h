@@ -386,6 +386,9 @@ int mq_f64_to_f32(const double* in64, double divisor, float* out32, int64_t n, v
  * split-K on the CUDA cores.  Process-wide; for tests and A/B measurement. */
 int mq_set_gemm_backend(int32_t backend);
 int mq_get_gemm_backend(void);
+/* Cap on the tcgen05 GEMM grid (default 148 = one CTA per SM); a smaller
+ * grid means fewer, deeper split-K partitions (A/B measurement). */
+int mq_set_tc_grid_cap(int32_t cap);
 /* Programmatic dependent launch for the step's kernel chains (default on):
  * kernel k+1 is scheduled while kernel k runs and waits on the device for
  * k's completion (griddepcontrol), hiding the launch gap.  Process-wide; for

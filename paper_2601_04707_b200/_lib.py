@@ -85,6 +85,7 @@ SIGNATURES = {
     "mq_set_gemm_backend": (C.c_int, [I32]),
     "mq_get_gemm_backend": (C.c_int, []),
     "mq_set_pdl": (C.c_int, [I32]),
+    "mq_set_tc_grid_cap": (C.c_int, [I32]),
     "mq_memcpy_async": (C.c_int, [P, P, I64, P]),
     "mq_memset_async": (C.c_int, [P, I32, I64, P]),
     "mq_get_pdl": (C.c_int, []),

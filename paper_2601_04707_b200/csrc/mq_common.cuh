@@ -102,6 +102,40 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 // ---------------------------------------------------------------------------
+// In-step timeline (MQ_TC_TRACE builds only): per kernel id, the earliest CTA
+// entry and the latest CTA exit (%globaltimer), read by mq_debug_timeline.
+#ifdef MQ_TC_TRACE
+static __device__ unsigned long long g_timeline[32][2];  // one copy per translation unit
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MQ_TL_BEGIN(id) \
+  do { if (threadIdx.x == 0) atomicMin(&::mq::g_timeline[id][0], ::mq::gtimer()); } while (0)
+#define MQ_TL_END(id) \
+  do { if (threadIdx.x == 0) atomicMax(&::mq::g_timeline[id][1], ::mq::gtimer()); } while (0)
+// reader/reset of this TU's copy: extern "C" mq_debug_timeline_<tag>
+#define MQ_TL_READER(tag)                                                             \
+  extern "C" int mq_debug_timeline_##tag(unsigned long long* out, int reset) {        \
+    if (reset) {                                                                      \
+      unsigned long long init[32][2];                                                 \
+      for (int i = 0; i < 32; ++i) {                                                  \
+        init[i][0] = ~0ull;                                                           \
+        init[i][1] = 0ull;                                                            \
+      }                                                                               \
+      return cudaMemcpyToSymbol(::mq::g_timeline, init, sizeof(init)) == cudaSuccess ? 0 : 2; \
+    }                                                                                 \
+    return cudaMemcpyFromSymbol(out, ::mq::g_timeline, sizeof(unsigned long long) * 64) == \
+                   cudaSuccess ? 0 : 2;                                               \
+  }
+#else
+#define MQ_TL_BEGIN(id) do {} while (0)
+#define MQ_TL_END(id) do {} while (0)
+#define MQ_TL_READER(tag)
+#endif
+
+// ---------------------------------------------------------------------------
 // Philox4x32-10 (Random123 constants), shared host/device so that host and GPU
 // draws are identical by construction.
 

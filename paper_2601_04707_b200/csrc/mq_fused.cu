@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
     const int32_t* __restrict__ m_dev, int N, float* __restrict__ act, int ldact, ZeroRange z0,
     ZeroRange z1) {
   MQ_PDL_ENTRY();
+  MQ_TL_BEGIN(5);
   constexpr int U = 4, SU = 4;
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   zero_range(z0, tid, nth);
   zero_range(z1, tid, nth);
+  MQ_TL_END(5);
 }
 
 // ------------------------------------------------------------ scatter bwd
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
     const float* __restrict__ dh, int lddh, const float* __restrict__ act, int ldact, int N,
     float* __restrict__ G) {
   MQ_PDL_ENTRY();
+  MQ_TL_BEGIN(7);
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
   const int n = *n_dst_dev;
@@ -424,6 +427,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
       }
     }
   }
+  MQ_TL_END(7);
 }
 
 // ------------------------------------------------------------ head
@@ -453,12 +457,27 @@ struct HeadArgs {
   int R;
 };
 
+#ifdef MQ_TC_TRACE
+__device__ unsigned long long g_head_trace[16];
+__device__ __forceinline__ void htrace(int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_head_trace[i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void htrace(int) {}
+#endif
+
 constexpr int kHeadRows = 8;               // target rows per CTA: one warp per row
 constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   MQ_PDL_ENTRY();
+  MQ_TL_BEGIN(6);
+  htrace(0);
   extern __shared__ __align__(16) float smem[];
   constexpr int R = kHeadRows;
   const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp;
@@ -506,6 +525,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
 
 
+  htrace(1);
   // 1. both[row] = [agg | h_dst]: agg bit-exact (sequential triplet order,
   //    nn.py:79-89); the row's gathers issued together
   {
@@ -564,33 +584,31 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
   __syncthreads();
 
-  // 2. logits = both W: thread (4-row quad, class), float4 over k.
-  const int n_items = (R / 4) * C;
-  for (int item = tid; item < n_items; item += kHeadThreads) {
-    const int ib = 4 * (item / C), c = item % C;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  htrace(2);
+  // 2. logits = both W: one (row, class) item per thread (all 256 busy),
+  //    float4 over k; consecutive classes read consecutive W columns.
+  for (int item = tid; item < R * C; item += kHeadThreads) {
+    const int r = item / C, c = item % C;
+    const float* br = both + r * d2p;
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll 4
     for (int k = 0; k < d2p; k += 4) {
-      const float w0 = Ws[(k + 0) * Cp + c], w1 = Ws[(k + 1) * Cp + c];
-      const float w2 = Ws[(k + 2) * Cp + c], w3 = Ws[(k + 3) * Cp + c];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 b = *reinterpret_cast<const float4*>(both + (ib + q) * d2p + k);
-        acc[q] = fmaf(b.x, w0, acc[q]);
-        acc[q] = fmaf(b.y, w1, acc[q]);
-        acc[q] = fmaf(b.z, w2, acc[q]);
-        acc[q] = fmaf(b.w, w3, acc[q]);
-      }
+      const float4 b = *reinterpret_cast<const float4*>(br + k);
+      acc0 = fmaf(b.x, Ws[(k + 0) * Cp + c], acc0);
+      acc1 = fmaf(b.y, Ws[(k + 1) * Cp + c], acc1);
+      acc0 = fmaf(b.z, Ws[(k + 2) * Cp + c], acc0);
+      acc1 = fmaf(b.w, Ws[(k + 3) * Cp + c], acc1);
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) dl[(ib + q) * C + c] = acc[q];
+    dl[r * C + c] = acc0 + acc1;
   }
-  // W^T (smem -> smem, conflict-free: Cp is odd) for dt = dl W^T in phase 4;
-  // the threads without a logits item start on it at once
+  // W^T (smem -> smem, conflict-free: Cp is odd) for dt = dl W^T in phase 4
   if (a.dh != nullptr) {
-    for (int i = tid; i < C * d2p; i += kHeadThreads) WsT[i] = Ws[(i % d2p) * Cp + i / d2p];
+    for (int c = warp; c < C; c += R)  // warp per class, lanes over k
+      for (int k = lane; k < d2p; k += 32) WsT[c * d2p + k] = Ws[k * Cp + c];
   }
   __syncthreads();
 
+  htrace(3);
   // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot
   {
     float* x = dl + warp * C;
@@ -632,6 +650,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     __syncwarp();
   }
 
+  htrace(4);
   // 4. dt = dl W^T -> dh: self half to the dst row, top half scattered over the
   //    row's edges (dh zeroed for rows [0, n_src) beforehand).  A lane owns 4
   //    consecutive k of [top | bot]; one v4 reduction per target row.
@@ -699,6 +718,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     if (s_bad) atomicOr(a.nonfinite, 1);
   }
 
+  htrace(5);
   // 5. this CTA's dW partial = both^T dl: thread (k octet, class), 8 k per item
   {
     float* part = a.part + (int64_t)blockIdx.x * d2 * C;
@@ -729,6 +749,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     }
   }
 
+  htrace(6);
   // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA
   //    order (mq_grad_src), so no grid-wide barrier is needed here.  The last
   //    CTA to finish commits the batch loss to the epoch's loss ring.
@@ -746,6 +767,8 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
       }
     }
   }
+  htrace(7);
+  MQ_TL_END(6);
 }
 
 // dW = fixed-order sum of the head's per-CTA partials (materialising API)
@@ -1023,6 +1046,13 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
   return MQ_OK;
 }
 
+#ifdef MQ_TC_TRACE
+extern "C" int mq_debug_head_trace(unsigned long long* out) {
+  MQ_CUDA(cudaMemcpyFromSymbol(out, g_head_trace, sizeof(unsigned long long) * 16));
+  return MQ_OK;
+}
+#endif
+
 int mq_sage_head_grad_seg(int32_t n_dst_max, int32_t d, int32_t n_classes, void* scratch,
                           int64_t offset, mq_grad_seg* out) {
   MQ_CHECK_ARG(scratch && out && n_dst_max >= 1 && d >= 1 && n_classes >= 1,
@@ -1055,3 +1085,5 @@ int mq_sage_dw_grad_seg(float* dw_parts, const int32_t* dw_nparts_dev, int32_t d
 }
 
 }  // extern "C"
+
+MQ_TL_READER(fused)

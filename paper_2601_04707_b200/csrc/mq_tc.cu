@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                    int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out,
                    int R) {
   MQ_PDL_ENTRY();
+  MQ_TL_BEGIN(MODE);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kStages + 1];
@@ -824,6 +825,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   }
   trace(29);
   cta_mark(1);
+  MQ_TL_END(MODE);
 }
 
 // fixed-order split reduction + layer epilogue (same decomposition as the GEMM)
@@ -847,12 +849,14 @@ __global__ void tc_reduce_kernel(const float* __restrict__ part, const int32_t* 
 // ------------------------------------------------------------ host side
 static int g_gemm_backend = 1;  // 1 = tcgen05 3xTF32, 0 = fp32 FFMA split-K
 
+static int g_tc_grid_cap = kNumSMs;  // experiments: fewer CTAs -> fewer, deeper splits
+
 inline int tc_grid(int m_max, int k_max) {
   const int tiles = (m_max + tc::BM - 1) / tc::BM;
   const int nkb = (k_max + tc::BK - 1) / tc::BK;
   long long cap = (long long)(tiles < 1 ? 1 : tiles) *
                   (nkb < 1 ? 1 : (nkb > tc::kMaxSplitsTc ? tc::kMaxSplitsTc : nkb));
-  return (int)(cap < kNumSMs ? cap : kNumSMs);
+  return (int)(cap < g_tc_grid_cap ? cap : g_tc_grid_cap);
 }
 
 inline bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -1042,6 +1046,12 @@ int mq_set_gemm_backend(int32_t backend) {
 
 int mq_get_gemm_backend(void) { return g_gemm_backend; }
 
+int mq_set_tc_grid_cap(int32_t cap) {
+  MQ_CHECK_ARG(cap >= 1 && cap <= kNumSMs, "mq_set_tc_grid_cap: 1..%d", kNumSMs);
+  g_tc_grid_cap = cap;
+  return MQ_OK;
+}
+
 #ifdef MQ_TC_TRACE
 int mq_debug_tc_cta(unsigned long long* out) {
   MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_cta, sizeof(unsigned long long) * 512));
@@ -1055,3 +1065,5 @@ int mq_debug_tc_trace(unsigned long long* out) {
 #endif
 
 }  // extern "C"
+
+MQ_TL_READER(tc)

@@ -118,12 +118,41 @@ __device__ __forceinline__ double grad_count(const double* g64, double scale, in
   return (g64 != nullptr && scale == 0.0) ? g64[n] : 1.0;
 }
 
+// Adam update of element i with gradient g (nn.py:191-206, NumPy-2 f32 op order)
+__device__ __forceinline__ bool adam_elem(float* __restrict__ w, float* __restrict__ m,
+                                          float* __restrict__ v, int64_t i, float g, float bc1,
+                                          float bc2, float lr) {
+  const float b1 = (float)0.9, b2 = (float)0.999;
+  const float c1 = (float)(1.0 - 0.9), c2 = (float)(1.0 - 0.999), eps = (float)1e-8;
+  float mi = __fmul_rn(m[i], b1);                         // m *= beta1
+  mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
+  float vi = __fmul_rn(v[i], b2);                         // v *= beta2
+  vi = __fadd_rn(vi, __fmul_rn(__fmul_rn(c2, g), g));     // v += (1-beta2)*g*g
+  const float mh = __fdiv_rn(mi, bc1);                    // m / (1 - beta1**t)
+  const float vh = __fdiv_rn(vi, bc2);                    // v / (1 - beta2**t)
+  const float upd = __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps));
+  const float wi = __fsub_rn(w[i], upd);                  // w -= lr*mh/(sqrt(vh)+eps)
+  m[i] = mi;
+  v[i] = vi;
+  w[i] = wi;
+  return !finite_f(wi);
+}
+
+// The first `coop_blocks` blocks resolve one many-partial segment (the fused
+// head's per-CTA dW partials) cooperatively: a block owns 32 consecutive
+// elements, warp q sums partials q, q+8, ... (all loads in flight at once),
+// warp 0 adds the 8 warp sums in warp order — fixed order, deterministic, ~1
+// L2 round trip instead of nparts/16.  The other blocks take every other
+// element one per thread.
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
                             const float* __restrict__ g32, const double* __restrict__ g64,
                             double scale, int64_t n, int32_t* __restrict__ step,
                             const float* __restrict__ bias, int bias_len, float lr,
-                            int32_t* __restrict__ nonfinite, GradSrc src) {
+                            int32_t* __restrict__ nonfinite, GradSrc src, int coop_seg,
+                            int coop_blocks) {
   MQ_PDL_ENTRY();
+  MQ_TL_BEGIN(8);
+  __shared__ float red[8][33];
   const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
   if (t < 1 || t > bias_len) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
@@ -132,27 +161,50 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
   }
   const float bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
   const double count = grad_count(g64, scale, n);
-  const float b1 = (float)0.9, b2 = (float)0.999;
-  const float c1 = (float)(1.0 - 0.9), c2 = (float)(1.0 - 0.999), eps = (float)1e-8;
   int bad = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float g = load_grad(src, g32, g64, scale, count, i);
-    float mi = __fmul_rn(m[i], b1);                         // m *= beta1
-    mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
-    float vi = __fmul_rn(v[i], b2);                         // v *= beta2
-    vi = __fadd_rn(vi, __fmul_rn(__fmul_rn(c2, g), g));     // v += (1-beta2)*g*g
-    const float mh = __fdiv_rn(mi, bc1);                    // m / (1 - beta1**t)
-    const float vh = __fdiv_rn(vi, bc2);                    // v / (1 - beta2**t)
-    const float upd = __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps));
-    const float wi = __fsub_rn(w[i], upd);                  // w -= lr*mh/(sqrt(vh)+eps)
-    m[i] = mi;
-    v[i] = vi;
-    w[i] = wi;
-    bad |= !finite_f(wi);
+  int64_t c_lo = 0, c_hi = 0;  // flat range of the cooperative segment
+  if (coop_blocks > 0) {
+    const mq_grad_seg& sg = src.s.seg[coop_seg];
+    c_lo = sg.offset;
+    c_hi = sg.offset + sg.size;
+  }
+  if ((int)blockIdx.x < coop_blocks) {
+    const mq_grad_seg& sg = src.s.seg[coop_seg];
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + lane;  // element within the segment
+    const int np = sg.nparts;
+    float acc = 0.f;
+    if (j < sg.size) {
+      float tv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int p = q + 8 * u;
+        tv[u] = p < np ? __ldcg(sg.part + (int64_t)p * sg.stride + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (q + 8 * u < np) acc += tv[u];
+      for (int p = q + 128; p < np; p += 8) acc += __ldcg(sg.part + (int64_t)p * sg.stride + j);
+    }
+    red[q][lane] = acc;
+    __syncthreads();
+    if (q == 0 && j < sg.size) {
+      float g = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) g += red[r][lane];
+      bad |= adam_elem(w, m, v, sg.offset + j, g, bc1, bc2, lr);
+    }
+  } else {
+    const int64_t nb = (int64_t)(gridDim.x - coop_blocks);
+    for (int64_t i = (int64_t)(blockIdx.x - coop_blocks) * blockDim.x + threadIdx.x; i < n;
+         i += nb * blockDim.x) {
+      if (i >= c_lo && i < c_hi) continue;
+      bad |= adam_elem(w, m, v, i, load_grad(src, g32, g64, scale, count, i), bc1, bc2, lr);
+    }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
   step_arrive(step, t);
+  MQ_TL_END(8);
 }
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
@@ -261,10 +313,23 @@ int mq_adam(float* w, float* m, float* v, const float* grad32, const double* gra
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_adam: exactly one gradient source");
   MQ_CHECK_ARG(src_ok(src), "mq_adam: bad deferred gradient source");
   cudaStream_t s = as_stream(stream);
+  // a kind-0 segment with many static partials (the head's) goes cooperative
+  int coop_seg = 0, coop_blocks = 0;
+  if (grad32 && src) {
+    for (int k = 0; k < src->nseg; ++k) {
+      const mq_grad_seg& sg = src->seg[k];
+      if (sg.kind == 0 && !sg.nparts_dev && sg.nparts > 32 && sg.size > 0) {
+        coop_seg = k;
+        coop_blocks = (int)((sg.size + 31) / 32);
+        break;
+      }
+    }
+  }
   {
     ProfScope ps(K_ADAM, s);
-    MQ_CUDA(launch_k(adam_kernel, dim3(elem_blocks(n)), dim3(256), 0, s, w, m, v, grad32, grad64, grad_scale, n, step_dev,
-                                               bias, bias_len, lr, nonfinite, make_src(src)));
+    MQ_CUDA(launch_k(adam_kernel, dim3(elem_blocks(n) + coop_blocks), dim3(256), 0, s, w, m, v, grad32, grad64, grad_scale, n, step_dev,
+                                               bias, bias_len, lr, nonfinite, make_src(src),
+                     coop_seg, coop_blocks));
   }
   MQ_LAUNCH_CHECK("adam");
   return MQ_OK;
@@ -357,3 +422,5 @@ int mq_scan_i32(const int32_t* in, const int32_t* n_dev, int32_t n_max, int32_t*
 }
 
 }  // extern "C"
+
+MQ_TL_READER(train)
