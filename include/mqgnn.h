@@ -438,6 +438,36 @@ int mq_full_aggregate(const int64_t* row_off, const int32_t* col, int64_t n_node
 int mq_accuracy(const float* logits, int32_t ld, int32_t n_classes, const int32_t* labels,
                 const int32_t* ids, int64_t n_ids, unsigned long long* correct_dev,
                 void* stream);
+/* The lean evaluate (memory O(n d_out) instead of O(n 2 d_out) + O(n C)),
+ * same reference semantics:
+ *   mq_full_transform_half: y = h W over n rows, W one (d_in x d_out) half of a
+ *     SAGE weight (W_top or W_bot); `part` as mq_full_transform_part_floats.
+ *   mq_full_aggregate_inplace: out[v] = relu?(f32(1/deg v) * sum Y_top[u] + out[v])
+ *     (out holds h W_bot on entry).
+ *   mq_full_aggregate_rows: agg[sel_pos[v]] = f32(1/deg v) * sum_u h[u] (CSR
+ *     order within each 1024-arc item) for the rows with sel_pos[v] >= 0 only
+ *     (the last layer's mean over the evaluated rows; hubs split across
+ *     warps like mq_full_aggregate, same scratch).
+ *   mq_full_linear_cat: out = relu?([agg | hv] W) over m rows (tcgen05 3xTF32);
+ *     `part` holds mq_full_linear_cat_part_floats floats.
+ *   mq_accuracy_rows: as mq_accuracy with logits row i belonging to ids[i]. */
+int mq_full_transform_half(const float* h, int32_t ldh, int64_t n_nodes, int32_t d_in,
+                           const float* W, int32_t d_out, float* y, int32_t ldy, float* part,
+                           void* stream);
+int mq_full_aggregate_inplace(const int64_t* row_off, const int32_t* col, int64_t n_nodes,
+                              int64_t n_arcs, const float* ytop, int32_t ldy, int32_t n_out,
+                              int32_t relu, float* out, int32_t ldo, void* scratch, void* stream);
+int mq_full_aggregate_rows(const int64_t* row_off, const int32_t* col, int64_t n_nodes,
+                           int64_t n_arcs, const float* h, int32_t ldh, int32_t d,
+                           const int32_t* sel_pos, float* agg, int32_t ldagg, void* scratch,
+                           void* stream);
+int64_t mq_full_linear_cat_part_floats(int64_t m, int32_t d_out);
+int mq_full_linear_cat(const float* agg, int32_t ldagg, const float* hv, int32_t ldhv, int64_t m,
+                       int32_t d_in, const float* W, int32_t d_out, float* out, int32_t ldo,
+                       int32_t relu, float* part, void* stream);
+int mq_accuracy_rows(const float* logits, int32_t ld, int32_t n_classes, const int32_t* labels,
+                     const int32_t* ids, int64_t n_ids, unsigned long long* correct_dev,
+                     void* stream);
 
 /* ------------------------------------------------- per-epoch cache refresh
  * GNS residency on the device (cache.py:41-108, samplers.py:113-135).

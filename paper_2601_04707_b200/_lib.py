@@ -99,6 +99,12 @@ SIGNATURES = {
     "mq_full_agg_scratch_bytes": (I64, [I64, I32]),
     "mq_full_aggregate": (C.c_int, [P, P, I64, I64, P, I32, I32, I32, P, I32, P, P]),
     "mq_accuracy": (C.c_int, [P, I32, I32, P, P, I64, P, P]),
+    "mq_full_transform_half": (C.c_int, [P, I32, I64, I32, P, I32, P, I32, P, P]),
+    "mq_full_aggregate_inplace": (C.c_int, [P, P, I64, I64, P, I32, I32, I32, P, I32, P, P]),
+    "mq_full_aggregate_rows": (C.c_int, [P, P, I64, I64, P, I32, I32, P, P, I32, P, P]),
+    "mq_full_linear_cat_part_floats": (I64, [I64, I32]),
+    "mq_full_linear_cat": (C.c_int, [P, I32, P, I32, I64, I32, P, I32, P, I32, I32, P, P]),
+    "mq_accuracy_rows": (C.c_int, [P, I32, I32, P, P, I64, P, P]),
     "mq_in_degrees": (C.c_int, [P, I64, I64, P, P, P]),
     "mq_degree_probs": (C.c_int, [P, I64, I64, P, P]),
     "mq_walk_scratch_bytes": (I64, [I64]),

@@ -95,8 +95,12 @@ __global__ void walk_init_kernel(const uint8_t* __restrict__ train, const long l
 
 // p_out[v] = d[v] * flow[v] + p[v], flow[v] = sum over the stored arcs of row v
 // of p[col] in CSR order (the stripped self loop re-inserted before the first
-// neighbour > v).  One warp per row: lanes fetch 32 arcs at a time, the sum is
-// carried sequentially through shuffles (identical in every lane).
+// neighbour > v).  One warp per row: the lanes fetch kWalkU x 32 arcs at a
+// time (all gathers in flight together, so a hub row costs one memory round
+// trip per 256 arcs), then the sum is carried sequentially through shuffles
+// (identical in every lane) — np.bincount's exact order.
+constexpr int kWalkU = 8;
+
 __global__ void __launch_bounds__(kThreads) walk_step_kernel(
     const int64_t* __restrict__ row_off, const int32_t* __restrict__ col,
     const int32_t* __restrict__ loops, int64_t n, const double* __restrict__ p,
@@ -109,22 +113,40 @@ __global__ void __launch_bounds__(kThreads) walk_step_kernel(
     bool loop = loops != nullptr && loops[v] > 0;
     const double pv = p[v];
     double acc = 0.0;
-    for (int64_t b = e0; b < e1; b += 32) {
-      const int m = (int)(e1 - b < 32 ? e1 - b : 32);
-      int32_t c = 0;
-      double x = 0.0;
-      if (lane < m) {
-        c = __ldg(col + b + lane);
-        x = p[c];
+    for (int64_t b = e0; b < e1; b += 32 * kWalkU) {
+      int32_t c[kWalkU];
+      double x[kWalkU];
+#pragma unroll
+      for (int u = 0; u < kWalkU; ++u) {
+        const int64_t e = b + 32 * u + lane;
+        c[u] = e < e1 ? __ldg(col + e) : 0;
       }
-      for (int t = 0; t < m; ++t) {
-        const int32_t ct = __shfl_sync(0xffffffffu, c, t);
-        const double xt = __shfl_sync(0xffffffffu, x, t);
-        if (loop && ct > v) {
-          acc = __dadd_rn(acc, pv);
-          loop = false;
+#pragma unroll
+      for (int u = 0; u < kWalkU; ++u) x[u] = b + 32 * u + lane < e1 ? p[c[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kWalkU; ++u) {
+        const int64_t bu = b + 32 * u;
+        if (bu >= e1) break;
+        const int m = (int)(e1 - bu < 32 ? e1 - bu : 32);
+        // the stored loop enters before the group's first neighbour > v
+        int ins = 32;
+        if (loop) {
+          const unsigned bal = __ballot_sync(0xffffffffu, lane < m && c[u] > v);
+          if (bal) {
+            ins = __ffs(bal) - 1;
+            loop = false;
+          }
         }
-        acc = __dadd_rn(acc, xt);
+        if (m == 32 && ins == 32) {  // unrolled, no insertion: a bare add chain
+#pragma unroll
+          for (int t = 0; t < 32; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, x[u], t));
+        } else {
+          for (int t = 0; t < m; ++t) {
+            const double xt = __shfl_sync(0xffffffffu, x[u], t);
+            if (t == ins) acc = __dadd_rn(acc, pv);
+            acc = __dadd_rn(acc, xt);
+          }
+        }
       }
     }
     if (loop) acc = __dadd_rn(acc, pv);
@@ -162,45 +184,20 @@ __global__ void pw_leaves_kernel(const double* __restrict__ a, const int64_t* __
   }
 }
 
-// Replays the recursion over the leaf sums (left to right), one thread.
-__global__ void pw_combine_kernel(const double* __restrict__ sums, int64_t n,
-                                  double* __restrict__ total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  // explicit stack: node length, partial sum of the left child, state
-  int64_t len[64];
-  double left[64];
-  int st[64];
-  int sp = 0;
-  int64_t leaf = 0;
-  len[0] = n;
-  st[0] = 0;
-  double ret = 0.0;
-  while (sp >= 0) {
-    const int64_t m = len[sp];
-    if (m <= kPwBlock) {  // leaf (or a whole array of < 8 elements)
-      ret = sums[leaf++];
-      --sp;
-      continue;
-    }
-    int64_t n2 = m / 2;
-    n2 -= n2 % 8;
-    if (st[sp] == 0) {  // descend left
-      st[sp] = 1;
-      ++sp;
-      len[sp] = n2;
-      st[sp] = 0;
-    } else if (st[sp] == 1) {  // left done, descend right
-      left[sp] = ret;
-      st[sp] = 2;
-      ++sp;
-      len[sp] = m - n2;
-      st[sp] = 0;
-    } else {
-      ret = __dadd_rn(left[sp], ret);
-      --sp;
-    }
-  }
-  *total = __dadd_rn(0.0, ret);
+// The recursion's internal nodes, one height level per launch: node i of the
+// level = sums[left[i]] + sums[right[i]] (the same additions, in the same
+// operand order, as numpy's pairwise_sum — just evaluated level-parallel).
+__global__ void pw_level_kernel(double* __restrict__ vals, const int32_t* __restrict__ left,
+                                const int32_t* __restrict__ right, int64_t lo, int64_t hi,
+                                int64_t base) {
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+       i += (int64_t)gridDim.x * blockDim.x)
+    vals[base + i] = __dadd_rn(vals[left[i]], vals[right[i]]);
+}
+
+__global__ void pw_total_kernel(const double* __restrict__ vals, int64_t root,
+                                double* __restrict__ total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *total = __dadd_rn(0.0, vals[root]);
 }
 
 __global__ void normalize_kernel(const double* __restrict__ p, const double* __restrict__ total,
@@ -355,28 +352,80 @@ inline int grid_for(int64_t n, int per = kThreads) {
   return (int)(g < 1 ? 1 : (g > kNumSMs * 16 ? kNumSMs * 16 : g));
 }
 
-// numpy pairwise-sum leaf starts for a length-n array (cached per n)
-const std::vector<int64_t>& pw_leaf_starts(int64_t n) {
+// numpy pairwise-sum tree for a length-n array (cached per n): leaf starts in
+// left-to-right order (node ids 0..L-1), internal nodes sorted by height
+// (ids L.., children ids in left/right), level boundaries.
+struct PwPlan {
+  std::vector<int64_t> starts;
+  std::vector<int32_t> left, right;
+  std::vector<int64_t> level_end;  // internal-node index bounds per height 1..H
+  int64_t root = 0;
+};
+
+const PwPlan& pw_plan(int64_t n) {
   static std::mutex mu;
-  static std::map<int64_t, std::vector<int64_t>> cache;
+  static std::map<int64_t, PwPlan> cache;
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(n);
   if (it != cache.end()) return it->second;
-  std::vector<int64_t> out;
-  std::vector<std::pair<int64_t, int64_t>> stack{{0, n}};
-  while (!stack.empty()) {
-    auto [s, m] = stack.back();
-    stack.pop_back();
-    if (m <= kPwBlock) {
-      out.push_back(s);
+  PwPlan P;
+  struct Node { int32_t l, r; int h; };
+  std::vector<Node> inner;  // post-order, ids L + k after renumbering
+  // iterative post-order recursion: frame (start, len, state, left id, left height)
+  struct Fr { int64_t s, m; int st; int64_t lid; int lh; };
+  std::vector<Fr> stk{{0, n, 0, 0, 0}};
+  int64_t ret_id = 0;
+  int ret_h = 0;
+  std::vector<int64_t> leaf_ids;  // leaves get ids in order of creation (left to right)
+  while (!stk.empty()) {
+    Fr& f = stk.back();
+    if (f.m <= kPwBlock) {
+      ret_id = (int64_t)P.starts.size();
+      ret_h = 0;
+      P.starts.push_back(f.s);
+      stk.pop_back();
       continue;
     }
-    int64_t n2 = m / 2;
+    int64_t n2 = f.m / 2;
     n2 -= n2 % 8;
-    stack.push_back({s + n2, m - n2});  // right after left
-    stack.push_back({s, n2});
+    if (f.st == 0) {
+      f.st = 1;
+      stk.push_back({f.s, n2, 0, 0, 0});
+    } else if (f.st == 1) {
+      f.lid = ret_id;
+      f.lh = ret_h;
+      f.st = 2;
+      const int64_t s2 = f.s + n2, m2 = f.m - n2;
+      stk.push_back({s2, m2, 0, 0, 0});
+    } else {
+      const int h = (f.lh > ret_h ? f.lh : ret_h) + 1;
+      inner.push_back({(int32_t)f.lid, (int32_t)ret_id, h});
+      ret_id = -(int64_t)inner.size();  // provisional: -(k+1) = internal node k
+      ret_h = h;
+      stk.pop_back();
+    }
   }
-  return cache.emplace(n, std::move(out)).first->second;
+  const int64_t L = (int64_t)P.starts.size();
+  // renumber internal nodes by height (stable): final id = L + position
+  int H = 0;
+  for (auto& nd : inner) H = nd.h > H ? nd.h : H;
+  std::vector<int64_t> cnt(H + 2, 0), pos(inner.size());
+  for (auto& nd : inner) cnt[nd.h]++;
+  std::vector<int64_t> off(H + 2, 0);
+  for (int h = 1; h <= H; ++h) off[h + 1] = off[h] + cnt[h];
+  std::vector<int64_t> fill(off);
+  for (size_t k = 0; k < inner.size(); ++k) pos[k] = fill[inner[k].h]++;
+  auto fin = [&](int64_t id) { return id >= 0 ? id : L + pos[-id - 1]; };
+  P.left.assign(inner.size(), 0);
+  P.right.assign(inner.size(), 0);
+  for (size_t k = 0; k < inner.size(); ++k) {
+    P.left[pos[k]] = (int32_t)fin(inner[k].l);
+    P.right[pos[k]] = (int32_t)fin(inner[k].r);
+  }
+  for (int h = 1; h <= H; ++h) P.level_end.push_back(off[h + 1]);
+  P.root = inner.empty() ? 0 : L + (int64_t)inner.size() - 1;
+  (void)leaf_ids;
+  return cache.emplace(n, std::move(P)).first->second;
 }
 
 }  // namespace rf
@@ -421,8 +470,8 @@ int mq_degree_probs(const int64_t* deg, int64_t n_nodes, int64_t total, double* 
 }
 
 int64_t mq_walk_scratch_bytes(int64_t n_nodes) {
-  const int64_t leaves = n_nodes / 64 + 2;
-  return 8 * (3 * n_nodes + 2 * leaves + 4) + 64;
+  const int64_t leaves = n_nodes / 64 + 2;  // internal nodes < leaves
+  return 8 * (3 * n_nodes + 2 * leaves) + 8 * (2 * leaves) + 8 * leaves + 64;
 }
 
 int mq_walk_probs(const int64_t* row_off, const int32_t* col, int64_t n_nodes, const int32_t* loops,
@@ -433,16 +482,24 @@ int mq_walk_probs(const int64_t* row_off, const int32_t* col, int64_t n_nodes, c
   MQ_CHECK_ARG(row_off && deg && train_mask && probs && bad_dev && scratch,
                "mq_walk_probs: null pointer");
   cudaStream_t s = as_stream(stream);
-  const std::vector<int64_t>& leaves = rf::pw_leaf_starts(n_nodes);
-  const int64_t nl = (int64_t)leaves.size();
+  const rf::PwPlan& plan = rf::pw_plan(n_nodes);
+  const int64_t nl = (int64_t)plan.starts.size();
+  const int64_t ni = (int64_t)plan.left.size();
   double* pa = static_cast<double*>(scratch);
   double* pb = pa + n_nodes;
   double* d = pb + n_nodes;
-  double* sums = d + n_nodes;
-  int64_t* starts = reinterpret_cast<int64_t*>(sums + nl);
-  double* total = reinterpret_cast<double*>(starts + nl);
+  double* sums = d + n_nodes;                 // leaves then internal nodes
+  int64_t* starts = reinterpret_cast<int64_t*>(sums + nl + ni);
+  int32_t* lft = reinterpret_cast<int32_t*>(starts + nl);
+  int32_t* rgt = lft + ni;
+  double* total = reinterpret_cast<double*>(starts + nl + ni + 1);
   MQ_CHECK_ARG(nl <= n_nodes / 64 + 2, "mq_walk_probs: internal leaf bound");
-  MQ_CUDA(cudaMemcpyAsync(starts, leaves.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, s));
+  MQ_CUDA(cudaMemcpyAsync(starts, plan.starts.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice,
+                          s));
+  if (ni) {
+    MQ_CUDA(cudaMemcpyAsync(lft, plan.left.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s));
+    MQ_CUDA(cudaMemcpyAsync(rgt, plan.right.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s));
+  }
   MQ_CUDA(cudaMemsetAsync(bad_dev, 0, sizeof(int32_t), s));
   {
     ProfScope ps(K_REFRESH_PROBS, s);
@@ -465,7 +522,12 @@ int mq_walk_probs(const int64_t* row_off, const int32_t* col, int64_t n_nodes, c
   {
     ProfScope ps(K_REFRESH_PROBS, s);
     rf::pw_leaves_kernel<<<rf::grid_for(nl), rf::kThreads, 0, s>>>(pa, starts, nl, n_nodes, sums);
-    rf::pw_combine_kernel<<<1, 32, 0, s>>>(sums, n_nodes, total);
+    int64_t lo = 0;
+    for (int64_t hi : plan.level_end) {
+      rf::pw_level_kernel<<<rf::grid_for(hi - lo), rf::kThreads, 0, s>>>(sums, lft, rgt, lo, hi, nl);
+      lo = hi;
+    }
+    rf::pw_total_kernel<<<1, 32, 0, s>>>(sums, plan.root, total);
     rf::normalize_kernel<<<rf::grid_for(n_nodes), rf::kThreads, 0, s>>>(pa, total, n_nodes, probs,
                                                                        bad_dev);
   }

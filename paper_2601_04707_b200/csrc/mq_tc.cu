@@ -995,6 +995,34 @@ int tc_linear_af(const float* agg, int ldagg, const float* h, int ldh, const int
 
 int64_t tc_af_part_floats(int64_t m_max, int64_t d_out) { return tc_part_floats(m_max, d_out); }
 
+// y = h W (one d_in x d_out half of a SAGE weight), host-known rows
+int tc_transform_half(const float* h, int ldh, int64_t n, int d_in, const float* W, int d_out,
+                      float* y, int ldy, float* part, cudaStream_t s) {
+  tc::Operands op{h, ldh, d_in, W, d_out, nullptr, d_out, (d_out + 15) / 16 * 16};
+  op.out = y;
+  op.ldo = ldy;
+  return run_tc_gemm<tc::kFwd>(op, nullptr, (int)n, (int)n, nullptr, d_in, d_in, part,
+                               EpiStore{y, ldy}, s, K_FULL_TRANSFORM, K_FULL_TRANSFORM_REDUCE);
+}
+
+// out = [relu] ([agg | hv] W) over m host-known rows (the lean evaluate's last layer)
+int tc_linear_cat_rows(const float* agg, int ldagg, const float* hv, int ldhv, int m, int d_in,
+                       const float* W, int d_out, float* out, int ldo, int relu, float* part,
+                       cudaStream_t s) {
+  tc::Operands op{agg, ldagg, d_in, W, d_out, nullptr, d_out, (d_out + 15) / 16 * 16};
+  op.x2 = hv;
+  op.ldx2 = ldhv;
+  op.out = out;
+  op.ldo = ldo;
+  op.relu = relu;
+  if (relu)
+    return run_tc_gemm<tc::kFwdCat>(op, nullptr, m, m, nullptr, 2 * d_in, 2 * d_in, part,
+                                    EpiLinearFwd{nullptr, 0, out, ldo}, s, K_FULL_TRANSFORM,
+                                    K_FULL_TRANSFORM_REDUCE);
+  return run_tc_gemm<tc::kFwdCat>(op, nullptr, m, m, nullptr, 2 * d_in, 2 * d_in, part,
+                                  EpiStore{out, ldo}, s, K_FULL_TRANSFORM, K_FULL_TRANSFORM_REDUCE);
+}
+
 // its weight gradient as deferred split-K partials [S][2 d_in][d_out]
 int tc_linear_af_bwd(const float* agg, int ldagg, const float* h, int ldh,
                      const int32_t* rows_dev, int rows_max, int d_in, const float* dh, int lddh,

@@ -81,6 +81,23 @@ def test_full_forward_hubs_isolated_and_loops():
                    onn.accuracy(ref[idx], g.labels[idx])) <= 0.005
 
 
+@pytest.mark.parametrize("tag", EVAL)
+def test_lean_evaluate_matches_reference(tag, monkeypatch):
+    """the memory-lean evaluate (in-place bottom half, aggregate-first last
+    layer over the evaluated rows in chunks) used when full_forward's
+    workspace does not fit"""
+    monkeypatch.setattr(mnn, "_full_fits", lambda g, st: False)
+    g = epoch_graph(G, str(G[f"eval/{tag}/graph"]))
+    dg = mq.DeviceGraph.from_csr(g, device="cuda:0")
+    for phase in (0, 1):
+        p = f"eval/{tag}/p{phase}"
+        ws = [G[f"{p}/w{l}"] for l in range(3) if f"{p}/w{l}" in G]
+        state = mq.ModelState(ws, device="cuda:0")
+        for mask, key in ((g.val_mask, "val_acc"), (g.test_mask, "test_acc")):
+            acc = mnn.evaluate(dg, state, mask, chunk=97)  # several chunks
+            assert abs(acc - float(G[f"{p}/{key}"][0])) <= 0.005 + 1e-12, (key, acc)
+
+
 def test_full_forward_cfg1_shape():
     from conftest import make_cfg1
     g = make_cfg1()
