@@ -502,6 +502,26 @@ int mq_refresh_select(const double* probs, int64_t n_nodes, int64_t budget, uint
 /* host restatement of the refresh contract's random(n) (tests) */
 int mq_refresh_uniforms_host(uint64_t seed, uint64_t epoch, int64_t n, double* out);
 
+/* ------------------------------------------------------------ graph ingest
+ * build_csr (graph.py:94-139) on the device: mq_build_csr_keys sorts the
+ * edge keys src * n + dst (LSD radix sort, stable warp-ranked scatter) and
+ * compacts the distinct ones into `uniq` (*n_unique_dev; *bad_dev = 1 if an
+ * endpoint is out of range); mq_build_csr_finish writes row_offsets (n+1,
+ * int64) and int32 columns.  edges: int64 [m][2].  scratch:
+ * mq_build_csr_scratch_bytes(m); uniq holds m entries.
+ * mq_narrow_cols: the MQG1 loader's u64 columns (graph.py:331-395) to int32
+ * (*bad_dev = 1 if a column is >= n).  mq_degree_buckets: the default
+ * features' one-hot index floor(log2(deg + 1)) (graph.py:142-149). */
+int64_t mq_build_csr_scratch_bytes(int64_t m);
+int mq_build_csr_keys(const int64_t* edges, int64_t m, int64_t n_nodes, void* scratch,
+                      unsigned long long* uniq, int64_t* n_unique_dev, int32_t* bad_dev,
+                      void* stream);
+int mq_build_csr_finish(const unsigned long long* uniq, int64_t n_unique, int64_t n_nodes,
+                        int64_t* row_off, int32_t* col, void* stream);
+int mq_narrow_cols(const unsigned long long* cols64, int64_t m, int64_t n_nodes, int32_t* cols32,
+                   int32_t* bad_dev, void* stream);
+int mq_degree_buckets(const int64_t* row_off, int64_t n_nodes, int32_t* bucket, void* stream);
+
 /* ------------------------------------------------------------- utilities */
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): the step's
  * pinned-host result read-back as a node of a captured graph. */

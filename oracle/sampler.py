@@ -10,6 +10,8 @@ Follows ``mqpipe/samplers.py`` of the reference:
 The reference's ``rng.choice`` is replaced by the injected Philox row stream
 (``oracle.philox``), the contract under which the reference itself produced
 the golden vectors in ``tests/golden``.
+
+* ``build_csr`` / ``degree_bucket_features`` — ``mqpipe/graph.py:94-149`` (ingest)
 """
 
 from __future__ import annotations
@@ -171,3 +173,26 @@ def build_minibatch(row_offsets, col_indices, features, labels, targets, fanouts
         misses = int(input_ids.size - hits)
     return OracleMiniBatch(batch_id, epoch, kept, labels[kept], blocks,
                            input_ids, features[input_ids].copy(), hits, misses)
+
+
+def build_csr(edges, num_nodes):
+    """graph.py:94-139: (row_offsets, col_indices) of the deduplicated,
+    sorted arc set (np.unique of src * n + dst)."""
+    arr = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    if arr.size and (arr.min() < 0 or arr.max() >= num_nodes):
+        raise ValueError("edge endpoint out of range")
+    keys = np.unique(arr[:, 0] * num_nodes + arr[:, 1]) if arr.size else np.empty(0, np.int64)
+    src, dst = keys // num_nodes, keys % num_nodes
+    row_offsets = np.zeros(num_nodes + 1, dtype=np.int64)
+    np.add.at(row_offsets, src + 1, 1)
+    return np.cumsum(row_offsets), dst.copy()
+
+
+def degree_bucket_features(row_offsets):
+    """graph.py:142-149: one-hot of floor(log2(out_degree + 1))."""
+    deg = np.diff(row_offsets)
+    buckets = np.floor(np.log2(deg + 1)).astype(np.int64)
+    dim = int(buckets.max()) + 1 if buckets.size else 1
+    feats = np.zeros((deg.size, dim), dtype=np.float32)
+    feats[np.arange(deg.size), buckets] = 1.0
+    return feats

@@ -5,7 +5,7 @@ Compute runs in hand-written CUDA kernels reached through the C-ABI library
 ``libmqgnn.so`` (include/mqgnn.h); there is no CPU fallback.
 """
 
-from .graph import DeviceGraph
+from .graph import DeviceGraph, build_csr, load
 from .cache import (DeviceCache, RefreshStream, cache_probs_degree, cache_probs_walk,
                     gather_features, lookup, refresh_cache, refresh_mask,
                     weighted_sample_without_replacement)

@@ -112,6 +112,11 @@ SIGNATURES = {
     "mq_refresh_scratch_bytes": (I64, [I64]),
     "mq_refresh_select": (C.c_int, [P, I64, I64, U64, U64, P, P, P, P]),
     "mq_refresh_uniforms_host": (C.c_int, [U64, U64, I64, P]),
+    "mq_build_csr_scratch_bytes": (I64, [I64]),
+    "mq_build_csr_keys": (C.c_int, [P, I64, I64, P, P, P, P, P]),
+    "mq_build_csr_finish": (C.c_int, [P, I64, I64, P, P, P]),
+    "mq_narrow_cols": (C.c_int, [P, I64, I64, P, P, P]),
+    "mq_degree_buckets": (C.c_int, [P, I64, P, P]),
     "mq_prep_scratch_bytes": (I64, [I32, I32]),
     "mq_prep_batches": (C.c_int, [P, P]),
     "mq_prof_enable": (C.c_int, [C.c_int]),

@@ -53,7 +53,8 @@
   X(K_REFRESH_SELECT, "refresh_select")         \
   X(K_SAGE_AF, "sage_linear_af")                \
   X(K_SAGE_AF_REDUCE, "sage_linear_af_reduce")  \
-  X(K_SAGE_AF_DW, "sage_linear_af_dw")
+  X(K_SAGE_AF_DW, "sage_linear_af_dw")          \
+  X(K_INGEST, "ingest")
 
 namespace mq {
 enum KernelId {

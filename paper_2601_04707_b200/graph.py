@@ -128,3 +128,104 @@ def _host(a):
     if isinstance(a, torch.Tensor):
         return a.detach().cpu().numpy()
     return a
+
+
+# ------------------------------------------------------------------ ingest
+MAGIC = b"MQG1"
+
+
+def _stream(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def build_csr(edges, num_nodes: int, features=None, labels=None, num_classes: int | None = None,
+              device=None):
+    """The reference's build_csr (graph.py:94-139) on the device: duplicate
+    arcs collapse, rows come out sorted; default features are the one-hot
+    degree buckets (graph.py:142-149).  Returns a GraphCSR-like ``SynthGraph``
+    whose arrays live on ``device`` (int64 row_offsets, int32 col_indices);
+    ``DeviceGraph.from_csr`` takes it as is."""
+    from .synth import SynthGraph
+    dev = torch.device(device or "cuda")
+    n = int(num_nodes)
+    if n < 1 or n >= INT32_MAX:
+        raise ValueError("num_nodes must lie in [1, 2^31 - 1)")
+    e = edges if isinstance(edges, torch.Tensor) else torch.as_tensor(
+        np.asarray(list(edges) if not isinstance(edges, np.ndarray) else edges, dtype=np.int64))
+    e = e.to(device=dev, dtype=torch.int64).reshape(-1, 2).contiguous()
+    m = int(e.shape[0])
+    lb = lib()
+    s = _stream(dev)
+    scr = torch.empty(int(lb.mq_build_csr_scratch_bytes(m)), dtype=torch.uint8, device=dev)
+    uniq = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    lb.mq_build_csr_keys(ptr(e), m, n, ptr(scr), ptr(uniq), ptr(cnt), ptr(bad), s)
+    if int(bad.item()):
+        raise ValueError("edge endpoint out of range")
+    nu = int(cnt.item())
+    del scr
+    row_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(nu, 1), dtype=torch.int32, device=dev)
+    lb.mq_build_csr_finish(ptr(uniq), nu, n, ptr(row_off), ptr(col), s)
+    col = col[:nu]
+    if features is None:
+        bucket = torch.empty(n, dtype=torch.int32, device=dev)
+        lb.mq_degree_buckets(ptr(row_off), n, ptr(bucket), s)
+        dim = int(bucket.max().item()) + 1
+        features = torch.zeros((n, dim), dtype=torch.float32, device=dev)
+        features[torch.arange(n, device=dev), bucket.long()] = 1.0
+    else:
+        features = _as_tensor(features, torch.float32, dev)
+        if features.shape[0] != n:
+            raise ValueError("features must have one row per node")
+    labels = (torch.zeros(n, dtype=torch.int32, device=dev) if labels is None
+              else _as_tensor(labels, torch.int32, dev))
+    if num_classes is None:
+        num_classes = int(labels.max().item()) + 1
+    empty = np.zeros(n, dtype=bool)
+    return SynthGraph(n, row_off, col, features.contiguous(), labels, int(num_classes),
+                      empty.copy(), empty.copy(), empty.copy())
+
+
+def load(path: str, device=None):
+    """Read the reference's MQG1 container (graph.py:325-395: magic, u64
+    header, u64 CSR arrays, f32 features, i32 labels, bit-packed masks)
+    straight to the device: u64 columns are narrowed to int32 by a kernel."""
+    from .synth import SynthGraph
+    dev = torch.device(device or "cuda")
+    raw = np.memmap(path, dtype=np.uint8, mode="r")
+    if raw.size < 36:
+        raise ValueError("buffer too short for header")
+    if bytes(raw[:4]) != MAGIC:
+        raise ValueError(f"bad magic {bytes(raw[:4])!r}")
+    n, e, d, c = (int(x) for x in np.frombuffer(raw[4:36].tobytes(), dtype="<u8"))
+    mask_bytes = (n + 7) // 8
+    off = 36
+    need = off + 8 * (n + 1) + 8 * e + 4 * n * d + 4 * n + 3 * mask_bytes
+    if raw.size < need:
+        raise ValueError(f"buffer truncated: need {need} bytes, have {raw.size}")
+
+    def take(count, dtype):
+        nonlocal off
+        nb = count * np.dtype(dtype).itemsize
+        a = np.frombuffer(raw, dtype=dtype, count=count, offset=off)
+        off += nb
+        return np.array(a)  # an owned, writable copy (the map is read-only)
+
+    row_off = torch.as_tensor(take(n + 1, "<u8").astype(np.int64)).to(dev)
+    cols64 = torch.as_tensor(take(e, "<u8").view(np.int64)).to(dev)
+    col = torch.empty(max(e, 1), dtype=torch.int32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib().mq_narrow_cols(ptr(cols64), e, n, ptr(col), ptr(bad), _stream(dev))
+    if int(bad.item()):
+        raise ValueError("column index out of range")
+    del cols64
+    feats = torch.as_tensor(take(n * d, "<f4").reshape(n, d)).to(dev)
+    labels = torch.as_tensor(take(n, "<i4")).to(dev)
+    masks = []
+    for _ in range(3):
+        bits = np.unpackbits(np.asarray(raw[off:off + mask_bytes]), bitorder="little")
+        masks.append(bits[:n].astype(bool))
+        off += mask_bytes
+    return SynthGraph(n, row_off, col[:e], feats, labels, c, *masks)

@@ -28,6 +28,7 @@ HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(HERE))
+sys.path.insert(0, str(HERE.parent))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import mqpipe  # noqa: E402
@@ -36,6 +37,7 @@ from mqpipe import cache as rcache  # noqa: E402
 from mqpipe import nn as rnn  # noqa: E402
 
 from make_golden import BatchKey, g8, synth_ref, with_self_loops  # noqa: E402
+from conftest import EDGES_8 as G8_EDGES  # noqa: E402
 from oracle.philox import RefreshRng  # noqa: E402
 
 
@@ -103,6 +105,24 @@ def main():
         out[f"{p}/params"] = np.array([frac, seed, epoch], dtype=np.float64)
         out[f"{p}/cached_ids"] = c.cached_ids
         out[f"{p}/positive"] = np.array([int(np.count_nonzero(probs > 0))])
+    # ---- ingest: the reference's build_csr (graph.py:94-139) and its MQG1 container
+    from mqpipe import graph as rgraph
+    rng = np.random.default_rng(31)
+    n = 1000
+    e_rand = rng.integers(0, n, size=(20000, 2))
+    e_rand = np.concatenate([e_rand, e_rand[:500], np.stack([np.arange(0, n, 9)] * 2, 1)])
+    rng.shuffle(e_rand)
+    hub = np.stack([np.zeros(3000, np.int64), rng.integers(0, 5000, 3000)], 1)
+    e_hub = np.concatenate([hub, hub[:, ::-1], rng.integers(0, 5000, size=(4000, 2))])
+    for name, edges, nn_ in (("g8", np.asarray(G8_EDGES), 8), ("rand", e_rand, n),
+                             ("hub", e_hub, 5000)):
+        g = rgraph.build_csr(edges, nn_)
+        out[f"ingest/{name}/edges"] = np.asarray(edges, dtype=np.int64)
+        out[f"ingest/{name}/n"] = np.array([nn_])
+        out[f"ingest/{name}/row_offsets"] = g.row_offsets
+        out[f"ingest/{name}/col_indices"] = g.col_indices
+        out[f"ingest/{name}/features"] = g.features
+    out["ingest/mqg1"] = np.frombuffer(rgraph.serialize(G2), dtype=np.uint8).copy()
     np.savez_compressed(HERE / "epoch.npz", **out)
     print("epoch.npz", os.path.getsize(HERE / "epoch.npz"))
 

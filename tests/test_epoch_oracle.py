@@ -59,3 +59,12 @@ def test_refresh_uniforms_contract():
     assert np.array_equal(u * 2.0 ** 53, np.floor(u * 2.0 ** 53))
     assert not np.array_equal(u[:10], refresh_uniforms(3, 2, 10))
     assert np.array_equal(u[:7], refresh_uniforms(3, 1, 7))
+
+
+@pytest.mark.parametrize("name", ["g8", "rand", "hub"])
+def test_oracle_build_csr_matches_reference(name):
+    from oracle.sampler import build_csr, degree_bucket_features
+    ro, col = build_csr(G[f"ingest/{name}/edges"], int(G[f"ingest/{name}/n"][0]))
+    assert np.array_equal(ro, G[f"ingest/{name}/row_offsets"])
+    assert np.array_equal(col, G[f"ingest/{name}/col_indices"])
+    assert np.array_equal(degree_bucket_features(ro), G[f"ingest/{name}/features"])

@@ -176,3 +176,47 @@ def test_refresh_odd_node_count_matches_oracle():
             assert np.array_equal(np.flatnonzero(got), ref)
     assert np.array_equal(mq.cache_probs_walk(dg, 5, 2).cpu().numpy(),
                           ocache.walk_probs(g.row_offsets, g.col_indices, g.train_mask, 5, 2))
+
+
+# ------------------------------------------------------------ graph ingest
+@pytest.mark.parametrize("name", ["g8", "rand", "hub"])
+def test_build_csr_matches_reference(name):
+    g = mq.build_csr(G[f"ingest/{name}/edges"], int(G[f"ingest/{name}/n"][0]), device="cuda:0")
+    assert np.array_equal(g.row_offsets.cpu().numpy(), G[f"ingest/{name}/row_offsets"])
+    assert np.array_equal(g.col_indices.cpu().numpy().astype(np.int64),
+                          G[f"ingest/{name}/col_indices"])
+    assert np.array_equal(g.features.cpu().numpy(), G[f"ingest/{name}/features"])
+    mq.DeviceGraph.from_csr(g, device="cuda:0")  # usable as is
+
+
+def test_build_csr_large_and_errors():
+    """several radix passes and many tiles against np.unique; range errors"""
+    from oracle.sampler import build_csr as obuild
+    rng = np.random.default_rng(5)
+    n = 3_000_017
+    e = rng.integers(0, n, size=(5_000_000, 2))
+    e[::7] = e[::7][:, ::-1]
+    e = np.concatenate([e, e[:100_000]])
+    g = mq.build_csr(e, n, features=np.zeros((n, 4), np.float32), device="cuda:0")
+    ro, col = obuild(e, n)
+    assert np.array_equal(g.row_offsets.cpu().numpy(), ro)
+    assert np.array_equal(g.col_indices.cpu().numpy().astype(np.int64), col)
+    with pytest.raises(ValueError):
+        mq.build_csr(np.array([[0, 5]]), 5, device="cuda:0")
+
+
+def test_load_reference_container(tmp_path):
+    p = tmp_path / "g2.mqg1"
+    p.write_bytes(G["ingest/mqg1"].tobytes())
+    g = mq.load(str(p), device="cuda:0")
+    assert np.array_equal(g.row_offsets.cpu().numpy(), G["g2/row_offsets"])
+    assert np.array_equal(g.col_indices.cpu().numpy().astype(np.int64), G["g2/col_indices"])
+    assert np.array_equal(g.features.cpu().numpy(), G["g2/features"])
+    assert np.array_equal(g.labels.cpu().numpy(), G["g2/labels"])
+    for k in ("train_mask", "val_mask", "test_mask"):
+        assert np.array_equal(getattr(g, k), G[f"g2/{k}"])
+    bad = bytearray(G["ingest/mqg1"].tobytes())
+    bad[:4] = b"XXXX"
+    (tmp_path / "bad.mqg1").write_bytes(bytes(bad))
+    with pytest.raises(ValueError):
+        mq.load(str(tmp_path / "bad.mqg1"), device="cuda:0")
