@@ -304,10 +304,17 @@ def run_ours(args):
     rank, world, local = env_rank()
     if world != args.gpus:
         args.gpus = world
+    # one GPU per rank (NCCL); MQ_DIST_BACKEND=gloo lets ranks share GPUs
+    # (a functional multi-rank check on a single-GPU box, not a perf setup)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MQ_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2601_04707_b200 as mq
     from paper_2601_04707_b200._lib import lib
     from paper_2601_04707_b200.runtime import epoch_permutation
