@@ -73,8 +73,8 @@ def parse():
                     help="launches per op in the per-kernel graph timing (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--queue-depth", type=int, default=None,
-                    help="batches per batched prep pass (MQ-GNN queue depth Q)")
+    ap.add_argument("--queue-depth", default=None,
+                    help="batches per batched prep pass (MQ-GNN queue depth Q), or 'auto'")
     ap.add_argument("--no-pdl", action="store_true", help="disable programmatic dependent launch")
     ap.add_argument("--layer0", default="auto", choices=["auto", "tf", "af"],
                     help="input layer transform-first / aggregate-first")
@@ -355,6 +355,14 @@ def run_ours(args):
         lib().mq_set_pdl(0)
     if os.environ.get("MQ_TC_GRID_CAP"):
         lib().mq_set_tc_grid_cap(int(os.environ["MQ_TC_GRID_CAP"]))
+    queue_choice = None
+    if args.queue_depth == "auto":  # the reference's --queue auto (autotune.py), measured
+        from paper_2601_04707_b200.autotune import auto_queue_depth
+        queue_choice = auto_queue_depth(g, model, fanouts=fanouts, batch_size=args.batch,
+                                        num_train=n_train, cache=cache, seed=args.seed)
+        args.queue_depth = queue_choice.depth
+    elif args.queue_depth is not None:
+        args.queue_depth = int(args.queue_depth)
     runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=args.batch, num_train=n_train,
                            cache=cache, optimizer="adam", seed=args.seed, world=world, rank=rank,
                            multi=world > 1, queue_depth=args.queue_depth,
@@ -553,6 +561,9 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (CSR+features ~1.1 GB), no flush",
                        "cuda_graph": True, "queue_depth": runner.Q,
                        "pdl": bool(lib().mq_get_pdl()), "pipeline": runner.pipeline,
+                       "queue_auto": None if queue_choice is None else {
+                           "cap": queue_choice.cap, "formula_eq24": queue_choice.formula_depth,
+                           "ms_per_window": queue_choice.ms_per_window},
                        "layer0": "aggregate-first" if getattr(runner.tw, "af0", False)
                                  else "transform-first"},
             "epoch_ms": ms_max / args.steps * windows, "windows_per_epoch": windows,

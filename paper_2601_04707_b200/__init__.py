@@ -20,5 +20,7 @@ from .pipeline import STAGES, PipelineStopped, PipelineTimeout, Trace, TraceEven
 from .runtime import (EpochStats, PipelineConfig, batch_rng, plan_epoch, run_epoch,
                       transfer_stage)
 from .trainer import StepRunner
+from .autotune import (AutotuneError, auto_queue_depth, compute_cap, compute_queue_size,
+                       steady_slice)
 
 __version__ = "0.1.0"

@@ -123,6 +123,24 @@ def main():
         out[f"ingest/{name}/col_indices"] = g.col_indices
         out[f"ingest/{name}/features"] = g.features
     out["ingest/mqg1"] = np.frombuffer(rgraph.serialize(G2), dtype=np.uint8).copy()
+
+    # ---- queue sizing formulas (autotune.py:29-34, 112-141)
+    from mqpipe import autotune as rauto
+    caps, qs, sl = [], [], []
+    for total, peak, mb in ((24 * 2**30, 10 * 2**30, 2**28), (100, 40, 10), (10**9, 5 * 10**8, 7),
+                            (50, 40, 10)):
+        try:
+            caps.append([total, peak, mb, rauto.compute_cap(total, peak, mb)])
+        except rauto.AutotuneError:
+            caps.append([total, peak, mb, -1])
+    for prep, comp, cap in ((7.0, 2.0, 10), (0.5, 3.0, 8), (30.0, 1.0, 6), (1.0, 1.0, 1)):
+        qs.append([prep, comp, cap, rauto.compute_queue_size(prep, comp, cap)])
+    for n in (5, 59, 60, 100, 41):
+        s_ = rauto.steady_slice(n)
+        sl.append([n, s_.start, s_.stop])
+    out["autotune/cap"] = np.array(caps, dtype=np.float64)
+    out["autotune/queue"] = np.array(qs, dtype=np.float64)
+    out["autotune/steady"] = np.array(sl, dtype=np.int64)
     np.savez_compressed(HERE / "epoch.npz", **out)
     print("epoch.npz", os.path.getsize(HERE / "epoch.npz"))
 

@@ -68,3 +68,19 @@ def test_oracle_build_csr_matches_reference(name):
     assert np.array_equal(ro, G[f"ingest/{name}/row_offsets"])
     assert np.array_equal(col, G[f"ingest/{name}/col_indices"])
     assert np.array_equal(degree_bucket_features(ro), G[f"ingest/{name}/features"])
+
+
+def test_queue_sizing_formulas_match_reference():
+    from paper_2601_04707_b200.autotune import (AutotuneError, compute_cap, compute_queue_size,
+                                                steady_slice)
+    for total, peak, mb, cap in G["autotune/cap"]:
+        if cap < 0:
+            with pytest.raises(AutotuneError):
+                compute_cap(total, peak, mb)
+        else:
+            assert compute_cap(total, peak, mb) == int(cap)
+    for prep, comp, cap, q in G["autotune/queue"]:
+        assert compute_queue_size(prep, comp, int(cap)) == int(q)
+    for n, a, b in G["autotune/steady"]:
+        s = steady_slice(int(n))
+        assert (s.start, s.stop) == (a, b)
