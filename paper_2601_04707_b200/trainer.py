@@ -138,16 +138,17 @@ class StepRunner:
         gi = next(i for i, grp in enumerate(self.groups) if sw in grp.slots)
         self.groups[gi].launch(self._prep_desc(gi, not setup), s)
 
-    def _enqueue_train(self, sw, s, commit=True):
+    def _enqueue_train(self, sw, s, commit=True, ring=None):
+        ring = self.loss_ring if ring is None else ring
         if self.fused:
-            self.tw.launch_train(self.dm, s, sw, ring=self.loss_ring if commit else None,
+            self.tw.launch_train(self.dm, s, sw, ring=ring if commit else None,
                                  ring_len=self.ring_len, world=self.world)
         else:
             self.tw.launch_forward(self.dm, s, sw)
             self.tw.launch_loss(self.dm, s, sw)
             if commit:
                 lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world,
-                                     ptr(self.loss_ring), self.ring_len, s)
+                                     ptr(ring), self.ring_len, s)
             self.tw.launch_backward(self.dm, s, sw)
         if self.grad64 is not None:
             src = self.tw.grad_src(self.dm) if self.fused else None
@@ -403,11 +404,11 @@ class StepRunner:
         self._stage = [torch.zeros((Q, 4), dtype=torch.int32, pin_memory=True) for _ in range(4)]
         self._stage_ev = [torch.cuda.Event() for _ in range(4)]
         self._stage_i = 0
-        self._loss_host = torch.zeros(2, dtype=torch.float64, pin_memory=True)
-        self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
-        # one pinned loss row per window of each slot group: the group graphs
-        # copy every window's loss out (D2H) as a node of the graph
-        self._loss_grp = torch.zeros((len(self.groups), Q), dtype=torch.float64, pin_memory=True)
+        # the step's loss commit (the head's last CTA) writes straight into this
+        # pinned, device-mapped ring (index batch_id % ring_len): the per-step
+        # D2H read-back needs no copy node between the step's kernels
+        self._loss_hring = torch.zeros(self.ring_len, dtype=torch.float64, pin_memory=True)
+        self._win_ev = [torch.cuda.Event() for _ in range(2)]
         self._grp_ev = [torch.cuda.Event() for _ in self.groups]
         phases = {}
         for gi, grp in enumerate(self.groups):
@@ -415,7 +416,7 @@ class StepRunner:
                 self._prep_desc(gi, True), s))
             for q, sw in enumerate(grp.slots):
                 def htrain(s, sw=sw):
-                    self._enqueue_train(sw, s, commit=False)
+                    self._enqueue_train(sw, s, commit=True, ring=self._loss_hring)
                     self._enqueue_update(s)
                 phases[f"htrain{gi}_{q}"] = htrain
         if self.use_graph:
@@ -426,9 +427,6 @@ class StepRunner:
                 def hgroup(s, gi=gi):
                     for q in range(Q):
                         phases[f"htrain{gi}_{q}"](s)
-                        lib().mq_memcpy_async(self._loss_grp[gi, q:q + 1].data_ptr(),
-                                              ptr(self.tw.loss), 8, s)
-                        self.tw.loss.zero_()
                 groups[f"hgroup{gi}"] = hgroup
             self._capture(groups)
         self._hphases = phases
@@ -467,8 +465,9 @@ class StepRunner:
         target batch (batch_id, targets) the step H2D-copies its inputs, trains,
         and D2H-reads its summed loss.  Batches are prepared Q at a time (the
         device queue); group j+1 is staged and prepared while group j trains.
-        A full group of Q windows runs as one graph whose nodes include each
-        window's loss D2H copy; the host reads group j's losses after group
+        A full group of Q windows runs as one graph; every window's loss is
+        written by the device into a pinned host ring (the D2H read-back of
+        the step's result) and the host reads group j's losses after group
         j+1 is enqueued, so the GPU never idles on the host.  Yields
         (batch_id, loss) in order."""
         batches = list(batches)
@@ -488,23 +487,22 @@ class StepRunner:
             self.ev_prep[gi].record(prep_s)
 
         stage_and_prep(0)
-        pending = []   # (kind, payload) of enqueued work whose losses are unread
-        nstep = 0
+        pending = []   # (event, [batch ids]) of enqueued work whose losses are unread
+        ring = self._loss_hring
+        slot_of = lambda bid: ((bid & 0xFFFFFFFF) // self.world) % self.ring_len  # noqa: E731
 
         def drain(keep):
             while len(pending) > keep:
-                kind, pay = pending.pop(0)
-                if kind == "group":
-                    gi, ids = pay
-                    self._grp_ev[gi].synchronize()
-                    vals = self._loss_grp[gi].tolist()
-                    for q, bid in enumerate(ids):
-                        yield bid, float(vals[q])
-                else:
-                    bid, slot = pay
-                    self._loss_ev[slot].synchronize()
-                    yield bid, float(self._loss_host[slot])
+                ev, ids = pending.pop(0)
+                ev.synchronize()
+                for bid in ids:
+                    yield bid, float(ring[slot_of(bid)])
 
+        def clash(ids):  # a pending loss would be overwritten before it is read
+            busy = {slot_of(b) for _, pids in pending for b in pids}
+            return any(slot_of(b) in busy for b in ids)
+
+        nwin = 0
         for j, chunk in enumerate(chunks):
             gi = j % ngroups
             if j + 1 < len(chunks) and self.pipeline:
@@ -512,28 +510,24 @@ class StepRunner:
             elif j > 0 and not self.pipeline:
                 stage_and_prep(j)
             self.stream.wait_event(self.ev_prep[gi])
+            ids = [bid for bid, _ in chunk]
             if self.use_graph and len(chunk) == Q and f"hgroup{gi}" in self.graphs:
-                # the group's previous losses must have been read before overwrite
-                yield from drain(0 if any(k == "group" and p[0] == gi for k, p in pending) else 1)
+                yield from drain(0 if clash(ids) else 1)
                 with torch.cuda.stream(self.stream):
                     self.graphs[f"hgroup{gi}"].replay()
-                self._grp_ev[gi].record(self.stream)
+                ev = self._grp_ev[gi]
+                ev.record(self.stream)
                 self.dm.host_steps += Q
-                nstep += Q
-                pending.append(("group", (gi, [bid for bid, _ in chunk])))
+                pending.append((ev, ids))
             else:
-                for q, (bid, _) in enumerate(chunk):
-                    slot = nstep % 2
-                    yield from drain(0 if any(k == "one" and p[1] == slot for k, p in pending)
-                                     else 1)
+                for q, bid in enumerate(ids):
+                    yield from drain(0 if clash([bid]) else 1)
                     self._hrun(f"htrain{gi}_{q}", self.stream)
-                    with torch.cuda.stream(self.stream):
-                        self._loss_host[slot:slot + 1].copy_(self.tw.loss, non_blocking=True)
-                        self.tw.loss.zero_()
-                    self._loss_ev[slot].record(self.stream)
+                    ev = self._win_ev[nwin % 2]
+                    nwin += 1
+                    ev.record(self.stream)
                     self.dm.host_steps += 1
-                    nstep += 1
-                    pending.append(("one", (bid, slot)))
+                    pending.append((ev, [bid]))
             self.ev_train[gi].record(self.stream)
             yield from drain(1)
         yield from drain(0)
