@@ -475,7 +475,7 @@ constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
-  MQ_PDL_ENTRY();
+  pdl_trigger();  // the batch's edges and labels (prep output) load before the wait
   MQ_TL_BEGIN(6);
   htrace(0);
   extern __shared__ __align__(16) float smem[];
@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
     s_val[warp][lane] = __ldg(&a.vals[e0 + lane]);
   }
   if (lane == 0) s_ne[warp] = ne;
+  pdl_wait();  // W, h and dh come from the preceding kernels
   if (Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0) {  // same layout: float4 copy
     const float4* src = reinterpret_cast<const float4*>(a.W);
     float4* dst = reinterpret_cast<float4*>(Ws);

@@ -613,7 +613,10 @@ __global__ void __launch_bounds__(kBlock, 1)
     tc_gemm_kernel(Operands op, const int32_t* m_dev, int m_static, const int32_t* k_dev,
                    int k_static, float* __restrict__ part, int32_t* __restrict__ nparts_out,
                    int R) {
-  MQ_PDL_ENTRY();
+  // PDL: TMEM allocation and barrier setup overlap the predecessor's tail;
+  // every operand read waits (pdl_wait) — the frontier counts (m_dev / k_dev)
+  // come from the prep pass, which completed before this graph segment
+  pdl_trigger();
   MQ_TL_BEGIN(MODE);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -627,7 +630,10 @@ __global__ void __launch_bounds__(kBlock, 1)
   const Work wk = choose_work(M, K, gridDim.x);
   const int items = wk.tiles_m * wk.S;
   if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
-  if ((int)blockIdx.x >= items || M <= 0) return;
+  if ((int)blockIdx.x >= items || M <= 0) {
+    pdl_wait();
+    return;
+  }
 
   trace(0);
   cta_mark(0);
@@ -642,6 +648,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();
   const uint32_t tmem = s_tmem;
   const int stage_bytes = Smem::stage_bytes(Np);
   const uint32_t smem_base = smem_u32(smem);
