@@ -277,17 +277,25 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
     const float* __restrict__ part, const int32_t* __restrict__ nparts_dev,
     const int32_t* __restrict__ m_dev, int N, float* __restrict__ act, int ldact, ZeroRange z0,
     ZeroRange z1) {
-  MQ_PDL_ENTRY();
+  pdl_trigger();
   MQ_TL_BEGIN(5);
   constexpr int U = 4, SU = 4;
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
+  // the block (prep output) is read ahead of the wait; the partials are not
   const int n = *n_dst_dev;
+  int r = blockIdx.x * warps + (threadIdx.x >> 5);
+  int pe0 = 0, pe1 = 0;
+  if (r < n) {
+    pe0 = row_ptr[r];
+    pe1 = row_ptr[r + 1];
+  }
+  pdl_wait();
   const int S = *nparts_dev;
   const int ldy = 2 * N;
   const int64_t stride = (int64_t)(*m_dev) * ldy;
-  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
-    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+  for (bool first = true; r < n; r += gridDim.x * warps, first = false) {
+    const int e0 = first ? pe0 : row_ptr[r], e1 = first ? pe1 : row_ptr[r + 1];
     float* out = act + (int64_t)r * ldact;
     for (int cb = 0; cb < ldact; cb += 64) {
       const int c = cb + 2 * lane;
@@ -377,16 +385,23 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
     const float* __restrict__ vals, const int32_t* __restrict__ n_dst_dev,
     const float* __restrict__ dh, int lddh, const float* __restrict__ act, int ldact, int N,
     float* __restrict__ G) {
-  MQ_PDL_ENTRY();
+  pdl_trigger();
   MQ_TL_BEGIN(7);
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
-  const int n = *n_dst_dev;
+  const int n = *n_dst_dev;  // the block (prep output) ahead of the wait; dh / act / G after
+  int r = blockIdx.x * warps + (threadIdx.x >> 5);
+  int pe0 = 0, pe1 = 0;
+  if (r < n) {
+    pe0 = row_ptr[r];
+    pe1 = row_ptr[r + 1];
+  }
+  pdl_wait();
   const int ldg = 2 * N;
   const bool vec2 = (N & 1) == 0 && (lddh & 1) == 0 && (ldact & 1) == 0 &&
                     (((uintptr_t)dh | (uintptr_t)act | (uintptr_t)G) & 7) == 0;
-  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < n; r += gridDim.x * warps) {
-    const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+  for (bool first = true; r < n; r += gridDim.x * warps, first = false) {
+    const int e0 = first ? pe0 : row_ptr[r], e1 = first ? pe1 : row_ptr[r + 1];
     if (vec2) {
       const int n2 = N / 2;
       for (int cb = 0; cb < n2; cb += 32) {
