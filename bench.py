@@ -530,7 +530,7 @@ def run_ours(args):
                         f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                     "algorithmic_bytes_per_launch": kd["bytes_per_launch"],
                     "avg_launch_us": kd["avg_launch_us"], "share_of_step": kd["share"],
-                    "timing": "CUDA-event time of the op replayed 20x in a CUDA graph "
+                    "timing": "CUDA-event time of the op replayed 20x in a CUDA graph (no PDL) "
                               "(warm, same buffers as the step)",
                     "choice": "largest share of the train-stream critical path"}
             if kd.get("tflops"):

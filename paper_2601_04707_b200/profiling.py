@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import torch
 
+from ._lib import lib
 from .engine import capture_graph
 from .prep import PREP_GATHER, PREP_RELABEL, PREP_SAMPLE
 
@@ -105,10 +106,17 @@ def op_table(runner, reps: int = 20, iters: int = 3) -> dict:
                 host.stage_mask = 0
         ops.append((name, prep_op))
     out = {}
-    for name, fn in ops:
-        out[name] = {"us": _time(fn, runner.stream, reps, iters)}
-        for t, v in zip(state, snap):  # undo accumulations before the next op
-            t.copy_(v)
+    # each op's replays run without programmatic dependent launch: otherwise
+    # copy k+1 of the same op launches into copy k's SMs and inflates both
+    pdl = int(lib().mq_get_pdl())
+    lib().mq_set_pdl(0)
+    try:
+        for name, fn in ops:
+            out[name] = {"us": _time(fn, runner.stream, reps, iters)}
+            for t, v in zip(state, snap):  # undo accumulations before the next op
+                t.copy_(v)
+    finally:
+        lib().mq_set_pdl(pdl)
     torch.cuda.synchronize(runner.device)
     dims = [runner.g.feature_dim] + [int(w.shape[1]) for w in runner.model.weights]
     models = op_models(counts, dims, runner.tw.sw.fanouts, runner.Q, runner.cache is not None,
