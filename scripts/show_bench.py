@@ -1,6 +1,9 @@
 """Summarise a bench.py output file (headline + per-kernel table)."""
 import json
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under `| head`
 
 lines = [l for l in open(sys.argv[1]).read().splitlines() if l.strip()]
 if not lines:
