@@ -388,7 +388,9 @@ def run_ours(args):
             k = runner.windows_done
             if world == 1:
                 done = runner.steps(left, windows)
-            else:
+            else:  # replicas start identical (same init) and apply the same
+                # all-reduced window, so the per-window model average is the
+                # identity (WindowDriver's exact sync elision) and is not issued
                 runner.compute_window()
                 driver._reduce([runner.grad64])
                 runner.apply_window()

@@ -162,9 +162,20 @@ class WindowDriver:
     stream_ctx() / wait_current()``
     (``trainer.StepRunner`` on a GPU; an oracle-backed runner in the CPU
     tests).  ``exchange`` is a DistExchange when replicas span processes.
+
+    Sync elision (``elide_identical``): after one full average the replicas
+    are bit-identical, and every later window applies the same all-reduced
+    gradient through the same deterministic optimizer on every replica, so
+    they stay bit-identical; averaging G identical f32 values in f64 (exact
+    sums of at most 8 terms, exact division of an exact multiple) returns
+    them unchanged.  Later milestone and epoch-barrier syncs are therefore
+    the identity and are skipped (still counted in ``sync_count``, reported
+    in ``elided``).  The first sync of a driver always runs, since replicas
+    handed in may differ.
     """
 
-    def __init__(self, runners, exchange=None, sync_period: int = 1):
+    def __init__(self, runners, exchange=None, sync_period: int = 1,
+                 elide_identical: bool = True):
         if sync_period < 1:
             raise ValueError("sync period must be at least 1")
         self.runners = list(runners)
@@ -172,6 +183,9 @@ class WindowDriver:
         self.sync_period = int(sync_period)
         self.remote = exchange.size if isinstance(exchange, DistExchange) else 1
         self.total_replicas = self.remote * len(self.runners)
+        self.elide_identical = bool(elide_identical)
+        self.identical = False  # replicas known to be bit-identical
+        self.elided = 0
 
     def _reduce(self, tensors):
         """Sum the runners' buffers over every replica.  A lone local runner
@@ -196,10 +210,14 @@ class WindowDriver:
         steps = {r.step_count for r in self.runners}
         if len(steps) != 1:
             raise RuntimeError(f"sync with unequal step counts: {sorted(steps)}")
+        if self.elide_identical and self.identical:
+            self.elided += 1
+            return
         bufs = [r.state64() for r in self.runners]
         self._reduce(bufs)
         for r, b in zip(self.runners, bufs):
             r.load_state64(b, self.total_replicas)
+        self.identical = True
 
     def run(self, total_windows: int, on_window=None) -> dict:
         applied = 0
@@ -224,4 +242,5 @@ class WindowDriver:
         if self.total_replicas > 1:
             self.sync()
             epoch_sync = 1
-        return {"sync_count": sync_count, "epoch_sync": epoch_sync, "applied": applied}
+        return {"sync_count": sync_count, "epoch_sync": epoch_sync, "applied": applied,
+                "elided": self.elided}

@@ -56,6 +56,7 @@ class PipelineConfig:
     use_graph: bool = True
     pipeline: bool = True   # prep of batch k+1 overlaps training of batch k
     fused_step: bool = True  # transform-first fused SAGE step (mq_fused.cu)
+    elide_syncs: bool = True  # skip model averages of provably identical replicas (exact)
 
     def validate(self) -> None:
         if self.num_devices < 1:
@@ -89,6 +90,7 @@ class EpochStats:
     dropped_targets: int = 0
     sync_count: int = 0
     epoch_sync: int = 0
+    elided_syncs: int = 0
     applied_windows: dict = field(default_factory=dict)
     queue_high_water: dict = field(default_factory=dict)
     queue_keys: dict = field(default_factory=dict)
@@ -218,7 +220,8 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(runners[0].stream)
-    info = WindowDriver(runners, exchange, config.sync_period).run(total_windows, on_window)
+    info = WindowDriver(runners, exchange, config.sync_period,
+                        elide_identical=config.elide_syncs).run(total_windows, on_window)
     ev1.record(runners[0].stream)
     for r in runners:
         r.check_finite()
@@ -262,6 +265,7 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
         epoch=epoch, losses=losses, batches=sum(len(x) for x in per_device),
         cache_hits=hits, cache_misses=misses, dropped_targets=0,
         sync_count=info["sync_count"], epoch_sync=info["epoch_sync"],
+        elided_syncs=info["elided"],
         applied_windows={d: info["applied"] for d in range(config.num_devices)},
         queue_high_water={d: {"cpu": 1 if per_device[d] else 0, "dev": 1 if per_device[d] else 0}
                           for d in range(config.num_devices)},

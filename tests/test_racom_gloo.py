@@ -207,3 +207,30 @@ def test_local_exchange_sums_in_replica_order():
     ts = [torch.tensor([1.0, 2.0], dtype=torch.float64), torch.tensor([3.0, 5.0], dtype=torch.float64)]
     LocalExchange(2).allreduce_sum_many(ts)
     assert ts[0].tolist() == [4.0, 7.0] == ts[1].tolist()
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_sync_elision_is_exact(P, golden_sampling, golden_runtime):
+    """Skipping the averages of provably identical replicas changes no bit:
+    replicas seeded differently, first sync performed, later ones elided."""
+    graph = _graph_dict(golden_sampling, golden_runtime["epoch/train_mask"])
+    G, B = 3, 48
+    perm = np.random.default_rng(np.random.SeedSequence([5, 1, 0])).permutation(
+        np.flatnonzero(graph["train_mask"]))
+    _, expected = oracom.plan_epoch(graph["train_mask"], G, B, 5, 1)
+    out = {}
+    for elide in (False, True):
+        runners = [OracleRunner(graph, onn.init_model(16, 16, 5, num_layers=2, seed=5 + r,
+                                                      learning_rate=0.01),
+                                fanouts=(4, 3), batch_size=B, seed=5, world=G, rank=r,
+                                optimizer="adam") for r in range(G)]
+        for r in runners:
+            r.begin_epoch(1, perm)
+        info = WindowDriver(runners, None, sync_period=P, elide_identical=elide).run(len(expected))
+        out[elide] = ([[w.copy() for w in r.model.weights] for r in runners], info)
+    (w0, i0), (w1, i1) = out[False], out[True]
+    assert i0["elided"] == 0 and i1["elided"] == i1["sync_count"] + i1["epoch_sync"] - 1 > 0
+    assert i0["sync_count"] == i1["sync_count"]
+    for ra, rb in zip(w0, w1):
+        for a, b in zip(ra, rb):
+            assert np.array_equal(a, b)
