@@ -355,6 +355,8 @@ def run_ours(args):
         lib().mq_set_pdl(0)
     if os.environ.get("MQ_TC_GRID_CAP"):
         lib().mq_set_tc_grid_cap(int(os.environ["MQ_TC_GRID_CAP"]))
+    if os.environ.get("MQ_TC_KERNEL"):  # A/B of the tcgen05 GEMM kernels (mqgnn.h)
+        lib().mq_set_tc_kernel(int(os.environ["MQ_TC_KERNEL"]))
     queue_choice = None
     if args.queue_depth == "auto":  # the reference's --queue auto (autotune.py), measured
         from paper_2601_04707_b200.autotune import auto_queue_depth

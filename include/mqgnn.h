@@ -389,6 +389,14 @@ int mq_get_gemm_backend(void);
 /* Cap on the tcgen05 GEMM grid (default 148 = one CTA per SM); a smaller
  * grid means fewer, deeper split-K partitions (A/B measurement). */
 int mq_set_tc_grid_cap(int32_t cap);
+/* tcgen05 GEMM kernel: 2 (default) = TMA-fed, warp-specialised (operand tiles
+ * by cp.async.bulk.tensor, one operand split into TMEM, double-buffered TMEM
+ * accumulator) for the forward / aggregate-first / input-gradient modes, the
+ * weight gradient on 1; 3 = TMA for every mode; 1 = cp.async staging with
+ * register transposes everywhere.  Shapes the TMA path does not cover (N > 128,
+ * unaligned pitches) run on 1.  Process-wide; A/B and tests. */
+int mq_set_tc_kernel(int32_t version);
+int mq_get_tc_kernel(void);
 /* Programmatic dependent launch for the step's kernel chains (default on):
  * kernel k+1 is scheduled while kernel k runs and waits on the device for
  * k's completion (griddepcontrol), hiding the launch gap.  Process-wide; for

@@ -86,6 +86,8 @@ SIGNATURES = {
     "mq_get_gemm_backend": (C.c_int, []),
     "mq_set_pdl": (C.c_int, [I32]),
     "mq_set_tc_grid_cap": (C.c_int, [I32]),
+    "mq_set_tc_kernel": (C.c_int, [I32]),
+    "mq_get_tc_kernel": (C.c_int, []),
     "mq_memcpy_async": (C.c_int, [P, P, I64, P]),
     "mq_memset_async": (C.c_int, [P, I32, I64, P]),
     "mq_get_pdl": (C.c_int, []),
@@ -129,7 +131,7 @@ SIGNATURES = {
 
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
                if res is C.c_int and name not in ("mq_version", "mq_prof_num_kernels",
-                                                       "mq_get_gemm_backend", "mq_get_pdl",
+                                                       "mq_get_gemm_backend", "mq_get_pdl", "mq_get_tc_kernel",
                                                        "mq_sage_dw_deferred",
                                                        "mq_sage_y_deferred")}
 

@@ -23,6 +23,8 @@
 //     stage's mbarrier, which releases the stage for the next refill;
 //   * warps 0-3 drain TMEM (tcgen05.ld 32x32b) and store the fp32 partial
 //     tile; a fixed-order split reduction applies the layer epilogue.
+#include <cuda.h>  // CUtensorMap (the encoder comes from the runtime's driver entry point)
+
 #include "mq_gemm.cuh"
 
 namespace mq {
@@ -139,9 +141,20 @@ __device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
   lo.w = tf32_rn(v.w - hi.w);
 }
 
+// v2 split: hi = tf32_rn(x) by integer rounding (2 ops), lo = x - hi exactly;
+// lo is left in fp32 and the tensor core's own tf32 read of it costs at most
+// 2^-10 |lo| <= 2^-21 |x| (v1 rounds lo explicitly: same bound, 6 more ops)
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void split4f(float4 v, float4& hi, float4& lo) {
+  hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+  lo = make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+}
+
 // ---- optional per-phase timeline of CTA 0 (build with -DMQ_TC_TRACE)
 #ifdef MQ_TC_TRACE
-__device__ unsigned long long g_tc_trace[32];
+__device__ unsigned long long g_tc_trace[64];
 __device__ __forceinline__ void trace(int i) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && i < 32) {
     unsigned long long t;
@@ -160,7 +173,15 @@ __device__ __forceinline__ void cta_mark(int i) {
 __device__ __forceinline__ void ktrace(bool on, uint32_t it, int p) {
   if (on && it < 3) trace(3 + 8 * (int)it + p);
 }
+__device__ __forceinline__ void trace_at(int i) {  // caller picks the thread
+  if (blockIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tc_trace[i] = t;
+  }
+}
 #else
+__device__ __forceinline__ void trace_at(int) {}
 __device__ __forceinline__ void trace(int) {}
 __device__ __forceinline__ void ktrace(bool, uint32_t, int) {}
 __device__ __forceinline__ void cta_mark(int) {}
@@ -619,7 +640,9 @@ __global__ void __launch_bounds__(kBlock, 1)
   pdl_trigger();
   MQ_TL_BEGIN(MODE);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, derived from smem_raw by an integer offset so the
+  // compiler keeps the shared address space (LDS / STS, not generic LD / ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t bars[kStages + 1];
   __shared__ uint32_t s_tmem;
 
@@ -851,6 +874,533 @@ __global__ void tc_reduce_kernel(const float* __restrict__ part, const int32_t* 
     for (int j = lane; j < N; j += 32) epi(i, j, fixed_order_sum(part + (int64_t)i * N + j, total, wk.S));
 }
 
+
+// ============================================================================
+// v2: TMA-fed, warp-specialised 3xTF32 GEMM (all five modes).
+//
+// Operand tiles arrive by TMA (cp.async.bulk.tensor, 128-byte swizzle) as
+// they are stored: K-major row blocks (FWD / FCAT / DX A, DX B) or 32 x 32
+// MN-major blocks (W / G / dh columns, and X^T for the weight gradients).
+// Converter warps split each landed tile into hi = tf32_rn(x) and
+// lo = tf32_rn(x - hi).  A goes to TENSOR MEMORY (tcgen05.st; each thread one
+// tile row, the MMA reads A from TMEM), so the shared-memory port carries only
+// the TMA writes, one read of A and the B traffic -- staging A hi / lo in
+// smem and reading it three times per k block made the converters, not the
+// tensor core, the bound.  B stays in smem, K-major with a 128-byte swizzle:
+// MN-major tiles are transposed through registers (a probe of kind::tf32 with
+// MN-major descriptors returned zeros on this part), DX's K-major W rows are
+// split in place.  The MMA warp issues the 3 x 4 tcgen05.mma per 32-wide k
+// block; epilogue warps drain a double-buffered TMEM accumulator while the
+// next tile's MMAs run.  Roles (448 threads):
+//   warp 0        TMA producer (one lane)
+//   warps 1..8    converters (256 threads)
+//   warp 9        TMEM owner + MMA issuer (one lane)
+//   warps 10..13  epilogue (TMEM lane quarter = warp % 4)
+// Pipelines: full[s] (TMA bytes) -> conv[s] (8 converter warps) -> MMA ->
+// empty[s] (tcgen05.commit) back to the producer; accf[b] / acce[b] between
+// the MMA warp and the epilogue per accumulator buffer.
+// Work split (split-K over k blocks, S from the live M / K as in v1) with a
+// CTA keeping ONE split for all its tiles: CTA b -> split b % S, tiles
+// b / S, b / S + G, ... (G = grid / S).  The numerics equal v1's (same hi/lo
+// split, same MMA order per k block); the aggregate-first modes run over a
+// padded concat (each K / M half rounded up to 32) so TMA boxes never
+// straddle the two sources.
+struct Maps {
+  CUtensorMap a, a2, b, b2;
+};
+
+struct Geo {
+  int kbA;  // FCAT / DX: k blocks of the first K source (ceil(d / 32))
+  int p1;   // DCAT: padded rows of the agg half of the output (ceil32(d_in))
+};
+
+__host__ __device__ constexpr bool a_mn(int mode) { return mode == kDw || mode == kDwCat; }
+__host__ __device__ constexpr bool b_mn(int mode) { return mode != kDx; }
+
+__host__ __device__ inline Work work2(int mode, const Geo& g, int M, int K, int grid) {
+  Work w;
+  const int mpad = mode == kDwCat ? 2 * g.p1 : M;
+  const int nkb = (mode == kFwdCat || mode == kDx) ? 2 * g.kbA : (K > 0 ? (K + BK - 1) / BK : 0);
+  w.tiles_m = (mpad + BM - 1) / BM;
+  if (w.tiles_m < 1) w.tiles_m = 1;
+  int S = (grid + w.tiles_m - 1) / w.tiles_m;
+  if (S > nkb) S = nkb;
+  if (S > kMaxSplitsTc) S = kMaxSplitsTc;
+  if (S < 1) S = 1;
+  w.kb_per = nkb > 0 ? (nkb + S - 1) / S : 0;
+  w.S = nkb > 0 ? (nkb + w.kb_per - 1) / w.kb_per : 1;
+  return w;
+}
+
+constexpr int kThreads2 = 448;
+constexpr int kMaxN2 = 128;                      // v2 covers N <= 128 (wider: v1)
+constexpr int kMaxBChunks = kMaxN2 * 8 / 128;  // B chunks per converter thread (group of 128)
+constexpr int kConvThreads = 256;
+constexpr int kConvGroups = 2;  // converter groups of 4 warps (alternate k blocks)
+constexpr int kMaxStages2 = 8;
+
+__host__ __device__ inline int b_tile_bytes(int mode, int Np) {
+  return b_mn(mode) ? 4096 * ((Np + 31) / 32) : 128 * Np;
+}
+// FWD / FCAT run transposed ("swapped"): Y^T = W^T X^T, so the weights are
+// the TMEM operand (A' = W^T: 32 scalar reads down a W column per thread, no
+// smem transpose) and the sampled rows the smem operand (B' = X rows, K-major
+// straight from TMA, split in place); the accumulator is features x rows.
+__host__ __device__ constexpr bool swapped(int mode) { return mode == kFwd || mode == kFwdCat; }
+__host__ __device__ inline int stage2_bytes(int mode, int Np) {
+  if (swapped(mode)) return b_tile_bytes(mode, Np) + 2 * 16384;  // W raw + X hi / lo
+  return 16384 + (mode == kDwCat ? 3 : 2) * b_tile_bytes(mode, Np);  // raw A + B hi/lo (+ mask)
+}
+// TMEM columns: accumulators 2 x cstride, then per stage A hi (32) | A lo (32)
+__host__ __device__ inline int tmem_cstride(int mode, int Np) {
+  return swapped(mode) ? BM : (Np + 31) / 32 * 32;
+}
+__host__ __device__ inline int max_stages_tmem(int mode, int Np) {
+  return (512 - 2 * tmem_cstride(mode, Np)) / 64;
+}
+
+// D[tmem] (+)= A[tmem] . B[smem], kind::tf32 (A: 128 lanes x 8 columns per K = 8)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// 32 lanes x 32 consecutive 32-bit columns (two x16 stores)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]);
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  tmem_st16(taddr, *reinterpret_cast<const float(*)[16]>(&v[0]));
+  tmem_st16(taddr + 16, *reinterpret_cast<const float(*)[16]>(&v[16]));
+}
+// 32 lanes x 16 consecutive 32-bit columns from 16 registers per thread
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 128-byte-swizzle K-major UMMA descriptor: 8-row groups 1024 B apart (SBO);
+// a K = 8 step advances the start by 32 B inside the swizzle atom.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr, uint32_t lbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads2, 1)
+    tc2_kernel(const __grid_constant__ Maps maps, Operands op, Geo geo, const int32_t* m_dev,
+               int m_static, const int32_t* k_dev, int k_static, float* __restrict__ part,
+               int32_t* __restrict__ nparts_out, int ST) {
+  pdl_trigger();
+  MQ_TL_BEGIN(MODE);
+  if (threadIdx.x == 0) trace_at(0);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps LDS / STS
+  __shared__ __align__(8) uint64_t full[kMaxStages2], conv[kMaxStages2], empty[kMaxStages2];
+  __shared__ __align__(8) uint64_t accf[2], acce[2];
+  __shared__ uint32_t s_tmem;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int M = m_dev ? *m_dev : m_static;
+  const int K = k_dev ? *k_dev : k_static;
+  const int Np = op.Np;
+  const Work wk = work2(MODE, geo, M, K, gridDim.x);
+  if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+  const int G = (int)gridDim.x / wk.S;  // CTAs per split
+  const int b = blockIdx.x;
+  if (M <= 0 || b >= G * wk.S) {
+    pdl_wait();
+    return;
+  }
+  const int s = b % wk.S;
+  const int nkb = (MODE == kFwdCat || MODE == kDx) ? 2 * geo.kbA : (K + BK - 1) / BK;
+  const int kb0 = s * wk.kb_per, kb1 = min(nkb, kb0 + wk.kb_per);
+  const int Mout = MODE == kDwCat ? 2 * op.d_in : M;  // rows of the stored result
+  float* dst = (wk.S == 1 && op.out) ? op.out : part + (int64_t)s * Mout * op.N;
+  const int ldd = (wk.S == 1 && op.out) ? op.ldo : op.N;
+  const bool relu = wk.S == 1 && op.out && op.relu;
+
+  if (kb0 >= kb1) {  // K == 0: the partial is zero
+    pdl_wait();
+    for (int t = b / wk.S; t < wk.tiles_m; t += G)
+      for (int e = tid; e < BM * op.N; e += kThreads2) {
+        const int r = t * BM + e / op.N;
+        if (r < Mout) dst[(int64_t)r * ldd + e % op.N] = 0.f;
+      }
+    return;
+  }
+
+  constexpr bool SW = swapped(MODE);
+  const int cstride = tmem_cstride(MODE, Np);
+  const uint32_t tmem_cols = 512;  // accumulators + the A operand stages (one CTA per SM)
+  if (warp == 9) tmem_alloc(&s_tmem, tmem_cols);
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&conv[i], 4);  // the 4 warps of the converter group
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = s_tmem;
+  const int BB = b_tile_bytes(MODE, Np);
+  const int SB = stage2_bytes(MODE, Np);
+  const uint32_t sbase = smem_u32(smem);
+  // smem stage: [A raw 16K | B hi | B lo | (DCAT) act mask]; A hi / lo go to TMEM
+  // swapped (FWD / FCAT): [W raw (BB) | X hi 16K | X lo 16K]; W^T hi / lo go to TMEM
+  const int t_first = b / wk.S;
+  if (tid == 0) trace_at(1);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const int nbox_b = (Np + 31) / 32;
+      uint32_t it = 0;
+      for (int t = t_first; t < wk.tiles_m; t += G) {
+        const int m0 = t * BM;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int st = it % ST;
+          if (it >= (uint32_t)ST) mbar_wait(&empty[st], ((it / ST) - 1) & 1);
+          if (it < 8) trace_at(2 + (int)it);
+          mbar_expect_tx(&full[st], 16384u + (uint32_t)BB * (MODE == kDwCat ? 2u : 1u));
+          // (swapped: the X rows land at sa, the W boxes at sb)
+          const uint32_t sa = SW ? sbase + st * SB + BB : sbase + st * SB;
+          const uint32_t sb = SW ? sbase + st * SB : sa + 16384, sm = sb + 2 * BB;
+          // ---- A
+          if (MODE == kFwd) {
+            tma2d(sa, &maps.a, kb * BK, m0, &full[st]);
+          } else if (MODE == kFwdCat || MODE == kDx) {
+            if (kb < geo.kbA) tma2d(sa, &maps.a, kb * BK, m0, &full[st]);
+            else tma2d(sa, &maps.a2, (kb - geo.kbA) * BK, m0, &full[st]);
+          } else if (MODE == kDw) {
+            for (int j = 0; j < 4; ++j) tma2d(sa + 4096 * j, &maps.a, m0 + 32 * j, kb * BK, &full[st]);
+          } else {  // kDwCat: padded rows [agg | h]
+            for (int j = 0; j < 4; ++j) {
+              const int m = m0 + 32 * j;
+              if (m < geo.p1) tma2d(sa + 4096 * j, &maps.a, m, kb * BK, &full[st]);
+              else tma2d(sa + 4096 * j, &maps.a2, m - geo.p1, kb * BK, &full[st]);
+            }
+          }
+          // ---- B
+          if (MODE == kFwd) {  // box j: 32 columns of W_top (n < h) or W_bot (N may be h alone)
+            for (int j = 0; j < nbox_b; ++j) {
+              const int n0 = 32 * j;
+              if (n0 < op.n_half) tma2d(sb + 4096 * j, &maps.b, n0, kb * BK, &full[st]);
+              else tma2d(sb + 4096 * j, &maps.b, n0 - op.n_half, op.d_in + kb * BK, &full[st]);
+            }
+          } else if (MODE == kFwdCat) {
+            const int row = kb < geo.kbA ? kb * BK : op.d_in + (kb - geo.kbA) * BK;
+            for (int j = 0; j < nbox_b; ++j) tma2d(sb + 4096 * j, &maps.b, 32 * j, row, &full[st]);
+          } else if (MODE == kDx) {
+            if (kb < geo.kbA) tma2d(sb, &maps.b, kb * BK, 0, &full[st]);
+            else tma2d(sb, &maps.b, (kb - geo.kbA) * BK, op.wd_in, &full[st]);
+          } else {
+            for (int j = 0; j < nbox_b; ++j) {
+              tma2d(sb + 4096 * j, &maps.b, 32 * j, kb * BK, &full[st]);
+              if (MODE == kDwCat) tma2d(sm + 4096 * j, &maps.b2, 32 * j, kb * BK, &full[st]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp <= 8) {
+    // ------------------------------------------------------------ converters
+    // kConvGroups groups of 4 warps take alternate k blocks, so the
+    // latency chain of one block (TMA wait, LDS, TMEM store, B transpose,
+    // fences) overlaps the next block's
+    const int g = (warp - 1) >> 2;
+    const int gt = tid - 32 - 128 * g;  // 0..127 within the group
+    const int q = warp & 3;             // TMEM lane quarter of this warp
+    const int m = 32 * q + lane;        // the A tile row this thread splits
+    uint32_t it = 0;
+    for (int t = t_first; t < wk.tiles_m; t += G) {
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        if ((int)(it % kConvGroups) != g) continue;
+        const int st = it % ST;
+        mbar_wait(&full[st], (it / ST) & 1);
+        if (gt == 0 && it < 8) trace_at(10 + (int)it);
+        const int krow0 = kb * BK;
+        if (SW) {
+          uint8_t* sw = smem + st * SB;  // W boxes (MN-major, 32 features x 32 k each)
+          uint8_t* sx = sw + BB;         // X rows (K-major), split in place
+          // ---- A' = W^T -> TMEM: thread = feature n = 32 q + lane, its 32 k
+          {
+            float hi[32], lo[32];
+            const bool live = 32 * q < Np;  // warp-uniform: features past Np stay zero
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float v = live ? *reinterpret_cast<const float*>(
+                  sw + q * 4096 + k * 128 + ((((lane >> 2) ^ (k & 7)) << 4) | ((lane & 3) << 2))) : 0.f;
+              hi[k] = tf32_hi(v);
+              lo[k] = v - hi[k];
+            }
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * cstride + 64 * st);
+            tmem_st32(ta, hi);
+            tmem_st32(ta + 32, lo);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          }
+          if (gt == 0 && it == 1) trace_at(33);
+          // ---- B' = X rows: in-place hi, lo beside (elementwise, conflict-free)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int o = (gt + 128 * i) * 16;
+            float4 hi, lo;
+            split4f(*reinterpret_cast<const float4*>(sx + o), hi, lo);
+            *reinterpret_cast<float4*>(sx + o) = hi;
+            *reinterpret_cast<float4*>(sx + 16384 + o) = lo;
+          }
+          if (gt == 0 && it == 1) trace_at(36);
+          tc_fence_before();
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[st]);
+          if (gt == 0 && it < 2) trace_at(30 + (int)it);
+          continue;
+        }
+        uint8_t* sa = smem + st * SB;
+        uint8_t* sb = sa + 16384;
+        // ---- A -> TMEM: thread = tile row m, all 32 k, split hi / lo into
+        // the stage's 32 + 32 TMEM columns (the MMA reads A from TMEM)
+        {
+          float hi[32], lo[32];
+          if (!a_mn(MODE)) {  // K-major rows (128-byte swizzle: chunk c at c ^ (m & 7))
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              float4 h4, l4;
+              split4f(*reinterpret_cast<const float4*>(sa + m * 128 + ((c ^ (m & 7)) << 4)), h4, l4);
+              hi[4 * c] = h4.x; hi[4 * c + 1] = h4.y; hi[4 * c + 2] = h4.z; hi[4 * c + 3] = h4.w;
+              lo[4 * c] = l4.x; lo[4 * c + 1] = l4.y; lo[4 * c + 2] = l4.z; lo[4 * c + 3] = l4.w;
+            }
+          } else {  // MN-major 32 x 32 box q: k row at k * 128, chunk (m % 32) / 4 at ^ (k & 7)
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              float v = *reinterpret_cast<const float*>(
+                  sa + q * 4096 + k * 128 + ((((lane >> 2) ^ (k & 7)) << 4) | ((lane & 3) << 2)));
+              if (krow0 + k >= K) v = 0.f;
+              hi[k] = tf32_hi(v);
+              lo[k] = v - hi[k];
+            }
+          }
+          if (gt == 0 && it == 1) trace_at(32);
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * cstride + 64 * st);
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (gt == 0 && it == 1) trace_at(33);
+        }
+        // ---- B (smem): MN-major tiles transposed to K-major through
+        // registers (read, sync the group, write hi over the raw tile and lo
+        // beside it); DX's W rows are K-major already
+        if (b_mn(MODE)) {
+          // one K-major 16-byte chunk (row n, k 4 k4 .. 4 k4 + 3) per item:
+          // four 32-bit reads down the MN tile (consecutive lanes = consecutive
+          // n: conflict-free) and one swizzled 16-byte store (conflict-free)
+          const int nch = Np * 8;
+          float4 rv[kMaxBChunks];
+#pragma unroll
+          for (int i = 0; i < kMaxBChunks; ++i) {
+            const int idx = gt + i * 128;
+            if (idx < nch) {
+              const int n = idx % Np, k4 = idx / Np;
+              const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
+              float tv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int k = 4 * k4 + u;
+                const int off = base + k * 128 + ((c ^ (k & 7)) << 4);
+                float v = *reinterpret_cast<const float*>(sb + off);
+                if (MODE == kDwCat && !(*reinterpret_cast<const float*>(sb + 2 * BB + off) > 0.f)) v = 0.f;
+                if (a_mn(MODE) && krow0 + k >= K) v = 0.f;  // rows past the live K
+                tv[u] = v;
+              }
+              rv[i] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+            }
+          }
+          if (gt == 0 && it == 1) trace_at(34);
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + g));
+          if (gt == 0 && it == 1) trace_at(35);
+#pragma unroll
+          for (int i = 0; i < kMaxBChunks; ++i) {
+            const int idx = gt + i * 128;
+            if (idx < nch) {
+              const int n = idx % Np, k4 = idx / Np;
+              const uint32_t o = (uint32_t)n * 128u + (uint32_t)((k4 ^ (n & 7)) << 4);
+              float4 hi, lo;
+              split4f(rv[i], hi, lo);
+              *reinterpret_cast<float4*>(sb + o) = hi;
+              *reinterpret_cast<float4*>(sb + BB + o) = lo;
+            }
+          }
+          if (gt == 0 && it == 1) trace_at(36);
+        } else {
+          for (int o = gt * 16; o < BB; o += 128 * 16) {
+            float4 hi, lo;
+            split4f(*reinterpret_cast<const float4*>(sb + o), hi, lo);
+            *reinterpret_cast<float4*>(sb + o) = hi;
+            *reinterpret_cast<float4*>(sb + BB + o) = lo;
+          }
+        }
+        tc_fence_before();
+        fence_async_smem();
+        __syncwarp();
+        if (gt == 0 && it == 1) trace_at(37);
+        if (lane == 0) mbar_arrive(&conv[st]);
+        if (gt == 0 && it < 2) trace_at(30 + (int)it);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // both operands K-major; swapped: N = the 128-row tile of X
+      const uint32_t idesc = instr_desc(SW ? BM : Np, false, false);
+      uint32_t it = 0, ti = 0;
+      for (int t = t_first; t < wk.tiles_m; t += G, ++ti) {
+        const uint32_t ab = ti & 1;
+        if (ti >= 2) mbar_wait(&acce[ab], ((ti >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + ab * (uint32_t)cstride;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int st = it % ST;
+          mbar_wait(&conv[st], (it / ST) & 1);
+          if (it < 8) trace_at(18 + (int)it);
+          tc_fence_after();
+          const uint32_t a_hi = tmem + (uint32_t)(2 * cstride + 64 * st), a_lo = a_hi + 32;
+          const uint32_t b_hi = SW ? sbase + st * SB + BB : sbase + st * SB + 16384;
+          const uint32_t b_lo = b_hi + (SW ? 16384 : BB);
+#pragma unroll
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t ko = 32u * j;  // K = 8 step inside the 128-byte swizzle atom
+            const uint64_t dbh = sw128_desc(b_hi + ko, 16), dbl = sw128_desc(b_lo + ko, 16);
+            const uint32_t acc = (kb == kb0 && j == 0) ? 0u : 1u;
+            mma_tf32_ts(d, a_lo + 8 * j, dbh, idesc, acc);  // small terms first (as v1)
+            mma_tf32_ts(d, a_hi + 8 * j, dbl, idesc, 1u);
+            mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, 1u);
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&accf[ab]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter
+    uint32_t ti = 0;
+    const bool vec = (op.N & 3) == 0 && (ldd & 3) == 0 && ((uintptr_t)dst & 15) == 0;
+    for (int t = t_first; t < wk.tiles_m; t += G, ++ti) {
+      const uint32_t ab = ti & 1;
+      mbar_wait(&accf[ab], (ti >> 1) & 1);
+      if (warp == 10 && lane == 0 && ti < 2) trace_at(26 + 2 * (int)ti);
+      tc_fence_after();
+      if (SW) {  // TMEM lane = output feature n, column = row of the tile
+        const int n = q * 32 + lane;
+        if (32 * q < op.N) {  // warp-uniform
+          for (int cb = 0; cb < BM; cb += 32) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * (uint32_t)cstride + (uint32_t)cb, v);
+            const int r0 = t * BM + cb;
+            if (n < op.N) {
+#pragma unroll
+              for (int u = 0; u < 32; ++u)
+                if (r0 + u < M) dst[(int64_t)(r0 + u) * ldd + n] = relu ? fmaxf(v[u], 0.f) : v[u];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (warp == 10 && lane == 0 && ti < 1) trace_at(27);
+        if (lane == 0) mbar_arrive(&acce[ab]);
+        continue;
+      }
+      const int p = t * BM + q * 32 + lane;  // row in the (padded) M space
+      int r = p;
+      if (MODE == kDwCat) r = p < geo.p1 ? (p < op.d_in ? p : -1)
+                                         : (p - geo.p1 < op.d_in ? op.d_in + p - geo.p1 : -1);
+      const bool ok = r >= 0 && r < Mout;
+      float* row = dst + (int64_t)(ok ? r : 0) * ldd;
+      for (int cb = 0; cb < Np; cb += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * (uint32_t)cstride + (uint32_t)cb, v);
+        if (!ok) continue;
+        if (relu) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) v[u] = fmaxf(v[u], 0.f);
+        }
+        if (vec && cb + 32 <= op.N) {
+#pragma unroll
+          for (int u = 0; u < 32; u += 4)
+            *reinterpret_cast<float4*>(row + cb + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            if (cb + u < op.N) row[cb + u] = v[u];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (warp == 10 && lane == 0 && ti < 1) trace_at(27);
+      if (lane == 0) mbar_arrive(&acce[ab]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tmem_cols);
+  }
+  if (tid == 0) trace_at(29);
+  MQ_TL_END(MODE);
+}
+
+template <class Epi>
+__global__ void tc2_reduce_kernel(const float* __restrict__ part, int mode, Geo geo,
+                                  const int32_t* m_dev, int m_static, const int32_t* k_dev,
+                                  int k_static, int N, int grid_gemm, Epi epi, bool direct) {
+  MQ_PDL_ENTRY();
+  const int M = m_dev ? *m_dev : m_static;
+  const int K = k_dev ? *k_dev : k_static;
+  const Work wk = work2(mode, geo, M, K, grid_gemm);
+  if (direct && wk.S == 1) return;
+  const int64_t total = (int64_t)M * N;
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < M; i += gridDim.x * wpb)
+    for (int j = lane; j < N; j += 32) epi(i, j, fixed_order_sum(part + (int64_t)i * N + j, total, wk.S));
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------ host side
@@ -883,11 +1433,128 @@ bool tc_async_ok(const tc::Operands& op) {
 
 constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the static barriers
 
+// ---- v2 launch: tensor maps over the operands, or -1 when a shape / pointer
+// falls outside what the TMA path covers (then v1 runs)
+static int g_tc_v2 = 1;
+
+typedef CUresult (*PFN_tmapEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_tmapEncode tmap_encoder() {
+  static PFN_tmapEncode fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmapEncode>(p);
+  }
+  return fn;
+}
+
+// row-major fp32 matrix (rows x cols, pitch ld floats), 128-byte swizzled boxes
+static bool tmap2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld,
+                   int box_c, int box_r) {
+  PFN_tmapEncode enc = tmap_encoder();
+  if (!enc || !base || cols < 1 || rows < 1 || !al16(base) || (ld & 3) || ld < cols) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE, class Epi>
+int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
+            const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
+            cudaStream_t s, int kid, int kid_red, bool skip_reduce, int32_t* nparts_out) {
+  using namespace tc;
+  if (!g_tc_v2 || op.Np > kMaxN2) return -1;
+  // DW (X^T G: both operands MN-major) pays an smem transpose of G per k
+  // block here and measures slower than v1's register staging: v1 keeps it
+  if (MODE == kDw && g_tc_v2 < 3) return -1;
+  const int SB = stage2_bytes(MODE, op.Np);
+  int ST = (kSmemBudget - 1024) / SB;
+  if (ST > kMaxStages2) ST = kMaxStages2;
+  if (ST > max_stages_tmem(MODE, op.Np)) ST = max_stages_tmem(MODE, op.Np);
+  if (ST < 2) return -1;
+  Maps mp;
+  Geo geo{0, 0};
+  bool ok = false;
+  const int mrows = m_max < 1 ? 1 : m_max, krows = k_max < 1 ? 1 : k_max;
+  if (MODE == kFwd) {
+    // W rows past d_in exist only when the bottom half is part of the product
+    ok = op.n_half % 32 == 0 && tmap2d(&mp.a, op.x, op.d_in, mrows, op.ldx, 32, BM) &&
+         tmap2d(&mp.b, op.w, op.n_half, (op.N > op.n_half ? 2 : 1) * op.d_in, op.n_half, 32, 32);
+    mp.a2 = mp.a;
+    mp.b2 = mp.b;
+  } else if (MODE == kFwdCat) {
+    geo.kbA = (op.d_in + BK - 1) / BK;
+    ok = tmap2d(&mp.a, op.x, op.d_in, mrows, op.ldx, 32, BM) &&
+         tmap2d(&mp.a2, op.x2, op.d_in, mrows, op.ldx2, 32, BM) &&
+         tmap2d(&mp.b, op.w, op.N, 2 * op.d_in, op.N, 32, 32);
+    mp.b2 = mp.b;
+  } else if (MODE == kDx) {
+    geo.kbA = (op.wd_out + BK - 1) / BK;
+    ok = (op.wd_out & 3) == 0 && tmap2d(&mp.a, op.x, op.wd_out, mrows, 2 * op.wd_out, 32, BM) &&
+         tmap2d(&mp.a2, op.x + op.wd_out, op.wd_out, mrows, 2 * op.wd_out, 32, BM) &&
+         tmap2d(&mp.b, op.w, op.wd_out, 2 * op.wd_in, op.wd_out, 32, op.Np);
+    mp.b2 = mp.b;
+  } else if (MODE == kDw) {
+    ok = tmap2d(&mp.a, op.x, op.d_in, krows, op.ldx, 32, 32) &&
+         tmap2d(&mp.b, op.g, op.N, krows, op.N, 32, 32);
+    mp.a2 = mp.a;
+    mp.b2 = mp.b;
+  } else {
+    geo.p1 = (op.d_in + 31) / 32 * 32;
+    ok = tmap2d(&mp.a, op.x, op.d_in, krows, op.ldx, 32, 32) &&
+         tmap2d(&mp.a2, op.x2, op.d_in, krows, op.ldx2, 32, 32) &&
+         tmap2d(&mp.b, op.g, op.N, krows, op.ldg, 32, 32) &&
+         tmap2d(&mp.b2, op.act, op.N, krows, op.ldact, 32, 32);
+  }
+  if (!ok) return -1;
+  static thread_local bool configured[5] = {};
+  if (!configured[MODE]) {
+    MQ_CUDA(cudaFuncSetAttribute(tc2_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget));
+    configured[MODE] = true;
+  }
+  const int grid = tc_grid(m_max, k_max);
+  {
+    ProfScope ps(kid, s);
+    MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2), (size_t)(ST * SB + 1024), s, mp,
+                     op, geo, m_dev, m_static, k_dev, k_static, part, nparts_out, ST));
+  }
+  MQ_LAUNCH_CHECK("tc2_gemm");
+  if (skip_reduce) return MQ_OK;
+  int64_t mn = (int64_t)(m_max < 1 ? 1 : m_max) * op.N;
+  int rb = ceil_div(mn, 256);
+  if (rb > kNumSMs * 4) rb = kNumSMs * 4;
+  {
+    ProfScope ps(kid_red, s);
+    MQ_CUDA(launch_k(tc2_reduce_kernel<Epi>, dim3(rb), dim3(256), 0, s, part, (int)MODE, geo, m_dev,
+                     m_static, k_dev, k_static, op.N, grid, epi, op.out != nullptr));
+  }
+  MQ_LAUNCH_CHECK("tc2_reduce");
+  return MQ_OK;
+}
+
 template <int MODE, class Epi>
 int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
                 const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
                 cudaStream_t s, int kid, int kid_red, bool skip_reduce = false,
                 int32_t* nparts_out = nullptr) {
+  {
+    const int r = run_tc2<MODE>(op, m_dev, m_static, m_max, k_dev, k_static, k_max, part, epi, s,
+                                kid, kid_red, skip_reduce, nparts_out);
+    if (r >= 0) return r;
+  }
   static thread_local bool configured[5][2] = {};
   const int base = tc::Smem::total(op.Np);
   int R = (kSmemBudget - base) / tc::raw_bytes(MODE, op.Np);
@@ -1081,6 +1748,15 @@ int mq_set_gemm_backend(int32_t backend) {
 
 int mq_get_gemm_backend(void) { return g_gemm_backend; }
 
+int mq_set_tc_kernel(int32_t version) {
+  MQ_CHECK_ARG(version >= 1 && version <= 3,
+               "mq_set_tc_kernel: 1 (cp.async staging), 2 (TMA; DW stays on 1) or 3 (TMA for all)");
+  g_tc_v2 = version == 1 ? 0 : version;
+  return MQ_OK;
+}
+
+int mq_get_tc_kernel(void) { return g_tc_v2 ? g_tc_v2 : 1; }
+
 int mq_set_tc_grid_cap(int32_t cap) {
   MQ_CHECK_ARG(cap >= 1 && cap <= kNumSMs, "mq_set_tc_grid_cap: 1..%d", kNumSMs);
   g_tc_grid_cap = cap;
@@ -1094,7 +1770,7 @@ int mq_debug_tc_cta(unsigned long long* out) {
 }
 
 int mq_debug_tc_trace(unsigned long long* out) {
-  MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_trace, sizeof(unsigned long long) * 32));
+  MQ_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_trace, sizeof(unsigned long long) * 64));
   return MQ_OK;
 }
 #endif

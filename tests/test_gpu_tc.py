@@ -41,12 +41,15 @@ def _normwise(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
 
 
-@pytest.fixture(params=[1, 0], ids=["tcgen05", "ffma"])
+@pytest.fixture(params=[(1, 2), (1, 3), (1, 1), (0, 2)],
+                ids=["tcgen05-tma", "tcgen05-tma-all", "tcgen05-cpasync", "ffma"])
 def backend(request):
-    old = lib().mq_get_gemm_backend()
-    lib().mq_set_gemm_backend(request.param)
-    yield request.param
+    old, old_k = lib().mq_get_gemm_backend(), lib().mq_get_tc_kernel()
+    lib().mq_set_gemm_backend(request.param[0])
+    lib().mq_set_tc_kernel(request.param[1])
+    yield request.param[0]
     lib().mq_set_gemm_backend(old)
+    lib().mq_set_tc_kernel(old_k)
 
 
 @pytest.mark.parametrize("rows,d_in,d_out", SHAPES)
@@ -103,8 +106,16 @@ def test_tf32_single_pass_would_fail():
     assert _normwise(one_pass, exact) > RTOL
 
 
+@pytest.fixture(params=[2, 3, 1], ids=["tma", "tma-all", "cpasync"])
+def tc_kernel(request):
+    old = lib().mq_get_tc_kernel()
+    lib().mq_set_tc_kernel(request.param)
+    yield request.param
+    lib().mq_set_tc_kernel(old)
+
+
 @pytest.mark.parametrize("rows,d_in,d_out", [(1131, 32, 32), (3262, 602, 64)])
-def test_transform_bwd_deterministic(rows, d_in, d_out):
+def test_transform_bwd_deterministic(tc_kernel, rows, d_in, d_out):
     """Two runs of the tcgen05 weight gradient give bit-identical results."""
     rng = np.random.default_rng(5)
     ld = (d_in + 3) // 4 * 4
@@ -126,7 +137,7 @@ def test_transform_bwd_deterministic(rows, d_in, d_out):
 
 @pytest.mark.parametrize("rows,d_in,d_out", [(2604, 100, 64), (777, 16, 16), (97, 64, 8),
                                              (30000, 100, 64), (0, 16, 16)])
-def test_aggregate_first_layer(rows, d_in, d_out):
+def test_aggregate_first_layer(tc_kernel, rows, d_in, d_out):
     """mq_sage_linear_af (act = relu([agg | h] W)) and mq_sage_linear_af_bwd
     (dW = [agg | h]^T (dh * (act > 0))) against fp64."""
     rng = np.random.default_rng(rows + d_in)
