@@ -1232,11 +1232,25 @@ __global__ void __launch_bounds__(kThreads2, 1)
           // n: conflict-free) and one swizzled 16-byte store (conflict-free)
           const int nch = Np * 8;
           float4 rv[kMaxBChunks];
+          int cn[kMaxBChunks], ck[kMaxBChunks];  // (n, k4) of item gt + 128 i, no divisions in the loop
+          {
+            int n = gt % Np, k4 = gt / Np;
+#pragma unroll
+            for (int i = 0; i < kMaxBChunks; ++i) {
+              cn[i] = n;
+              ck[i] = k4;
+              n += 128;
+              while (n >= Np) {
+                n -= Np;
+                ++k4;
+              }
+            }
+          }
 #pragma unroll
           for (int i = 0; i < kMaxBChunks; ++i) {
             const int idx = gt + i * 128;
             if (idx < nch) {
-              const int n = idx % Np, k4 = idx / Np;
+              const int n = cn[i], k4 = ck[i];
               const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
               float tv[4];
 #pragma unroll
@@ -1258,7 +1272,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           for (int i = 0; i < kMaxBChunks; ++i) {
             const int idx = gt + i * 128;
             if (idx < nch) {
-              const int n = idx % Np, k4 = idx / Np;
+              const int n = cn[i], k4 = ck[i];
               const uint32_t o = (uint32_t)n * 128u + (uint32_t)((k4 ^ (n & 7)) << 4);
               float4 hi, lo;
               split4f(rv[i], hi, lo);

@@ -66,9 +66,19 @@ def op_models(counts: dict, dims: list, fanouts, Q: int, cached: bool, n_params:
                                      + 4 * (nd + 1), "units": "1 batch"}
         m[f"sage_scatter_bwd_l{l}"] = {"bytes": 2 * 4 * nd * dout + 4 * ns * 2 * dout + 8 * nnz,
                                        "units": "1 batch"}
-        m[f"sage_transform_bwd_l{l}"] = {"bytes": 4 * (ns * d + ns * 2 * dout + 2 * d * dout)
-                                         + (4 * ns * d * 2 * dout if l > 0 else 0),
-                                         "flops": fl * (2 if l > 0 else 1), "units": "1 batch"}
+        # dW = h^T G (+ for l > 0 the input gradient dh = G W^T: one more read
+        # of G and W, one write of dh)
+        m[f"sage_transform_bwd_l{l}"] = {
+            "bytes": 4 * (ns * d + ns * 2 * dout + 2 * d * dout)
+            + (4 * (ns * 2 * dout + 2 * d * dout + ns * d) if l > 0 else 0),
+            "flops": fl * (2 if l > 0 else 1), "units": "1 batch"}
+        if l == 0:  # aggregate-first input layer (mq_spmm_fwd + mq_sage_linear_af[_bwd])
+            m["sage_spmm_l0"] = {"bytes": 4 * d * (nnz + nd) + 8 * nnz + 4 * (nd + 1),
+                                 "units": "1 batch"}
+            m["sage_linear_af_l0"] = {"bytes": 4 * (nd * 2 * d + 2 * d * dout + nd * dout),
+                                      "flops": 2.0 * nd * 2 * d * dout, "units": "1 batch"}
+            m["sage_linear_af_bwd_l0"] = {"bytes": 4 * (nd * 2 * d + 2 * nd * dout),
+                                          "flops": 2.0 * nd * 2 * d * dout, "units": "1 batch"}
     nd, ns, nnz = hops[0]
     d = dims[L - 1]
     m["sage_head"] = {"bytes": 4 * d * ns + 8 * nnz + 4 * 2 * d * C + 4 * B
