@@ -1147,6 +1147,24 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int gt = tid - 32 - 128 * g;  // 0..127 within the group
     const int q = warp & 3;             // TMEM lane quarter of this warp
     const int m = 32 * q + lane;        // the A tile row this thread splits
+    // B transposition items of this thread: chunk (row n, k4) for item gt + 128 i
+    const int nit = (Np * 8 - gt + 127) / 128;  // items this thread owns (<= kMaxBChunks)
+    int cn[kMaxBChunks], ck[kMaxBChunks];
+    {
+      const int q128 = 128 / Np, r128 = 128 % Np;
+      int n = gt % Np, k4 = gt / Np;
+#pragma unroll
+      for (int i = 0; i < kMaxBChunks; ++i) {
+        cn[i] = n;
+        ck[i] = k4;
+        n += r128;
+        k4 += q128;
+        if (n >= Np) {
+          n -= Np;
+          ++k4;
+        }
+      }
+    }
     uint32_t it = 0;
     for (int t = t_first; t < wk.tiles_m; t += G) {
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -1194,32 +1212,38 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         uint8_t* sa = smem + st * SB;
         uint8_t* sb = sa + 16384;
-        // ---- A -> TMEM: thread = tile row m, all 32 k, split hi / lo into
-        // the stage's 32 + 32 TMEM columns (the MMA reads A from TMEM)
+        // ---- A -> TMEM: thread = tile row m, all 32 k (two halves of 16),
+        // split hi / lo into the stage's 32 + 32 TMEM columns (the MMA reads A
+        // from TMEM)
         {
-          float hi[32], lo[32];
-          if (!a_mn(MODE)) {  // K-major rows (128-byte swizzle: chunk c at c ^ (m & 7))
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * cstride + 64 * st);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              float4 h4, l4;
-              split4f(*reinterpret_cast<const float4*>(sa + m * 128 + ((c ^ (m & 7)) << 4)), h4, l4);
-              hi[4 * c] = h4.x; hi[4 * c + 1] = h4.y; hi[4 * c + 2] = h4.z; hi[4 * c + 3] = h4.w;
-              lo[4 * c] = l4.x; lo[4 * c + 1] = l4.y; lo[4 * c + 2] = l4.z; lo[4 * c + 3] = l4.w;
-            }
-          } else {  // MN-major 32 x 32 box q: k row at k * 128, chunk (m % 32) / 4 at ^ (k & 7)
+          for (int hh = 0; hh < 2; ++hh) {
+            float hi[16], lo[16];
+            if (!a_mn(MODE)) {  // K-major rows (128-byte swizzle: chunk c at c ^ (m & 7))
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              float v = *reinterpret_cast<const float*>(
-                  sa + q * 4096 + k * 128 + ((((lane >> 2) ^ (k & 7)) << 4) | ((lane & 3) << 2)));
-              if (krow0 + k >= K) v = 0.f;
-              hi[k] = tf32_hi(v);
-              lo[k] = v - hi[k];
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const int c = 4 * hh + c4;
+                float4 h4, l4;
+                split4f(*reinterpret_cast<const float4*>(sa + m * 128 + ((c ^ (m & 7)) << 4)), h4, l4);
+                hi[4 * c4] = h4.x; hi[4 * c4 + 1] = h4.y; hi[4 * c4 + 2] = h4.z; hi[4 * c4 + 3] = h4.w;
+                lo[4 * c4] = l4.x; lo[4 * c4 + 1] = l4.y; lo[4 * c4 + 2] = l4.z; lo[4 * c4 + 3] = l4.w;
+              }
+            } else {  // MN-major 32 x 32 box q: k row at k * 128, chunk (m % 32) / 4 at ^ (k & 7)
+#pragma unroll
+              for (int kk = 0; kk < 16; ++kk) {
+                const int k = 16 * hh + kk;
+                float v = *reinterpret_cast<const float*>(
+                    sa + q * 4096 + k * 128 + ((((lane >> 2) ^ (k & 7)) << 4) | ((lane & 3) << 2)));
+                if (krow0 + k >= K) v = 0.f;
+                hi[kk] = tf32_hi(v);
+                lo[kk] = v - hi[kk];
+              }
             }
+            tmem_st16(ta + 16 * hh, hi);
+            tmem_st16(ta + 32 + 16 * hh, lo);
           }
           if (gt == 0 && it == 1) trace_at(32);
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * cstride + 64 * st);
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           if (gt == 0 && it == 1) trace_at(33);
         }
@@ -1230,52 +1254,49 @@ __global__ void __launch_bounds__(kThreads2, 1)
           // one K-major 16-byte chunk (row n, k 4 k4 .. 4 k4 + 3) per item:
           // four 32-bit reads down the MN tile (consecutive lanes = consecutive
           // n: conflict-free) and one swizzled 16-byte store (conflict-free)
-          const int nch = Np * 8;
-          float4 rv[kMaxBChunks];
-          int cn[kMaxBChunks], ck[kMaxBChunks];  // (n, k4) of item gt + 128 i, no divisions in the loop
-          {
-            int n = gt % Np, k4 = gt / Np;
-#pragma unroll
-            for (int i = 0; i < kMaxBChunks; ++i) {
-              cn[i] = n;
-              ck[i] = k4;
-              n += 128;
-              while (n >= Np) {
-                n -= Np;
-                ++k4;
-              }
-            }
-          }
+          // all reads first (unconditional; items past nit re-read item 0),
+          // so the 4 x kMaxBChunks loads issue back to back
+          float rvv[kMaxBChunks][4];
 #pragma unroll
           for (int i = 0; i < kMaxBChunks; ++i) {
-            const int idx = gt + i * 128;
-            if (idx < nch) {
-              const int n = cn[i], k4 = ck[i];
+            const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
+            const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int k = 4 * k4 + u;
+              rvv[i][u] = *reinterpret_cast<const float*>(sb + base + k * 128 + ((c ^ (k & 7)) << 4));
+            }
+          }
+          if (MODE == kDwCat) {  // dz = dh * (act > 0)
+#pragma unroll
+            for (int i = 0; i < kMaxBChunks; ++i) {
+              const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
               const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
-              float tv[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int k = 4 * k4 + u;
-                const int off = base + k * 128 + ((c ^ (k & 7)) << 4);
-                float v = *reinterpret_cast<const float*>(sb + off);
-                if (MODE == kDwCat && !(*reinterpret_cast<const float*>(sb + 2 * BB + off) > 0.f)) v = 0.f;
-                if (a_mn(MODE) && krow0 + k >= K) v = 0.f;  // rows past the live K
-                tv[u] = v;
+                if (!(*reinterpret_cast<const float*>(sb + 2 * BB + base + k * 128 + ((c ^ (k & 7)) << 4)) > 0.f))
+                  rvv[i][u] = 0.f;
               }
-              rv[i] = make_float4(tv[0], tv[1], tv[2], tv[3]);
             }
+          }
+          if (a_mn(MODE) && krow0 + BK > K) {  // the last k block: rows past the live K
+#pragma unroll
+            for (int i = 0; i < kMaxBChunks; ++i)
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (krow0 + 4 * ck[i] + u >= K) rvv[i][u] = 0.f;
           }
           if (gt == 0 && it == 1) trace_at(34);
           asm volatile("bar.sync %0, 128;" ::"r"(1 + g));
           if (gt == 0 && it == 1) trace_at(35);
 #pragma unroll
           for (int i = 0; i < kMaxBChunks; ++i) {
-            const int idx = gt + i * 128;
-            if (idx < nch) {
+            if (i < nit) {
               const int n = cn[i], k4 = ck[i];
               const uint32_t o = (uint32_t)n * 128u + (uint32_t)((k4 ^ (n & 7)) << 4);
               float4 hi, lo;
-              split4f(rv[i], hi, lo);
+              split4f(make_float4(rvv[i][0], rvv[i][1], rvv[i][2], rvv[i][3]), hi, lo);
               *reinterpret_cast<float4*>(sb + o) = hi;
               *reinterpret_cast<float4*>(sb + BB + o) = lo;
             }

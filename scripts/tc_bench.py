@@ -27,7 +27,7 @@ def timeit(fn, reps=20):
 def trace():
     if not hasattr(lib().dll, "mq_debug_tc_trace"):
         return ""
-    if lib().mq_get_tc_kernel() == 2:
+    if lib().mq_get_tc_kernel() >= 2:
         buf = (C.c_ulonglong * 64)()
         lib().dll.mq_debug_tc_trace(buf)
         t = [int(x) for x in buf]
