@@ -490,7 +490,13 @@ constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
+// The scatter that follows launches at this trigger.  Measured A/B (-D
+// MQ_HEAD_LATE_TRIGGER: trigger after the dW partials): device-resident step
+// 61.1 -> 59.7 us, host-buffer (e2e) step 61.6 -> 62.3 us; e2e is the
+// headline, so the early trigger stays the default.
+#ifndef MQ_HEAD_LATE_TRIGGER
   pdl_trigger();  // the batch's edges and labels (prep output) load before the wait
+#endif
   MQ_TL_BEGIN(6);
   htrace(0);
   extern __shared__ __align__(16) float smem[];
@@ -766,6 +772,9 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
 
   htrace(6);
+#ifdef MQ_HEAD_LATE_TRIGGER
+  pdl_trigger();
+#endif
   // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA
   //    order (mq_grad_src), so no grid-wide barrier is needed here.  The last
   //    CTA to finish commits the batch loss to the epoch's loss ring.

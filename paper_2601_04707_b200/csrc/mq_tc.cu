@@ -23,7 +23,8 @@
 //     stage's mbarrier, which releases the stage for the next refill;
 //   * warps 0-3 drain TMEM (tcgen05.ld 32x32b) and store the fp32 partial
 //     tile; a fixed-order split reduction applies the layer epilogue.
-#include <cuda.h>  // CUtensorMap (the encoder comes from the runtime's driver entry point)
+#include <cuda.h>
+#include <stdlib.h>  // CUtensorMap (the encoder comes from the runtime's driver entry point)
 
 #include "mq_gemm.cuh"
 
@@ -1560,7 +1561,14 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
                                  kSmemBudget));
     configured[MODE] = true;
   }
-  const int grid = tc_grid(m_max, k_max);
+  int grid = tc_grid(m_max, k_max);
+  {  // experiment knob: cap the v2 grid (fewer, deeper k splits -> less partial traffic)
+    static const int cap2 = [] {
+      const char* e = getenv("MQ_TC2_GRID_CAP");
+      return e ? atoi(e) : 0;
+    }();
+    if (cap2 > 0 && grid > cap2) grid = cap2;
+  }
   {
     ProfScope ps(kid, s);
     MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2), (size_t)(ST * SB + 1024), s, mp,

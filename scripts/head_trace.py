@@ -3,7 +3,7 @@ Reddit-shaped step (MQ_TC_TRACE library: libmqgnn_trace.so)."""
 import ctypes as C
 import os
 import sys
-os.environ["MQGNN_LIB"] = os.path.join(os.path.dirname(__file__), "..", "paper_2601_04707_b200",
+os.environ["MQGNN_LIB"] = os.environ.get("MQ_TRACE_LIB") or os.path.join(os.path.dirname(__file__), "..", "paper_2601_04707_b200",
                                        "libmqgnn_trace.so")
 import torch
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
