@@ -911,8 +911,9 @@ struct Maps {
 };
 
 struct Geo {
-  int kbA;  // FCAT / DX: k blocks of the first K source (ceil(d / 32))
-  int p1;   // DCAT: padded rows of the agg half of the output (ceil32(d_in))
+  int kbA;     // FCAT / DX: k blocks of the first K source (ceil(d / 32))
+  int p1;      // DCAT: padded rows of the agg half of the output (ceil32(d_in))
+  int nf = 0;  // DW: feature columns per tile (the MMA N of the swapped product)
 };
 
 __host__ __device__ constexpr bool a_mn(int mode) { return mode == kDw || mode == kDwCat; }
@@ -947,7 +948,13 @@ __host__ __device__ inline int b_tile_bytes(int mode, int Np) {
 // the TMEM operand (A' = W^T: 32 scalar reads down a W column per thread, no
 // smem transpose) and the sampled rows the smem operand (B' = X rows, K-major
 // straight from TMA, split in place); the accumulator is features x rows.
-__host__ __device__ constexpr bool swapped(int mode) { return mode == kFwd || mode == kFwdCat; }
+// The weight gradient P = X^T G runs swapped too (P^T = G^T X): G's columns
+// go to TMEM by scalar reads, X^T (d_in <= 128 features) is the transposed
+// smem operand -- half the transposition of the unswapped order at 2 d_out =
+// 128 > d_in.
+__host__ __device__ constexpr bool swapped(int mode) {
+  return mode == kFwd || mode == kFwdCat || mode == kDw;
+}
 __host__ __device__ inline int stage2_bytes(int mode, int Np) {
   if (swapped(mode)) return b_tile_bytes(mode, Np) + 2 * 16384;  // W raw + X hi / lo
   return 16384 + (mode == kDwCat ? 3 : 2) * b_tile_bytes(mode, Np);  // raw A + B hi/lo (+ mask)
@@ -1149,23 +1156,73 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int q = warp & 3;             // TMEM lane quarter of this warp
     const int m = 32 * q + lane;        // the A tile row this thread splits
     // B transposition items of this thread: chunk (row n, k4) for item gt + 128 i
-    const int nit = (Np * 8 - gt + 127) / 128;  // items this thread owns (<= kMaxBChunks)
+    const int Nt = MODE == kDw ? geo.nf : Np;  // rows of the transposed smem operand
+    const int nit = (Nt * 8 - gt + 127) / 128;  // items this thread owns (<= kMaxBChunks)
     int cn[kMaxBChunks], ck[kMaxBChunks];
     {
-      const int q128 = 128 / Np, r128 = 128 % Np;
-      int n = gt % Np, k4 = gt / Np;
+      const int q128 = 128 / Nt, r128 = 128 % Nt;
+      int n = gt % Nt, k4 = gt / Nt;
 #pragma unroll
       for (int i = 0; i < kMaxBChunks; ++i) {
         cn[i] = n;
         ck[i] = k4;
         n += r128;
         k4 += q128;
-        if (n >= Np) {
-          n -= Np;
+        if (n >= Nt) {
+          n -= Nt;
           ++k4;
         }
       }
     }
+    // MN-major 32 x 32 boxes at `raw` -> K-major 128-byte-swizzled rows (hi over
+    // the raw tile, lo at raw + lo_off): four 32-bit reads down the tile per
+    // 16-byte chunk (consecutive lanes = consecutive rows: conflict-free), all
+    // reads issued first, the converter group synced, then swizzled stores
+    auto transpose_mn = [&](uint8_t* raw, int lo_off, const uint8_t* mask, int krow0) {
+      float rvv[kMaxBChunks][4];
+#pragma unroll
+      for (int i = 0; i < kMaxBChunks; ++i) {
+        const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
+        const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = 4 * k4 + u;
+          rvv[i][u] = *reinterpret_cast<const float*>(raw + base + k * 128 + ((c ^ (k & 7)) << 4));
+        }
+      }
+      if (mask != nullptr) {  // DCAT: dz = dh * (act > 0)
+#pragma unroll
+        for (int i = 0; i < kMaxBChunks; ++i) {
+          const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
+          const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = 4 * k4 + u;
+            if (!(*reinterpret_cast<const float*>(mask + base + k * 128 + ((c ^ (k & 7)) << 4)) > 0.f))
+              rvv[i][u] = 0.f;
+          }
+        }
+      }
+      if (a_mn(MODE) && krow0 + BK > K) {  // the last k block: rows past the live K
+#pragma unroll
+        for (int i = 0; i < kMaxBChunks; ++i)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (krow0 + 4 * ck[i] + u >= K) rvv[i][u] = 0.f;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g));
+#pragma unroll
+      for (int i = 0; i < kMaxBChunks; ++i) {
+        if (i < nit) {
+          const int n = cn[i], k4 = ck[i];
+          const uint32_t o = (uint32_t)n * 128u + (uint32_t)((k4 ^ (n & 7)) << 4);
+          float4 hi, lo;
+          split4f(make_float4(rvv[i][0], rvv[i][1], rvv[i][2], rvv[i][3]), hi, lo);
+          *reinterpret_cast<float4*>(raw + o) = hi;
+          *reinterpret_cast<float4*>(raw + lo_off + o) = lo;
+        }
+      }
+    };
     uint32_t it = 0;
     for (int t = t_first; t < wk.tiles_m; t += G) {
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -1183,8 +1240,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const bool live = 32 * q < Np;  // warp-uniform: features past Np stay zero
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-              const float v = live ? *reinterpret_cast<const float*>(
+              float v = live ? *reinterpret_cast<const float*>(
                   sw + q * 4096 + k * 128 + ((((lane >> 2) ^ (k & 7)) << 4) | ((lane & 3) << 2))) : 0.f;
+              if (MODE == kDw && krow0 + k >= K) v = 0.f;  // rows past the live K
               hi[k] = tf32_hi(v);
               lo[k] = v - hi[k];
             }
@@ -1194,14 +1252,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
           if (gt == 0 && it == 1) trace_at(33);
-          // ---- B' = X rows: in-place hi, lo beside (elementwise, conflict-free)
+          if (MODE == kDw) {  // ---- B' = X^T (feature boxes): transposed
+            transpose_mn(sx, 16384, nullptr, krow0);
+          } else {  // ---- B' = X rows: in-place hi, lo beside (elementwise, conflict-free)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int o = (gt + 128 * i) * 16;
-            float4 hi, lo;
-            split4f(*reinterpret_cast<const float4*>(sx + o), hi, lo);
-            *reinterpret_cast<float4*>(sx + o) = hi;
-            *reinterpret_cast<float4*>(sx + 16384 + o) = lo;
+            for (int i = 0; i < 8; ++i) {
+              const int o = (gt + 128 * i) * 16;
+              float4 hi, lo;
+              split4f(*reinterpret_cast<const float4*>(sx + o), hi, lo);
+              *reinterpret_cast<float4*>(sx + o) = hi;
+              *reinterpret_cast<float4*>(sx + 16384 + o) = lo;
+            }
           }
           if (gt == 0 && it == 1) trace_at(36);
           tc_fence_before();
@@ -1252,56 +1313,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         // registers (read, sync the group, write hi over the raw tile and lo
         // beside it); DX's W rows are K-major already
         if (b_mn(MODE)) {
-          // one K-major 16-byte chunk (row n, k 4 k4 .. 4 k4 + 3) per item:
-          // four 32-bit reads down the MN tile (consecutive lanes = consecutive
-          // n: conflict-free) and one swizzled 16-byte store (conflict-free)
-          // all reads first (unconditional; items past nit re-read item 0),
-          // so the 4 x kMaxBChunks loads issue back to back
-          float rvv[kMaxBChunks][4];
-#pragma unroll
-          for (int i = 0; i < kMaxBChunks; ++i) {
-            const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
-            const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int k = 4 * k4 + u;
-              rvv[i][u] = *reinterpret_cast<const float*>(sb + base + k * 128 + ((c ^ (k & 7)) << 4));
-            }
-          }
-          if (MODE == kDwCat) {  // dz = dh * (act > 0)
-#pragma unroll
-            for (int i = 0; i < kMaxBChunks; ++i) {
-              const int n = i < nit ? cn[i] : cn[0], k4 = i < nit ? ck[i] : ck[0];
-              const int base = (n >> 5) * 4096 + (n & 3) * 4, c = (n & 31) >> 2;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int k = 4 * k4 + u;
-                if (!(*reinterpret_cast<const float*>(sb + 2 * BB + base + k * 128 + ((c ^ (k & 7)) << 4)) > 0.f))
-                  rvv[i][u] = 0.f;
-              }
-            }
-          }
-          if (a_mn(MODE) && krow0 + BK > K) {  // the last k block: rows past the live K
-#pragma unroll
-            for (int i = 0; i < kMaxBChunks; ++i)
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (krow0 + 4 * ck[i] + u >= K) rvv[i][u] = 0.f;
-          }
-          if (gt == 0 && it == 1) trace_at(34);
-          asm volatile("bar.sync %0, 128;" ::"r"(1 + g));
-          if (gt == 0 && it == 1) trace_at(35);
-#pragma unroll
-          for (int i = 0; i < kMaxBChunks; ++i) {
-            if (i < nit) {
-              const int n = cn[i], k4 = ck[i];
-              const uint32_t o = (uint32_t)n * 128u + (uint32_t)((k4 ^ (n & 7)) << 4);
-              float4 hi, lo;
-              split4f(make_float4(rvv[i][0], rvv[i][1], rvv[i][2], rvv[i][3]), hi, lo);
-              *reinterpret_cast<float4*>(sb + o) = hi;
-              *reinterpret_cast<float4*>(sb + BB + o) = lo;
-            }
-          }
+          transpose_mn(sb, BB, MODE == kDwCat ? sb + 2 * BB : nullptr, krow0);
           if (gt == 0 && it == 1) trace_at(36);
         } else {
           for (int o = gt * 16; o < BB; o += 128 * 16) {
@@ -1323,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       // both operands K-major; swapped: N = the 128-row tile of X
-      const uint32_t idesc = instr_desc(SW ? BM : Np, false, false);
+      const uint32_t idesc = instr_desc(SW ? (MODE == kDw ? geo.nf : BM) : Np, false, false);
       uint32_t it = 0, ti = 0;
       for (int t = t_first; t < wk.tiles_m; t += G, ++ti) {
         const uint32_t ab = ti & 1;
@@ -1512,9 +1524,10 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
             cudaStream_t s, int kid, int kid_red, bool skip_reduce, int32_t* nparts_out) {
   using namespace tc;
   if (!g_tc_v2 || op.Np > kMaxN2) return -1;
-  // DW (X^T G: both operands MN-major) pays an smem transpose of G per k
-  // block here and measures slower than v1's register staging: v1 keeps it
-  if (MODE == kDw && g_tc_v2 < 3) return -1;
+  // DW (X^T G, both operands MN-major) runs swapped, transposing X^T: a win
+  // while d_in <= 128 (<= 2 d_out); wider inputs (Reddit's 602) transpose as
+  // much as the unswapped order and v1's register staging is faster there
+  if (MODE == kDw && op.d_in > 128 && g_tc_v2 < 3) return -1;
   const int SB = stage2_bytes(MODE, op.Np);
   int ST = (kSmemBudget - 1024) / SB;
   if (ST > kMaxStages2) ST = kMaxStages2;
@@ -1543,6 +1556,7 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
          tmap2d(&mp.b, op.w, op.wd_out, 2 * op.wd_in, op.wd_out, 32, op.Np);
     mp.b2 = mp.b;
   } else if (MODE == kDw) {
+    geo.nf = op.d_in >= 128 ? 128 : (op.d_in + 15) / 16 * 16;
     ok = tmap2d(&mp.a, op.x, op.d_in, krows, op.ldx, 32, 32) &&
          tmap2d(&mp.b, op.g, op.N, krows, op.N, 32, 32);
     mp.a2 = mp.a;

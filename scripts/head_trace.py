@@ -21,7 +21,8 @@ cache = mq.refresh_cache(g, mq.cache_probs_degree(g), args.cache_fraction, mq.Re
 model = mq.init_model(g.feature_dim, args.hidden, g.num_classes, num_layers=len(fanouts), seed=0,
                       learning_rate=1e-3, device=dev)
 n_train = int(g.train_mask.sum())
-runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=1024, num_train=n_train, cache=cache)
+runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=1024, num_train=n_train, cache=cache,
+                       layer0=args.layer0)
 runner.capture()
 runner.begin_epoch(0, epoch_permutation(g.train_mask, 0, 0))
 runner.steps(8)
