@@ -1524,10 +1524,11 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
             cudaStream_t s, int kid, int kid_red, bool skip_reduce, int32_t* nparts_out) {
   using namespace tc;
   if (!g_tc_v2 || op.Np > kMaxN2) return -1;
-  // DW (X^T G, both operands MN-major) runs swapped, transposing X^T: a win
-  // while d_in <= 128 (<= 2 d_out); wider inputs (Reddit's 602) transpose as
-  // much as the unswapped order and v1's register staging is faster there
-  if (MODE == kDw && op.d_in > 128 && g_tc_v2 < 3) return -1;
+  // DW (X^T G, both operands MN-major) runs swapped, transposing X^T.  In the
+  // fused step (deferred partials) it wins at every width (Reddit's 602-d
+  // layer: 12.6 -> 11.6 us); the materialising per-op call with d_in > 128
+  // measures faster on v1 (21 vs 29 us with its split reduction)
+  if (MODE == kDw && op.d_in > 128 && !skip_reduce && g_tc_v2 < 3) return -1;
   const int SB = stage2_bytes(MODE, op.Np);
   int ST = (kSmemBudget - 1024) / SB;
   if (ST > kMaxStages2) ST = kMaxStages2;
