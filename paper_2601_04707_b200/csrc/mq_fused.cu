@@ -534,10 +534,15 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
   if (lane == 0) s_ne[warp] = ne;
   pdl_wait();  // W, h and dh come from the preceding kernels
-  if (Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0) {  // same layout: float4 copy
+  const bool w_async = Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0;
+  if (w_async) {  // same layout: 16-byte cp.async, landing while phase 1 aggregates
     const float4* src = reinterpret_cast<const float4*>(a.W);
-    float4* dst = reinterpret_cast<float4*>(Ws);
-    for (int i = tid; i < d2 * C / 4; i += kHeadThreads) dst[i] = __ldg(src + i);
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(Ws));
+    for (int i = tid; i < d2 * C / 4; i += kHeadThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16u * (uint32_t)i),
+                   "l"(src + i)
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     for (int i = d2 * C + tid; i < d2p * Cp; i += kHeadThreads) Ws[i] = 0.f;
   } else {
     for (int i = tid; i < d2p * C; i += kHeadThreads) {
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
       for (int c = d2 + lane; c < d2p; c += 32) brow[c] = 0.f;
     }
   }
+  if (w_async) asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
 
   htrace(2);
