@@ -30,6 +30,10 @@
 
 #include "mq_gemm.cuh"
 
+#ifndef MQ_AGG_SU
+#define MQ_AGG_SU 4  // split partials loaded per batch in sage_aggregate_parts
+#endif
+
 namespace mq {
 
 // tcgen05 3xTF32 path (mq_tc.cu)
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
     ZeroRange z1) {
   pdl_trigger();
   MQ_TL_BEGIN(5);
-  constexpr int U = 4, SU = 4;
+  constexpr int U = 4, SU = MQ_AGG_SU;
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
   // the block (prep output) is read ahead of the wait; the partials are not
