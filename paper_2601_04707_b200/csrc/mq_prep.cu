@@ -266,30 +266,73 @@ __global__ void __launch_bounds__(kGatherThreads) gather_q_kernel(
   float* outq = out.at(q);
   const int lane = threadIdx.x & 31;
   const int warps = kGatherThreads / 32;
-  int64_t row = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
-  const int64_t stride = (int64_t)gridDim.x * warps;
+  // A warp takes 32 rows at a time: lane i resolves row i's id, cache slot
+  // and source pointer (the dependent loads of all 32 rows in flight at once),
+  // then the warp copies the rows kRowsInFlight at a time, lanes over the
+  // row's 16-byte chunks (coalesced).
+  // Rows wider than 512 B (Reddit's 602-d) keep one row per warp pass with
+  // four 16-byte chunks per lane in flight.
+  constexpr int kRowsInFlight = 4;
   unsigned int hits = 0, miss = 0;
-  for (; row < n; row += stride) {
-    const int32_t id = idq[row];
-    const float4* src;
-    const int32_t slot = slot_of ? slot_of[id] : -1;
-    if (slot >= 0) {
-      src = reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch);
-      ++hits;
-    } else {
-      src = reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
-      ++miss;
+  if (d4 > 32) {
+    int64_t row = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+    const int64_t rstride = (int64_t)gridDim.x * warps;
+    for (; row < n; row += rstride) {
+      const int32_t id = idq[row];
+      const float4* src;
+      const int32_t slot = slot_of ? slot_of[id] : -1;
+      if (slot >= 0) {
+        src = reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch);
+        ++hits;
+      } else {
+        src = reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
+        ++miss;
+      }
+      float4* dst = reinterpret_cast<float4*>(outq + row * out_pitch);
+      int c = lane;
+      for (; c + 96 < d4; c += 128) {
+        const float4 a = src[c], b = src[c + 32], e = src[c + 64], f = src[c + 96];
+        dst[c] = a;
+        dst[c + 32] = b;
+        dst[c + 64] = e;
+        dst[c + 96] = f;
+      }
+      for (; c < d4; c += 32) dst[c] = src[c];
     }
-    float4* dst = reinterpret_cast<float4*>(outq + row * out_pitch);
-    int c = lane;
-    for (; c + 96 < d4; c += 128) {
-      const float4 a = src[c], b = src[c + 32], e = src[c + 64], f = src[c + 96];
-      dst[c] = a;
-      dst[c + 32] = b;
-      dst[c + 64] = e;
-      dst[c + 96] = f;
+  }
+  int64_t row0 = ((int64_t)blockIdx.x * warps + (threadIdx.x >> 5)) * 32;
+  const int64_t stride = (int64_t)gridDim.x * warps * 32;
+  for (; d4 <= 32 && row0 < n; row0 += stride) {
+    const int m = (int)min((int64_t)32, (int64_t)n - row0);
+    const float4* my_src = nullptr;
+    bool hit = false;
+    if (lane < m) {
+      const int32_t id = idq[row0 + lane];
+      const int32_t slot = slot_of ? slot_of[id] : -1;
+      hit = slot >= 0;
+      my_src = hit ? reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch)
+                   : reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
     }
-    for (; c < d4; c += 32) dst[c] = src[c];
+    // warp-uniform counts (lane 0 reports them, as on the wide path)
+    const unsigned hb = __ballot_sync(0xffffffffu, hit);
+    hits += __popc(hb);
+    miss += (unsigned)m - __popc(hb);
+    const unsigned long long my_addr = reinterpret_cast<unsigned long long>(my_src);
+    for (int j = 0; j < m; j += kRowsInFlight) {
+      const float4* src[kRowsInFlight];
+#pragma unroll
+      for (int u = 0; u < kRowsInFlight; ++u)
+        src[u] = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, my_addr, (j + u) & 31));
+      for (int c = lane; c < d4; c += 32) {
+        float4 v[kRowsInFlight];
+#pragma unroll
+        for (int u = 0; u < kRowsInFlight; ++u)
+          if (j + u < m) v[u] = src[u][c];
+#pragma unroll
+        for (int u = 0; u < kRowsInFlight; ++u)
+          if (j + u < m) reinterpret_cast<float4*>(outq + (row0 + j + u) * out_pitch)[c] = v[u];
+      }
+    }
   }
   if (slot_of != nullptr && lane == 0) {
     atomicAdd(&s_hits, hits);
@@ -437,7 +480,8 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
   if (mask & MQ_PREP_GATHER) {
     ProfScope ps(K_GATHER, s);
     const int warps = kGatherThreads / 32;
-    int blocks = ceil_div(last.n_src_max, warps);
+    // narrow rows: 32 rows per warp pass; wide rows: one row per warp pass
+    int blocks = ceil_div(last.n_src_max, dv4 > 32 ? warps : warps * 32);
     const int cap = ceil_div(kNumSMs * 16, Q);
     if (blocks > cap) blocks = cap;
     gather_q_kernel<<<dim3(blocks, Q), kGatherThreads, 0, s>>>(
