@@ -314,6 +314,29 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
           my_val = __ldg(&vals[me]);
         }
         const int m = min(32, e1 - eb);
+        if (S == 1) {  // one split (wide frontiers): 16 neighbour rows in flight
+          constexpr int U1 = 16;
+          for (int t0 = 0; t0 < m; t0 += U1) {
+            float2 ld[U1];
+            float val[U1];
+#pragma unroll
+            for (int u = 0; u < U1; ++u) {
+              const int32_t cu = __shfl_sync(0xffffffffu, my_col, (t0 + u) & 31);
+              val[u] = __shfl_sync(0xffffffffu, my_val, (t0 + u) & 31);
+              ld[u] = (active && t0 + u < m)
+                          ? __ldcg(reinterpret_cast<const float2*>(part + (int64_t)cu * ldy + c))
+                          : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U1; ++u) {
+              if (t0 + u < m) {
+                acc.x = fmaf(val[u], ld[u].x, acc.x);
+                acc.y = fmaf(val[u], ld[u].y, acc.y);
+              }
+            }
+          }
+          continue;
+        }
         for (int t0 = 0; t0 < m; t0 += U) {
           int32_t col[U];
           float val[U];
