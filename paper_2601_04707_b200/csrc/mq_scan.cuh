@@ -89,23 +89,34 @@ __device__ __forceinline__ void scan_tile(const Load& load, const Store& store, 
     }
     if (lane < kScanThreads / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
     int64_t agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
-    if (lane == 0) {
-      int64_t excl = 0;
-      if (tile == 0) {
-        st_relaxed(&status[0], kFlagPre | (unsigned long long)agg);
-      } else {
-        st_relaxed(&status[tile], kFlagAgg | (unsigned long long)agg);
-        int p = tile - 1;
-        while (true) {
-          unsigned long long w2 = ld_relaxed(&status[p]);
-          unsigned long long flag = w2 & ~kValMask;
-          if (flag == 0) continue;
-          excl += (int64_t)(w2 & kValMask);
-          if (flag == kFlagPre) break;
-          --p;
-        }
-        st_relaxed(&status[tile], kFlagPre | (unsigned long long)(excl + agg));
+    // decoupled look-back, a window of 32 predecessors per step (lane l reads
+    // tile p - l): stop at the nearest published inclusive prefix, re-read
+    // while a closer predecessor has published nothing yet
+    int64_t excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_relaxed(&status[0], kFlagPre | (unsigned long long)agg);
+    } else {
+      if (lane == 0) st_relaxed(&status[tile], kFlagAgg | (unsigned long long)agg);
+      int p = tile - 1;
+      while (true) {
+        const int idx = p - lane;
+        const unsigned long long w2 = idx >= 0 ? ld_relaxed(&status[idx]) : kFlagPre;
+        const unsigned long long flag = w2 & ~kValMask;
+        const unsigned pre = __ballot_sync(0xffffffffu, flag == kFlagPre);
+        const unsigned inv = __ballot_sync(0xffffffffu, flag == 0);
+        const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest prefix in the window
+        const unsigned closer = stop == 32 ? 0xffffffffu : ((1u << stop) - 1u);
+        if (inv & closer) continue;  // a nearer tile has not published yet
+        int64_t part = lane <= stop ? (int64_t)(w2 & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
+        if (stop < 32) break;
+        p -= 32;
       }
+      if (lane == 0) st_relaxed(&status[tile], kFlagPre | (unsigned long long)(excl + agg));
+    }
+    if (lane == 0) {
       s_excl = excl;
       if (base + kScanTile >= n) store.total(n, excl + agg);
     }
