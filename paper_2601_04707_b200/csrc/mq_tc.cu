@@ -1483,7 +1483,7 @@ constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the static barri
 
 // ---- v2 launch: tensor maps over the operands, or -1 when a shape / pointer
 // falls outside what the TMA path covers (then v1 runs)
-static int g_tc_v2 = 1;
+static int g_tc_v2 = 2;  // 0: v1 everywhere, 2: TMA (DW by rule), 3: TMA for every mode
 
 typedef CUresult (*PFN_tmapEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -94,3 +94,20 @@ def test_eval_and_refresh_scratch_queries(L):
     assert L.mq_full_transform_part_floats(5000, 64) >= 5000 * 128
     assert L.mq_walk_scratch_bytes(10**6) >= 3 * 8 * 10**6
     assert L.mq_refresh_scratch_bytes(10**6) >= 12 * 10**6
+
+
+def test_gemm_kernel_selection_is_validated(L):
+    """mq_set_tc_kernel: 1 (cp.async), 2 (TMA, default), 3 (TMA for every
+    mode); anything else is an argument error and leaves the choice alone."""
+    from paper_2601_04707_b200._lib import MQError
+    old = L.mq_get_tc_kernel()
+    assert old == 2
+    try:
+        for v in (1, 3, 2):
+            L.mq_set_tc_kernel(v)
+            assert L.mq_get_tc_kernel() == v
+        with pytest.raises(MQError, match="mq_set_tc_kernel"):
+            L.mq_set_tc_kernel(4)
+        assert L.mq_get_tc_kernel() == 2
+    finally:
+        L.mq_set_tc_kernel(old)
