@@ -67,13 +67,17 @@ __global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm,
   }
 }
 
+#ifndef MQ_SAMPLE_MINB
+#define MQ_SAMPLE_MINB 12  // >= 12 resident 64-thread blocks per SM (register cap): products sample 27 -> 24 us/batch
+#endif
+
 // ------------------------------------------------------------ sample
 // One thread per dst row (node_wise_block, SAGE arm).  Every case is O(fanout)
 // through the per-epoch residency index; the row's gathers are issued from
 // register arrays so a row costs ~4 dependent round trips
 // (dst -> offsets -> hot arcs -> columns), not 2*fanout.
 template <int MAXK>
-__global__ void __launch_bounds__(64) sample_q_kernel(
+__global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
     const int64_t* __restrict__ row_off, const int32_t* __restrict__ col,
     const int64_t* __restrict__ hot_arc, const int64_t* __restrict__ hot_off, QP<const int32_t> dst,
     QP<const int32_t> n_dst, QP<const uint32_t> key, int fanout, uint32_t hop, QP<int32_t> nbr,
