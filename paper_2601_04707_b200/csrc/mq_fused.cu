@@ -517,12 +517,12 @@ constexpr int kHeadThreads = 32 * kHeadRows;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
-// The scatter that follows launches at this trigger.  Measured A/B (-D
-// MQ_HEAD_LATE_TRIGGER: trigger after the dW partials): device-resident step
-// 61.1 -> 59.7 us, host-buffer (e2e) step 61.6 -> 62.3 us; e2e is the
-// headline, so the early trigger stays the default.
-#ifndef MQ_HEAD_LATE_TRIGGER
-  pdl_trigger();  // the batch's edges and labels (prep output) load before the wait
+// The scatter that follows launches at the head's trigger, issued after the
+// dW partials: scatter CTAs launched at the head's entry slowed the head more
+// than their early start saved (device step 60.2 -> 58.8 us, host-buffer
+// step 61.2 -> 59.6 us).  -DMQ_HEAD_EARLY_TRIGGER restores the entry trigger.
+#ifdef MQ_HEAD_EARLY_TRIGGER
+  pdl_trigger();
 #endif
   MQ_TL_BEGIN(6);
   htrace(0);
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
 
   htrace(6);
-#ifdef MQ_HEAD_LATE_TRIGGER
+#ifndef MQ_HEAD_EARLY_TRIGGER
   pdl_trigger();
 #endif
   // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA

@@ -402,6 +402,10 @@ class StepRunner:
         # that read it (4 groups earlier) have executed, so the host never waits
         # on the group that is about to train
         self._stage = [torch.zeros((Q, 4), dtype=torch.int32, pin_memory=True) for _ in range(4)]
+        # the group's targets, staged host-side by memcpy and sent as ONE H2D
+        # copy (per-slot tensor copies cost ~10 us of host time each)
+        self._tstage = [torch.zeros(tuple(self.groups[0].targets.shape), dtype=torch.int32,
+                                    pin_memory=True) for _ in range(4)]
         self._stage_ev = [torch.cuda.Event() for _ in range(4)]
         self._stage_i = 0
         # the step's loss commit (the head's last CTA) writes straight into this
@@ -446,16 +450,18 @@ class StepRunner:
         st = self._stage[si]
         self._stage_ev[si].synchronize()
         sv = st.numpy().view(np.uint32)
+        tv = self._tstage[si].numpy()
         for q in range(self.Q):
             if q < len(group):
                 bid, t = group[q]
-                sv[q] = (int(t.numel()), self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF,
+                tn = t.numpy()
+                tv[q, :tn.size] = tn
+                sv[q] = (tn.size, self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF,
                          bid & 0xFFFFFFFF)
             else:
                 sv[q] = (0, self.seed & 0xFFFFFFFF, self.epoch & 0xFFFFFFFF, 0)
         with torch.cuda.stream(stream):
-            for q, (bid, t) in enumerate(group):
-                grp.targets[q, :t.numel()].copy_(t, non_blocking=True)
+            grp.targets.copy_(self._tstage[si], non_blocking=True)
             grp.n_targets.copy_(st[:, 0:1], non_blocking=True)
             grp.key.copy_(st[:, 1:4], non_blocking=True)
         self._stage_ev[si].record(stream)
@@ -488,7 +494,7 @@ class StepRunner:
 
         stage_and_prep(0)
         pending = []   # (event, [batch ids]) of enqueued work whose losses are unread
-        ring = self._loss_hring
+        ring = self._loss_hring.numpy()  # pinned, device-written: a NumPy view reads it directly
         slot_of = lambda bid: ((bid & 0xFFFFFFFF) // self.world) % self.ring_len  # noqa: E731
 
         def drain(keep):
