@@ -501,11 +501,13 @@ struct HeadArgs {
 
 #ifdef MQ_TC_TRACE
 __device__ unsigned long long g_head_trace[16];
+__device__ unsigned long long g_head_cta[256][8];  // every CTA's phase times
 __device__ __forceinline__ void htrace(int i) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_head_trace[i] = t;
+    if (blockIdx.x == 0) g_head_trace[i] = t;
+    if (blockIdx.x < 256 && i < 8) g_head_cta[blockIdx.x][i] = t;
   }
 }
 #else
@@ -513,7 +515,12 @@ __device__ __forceinline__ void htrace(int) {}
 #endif
 
 constexpr int kHeadRows = 8;               // target rows per CTA: one warp per row
-constexpr int kHeadThreads = 32 * kHeadRows;
+// two warps per target row: the row phases (aggregation, CE, dt) use the
+// first kHeadRows warps, the dense phases (logits, W^T, dW partial) all of them
+// (logits 3.55 -> 2.62 us, dW partial 1.8 -> 1.2 us per CTA; spreading the dt
+// scatter over all warps as well measured slower: 3.8 -> 4.2 us)
+constexpr int kHeadWarps = 2 * kHeadRows;
+constexpr int kHeadThreads = 32 * kHeadWarps;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
@@ -539,10 +546,11 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   __shared__ double s_loss[R];
   __shared__ int s_bad;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // warp <-> row
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // warp <-> row (warp < R)
   const int n = *a.n_dst_dev;
-  const int r = blockIdx.x * R + warp;
-  const bool live = r < n;
+  const bool row_warp = warp < R;
+  const int r = blockIdx.x * R + (row_warp ? warp : 0);
+  const bool live = row_warp && r < n;
   if (tid == 0) s_bad = 0;
   // this row's edges and label first: their latency overlaps the W copy
   int e0 = 0, ne = 0, lab = -1;
@@ -555,11 +563,11 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
       ne = kHeadMaxEdges;
     }
   }
-  if (lane < ne) {
+  if (row_warp && lane < ne) {
     s_col[warp][lane] = __ldg(&a.cols[e0 + lane]);
     s_val[warp][lane] = __ldg(&a.vals[e0 + lane]);
   }
-  if (lane == 0) s_ne[warp] = ne;
+  if (row_warp && lane == 0) s_ne[warp] = ne;
   pdl_wait();  // W, h and dh come from the preceding kernels
   const bool w_async = Cp == C && ((uintptr_t)a.W & 15) == 0 && ((d2 * C) & 3) == 0;
   if (w_async) {  // same layout: 16-byte cp.async, landing while phase 1 aggregates
@@ -584,7 +592,8 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   //    nn.py:79-89); the row's gathers issued together
   {
     float* brow = both + warp * d2p;
-    if (!live) {
+    if (!row_warp) {
+    } else if (!live) {
       for (int c = lane; c < d2p; c += 32) brow[c] = 0.f;
     } else {
       __syncwarp();
@@ -658,14 +667,14 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
   // W^T (smem -> smem, conflict-free: Cp is odd) for dt = dl W^T in phase 4
   if (a.dh != nullptr) {
-    for (int c = warp; c < C; c += R)  // warp per class, lanes over k
+    for (int c = warp; c < C; c += kHeadWarps)  // warp per class, lanes over k
       for (int k = lane; k < d2p; k += 32) WsT[c * d2p + k] = Ws[k * Cp + c];
   }
   __syncthreads();
 
   htrace(3);
   // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot
-  {
+  if (row_warp) {
     float* x = dl + warp * C;
     double wloss = 0.0;
     int bad = 0;
@@ -1107,6 +1116,10 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
 #ifdef MQ_TC_TRACE
 extern "C" int mq_debug_head_trace(unsigned long long* out) {
   MQ_CUDA(cudaMemcpyFromSymbol(out, g_head_trace, sizeof(unsigned long long) * 16));
+  return MQ_OK;
+}
+extern "C" int mq_debug_head_cta(unsigned long long* out) {  // [256][8] phase times
+  MQ_CUDA(cudaMemcpyFromSymbol(out, g_head_cta, sizeof(unsigned long long) * 256 * 8));
   return MQ_OK;
 }
 #endif

@@ -21,6 +21,8 @@ exchange: [train + pack] -> f64 all-reduce of [grads | contributor count]
 
 from __future__ import annotations
 
+import gc
+
 import ctypes as C
 
 import numpy as np
@@ -480,6 +482,17 @@ class StepRunner:
         if not batches:
             return
         self.capture_host_input()
+        # the loop is host-bound at ~60 us per batch: a cyclic-GC pass over
+        # the process heap (milliseconds) would stall the device queue
+        gc_was = gc.isenabled()
+        gc.disable()
+        try:
+            yield from self._run_host_batches(batches)
+        finally:
+            if gc_was:
+                gc.enable()
+
+    def _run_host_batches(self, batches):
         Q = self.Q
         chunks = [batches[i:i + Q] for i in range(0, len(batches), Q)]
         prep_s = self.prep_stream if self.pipeline else self.stream

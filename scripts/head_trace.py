@@ -39,6 +39,17 @@ lib().dll.mq_debug_head_trace(buf)
 t = [int(x) for x in buf]
 print("head phases (us from entry):", " ".join(f"{i}:{(t[i] - t[0]) / 1e3:.2f}" for i in range(8)))
 print("  1 W/W^T staged, 2 aggregated, 3 logits, 4 CE, 5 dt atomics, 6 dW partial, 7 end")
+cta = (C.c_ulonglong * (256 * 8))()
+lib().dll.mq_debug_head_cta(cta)
+n_cta = -(-1024 // 8)
+rows = [[int(cta[8 * b + i]) for i in range(8)] for b in range(n_cta)]
+t0 = min(r[0] for r in rows)
+import statistics as _st
+print("  per-CTA phase durations (us) min / median / max over", n_cta, "CTAs; start skew",
+      f"{(max(r[0] for r in rows) - t0) / 1e3:.2f}, last end {(max(r[7] for r in rows) - t0) / 1e3:.2f}")
+for i in range(1, 8):
+    d = [(r[i] - r[i - 1]) / 1e3 for r in rows]
+    print(f"    phase {i}: {min(d):6.2f} {_st.median(d):6.2f} {max(d):6.2f}")
 
 # ---- in-step timeline of one window: first CTA entry / last CTA exit per kernel
 names = {0: "tc FWD", 1: "tc DW", 2: "tc FCAT", 3: "tc DCAT", 4: "tc DX", 5: "aggregate",
@@ -66,3 +77,13 @@ for i, (a, b) in sorted(rows.items(), key=lambda kv: kv[1][0]):
     print(f"  {names.get(i, i):10s} {(a - t0) / 1e3:7.2f} -> {(b - t0) / 1e3:7.2f} us "
           f"({(b - a) / 1e3:5.2f}){gap}")
     prev = b
+
+# ---- the in-step head's per-CTA phases (the last head launch was in-step)
+lib().dll.mq_debug_head_cta(cta)
+rows = [[int(cta[8 * b + i]) for i in range(8)] for b in range(n_cta)]
+t0 = min(r[0] for r in rows)
+print("  in-step head, per-CTA phase durations (us) min / median / max; start skew",
+      f"{(max(r[0] for r in rows) - t0) / 1e3:.2f}, last end {(max(r[7] for r in rows) - t0) / 1e3:.2f}")
+for i in range(1, 8):
+    d = [(r[i] - r[i - 1]) / 1e3 for r in rows]
+    print(f"    phase {i}: {min(d):6.2f} {_st.median(d):6.2f} {max(d):6.2f}")
