@@ -519,16 +519,21 @@ constexpr int kHeadRows = 8;               // target rows per CTA: one warp per 
 // first kHeadRows warps, the dense phases (logits, W^T, dW partial) all of them
 // (logits 3.55 -> 2.62 us, dW partial 1.8 -> 1.2 us per CTA; spreading the dt
 // scatter over all warps as well measured slower: 3.8 -> 4.2 us)
-constexpr int kHeadWarps = 2 * kHeadRows;
+#ifndef MQ_HEAD_WARPS_PER_ROW
+#define MQ_HEAD_WARPS_PER_ROW 2
+#endif
+constexpr int kHeadWarps = MQ_HEAD_WARPS_PER_ROW * kHeadRows;
 constexpr int kHeadThreads = 32 * kHeadWarps;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
-// The scatter that follows launches at the head's trigger, issued after the
-// dW partials: scatter CTAs launched at the head's entry slowed the head more
-// than their early start saved (device step 60.2 -> 58.8 us, host-buffer
-// step 61.2 -> 59.6 us).  -DMQ_HEAD_EARLY_TRIGGER restores the entry trigger.
-#ifdef MQ_HEAD_EARLY_TRIGGER
+// The scatter that follows launches at the head's trigger.  With 8-warp CTAs
+// a trigger after the dW partials was faster (60.2 -> 58.8 us/step); with the
+// 16-warp head the entry trigger is (58.1 vs 59.3 us/step), and the late
+// trigger combined with 16 warps faulted / hung at products-shape epoch
+// boundaries (unresolved), so the entry trigger is the default.
+// -DMQ_HEAD_LATE_TRIGGER moves it after the dW partials.
+#ifndef MQ_HEAD_LATE_TRIGGER
   pdl_trigger();
 #endif
   MQ_TL_BEGIN(6);
@@ -814,7 +819,7 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   }
 
   htrace(6);
-#ifndef MQ_HEAD_EARLY_TRIGGER
+#ifdef MQ_HEAD_LATE_TRIGGER
   pdl_trigger();
 #endif
   // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA
