@@ -653,9 +653,15 @@ __global__ void __launch_bounds__(kBlock, 1)
   const int Np = op.Np;
   const Work wk = choose_work(M, K, gridDim.x);
   const int items = wk.tiles_m * wk.S;
-  if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+  // the split count is published only after the wait: with programmatic
+  // dependent launch this grid may start while the previous window's optimizer
+  // still reads the same counter
+  auto publish_nparts = [&]() {
+    if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+  };
   if ((int)blockIdx.x >= items || M <= 0) {
     pdl_wait();
+    publish_nparts();
     return;
   }
 
@@ -673,6 +679,7 @@ __global__ void __launch_bounds__(kBlock, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  publish_nparts();
   const uint32_t tmem = s_tmem;
   const int stage_bytes = Smem::stage_bytes(Np);
   const uint32_t smem_base = smem_u32(smem);
@@ -1040,11 +1047,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int K = k_dev ? *k_dev : k_static;
   const int Np = op.Np;
   const Work wk = work2(MODE, geo, M, K, gridDim.x);
-  if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+  // published after the wait (see tc_gemm_kernel): the previous window's
+  // optimizer may still read this counter when the grid starts
+  auto publish_nparts = [&]() {
+    if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+  };
   const int G = (int)gridDim.x / wk.S;  // CTAs per split
   const int b = blockIdx.x;
   if (M <= 0 || b >= G * wk.S) {
     pdl_wait();
+    publish_nparts();
     return;
   }
   const int s = b % wk.S;
@@ -1057,6 +1069,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
   if (kb0 >= kb1) {  // K == 0: the partial is zero
     pdl_wait();
+    publish_nparts();
     for (int t = b / wk.S; t < wk.tiles_m; t += G)
       for (int e = tid; e < BM * op.N; e += kThreads2) {
         const int r = t * BM + e / op.N;
@@ -1085,6 +1098,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
   __syncthreads();
   tc_fence_after();
   pdl_wait();
+  publish_nparts();
   const uint32_t tmem = s_tmem;
   const int BB = b_tile_bytes(MODE, Np);
   const int SB = stage2_bytes(MODE, Np);
