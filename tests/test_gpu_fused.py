@@ -129,6 +129,24 @@ def test_fused_af_products_like_widths():
     _fused_vs_oracle(hg, (15, 10, 5), 64, 512, seed=12, windows=2, layer0="af")
 
 
+def test_fused_wide_input_layer():
+    """Reddit-like input width (602-d, pitch 604, transform-first): the
+    swapped tcgen05 weight gradient with X^T tiled over 5 feature tiles and
+    deferred split-K partials, against the oracle."""
+    rng = np.random.default_rng(31)
+    n = 4000
+    src = rng.integers(0, n, 60_000)
+    dst = (src + rng.integers(1, 500, src.size)) % n
+    keys = np.unique(np.concatenate([src * n + dst, dst * n + src]))
+    s, d = keys // n, keys % n
+    ro = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(s, minlength=n), out=ro[1:])
+    feats = rng.standard_normal((n, 602)).astype(np.float32)
+    labels = rng.integers(0, 41, n).astype(np.int32)
+    hg = HostGraph(ro, d, feats, labels, 41, rng.random(n) < 0.4)
+    _fused_vs_oracle(hg, (10, 5), 64, 512, seed=17, windows=2, layer0="tf")
+
+
 def test_fused_one_layer(golden_sampling):
     hg = make_g2(golden_sampling)
     _fused_vs_oracle(hg, (7,), 16, 128, seed=6, windows=2)
