@@ -196,3 +196,57 @@ class PrepGroup:
 
     def launch(self, desc: PrepDesc, stream: int):
         lib().mq_prep_batches(C.byref(desc), stream)
+
+    # ------------------------------------------------ host staging / read-back
+    def stage(self, batches, seed: int, epoch: int):
+        """Host-staged slot contents (the descriptor with cursor=None):
+        ``batches`` = [(batch_id, int targets)] for slots 0..len-1, the rest
+        empty (n = 0).  Synchronous; for tests and the drop-in API."""
+        import numpy as np
+        if len(batches) > self.Q:
+            raise ValueError("more batches than slots")
+        tg = np.zeros(tuple(self.targets.shape), dtype=np.int32)
+        meta = np.zeros((self.Q, 4), dtype=np.uint32)
+        for q in range(self.Q):
+            meta[q, 1:3] = (seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF)
+            if q < len(batches):
+                bid, t = batches[q]
+                t = np.asarray(t, dtype=np.int64).ravel()
+                if t.size > self.batch_size:
+                    raise ValueError("batch larger than the slot")
+                tg[q, :t.size] = t
+                meta[q, 0] = t.size
+                meta[q, 3] = bid & 0xFFFFFFFF
+        dev = self.targets.device
+        self.targets.copy_(torch.from_numpy(tg).to(dev))
+        m = torch.from_numpy(meta.view(np.int32)).to(dev)
+        self.n_targets.copy_(m[:, 0:1])
+        self.key.copy_(m[:, 1:4])
+
+    def minibatch(self, q: int, epoch: int = 0, with_features: bool = True):
+        """Slot ``q`` as a reference-shaped ``MiniBatch`` (samplers.py:49-72):
+        bottom-up blocks, targets, labels and the gathered input features,
+        copied out of the slot buffers — the parity read-back of the
+        production prep pass."""
+        from .samplers import Block, MiniBatch
+        torch.cuda.synchronize(self.targets.device)
+        dev = self.targets.device
+        n = int(self.n_targets[q, 0])
+        counts = torch.stack([hb.counts[q] for hb in self.hops]).cpu().numpy()
+        tg = self.targets[q, :n].clone()
+        blocks, nd, dst = [], n, tg
+        for h, hb in enumerate(self.hops):
+            n_src, nnz = int(counts[h, 0]), int(counts[h, 1])
+            blk = Block(rows=hb.rows[q, :nnz].clone(), cols=hb.cols[q, :nnz].clone(),
+                        values=hb.vals[q, :nnz].clone(), src_ids=hb.src_ids[q, :n_src].clone(),
+                        dst_ids=dst, row_ptr=hb.row_ptr[q, :nd + 1].clone(),
+                        dst_in_src=torch.arange(nd, device=dev, dtype=torch.int32))
+            blocks.append(blk)
+            dst, nd = blk.src_ids, n_src
+        blocks.reverse()
+        n_in = int(counts[-1, 0])
+        feats = (self.x0[q, :n_in, :self.graph.feature_dim].clone() if with_features else None)
+        bid = int(self.key[q, 2].item()) & 0xFFFFFFFF
+        return MiniBatch(batch_id=bid, epoch=epoch, target_ids=tg,
+                         target_labels=self.labels[q, :n].clone(), layers=tuple(blocks),
+                         input_ids=blocks[0].src_ids, features=feats)
