@@ -351,7 +351,12 @@ int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_
  * all-reduced contributor count packed by mq_pack_grads (expected[k],
  * runtime.py:115-116).  step_dev is incremented on device; bias[2*(t-1)],
  * bias[2*(t-1)+1] hold float32(1 - 0.9**t), float32(1 - 0.999**t) for
- * t = 1..bias_len; lr is float32(learning_rate).  nonfinite[0] |= 1 on a
+ * t = 1..bias_len; steps past bias_len read the last row, which is exact
+ * when the table reaches the saturated (1.0f, 1.0f) row (bias_len >= 17,400;
+ * the Python side allocates 65,536 once and never reallocates it, so captured
+ * graphs keep a valid pointer).  lr points at float32(learning_rate) in
+ * device memory, read by every launch (a captured step follows
+ * ModelState.learning_rate changes).  nonfinite[0] |= 1 on a
  * non-finite weight.  step_dev points at TWO int32: [0] the update count t,
  * [1] an arrival counter that must be 0 at rest (the launch's last CTA
  * publishes t+1 and resets it, so the bump costs no extra launch).  With
@@ -359,11 +364,11 @@ int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_
  * split-K segments (mq_grad_src). */
 int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
             double grad_scale, int64_t n, int32_t* step_dev, const float* bias,
-            int32_t bias_len, float lr, int32_t* nonfinite, const mq_grad_src* src,
+            int32_t bias_len, const float* lr, int32_t* nonfinite, const mq_grad_src* src,
             void* stream);
-/* sgd_step (nn.py:209-215) */
+/* sgd_step (nn.py:209-215); lr as in mq_adam (device float32) */
 int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale,
-           int64_t n, int32_t* step_dev, float lr, int32_t* nonfinite,
+           int64_t n, int32_t* step_dev, const float* lr, int32_t* nonfinite,
            const mq_grad_src* src, void* stream);
 /* out64[i] = (double)grad[i] for i < n and out64[n] = (n_targets_dev[0] > 0):
  * one f64 buffer carries the window's gradient sum and contributor count

@@ -60,8 +60,8 @@ SIGNATURES = {
                                      P, P]),
     "mq_softmax_ce": (C.c_int, [P, I32, P, P, I32, I32, P, I32, P, P, P]),
     "mq_gather_labels": (C.c_int, [P, P, P, I32, P, P]),
-    "mq_adam": (C.c_int, [P, P, P, P, P, F64, I64, P, P, I32, F32, P, P, P]),
-    "mq_sgd": (C.c_int, [P, P, P, F64, I64, P, F32, P, P, P]),
+    "mq_adam": (C.c_int, [P, P, P, P, P, F64, I64, P, P, I32, P, P, P, P]),
+    "mq_sgd": (C.c_int, [P, P, P, F64, I64, P, P, P, P, P]),
     "mq_f32_to_f64": (C.c_int, [P, P, I64, P]),
     "mq_pack_grads": (C.c_int, [P, I64, P, P, P, P]),
     "mq_grad_reduce": (C.c_int, [P, P, I64, P, P]),

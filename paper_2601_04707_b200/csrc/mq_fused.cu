@@ -522,6 +522,9 @@ constexpr int kHeadRows = 8;               // target rows per CTA: one warp per 
 #ifndef MQ_HEAD_WARPS_PER_ROW
 #define MQ_HEAD_WARPS_PER_ROW 2
 #endif
+#if defined(MQ_HEAD_LATE_TRIGGER) && MQ_HEAD_WARPS_PER_ROW > 1
+#error "MQ_HEAD_LATE_TRIGGER with the multi-warp head faulted intermittently (DESIGN.md 7b): unsupported"
+#endif
 constexpr int kHeadWarps = MQ_HEAD_WARPS_PER_ROW * kHeadRows;
 constexpr int kHeadThreads = 32 * kHeadWarps;
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets

@@ -147,19 +147,24 @@ __device__ __forceinline__ bool adam_elem(float* __restrict__ w, float* __restri
 __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
                             const float* __restrict__ g32, const double* __restrict__ g64,
                             double scale, int64_t n, int32_t* __restrict__ step,
-                            const float* __restrict__ bias, int bias_len, float lr,
+                            const float* __restrict__ bias, int bias_len,
+                            const float* __restrict__ lr_dev,
                             int32_t* __restrict__ nonfinite, GradSrc src, int coop_seg,
                             int coop_blocks) {
   MQ_PDL_ENTRY();
   MQ_TL_BEGIN(8);
   __shared__ float red[8][33];
   const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
-  if (t < 1 || t > bias_len) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // bias table exhausted
+  if (t < 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // step counter wrapped
     step_arrive(step, t);
     return;
   }
-  const float bc1 = bias[2 * (t - 1)], bc2 = bias[2 * (t - 1) + 1];
+  // the table ends at float32(1 - beta**t) == 1.0f for both betas (t > ~17.3k),
+  // so every later step reads its last row exactly (mqgnn.h mq_adam)
+  const int tb = t < bias_len ? t : bias_len;
+  const float bc1 = bias[2 * (tb - 1)], bc2 = bias[2 * (tb - 1) + 1];
+  const float lr = *lr_dev;  // float32(learning_rate), read per launch (graph replays follow it)
   const double count = grad_count(g64, scale, n);
   int bad = 0;
   int64_t c_lo = 0, c_hi = 0;  // flat range of the cooperative segment
@@ -208,11 +213,13 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
 }
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g32,
-                           const double* __restrict__ g64, double scale, int64_t n, float lr,
+                           const double* __restrict__ g64, double scale, int64_t n,
+                           const float* __restrict__ lr_dev,
                            int32_t* __restrict__ step, int32_t* __restrict__ nonfinite,
                            GradSrc src) {
   MQ_PDL_ENTRY();
   const int t = step[0] + 1;
+  const float lr = *lr_dev;
   const double count = grad_count(g64, scale, n);
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -308,8 +315,9 @@ int mq_softmax_ce(const float* logits, int32_t ld, const int32_t* labels, const 
 
 int mq_adam(float* w, float* m, float* v, const float* grad32, const double* grad64,
             double grad_scale, int64_t n, int32_t* step_dev, const float* bias, int32_t bias_len,
-            float lr, int32_t* nonfinite, const mq_grad_src* src, void* stream) {
-  MQ_CHECK_ARG(w && m && v && step_dev && bias && nonfinite, "mq_adam: null pointer");
+            const float* lr, int32_t* nonfinite, const mq_grad_src* src, void* stream) {
+  MQ_CHECK_ARG(w && m && v && step_dev && bias && lr && nonfinite, "mq_adam: null pointer");
+  MQ_CHECK_ARG(bias_len >= 1, "mq_adam: empty bias-correction table");
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_adam: exactly one gradient source");
   MQ_CHECK_ARG(src_ok(src), "mq_adam: bad deferred gradient source");
   cudaStream_t s = as_stream(stream);
@@ -336,8 +344,9 @@ int mq_adam(float* w, float* m, float* v, const float* grad32, const double* gra
 }
 
 int mq_sgd(float* w, const float* grad32, const double* grad64, double grad_scale, int64_t n,
-           int32_t* step_dev, float lr, int32_t* nonfinite, const mq_grad_src* src, void* stream) {
-  MQ_CHECK_ARG(w && step_dev && nonfinite, "mq_sgd: null pointer");
+           int32_t* step_dev, const float* lr, int32_t* nonfinite, const mq_grad_src* src,
+           void* stream) {
+  MQ_CHECK_ARG(w && step_dev && lr && nonfinite, "mq_sgd: null pointer");
   MQ_CHECK_ARG((grad32 == nullptr) != (grad64 == nullptr), "mq_sgd: exactly one gradient source");
   MQ_CHECK_ARG(src_ok(src), "mq_sgd: bad deferred gradient source");
   cudaStream_t s = as_stream(stream);

@@ -132,6 +132,10 @@ class DeviceModel:
         n = self.offsets[-1]
         self.num_params = n
         self.device = device
+        # float32(learning_rate) in device memory: the optimizer kernels read it
+        # per launch, so captured step graphs follow learning-rate changes
+        self.lr_dev = torch.zeros(1, dtype=torch.float32, device=device)
+        self._lr = None
         self.learning_rate = float(learning_rate)
         self.flat_w = torch.zeros(n, dtype=torch.float32, device=device)
         self.flat_m = torch.zeros(n, dtype=torch.float32, device=device)
@@ -146,22 +150,29 @@ class DeviceModel:
         # [update count t, optimizer arrival counter] (mqgnn.h mq_adam)
         self.step_dev = torch.tensor([step_count, 0], dtype=torch.int32, device=device)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=device)
-        self.bias_len = 0
-        self.bias = None
-        self.ensure_bias(max(bias_len, step_count + 1))
+        self.bias, self.bias_len = _bias_table(max(bias_len, BIAS_SATURATED), device)
         self.host_steps = step_count
 
     def ensure_bias(self, steps: int):
-        """float32(1 - beta1**t), float32(1 - beta2**t) for t = 1..steps, computed
-        with Python floats exactly as nn.py:202-203 does."""
-        if steps <= self.bias_len:
-            return
-        t = np.arange(1, steps + 1, dtype=np.float64)
-        tab = np.empty((steps, 2), dtype=np.float32)
-        tab[:, 0] = np.array([1 - 0.9 ** int(k) for k in t], dtype=np.float64).astype(np.float32)
-        tab[:, 1] = np.array([1 - 0.999 ** int(k) for k in t], dtype=np.float64).astype(np.float32)
-        self.bias = torch.as_tensor(tab.reshape(-1), device=self.device)
-        self.bias_len = steps
+        """The bias-correction table is allocated once and never replaced:
+        captured graphs hold its pointer.  It ends at the saturated row
+        (1.0f, 1.0f), which the kernel reads for every later step — exactly
+        float32(1 - beta**t) there (mqgnn.h mq_adam)."""
+        return None
+
+    @property
+    def learning_rate(self) -> float:
+        return self._lr
+
+    @learning_rate.setter
+    def learning_rate(self, lr: float):
+        lr = float(lr)
+        if lr != self._lr:
+            self._lr = lr
+            # synchronous: graphs replayed later on any stream read the new value
+            self.lr_dev.fill_(float(np.float32(lr)))
+            if self.lr_dev.is_cuda:
+                torch.cuda.synchronize(self.lr_dev.device)
 
     def view(self, flat, i):
         a, b = self.shapes[i]
@@ -180,6 +191,24 @@ class DeviceModel:
     @property
     def lr32(self) -> float:
         return float(np.float32(self.learning_rate))
+
+
+# float32(1 - 0.999**t) == 1.0f from t ~ 17.3k on; past this length both
+# columns are exactly 1.0f, so clamping t to the last row is exact
+BIAS_SATURATED = 1 << 16
+
+
+def _bias_table(steps: int, device):
+    """float32(1 - beta1**t), float32(1 - beta2**t) for t = 1..steps, computed
+    with Python floats exactly as nn.py:202-203 does."""
+    tab = np.empty((steps, 2), dtype=np.float32)
+    tab[:, 0] = np.array([1 - 0.9 ** k for k in range(1, steps + 1)],
+                         dtype=np.float64).astype(np.float32)
+    tab[:, 1] = np.array([1 - 0.999 ** k for k in range(1, steps + 1)],
+                         dtype=np.float64).astype(np.float32)
+    if not (tab[-1] == 1.0).all():
+        raise ValueError("bias table must reach the saturated (1, 1) row")
+    return torch.as_tensor(tab.reshape(-1), device=device), steps
 
 
 def _t(a, device):
@@ -314,10 +343,10 @@ class TrainWorkspace:
         if optimizer == "adam":
             lib().mq_adam(ptr(model.flat_w), ptr(model.flat_m), ptr(model.flat_v), g32, g64, scale,
                           model.num_params, ptr(model.step_dev), ptr(model.bias), model.bias_len,
-                          model.lr32, ptr(model.nonfinite), psrc, stream)
+                          ptr(model.lr_dev), ptr(model.nonfinite), psrc, stream)
         elif optimizer == "sgd":
             lib().mq_sgd(ptr(model.flat_w), g32, g64, scale, model.num_params,
-                         ptr(model.step_dev), model.lr32, ptr(model.nonfinite), psrc, stream)
+                         ptr(model.step_dev), ptr(model.lr_dev), ptr(model.nonfinite), psrc, stream)
         else:
             raise ValueError(f"unknown optimizer {optimizer!r}")
 

@@ -113,7 +113,7 @@ def _check(state: ModelState, name: str):
         raise FloatingPointError(f"{name} contains NaN or Inf")
     if flag & 2:
         state.dev.nonfinite.zero_()
-        raise RuntimeError("Adam bias-correction table exhausted")
+        raise RuntimeError("optimizer step counter overflow")
 
 
 def _finite_or_raise(name, t):
@@ -237,7 +237,7 @@ def adam_step(state: ModelState, grads: list) -> ModelState:
     d = state.dev
     d.ensure_bias(d.host_steps + 1)
     lib().mq_adam(ptr(d.flat_w), ptr(d.flat_m), ptr(d.flat_v), ptr(d.flat_g), None, 1.0,
-                  d.num_params, ptr(d.step_dev), ptr(d.bias), d.bias_len, d.lr32,
+                  d.num_params, ptr(d.step_dev), ptr(d.bias), d.bias_len, ptr(d.lr_dev),
                   ptr(d.nonfinite), None, current_stream(d.device))
     d.host_steps += 1
     _check(state, "adam_step")
@@ -247,7 +247,7 @@ def adam_step(state: ModelState, grads: list) -> ModelState:
 def sgd_step(state: ModelState, grads: list) -> ModelState:
     _flat_grad(state, grads)
     d = state.dev
-    lib().mq_sgd(ptr(d.flat_w), ptr(d.flat_g), None, 1.0, d.num_params, ptr(d.step_dev), d.lr32,
+    lib().mq_sgd(ptr(d.flat_w), ptr(d.flat_g), None, 1.0, d.num_params, ptr(d.step_dev), ptr(d.lr_dev),
                  ptr(d.nonfinite), None, current_stream(d.device))
     d.host_steps += 1
     _check(state, "sgd_step")

@@ -133,8 +133,12 @@ def batch_rng(config: PipelineConfig, epoch: int, batch_id: int) -> PhiloxStream
 
 def transfer_stage(batch, cache, g, transfer_model=None, rng=None):
     """Serve cached rows from HBM, misses from the store (runtime.py:127-143).
-    Returns (batch, miss_bytes) — the bytes that crossed the host link when
-    the store is pinned host memory."""
+
+    Returns ``(batch, delay_ms)`` like the reference: ``delay_ms`` is the
+    reference transfer model's price of the miss bytes
+    (``transfer_model.delay_ms(miss_bytes, rng)``, timing.py:86-94) or 0.0.
+    The bytes that crossed the host link (misses, when the store is pinned
+    host memory) are left on ``batch.miss_bytes``."""
     ids = batch.input_ids
     if cache is not None:
         hit = cache.cached_mask[ids.long()]
@@ -144,7 +148,9 @@ def transfer_stage(batch, cache, g, transfer_model=None, rng=None):
     else:
         miss_rows = int(ids.numel())
     batch.features = gather_features(cache, g, ids, count_hits=cache is not None).clone()
-    return batch, miss_rows * g.feature_dim * 4
+    batch.miss_bytes = miss_rows * g.feature_dim * 4
+    delay = float(transfer_model.delay_ms(batch.miss_bytes, rng)) if transfer_model else 0.0
+    return batch, delay
 
 
 def _distributed():

@@ -128,6 +128,7 @@ class MiniBatch:
     cache_misses: int = 0
     dropped_targets: int = 0
     method: str = "sage"
+    miss_bytes: int = 0  # feature bytes served from the (host) store by transfer_stage
 
     def digest(self) -> str:
         """Same SHA-256 as the reference (samplers.py:63-72) over int64 ids,

@@ -35,6 +35,23 @@ from .prep import PrepGroup, PrepShared
 DEFAULT_QUEUE_DEPTH = 8  # measured best on B200 (autotune.auto_queue_depth: 2 < 4 < 8)
 
 
+def raise_device_flag(dm):
+    """Raise for the device status word the step kernels set (and clear it):
+    bit 0 a non-finite loss / weight (nn.py:74-76), bit 1 an optimizer step
+    counter overflow, bit 2 a block row longer than MQ_MAX_FANOUT (structural,
+    the head truncated it)."""
+    flag = int(dm.nonfinite.item())
+    if not flag:
+        return
+    dm.nonfinite.zero_()
+    if flag & 4:
+        raise ValueError("a sampled block row has more edges than the fused head supports "
+                         "(MQ_MAX_FANOUT): the fanout is too large for the fused step")
+    if flag & 2:
+        raise RuntimeError("optimizer step counter overflow")
+    raise FloatingPointError("training step produced NaN or Inf")
+
+
 class StepRunner:
     """Per-iteration path for one replica on one GPU."""
 
@@ -384,12 +401,7 @@ class StepRunner:
 
     def check_finite(self):
         self.stream.synchronize()
-        flag = int(self.dm.nonfinite.item())
-        if flag:
-            self.dm.nonfinite.zero_()
-            if flag & 2:
-                raise RuntimeError("Adam bias-correction table exhausted")
-            raise FloatingPointError("training step produced NaN or Inf")
+        raise_device_flag(self.dm)
 
     # ------------------------------------------------- host-input (e2e) path
     def capture_host_input(self):
@@ -550,6 +562,7 @@ class StepRunner:
             self.ev_train[gi].record(self.stream)
             yield from drain(1)
         yield from drain(0)
+        raise_device_flag(self.dm)
 
     def step_from_host(self, targets_pinned: torch.Tensor, batch_id: int) -> float:
         """Single synchronous step from one host batch."""
