@@ -80,6 +80,10 @@ def parse():
                     help="input layer transform-first / aggregate-first")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="prep and train on one stream (no multi-queue overlap)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "collective"],
+                    help="N > 1: RaCoM over peer memory (in-graph) or a host-issued all-reduce")
+    ap.add_argument("--staleness", type=int, default=0, choices=[0, 1],
+                    help="N > 1 peer exchange: 0 parity schedule, 1 pipelined (one-window stale)")
     return ap.parse_args()
 
 
@@ -303,23 +307,56 @@ def run_reference_arm(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: start N ranks, one per GPU, with
+    the torchrun environment (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*)."""
+    import torch
+    import torch.multiprocessing as mp
+    share = os.environ.get("MQ_DIST_BACKEND") == "gloo"
+    if not share and torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but {torch.cuda.device_count()} CUDA "
+                                   f"device(s) visible (MQ_DIST_BACKEND=gloo shares one GPU "
+                                   f"for a functional run)"}), flush=True)
+        return 2
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.start_processes(_spawned_rank, args=(args, port), nprocs=args.gpus, join=True,
+                       start_method="spawn")
+    return 0
+
+
+def _spawned_rank(rank, args, port):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(args.gpus),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     rank, world, local = env_rank()
     if world != args.gpus:
-        args.gpus = world
-    # one GPU per rank (NCCL); MQ_DIST_BACKEND=gloo lets ranks share GPUs
-    # (a functional multi-rank check on a single-GPU box, not a perf setup)
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank; MQ_DIST_BACKEND=gloo lets ranks share GPUs (a
+    # functional multi-rank check on a single-GPU box, not a perf setup)
+    share = os.environ.get("MQ_DIST_BACKEND") == "gloo"
+    if not share and world > torch.cuda.device_count():
+        raise SystemExit(f"{world} ranks but {torch.cuda.device_count()} GPUs")
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        backend = os.environ.get("MQ_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+        # host plumbing only (handle exchange, barriers, the max over ranks):
+        # the data path is the peer-memory exchange inside the step graphs
+        if share:
+            dist.init_process_group("gloo")
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2601_04707_b200 as mq
     from paper_2601_04707_b200._lib import lib
     from paper_2601_04707_b200.runtime import epoch_permutation
@@ -370,10 +407,19 @@ def run_ours(args):
         args.queue_depth = queue_choice.depth
     elif args.queue_depth is not None:
         args.queue_depth = int(args.queue_depth)
+    fx, exchange_kind = None, None
+    if world > 1:
+        peer_ok = args.exchange == "peer" and (share or all(
+            torch.cuda.can_device_access_peer(local, q) for q in range(world) if q != local))
+        if peer_ok:  # RaCoM publish/apply over NVLink peer memory, inside the graphs
+            fx = mq.PeerExchange(model.dev.num_params, dev, lag=args.staleness, ring=4)
+            exchange_kind = f"peer memory (NVLink P2P), staleness {args.staleness}"
+        else:
+            exchange_kind = "torch.distributed all_reduce (f64), host-issued"
     runner = mq.StepRunner(g, model, fanouts=fanouts, batch_size=args.batch, num_train=n_train,
                            cache=cache, optimizer="adam", seed=args.seed, world=world, rank=rank,
                            multi=world > 1, queue_depth=args.queue_depth,
-                           pipeline=not args.no_pipeline, layer0=args.layer0)
+                           pipeline=not args.no_pipeline, layer0=args.layer0, exchange=fx)
     exchange = mq.DistExchange() if world > 1 else None
     driver = mq.WindowDriver([runner], exchange, sync_period=1)
     t0 = time.perf_counter()
@@ -390,10 +436,11 @@ def run_ours(args):
         left = n
         while left > 0:
             if runner.windows_done >= windows:
+                runner.finish()  # a lagged exchange applies its held-back window
                 epoch[0] += 1
                 runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
             k = runner.windows_done
-            if world == 1:
+            if world == 1 or fx is not None:  # whole slot groups as one graph each
                 done = runner.steps(left, windows)
             else:  # replicas start identical (same init) and apply the same
                 # all-reduced window, so the per-window model average is the
@@ -455,27 +502,41 @@ def run_ours(args):
                 "flops_per_launch": rec.get("flops"), "tflops": rec.get("tflops"),
             }
         per_kernel["_counts"] = tab["counts"]
+    if world > 1:  # the other ranks' next steps wait on rank 0's exchange
+        dist.barrier()
     # ----------------------------- e2e through the host-buffer entry point ---
     e2e = None
-    if world == 1:
+    if world == 1 or fx is not None:
+        if fx is not None:  # epoch boundary: nothing held back by a lagged exchange
+            runner.finish()
         runner.capture_host_input()
         perm_e2e = epoch_permutation(g.train_mask, args.seed, 100)
         B = args.batch
-        nb = min(args.e2e_steps, len(perm_e2e) // B)
-        host_batches = [(j, torch.from_numpy(perm_e2e[j * B:(j + 1) * B].astype(np.int32))
+        # the round-robin deal (runtime.py:111-113): this rank's batches j = rank, rank + N, ...
+        nb = min(args.e2e_steps, len(perm_e2e) // (B * world))
+        host_batches = [(j * world + rank,
+                         torch.from_numpy(perm_e2e[(j * world + rank) * B:
+                                                   (j * world + rank + 1) * B].astype(np.int32))
                          .pin_memory()) for j in range(nb)]
         for _ in runner.run_host_batches(host_batches[:5]):
             pass
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0.record(runner.stream)
         seeds = 0
-        for bid, _loss in runner.run_host_batches(host_batches):
-            seeds += int(host_batches[bid][1].numel())
+        for _bid, _loss in runner.run_host_batches(host_batches):
+            pass
+        seeds = sum(int(t.numel()) for _, t in host_batches) * world
         e1.record(runner.stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
         e2e = {"value": seeds / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * B + 16,
                "d2h_bytes_per_step": 8, "steps": nb, "ms_per_step": e2e_ms / nb,
                "entry": "StepRunner.run_host_batches (per batch: pinned targets H2D, graph, loss D2H)"}
@@ -568,6 +629,7 @@ def run_ours(args):
                        "hidden": args.hidden, "cache_fraction": args.cache_fraction,
                        "optimizer": "adam", "feature_placement": args.feature_placement,
                        "parallelism": f"dp{world} (RaCoM sync P=1)" if world > 1 else "dp1",
+                       "exchange": exchange_kind,
                        "l2": "inputs larger than L2 (CSR+features ~1.1 GB), no flush",
                        "cuda_graph": True, "queue_depth": runner.Q,
                        "pdl": bool(lib().mq_get_pdl()), "pipeline": runner.pipeline,
@@ -595,6 +657,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # no launcher: spawn the ranks
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -535,6 +535,63 @@ int mq_narrow_cols(const unsigned long long* cols64, int64_t m, int64_t n_nodes,
                    int32_t* bad_dev, void* stream);
 int mq_degree_buckets(const int64_t* row_off, int64_t n_nodes, int32_t* bucket, void* stream);
 
+/* ------------------------------------------------- RaCoM over peer memory
+ * share_gradient + Accumulator + apply_update (racom.py:36-87, 142-184;
+ * runtime.py:167-195) as two stream-ordered kernels per window, with no host
+ * synchronisation and no collective library on the data path, so a
+ * multi-rank window is capturable into a CUDA graph.  Every rank owns an
+ * arena (mq_peer_alloc: cudaMalloc, zeroed) holding
+ *   [0, 64)            flags: u64 per source rank — windows that rank has
+ *                      published, written remotely by that rank
+ *   [64, 128)          counters: u64 [published, applied]
+ *   [256, ...)         ring x (n + 1) f32 gradient slots: [grads | contributor]
+ *                      (each slot padded to 256 B; the packets are f32 as in
+ *                      the reference, the f64 accumulation happens on apply)
+ * exported to the other ranks with mq_ipc_export / mq_ipc_open (NVLink P2P
+ * mappings across GPUs; a plain alias within one process).
+ *
+ * mq_racom_publish: window k = counters[published]: the resolved f32 window
+ *   gradient (grad32 through the deferred split-K segments src, as mq_adam)
+ *   is written to this rank's slot k % ring with the contributor flag
+ *   (n_targets_dev[0] > 0), then flags[rank] = k + 1 is stored (release,
+ *   system scope) into EVERY rank's arena.
+ * mq_racom_apply: if published - applied > lag, window k = applied is
+ *   applied: wait (acquire, system scope; bounded by timeout_ns, 0 = 30 s)
+ *   until every rank has published k + 1 windows, form the Accumulator's f64
+ *   running mean over the contributing ranks in rank order
+ *   (mean += (g_q - mean) / count, racom.py:47-57 — the reference's serial
+ *   arrival order, so the mean is bit-identical to its Accumulator), cast to
+ *   f32 (nn.py:197) and run the Adam / SGD update of mq_adam / mq_sgd.
+ *   lag = 0: parity schedule (apply the window just published); lag = 1:
+ *   pipelined schedule (window k applied after window k+1's backward, so
+ *   every gradient misses exactly one update).  A timed-out wait sets
+ *   nonfinite[0] |= 8 and skips the update.
+ * Both kernels size their grid to stay co-resident (<= one CTA per SM). */
+#define MQ_MAX_PEERS 8
+#define MQ_PEER_HEADER_BYTES 256
+typedef struct mq_ipc_handle { char bytes[64]; } mq_ipc_handle;
+typedef struct mq_peer_exchange {
+  int32_t world, rank, ring, pad_;
+  int64_t n;                     /* gradient elements per slot (+1 contributor flag) */
+  int64_t timeout_ns;            /* bound on the apply wait; 0 = 30 s */
+  char* arena[MQ_MAX_PEERS];     /* every rank's arena, mapped into this process */
+} mq_peer_exchange;
+int64_t mq_peer_arena_bytes(int64_t n, int32_t ring);
+int mq_peer_alloc(int64_t bytes, void** out);
+int mq_peer_free(void* p);
+int mq_ipc_export(void* dev_ptr, mq_ipc_handle* out);
+int mq_ipc_open(const mq_ipc_handle* h, void** out);
+int mq_ipc_close(void* p);
+int mq_racom_publish(const mq_peer_exchange* ex, const float* grad32, const mq_grad_src* src,
+                     const int32_t* n_targets_dev, void* stream);
+int mq_racom_apply(const mq_peer_exchange* ex, int32_t optimizer /* 0 adam, 1 sgd */,
+                   int32_t lag, float* w, float* m, float* v, int32_t* step_dev,
+                   const float* bias, int32_t bias_len, const float* lr, int32_t* nonfinite,
+                   void* stream);
+/* counters[0..1] and the flag words of this rank's arena, read back (tests) */
+int mq_peer_state(const mq_peer_exchange* ex, unsigned long long* out4 /* pub, applied, min flag, max flag */,
+                  void* stream);
+
 /* ------------------------------------------------------------- utilities */
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): the step's
  * pinned-host result read-back as a node of a captured graph. */

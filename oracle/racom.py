@@ -80,8 +80,14 @@ def compute_sync_period(num_nodes, num_edges, num_devices, scale_k=1.0):
 
 def run_epoch_serial(graph, models, *, fanouts, batch_size, seed, epoch,
                      optimizer="adam", sync_period=1, cached_mask=None,
-                     capture_weights=False):
-    """Zero-delay serial schedule; returns (losses{bid: loss}, weight_traces)."""
+                     capture_weights=False, staleness=0):
+    """Zero-delay serial schedule; returns (losses{bid: loss}, weight_traces).
+
+    staleness=1 is the pipelined RaCoM schedule (the threaded
+    reference's one-window run-ahead, runtime.py:489-511, made deterministic):
+    window k's gradients are computed before window k-1's mean is applied,
+    so every gradient misses exactly one update; the last window is applied
+    at the epoch barrier.  Milestone syncs count processed windows."""
     G = len(models)
     per_device, expected = plan_epoch(graph["train_mask"], G, batch_size, seed,
                                       epoch)
@@ -90,6 +96,7 @@ def run_epoch_serial(graph, models, *, fanouts, batch_size, seed, epoch,
     traces = {d: [] for d in range(G)}
     applied = 0
     milestone = sync_period
+    pending = None
     for k in range(len(expected)):
         acc = RunningMean()
         for d in range(G):
@@ -106,14 +113,22 @@ def run_epoch_serial(graph, models, *, fanouts, batch_size, seed, epoch,
             losses[bid] = loss
             acc.add(grads)
         assert acc.count == expected[k]
-        for d in range(G):
-            step(models[d], acc.mean)
-            if capture_weights:
-                traces[d].append((k, [w.copy() for w in models[d].weights]))
+        if staleness:
+            ready, pending = pending, acc.mean
+        else:
+            ready = acc.mean
+        if ready is not None:
+            for d in range(G):
+                step(models[d], ready)
+                if capture_weights:
+                    traces[d].append((k, [w.copy() for w in models[d].weights]))
         applied += 1
         if applied >= milestone:
             sync_models(models)
             milestone += sync_period
+    if staleness and pending is not None:
+        for d in range(G):
+            step(models[d], pending)
     if G > 1:
         sync_models(models)
     return losses, traces

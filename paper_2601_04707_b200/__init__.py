@@ -19,7 +19,8 @@ from .racom import (DistExchange, LocalExchange, WindowDriver, apply_update, com
 from .pipeline import STAGES, PipelineStopped, PipelineTimeout, Trace, TraceEvent, utilization
 from .runtime import (EpochStats, PipelineConfig, batch_rng, plan_epoch, run_epoch,
                       transfer_stage)
-from .trainer import StepRunner
+from .trainer import PeerTimeout, StepRunner
+from .peer import PeerExchange
 from .autotune import (AutotuneError, auto_queue_depth, compute_cap, compute_queue_size,
                        steady_slice)
 

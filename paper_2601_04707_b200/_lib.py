@@ -127,6 +127,15 @@ SIGNATURES = {
     "mq_prof_kernel_name": (C.c_char_p, [C.c_int]),
     "mq_prof_read": (C.c_int, [P, P, I32]),
     "mq_launch_count": (I64, []),
+    "mq_peer_arena_bytes": (I64, [I64, I32]),
+    "mq_peer_alloc": (C.c_int, [I64, P]),
+    "mq_peer_free": (C.c_int, [P]),
+    "mq_ipc_export": (C.c_int, [P, P]),
+    "mq_ipc_open": (C.c_int, [P, P]),
+    "mq_ipc_close": (C.c_int, [P]),
+    "mq_racom_publish": (C.c_int, [P, P, P, P, P]),
+    "mq_racom_apply": (C.c_int, [P, I32, I32, P, P, P, P, P, I32, P, P, P]),
+    "mq_peer_state": (C.c_int, [P, P, P]),
 }
 
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()

@@ -54,7 +54,9 @@
   X(K_SAGE_AF, "sage_linear_af")                \
   X(K_SAGE_AF_REDUCE, "sage_linear_af_reduce")  \
   X(K_SAGE_AF_DW, "sage_linear_af_dw")          \
-  X(K_INGEST, "ingest")
+  X(K_INGEST, "ingest")                         \
+  X(K_RACOM_PUBLISH, "racom_publish")           \
+  X(K_RACOM_APPLY, "racom_apply")
 
 namespace mq {
 enum KernelId {

@@ -223,10 +223,13 @@ class WindowDriver:
         applied = 0
         milestone = self.sync_period
         sync_count = 0
+        # runners whose window already contains the exchange (peer memory,
+        # peer.PeerExchange) need no host-issued reduction
+        fused = all(getattr(r, "fx", None) is not None for r in self.runners)
         for k in range(total_windows):
             for r in self.runners:
                 r.compute_window()
-            if self.total_replicas > 1:
+            if self.total_replicas > 1 and not fused:
                 self._reduce([r.grad64 for r in self.runners])
             for r in self.runners:
                 r.apply_window()
@@ -238,6 +241,10 @@ class WindowDriver:
                     self.sync()
                 milestone += self.sync_period
                 sync_count += 1
+        for r in self.runners:  # the pipelined schedule's held-back window
+            fin = getattr(r, "finish", None)
+            if fin is not None:
+                fin()
         epoch_sync = 0
         if self.total_replicas > 1:
             self.sync()

@@ -57,6 +57,14 @@ class PipelineConfig:
     pipeline: bool = True   # prep of batch k+1 overlaps training of batch k
     fused_step: bool = True  # transform-first fused SAGE step (mq_fused.cu)
     elide_syncs: bool = True  # skip model averages of provably identical replicas (exact)
+    # gradient exchange of multi-process runs: "peer" = fused publish/apply
+    # kernels over NVLink peer memory (peer.PeerExchange, graph-captured),
+    # "collective" = host-issued torch.distributed all-reduce; "auto" = peer
+    exchange: str = "auto"
+    # 0: the reference's serial parity schedule (window k applied before
+    # batch k+1); 1: pipelined RaCoM, window k applied after batch k+1's
+    # backward (every gradient misses exactly one update)
+    staleness: int = 0
 
     def validate(self) -> None:
         if self.num_devices < 1:
@@ -75,9 +83,10 @@ class PipelineConfig:
             raise NotImplementedError("the device runtime trains GraphSAGE node-wise batches")
         if self.timing_mode != "real" or self.stage_durations:
             raise NotImplementedError("simulated stage timings belong to the reference simulator")
-        dm = self.delay_model
-        if dm is not None and getattr(dm, "kind", "none") != "none":
-            raise NotImplementedError("gradient delay injection is not modelled on devices")
+        if self.exchange not in ("auto", "peer", "collective"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
+        if self.staleness not in (0, 1):
+            raise ValueError("staleness must be 0 (parity) or 1 (pipelined)")
 
 
 @dataclass
@@ -158,10 +167,26 @@ def _distributed():
     return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
 
 
-def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
+def _peer_for(replica, config, world, rank):
+    """The replica's peer-memory exchange (arena + mapped peers), created once
+    per (world, staleness) and reused across epochs."""
+    from .peer import PeerExchange
+    key = (world, rank, config.staleness)
+    px = getattr(replica, "_peer", None)
+    if px is None or px[0] != key:
+        if px is not None:
+            px[1].close()
+        ex = PeerExchange(replica.dev.num_params, replica.device, lag=config.staleness,
+                          ring=4, timeout_s=config.queue_timeout)
+        replica._peer = (key, ex)
+        return ex
+    return px[1]
+
+
+def _runner_for(replica, g, cache, config, world, rank, multi, num_train, exchange=None):
     key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
            config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline,
-           config.fused_step, config.queue_capacity)
+           config.fused_step, config.queue_capacity, id(exchange))
     r = getattr(replica, "_runner", None)
     if r is None or r[0] != key:
         runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
@@ -169,7 +194,7 @@ def _runner_for(replica, g, cache, config, world, rank, multi, num_train):
                             optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
                             multi=multi, use_graph=config.use_graph,
                             pipeline=config.pipeline, fused=config.fused_step,
-                            queue_depth=config.queue_capacity)
+                            queue_depth=config.queue_capacity, exchange=exchange)
         replica._runner = (key, runner)
         return runner, True
     return r[1], False
@@ -199,6 +224,10 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
         world = config.num_devices
         exchange = None
         local_ranks = list(range(world))
+    if config.staleness and not dist_mode:
+        raise NotImplementedError("the pipelined (staleness 1) schedule runs over the peer "
+                                  "exchange: one process per device")
+    use_peer = dist_mode and config.exchange in ("auto", "peer") and g.device.type == "cuda"
     per_device, expected = plan_epoch(g, config, epoch)
     total_windows = len(expected)
     perm = epoch_permutation(g.train_mask, config.seed, epoch)
@@ -208,14 +237,25 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
     torch.cuda.synchronize(g.device)
     hm0 = cache.hit_miss.clone() if cache is not None else None
     for d, rep in zip(local_ranks, replicas):
-        r, fresh = _runner_for(rep, g, cache, config, world, d, multi, perm.size)
+        fx = _peer_for(rep, config, world, d) if use_peer else None
+        r, fresh = _runner_for(rep, g, cache, config, world, d, multi, perm.size, fx)
         r.begin_epoch(epoch, perm)
         if config.use_graph:
             r.capture()
         runners.append(r)
     weight_traces = {d: [] for d in local_ranks}
 
+    # straggler injection (the reference's gradient delay model, racom.py:172-184,
+    # runtime.py:545-547): this process holds back each window's launch by a
+    # delay draw.  The device schedule is fixed (every rank folds the packets
+    # of a window in rank order), so delays change timing, never results.
+    dm = config.delay_model
+    delay_rng = (np.random.default_rng(np.random.SeedSequence([config.seed, epoch, 2, local_ranks[0]]))
+                 if dm is not None and getattr(dm, "kind", "none") != "none" else None)
+
     def on_window(k):
+        if delay_rng is not None and k + 1 < total_windows:
+            time.sleep(dm.sample(delay_rng) / 1e3)
         if config.capture_weights:
             for d, r in zip(local_ranks, runners):
                 r.sync_point()

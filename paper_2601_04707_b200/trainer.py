@@ -14,9 +14,12 @@ fills group 1-i with the next Q batches in ONE batched pass
 (mq_prep_batches).  Cross-stream order is carried by CUDA events recorded
 between graph launches, so the host never synchronises.
 
-Multi-replica (RaCoM) windows split the train graph around the gradient
-exchange: [train + pack] -> f64 all-reduce of [grads | contributor count]
-(NCCL in production, gloo / in-process in tests) -> update graph.
+Multi-replica (RaCoM) windows either run the fused peer-memory exchange
+inside the train graph ([train -> mq_racom_publish -> mq_racom_apply],
+peer.PeerExchange: no host synchronisation, group graphs as for one replica)
+or split the train graph around a host-issued collective: [train + pack] ->
+f64 all-reduce of [grads | contributor count] (torch.distributed, or
+in-process replicas) -> update graph.
 """
 
 from __future__ import annotations
@@ -30,20 +33,29 @@ import torch
 
 from ._lib import lib, ptr
 from .engine import FusedTrainWorkspace, TrainWorkspace, capture_graph
+from .pipeline import PipelineTimeout
 from .prep import PrepGroup, PrepShared
 
 DEFAULT_QUEUE_DEPTH = 8  # measured best on B200 (autotune.auto_queue_depth: 2 < 4 < 8)
+
+
+class PeerTimeout(PipelineTimeout):
+    """A rank waited past the timeout for a peer's window gradient (the
+    reference's PipelineTimeout at the rendezvous, pipeline.py:101-106)."""
 
 
 def raise_device_flag(dm):
     """Raise for the device status word the step kernels set (and clear it):
     bit 0 a non-finite loss / weight (nn.py:74-76), bit 1 an optimizer step
     counter overflow, bit 2 a block row longer than MQ_MAX_FANOUT (structural,
-    the head truncated it)."""
+    the head truncated it), bit 3 a peer-exchange wait that timed out."""
     flag = int(dm.nonfinite.item())
     if not flag:
         return
     dm.nonfinite.zero_()
+    if flag & 8:
+        raise PeerTimeout("a peer rank never published its window gradient (RaCoM apply "
+                          "timed out); the replica skipped that update")
     if flag & 4:
         raise ValueError("a sampled block row has more edges than the fused head supports "
                          "(MQ_MAX_FANOUT): the fanout is too large for the fused step")
@@ -59,7 +71,7 @@ class StepRunner:
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
                  multi: bool = False, use_graph: bool = True, pipeline: bool = True,
                  ring_len: int = 1 << 16, fused: bool = True, queue_depth: int | None = None,
-                 layer0: str = "auto"):
+                 layer0: str = "auto", exchange=None):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         Q = DEFAULT_QUEUE_DEPTH if queue_depth is None else int(queue_depth)
@@ -73,6 +85,11 @@ class StepRunner:
         self.seed = int(seed)
         self.world, self.rank = int(world), int(rank)
         self.multi = bool(multi)
+        # fused peer-memory exchange (peer.PeerExchange): publish + apply run
+        # inside the train graph, so multi-rank windows need no host step
+        self.fx = exchange if getattr(exchange, "fused", False) else None
+        if self.fx is not None and (self.fx.world != self.world or self.fx.rank != self.rank):
+            raise ValueError("peer exchange world/rank differ from the runner's")
         self.use_graph = use_graph
         self.pipeline = bool(pipeline)
         self.Q = Q
@@ -100,7 +117,7 @@ class StepRunner:
         self.ring_len = int(ring_len)
         self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
         self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
-                       if self.multi else None)
+                       if self.multi and self.fx is None else None)
         self.stream = torch.cuda.Stream(device=dev)       # train stream
         self.prep_stream = torch.cuda.Stream(device=dev)  # sample + transfer stream
         self.ev_prep = [torch.cuda.Event() for _ in self.groups]
@@ -169,13 +186,18 @@ class StepRunner:
                 lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world,
                                      ptr(ring), self.ring_len, s)
             self.tw.launch_backward(self.dm, s, sw)
-        if self.grad64 is not None:
+        if self.fx is not None:
+            self.fx.publish(self.dm.flat_g, self.tw.grad_src(self.dm) if self.fused else None,
+                            sw.n_targets, s)
+        elif self.grad64 is not None:
             src = self.tw.grad_src(self.dm) if self.fused else None
             lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(sw.n_targets),
                                 ptr(self.grad64), C.byref(src) if src is not None else None, s)
 
     def _enqueue_update(self, s):
-        if self.grad64 is None:
+        if self.fx is not None:
+            self.fx.apply(self.dm, self.optimizer, s)
+        elif self.grad64 is None:
             self.tw.launch_optimizer(self.dm, self.optimizer, s)
         else:  # scale 0: divide by the all-reduced contributor count (expected[k])
             self.tw.launch_optimizer(self.dm, self.optimizer, s, grad64=self.grad64, scale=0.0)
@@ -189,12 +211,18 @@ class StepRunner:
             for q, sw in enumerate(grp.slots):
                 def train(s, sw=sw):
                     self._enqueue_train(sw, s)
-                    if not self.multi:
+                    if self._host_exchange is False:
                         self._enqueue_update(s)
                 ph[f"train{gi}_{q}"] = train
-        if self.multi:
+        if self._host_exchange:
             ph["update"] = self._enqueue_update
         return ph
+
+    @property
+    def _host_exchange(self) -> bool:
+        """True when the window's gradient exchange is issued by the host
+        between a train graph and an update graph."""
+        return self.multi and self.fx is None
 
     # ----------------------------------------------------------------- graphs
     def _state_tensors(self):
@@ -211,6 +239,10 @@ class StepRunner:
         with torch.cuda.stream(self.stream):
             for fn in phases.values():
                 fn(self.stream.cuda_stream)
+        # a lagged peer exchange holds the last warm-up window back: apply it
+        # now (every rank warms the same windows) so the first real window
+        # starts with nothing pending
+        self.finish()
         torch.cuda.synchronize(self.device)
         for t, v in zip(self._state_tensors(), snap):
             t.copy_(v)
@@ -237,7 +269,7 @@ class StepRunner:
         phases = self._phases()
         self._warm(phases)
         self._capture(phases)
-        if self.pipeline and not self.multi:
+        if self.pipeline and not self._host_exchange:
             for gi in range(2):
                 def group(s, gi=gi):
                     cur = torch.cuda.current_stream(self.device)
@@ -258,7 +290,7 @@ class StepRunner:
         graphs were captured): the train graph plus 1/Q of a prep pass."""
         ph = self.launches_per_phase
         n = ph.get("train0_0", 0) + ph.get("prep0", 0) / self.Q
-        if self.multi:
+        if self._host_exchange:
             n += ph.get("update", 0)
         return n
 
@@ -276,7 +308,7 @@ class StepRunner:
         self.use_graph = False
         try:
             self.compute_window()
-            if not self.multi:
+            if not self._host_exchange:
                 self.apply_window()
         finally:
             self.use_graph = g
@@ -306,14 +338,21 @@ class StepRunner:
         self._last = (gi, q)
 
     def apply_window(self):
-        if self.multi:
+        if self._host_exchange:
             self._run("update", self.stream)
         self.dm.host_steps += 1
         self.windows_done += 1
 
+    def finish(self):
+        """End of epoch: apply what the pipelined schedule still holds back
+        (lag 1: the last window), so every window is applied at the barrier."""
+        if self.fx is not None and self.fx.lag > 0:
+            with torch.cuda.stream(self.stream):
+                self.fx.apply(self.dm, self.optimizer, self.stream.cuda_stream, lag=0)
+
     def step(self):
         """One window (async; nothing is read back)."""
-        if self.multi:
+        if self._host_exchange:
             raise RuntimeError("multi-replica runners need the exchange: use racom.WindowDriver")
         self.compute_window()
         self.apply_window()
@@ -322,7 +361,7 @@ class StepRunner:
         """Up to n windows of this epoch (async).  Whole slot groups run as ONE
         graph launch each (prep of the next group forked inside it), the
         rest window by window.  Returns the number of windows issued."""
-        if self.multi:
+        if self._host_exchange:
             raise RuntimeError("multi-replica runners need the exchange: use racom.WindowDriver")
         if epoch_windows is None:
             epoch_windows = -(-self.num_train // (self.batch_size * self.world))
@@ -409,8 +448,9 @@ class StepRunner:
         and whose train step leaves the batch loss for a per-step read-back."""
         if self._hphases is not None:
             return
-        if self.multi:
-            raise NotImplementedError("host-input steps are single-replica")
+        if self._host_exchange:
+            raise NotImplementedError("host-input steps need the fused (peer) exchange "
+                                      "when replicas span processes")
         Q = self.Q
         # a ring of pinned staging rows: a row set is reused only after the copies
         # that read it (4 groups earlier) have executed, so the host never waits

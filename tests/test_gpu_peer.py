@@ -1,0 +1,267 @@
+"""GPU: RaCoM over peer memory (mq_racom_publish / mq_racom_apply, peer.py).
+
+Only one GPU is available to this build, so multi-rank runs put every rank's
+process on cuda:0: the arenas are mapped between processes through CUDA IPC
+exactly as between GPUs (NVLink P2P), the flag protocol and the rank-ordered
+f64 fold are the same, and the host plumbing (handle exchange, epoch-barrier
+sync) runs over gloo.
+
+* kernel unit test (one process, in-process arenas): the applied update is
+  bit-identical to the reference Accumulator's running mean (racom.py:47-57)
+  followed by adam_step / sgd_step (nn.py:191-215), including a window with a
+  missing contributor (expected[k] < G);
+* whole epochs with 2 and 3 ranks (parity schedule) vs the reference's own
+  run_epoch (golden fixtures, the same bars as test_gpu_runtime) and vs the
+  in-process replicas, every rank's replica bit-identical to the others;
+* the pipelined schedule (staleness 1) vs the oracle's staleness-1 schedule;
+* straggler injection (the reference's delay model) changes nothing;
+* a rank that never publishes makes its peers raise PeerTimeout.
+"""
+
+import contextlib
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+from conftest import load_golden, make_g2  # noqa: E402
+
+
+def _free_port():
+    with contextlib.closing(socket.socket(socket.AF_INET, socket.SOCK_STREAM)) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# ----------------------------------------------------------- kernel unit test
+@pytest.mark.parametrize("optimizer", ["adam", "sgd"])
+def test_publish_apply_equal_accumulator_and_optimizer(optimizer):
+    import paper_2601_04707_b200 as mq
+    from oracle import nn as onn
+    from oracle.racom import RunningMean
+    from paper_2601_04707_b200.peer import PeerExchange
+
+    G, n = 3, 1000
+    shapes = [(20, 30), (40, 10)]
+    rng = np.random.default_rng(3)
+    w0 = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    reps = [mq.ModelState([w.copy() for w in w0], learning_rate=0.01, device="cuda")
+            for _ in range(G)]
+    exs = PeerExchange.local_group(n, "cuda", G, ring=4, lag=0, timeout_s=5.0)
+    om = onn.OracleModel([w.copy() for w in w0], learning_rate=0.01)
+    s = torch.cuda.current_stream().cuda_stream
+    for k in range(4):
+        grads = [[rng.standard_normal(sh).astype(np.float32) for sh in shapes] for _ in range(G)]
+        absent = 2 if k == 2 else None  # window 2: rank 2 has no batch (expected = 2)
+        acc = RunningMean()
+        for q in range(G):
+            flat = torch.from_numpy(np.concatenate([g.ravel() for g in grads[q]])).cuda()
+            nt = torch.tensor([0 if q == absent else 64], dtype=torch.int32, device="cuda")
+            exs[q].publish(flat, None, nt, s)
+            if q != absent:
+                acc.add(grads[q])
+        for q in range(G):
+            exs[q].apply(reps[q].dev, optimizer, s)
+        torch.cuda.synchronize()
+        (onn.adam_step if optimizer == "adam" else onn.sgd_step)(om, acc.mean)
+        for q in range(G):
+            reps[q].dev.host_steps += 1
+            for l in range(2):
+                np.testing.assert_array_equal(reps[q].weights[l].cpu().numpy(), om.weights[l])
+                if optimizer == "adam":
+                    np.testing.assert_array_equal(reps[q].m[l].cpu().numpy(), om.m[l])
+                    np.testing.assert_array_equal(reps[q].v[l].cpu().numpy(), om.v[l])
+    st = exs[0].state()
+    assert st["published"] == 4 and st["applied"] == 4 and st["min_flag"] == 4
+    assert int(reps[0].dev.nonfinite.item()) == 0
+
+
+def test_lagged_apply_holds_back_one_window():
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200.peer import PeerExchange
+    n = 64
+    rep = mq.ModelState([np.zeros((8, 8), np.float32)], learning_rate=0.1, device="cuda")
+    ex = PeerExchange.local_group(n, "cuda", 1, ring=4, lag=1)[0]
+    s = torch.cuda.current_stream().cuda_stream
+    nt = torch.tensor([1], dtype=torch.int32, device="cuda")
+    for k in range(3):
+        ex.publish(torch.full((n,), float(k + 1), device="cuda"), None, nt, s)
+        ex.apply(rep.dev, "sgd", s)
+        torch.cuda.synchronize()
+        # windows 0..k-1 applied: w = -0.1 * (1 + ... + k)
+        expect = np.float32(0.0)
+        for j in range(k):
+            expect = np.float32(expect - np.float32(0.1) * np.float32(j + 1))
+        assert ex.state()["applied"] == k
+        assert np.all(rep.weights[0].cpu().numpy() == expect)
+    ex.apply(rep.dev, "sgd", s, lag=0)  # the epoch barrier's drain
+    assert ex.state()["applied"] == 3
+
+
+def test_missing_peer_times_out():
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200.peer import PeerExchange
+    from paper_2601_04707_b200.trainer import raise_device_flag
+    n = 64
+    rep = mq.ModelState([np.ones((8, 8), np.float32)], learning_rate=0.1, device="cuda")
+    exs = PeerExchange.local_group(n, "cuda", 2, ring=4, lag=0, timeout_s=0.2)
+    s = torch.cuda.current_stream().cuda_stream
+    nt = torch.tensor([1], dtype=torch.int32, device="cuda")
+    exs[0].publish(torch.ones(n, device="cuda"), None, nt, s)  # rank 1 never publishes
+    exs[0].apply(rep.dev, "sgd", s)
+    torch.cuda.synchronize()
+    assert np.all(rep.weights[0].cpu().numpy() == 1.0)  # no update applied
+    with pytest.raises(mq.PeerTimeout):
+        raise_device_flag(rep.dev)
+
+
+# ------------------------------------------------------- multi-process epochs
+CASES = {"2dev_adam": (2, "adam", 1, "g2/mask10"), "2dev_sgd_p3": (2, "sgd", 3, None),
+         "3dev_adam_p2": (3, "adam", 2, "g2/mask1")}
+
+
+def _cfg(mq, G, opt, P, staleness=0, delay=None):
+    return mq.PipelineConfig(num_devices=G, batch_size=64,
+                             sampler=mq.SamplerParams("sage", (4, 3), num_layers=2),
+                             optimizer=opt, sync_period=P, seed=5, exchange="peer",
+                             staleness=staleness, delay_model=delay, queue_timeout=60.0)
+
+
+def _worker(rank, world, port, name, staleness, delay, epochs, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200.graph import DeviceGraph
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gs, rt = load_golden("sampling.npz"), load_golden("runtime.npz")
+        hg = make_g2(gs)
+        hg.train_mask = rt["epoch/train_mask"]
+        g = DeviceGraph.from_csr(hg)
+        G, opt, P, mask_name = CASES[name]
+        cache = mq.DeviceCache(g, gs[mask_name]) if mask_name else None
+        rep = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        dm = None
+        if delay:
+            from paper_2601_04707_b200.timing import DurationModel
+            dm = DurationModel("uniform", 1.0, 8.0) if rank == 1 else None
+        losses, syncs, hits = {}, [], [0, 0]
+        for e in range(epochs):
+            st, _ = mq.run_epoch(g, cache, [rep], _cfg(mq, G, opt, P, staleness, dm), epoch=1 + e)
+            losses.update({(e, b): v for b, v in st.losses.items()})
+            syncs.append([st.sync_count, st.epoch_sync])
+            hits = [hits[0] + st.cache_hits, hits[1] + st.cache_misses]
+        keys = sorted(losses)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
+                 keys=np.array(keys), losses=np.array([losses[k] for k in keys]),
+                 syncs=np.array(syncs), hits=np.array(hits),
+                 w0=rep.weights[0].cpu().numpy(), w1=rep.weights[1].cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(tmp_path, name, staleness=0, delay=False, epochs=1):
+    G = CASES[name][0]
+    out = tmp_path / f"{name}_{staleness}_{int(delay)}"
+    out.mkdir()
+    mp.start_processes(_worker, args=(G, _free_port(), name, staleness, delay, epochs, str(out)),
+                       nprocs=G, join=True, start_method="spawn")
+    return [np.load(out / f"rank{r}.npz") for r in range(G)]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_peer_ranks_match_reference_epoch(tmp_path, name):
+    rt = load_golden("runtime.npz")
+    res = _run(tmp_path, name)
+    bids = rt[f"epoch/{name}/loss_bids"].tolist()
+    r0 = res[0]
+    assert [int(k[1]) for k in r0["keys"]] == bids
+    np.testing.assert_allclose(r0["losses"], rt[f"epoch/{name}/losses"], rtol=1e-4)
+    assert r0["syncs"][0].tolist() == rt[f"epoch/{name}/sync_count"].tolist()
+    assert r0["hits"].tolist() == rt[f"epoch/{name}/hits"].tolist()
+    for l in range(2):
+        w = rt[f"epoch/{name}/w{l}"]
+        assert np.abs(r0[f"w{l}"] - w).max() <= 1e-4 * np.abs(w).max()
+        for r in res[1:]:  # every rank folds the same packets in the same order
+            np.testing.assert_array_equal(r[f"w{l}"], r0[f"w{l}"])
+
+
+def test_peer_matches_in_process_replicas(tmp_path):
+    """2 processes over peer memory == 2 replicas in one process (the
+    reference's simulated devices) to acceptance criterion 03's 1e-6."""
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200.graph import DeviceGraph
+    gs, rt = load_golden("sampling.npz"), load_golden("runtime.npz")
+    hg = make_g2(gs)
+    hg.train_mask = rt["epoch/train_mask"]
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, gs["g2/mask10"])
+    base = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+    reps = [base.copy() for _ in range(2)]
+    cfg = _cfg(mq, 2, "adam", 1)
+    cfg.exchange = "collective"
+    loc = {}
+    for e in range(2):
+        st, _ = mq.run_epoch(g, cache, reps, cfg, epoch=1 + e)
+        loc.update({(e, b): v for b, v in st.losses.items()})
+    res = _run(tmp_path, "2dev_adam", epochs=2)
+    keys = sorted(loc)
+    np.testing.assert_allclose(res[0]["losses"], [loc[k] for k in keys], rtol=1e-6)
+    for l in range(2):
+        w = reps[0].weights[l].cpu().numpy()
+        assert np.abs(res[0][f"w{l}"] - w).max() <= 1e-6 * np.abs(w).max()
+
+
+def test_pipelined_staleness_one_matches_oracle_schedule(tmp_path):
+    from oracle import nn as onn
+    from oracle import racom as oracom
+    gs, rt = load_golden("sampling.npz"), load_golden("runtime.npz")
+    hg = make_g2(gs)
+    graph = {"row_offsets": hg.row_offsets, "col_indices": hg.col_indices,
+             "features": hg.features, "labels": hg.labels, "train_mask": rt["epoch/train_mask"]}
+    models = [onn.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+              for _ in range(2)]
+    ref = {}
+    for e in range(2):
+        losses, _ = oracom.run_epoch_serial(graph, models, fanouts=(4, 3), batch_size=64,
+                                            seed=5, epoch=1 + e, optimizer="adam",
+                                            sync_period=1, cached_mask=gs["g2/mask10"],
+                                            staleness=1)
+        ref.update({(e, b): v for b, v in losses.items()})
+    res = _run(tmp_path, "2dev_adam", staleness=1, epochs=2)
+    keys = sorted(ref)
+    assert [tuple(int(x) for x in k) for k in res[0]["keys"]] == keys
+    np.testing.assert_allclose(res[0]["losses"], [ref[k] for k in keys], rtol=1e-4)
+    for l in range(2):
+        w = models[0].weights[l]
+        assert np.abs(res[0][f"w{l}"] - w).max() <= 1e-4 * np.abs(w).max()
+        np.testing.assert_array_equal(res[1][f"w{l}"], res[0][f"w{l}"])
+    # the schedule differs from the parity one: staleness is real
+    par = _run(tmp_path, "2dev_adam", staleness=0, epochs=2)
+    assert not np.array_equal(par[0]["w0"], res[0]["w0"])
+
+
+def test_straggler_injection_changes_nothing(tmp_path):
+    """A rank delayed by the reference's uniform(1, 8) ms gradient-delay model
+    trains the same: the fold order is fixed by rank, not by arrival.  (The
+    backward's fp32 scatter atomics make two runs differ in the last bits, so
+    the bar is acceptance criterion 03's 1e-6, not bit equality; within one
+    run every rank is bit-identical.)"""
+    plain = _run(tmp_path, "2dev_adam")
+    slow = _run(tmp_path, "2dev_adam", delay=True)
+    for a, b in zip(plain, slow):
+        np.testing.assert_allclose(b["losses"], a["losses"], rtol=1e-6)
+        for l in range(2):
+            w = a[f"w{l}"]
+            assert np.abs(b[f"w{l}"] - w).max() <= 1e-6 * np.abs(w).max()
+    for l in range(2):
+        np.testing.assert_array_equal(slow[0][f"w{l}"], slow[1][f"w{l}"])
