@@ -66,7 +66,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--hidden", type=int, default=64)
     ap.add_argument("--cache-fraction", type=float, default=0.01)
-    ap.add_argument("--feature-placement", default="hbm", choices=["hbm", "host"])
+    ap.add_argument("--feature-placement", default="hbm", choices=["hbm", "host", "sharded"],
+                    help="feature table in HBM, pinned host memory, or node-partitioned "
+                         "across the ranks (remote rows over NVLink P2P)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--profile-steps", type=int, default=20,
@@ -93,11 +95,13 @@ def env_rank():
 
 
 # --------------------------------------------------------------------- inputs
-def build_inputs(args, device):
-    """Synthetic graph (GPU generator when a GPU exists) + degree-mode cache mask."""
+def build_inputs(args, device, feature_shard=None):
+    """Synthetic graph (GPU generator when a GPU exists) + degree-mode cache mask;
+    ``feature_shard=(G, r)`` generates only this rank's feature rows."""
     from paper_2601_04707_b200 import synth
     t0 = time.perf_counter()
-    sg, fanouts = synth.generate_shape(args.shape, seed=args.seed, device=device)
+    sg, fanouts = synth.generate_shape(args.shape, seed=args.seed, device=device,
+                                       feature_shard=feature_shard)
     t_gen = time.perf_counter() - t0
     return sg, fanouts, t_gen
 
@@ -362,12 +366,14 @@ def run_ours(args):
     from paper_2601_04707_b200.runtime import epoch_permutation
 
     setup = {}
-    sg, fanouts, setup["graph_gen_s"] = build_inputs(args, f"cuda:{local}")
+    sharded = args.feature_placement == "sharded"
+    sg, fanouts, setup["graph_gen_s"] = build_inputs(
+        args, f"cuda:{local}", feature_shard=(world, rank) if sharded else None)
     t0 = time.perf_counter()
     g = mq.DeviceGraph.from_csr(sg, device=dev, feature_placement=args.feature_placement)
     torch.cuda.synchronize()
     setup["upload_s"] = time.perf_counter() - t0
-    if args.shape == "papers":  # 57 GB of features: no host copy for the CPU leg
+    if args.shape == "papers" or sharded:  # no host copy of the features for the CPU leg
         args.no_cpu_baseline = True
     if args.no_cpu_baseline:  # the generator's device arrays are not needed any more
         sg.col_indices = sg.row_offsets = sg.labels = None

@@ -39,6 +39,8 @@ extern "C" {
 #define MQ_ERR_STATE 3
 
 #define MQ_MAX_FANOUT 32
+/* ranks of one RaCoM exchange / shards of a partitioned feature store */
+#define MQ_MAX_PEERS 8
 
 /* Deferred split-K gradient reduction.  A flat gradient
  * element i in [offset, offset + size) is the fixed-order sum over p <
@@ -184,6 +186,11 @@ typedef struct mq_prep_desc {
   uint32_t stage_mask;  /* 0 = all; else bits MQ_PREP_* select stages (profiling) */
   unsigned long long* hit_miss;
   const int32_t* all_labels; int32_t* labels; int64_t labels_s;
+  /* seed-partitioned feature store (n_shards >= 2; then `store` is unused):
+   * node v's row lives on shard v % n_shards at row v / n_shards, pitch
+   * store_pitch — one table per rank, the others' mapped over NVLink P2P
+   * (mq_ipc_open), so misses of remote rows are read peer-to-peer */
+  const float* store_shard[MQ_MAX_PEERS]; int32_t n_shards, pad2_;
 } mq_prep_desc;
 #define MQ_PREP_SETUP 1u
 #define MQ_PREP_SAMPLE 2u
@@ -204,6 +211,15 @@ int mq_gather(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_o
               const float* store, int32_t store_pitch, const int32_t* ids,
               const int32_t* n_dev, int32_t n_max, int32_t d, float* out,
               int32_t out_pitch, unsigned long long* hit_miss, void* stream);
+
+/* mq_gather over a seed-partitioned store: misses read node v's row from
+ * shards[v % n_shards] at row v / n_shards (remote shards peer-mapped over
+ * NVLink).  shards is a HOST array of 1..MQ_MAX_PEERS device pointers. */
+int mq_gather_sharded(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
+                      const float* const* shards, int32_t n_shards, int32_t store_pitch,
+                      const int32_t* ids, const int32_t* n_dev, int32_t n_max, int32_t d,
+                      float* out, int32_t out_pitch, unsigned long long* hit_miss,
+                      void* stream);
 
 /* ---------------------------------------------------------- SAGE numerics
  * block_apply (nn.py:79-89): agg[r] = sum over the row's triplets, in order,
@@ -567,7 +583,6 @@ int mq_degree_buckets(const int64_t* row_off, int64_t n_nodes, int32_t* bucket, 
  *   every gradient misses exactly one update).  A timed-out wait sets
  *   nonfinite[0] |= 8 and skips the update.
  * Both kernels size their grid to stay co-resident (<= one CTA per SM). */
-#define MQ_MAX_PEERS 8
 #define MQ_PEER_HEADER_BYTES 256
 typedef struct mq_ipc_handle { char bytes[64]; } mq_ipc_handle;
 typedef struct mq_peer_exchange {

@@ -65,8 +65,9 @@ class DeviceCache:
                                      stream)
             table = torch.zeros((max(self.size, 1), g.pitch), dtype=torch.float32, device=dev)
             if self.size:
-                src = g.features.index_select(0, self.cached_ids.to(g.features.device))
-                table[:self.size] = src.to(dev)
+                ids32 = self.cached_ids.to(torch.int32)
+                nd = torch.tensor([self.size], dtype=torch.int32, device=dev)
+                g.gather_rows(ids32, nd, self.size, table, g.pitch, stream)
             self.table = table
             self.hit_miss = torch.zeros(2, dtype=torch.int64, device=dev)
         self._lock = threading.Lock()
@@ -243,13 +244,10 @@ def gather_features(cache: DeviceCache | None, g: DeviceGraph, ids, *, out=None,
     if out is None:
         out = torch.empty((max(n, 1), pitch), dtype=torch.float32, device=g.device)
     stream = torch.cuda.current_stream(g.device).cuda_stream
-    if cache is None:
-        lib().mq_gather(None, 0, None, ptr(g.features), g.pitch, ptr(ids), ptr(n_dev), n,
-                        g.feature_dim, ptr(out), pitch, None, stream)
-    else:
+    hm = None
+    if cache is not None:
         hm = cache.hit_miss if count_hits else torch.zeros(2, dtype=torch.int64, device=g.device)
-        lib().mq_gather(ptr(cache.table), g.pitch, ptr(cache.slot_of), ptr(g.features), g.pitch,
-                        ptr(ids), ptr(n_dev), n, g.feature_dim, ptr(out), pitch, ptr(hm), stream)
+    g.gather_rows(ids, n_dev, n, out, pitch, stream, cache=cache, hit_miss=hm)
     return out[:n, :g.feature_dim]
 
 

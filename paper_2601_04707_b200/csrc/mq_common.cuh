@@ -230,6 +230,34 @@ __host__ __device__ __forceinline__ void fisher_yates(RowStream& rs, IdxT n, int
   }
 }
 
+// Feature store: one table, or a seed-partitioned one whose node v lives on
+// shard v % n at row v / n (remote shards are peer-mapped NVLink memory).
+struct StoreRef {
+  const float* base[MQ_MAX_PEERS];
+  int n;
+  int pitch;
+  __device__ __forceinline__ const float* row(int64_t id) const {
+    if (n <= 1) return base[0] + id * pitch;
+    const int64_t o = id % n;
+    return base[o] + (id / n) * pitch;
+  }
+};
+
+inline StoreRef make_store(const float* store, const float* const* shards, int n_shards,
+                           int pitch) {
+  StoreRef r;
+  memset(&r, 0, sizeof(r));
+  r.pitch = pitch;
+  if (n_shards >= 2) {
+    r.n = n_shards;
+    for (int q = 0; q < n_shards; ++q) r.base[q] = shards[q];
+  } else {
+    r.n = 1;
+    r.base[0] = n_shards == 1 ? shards[0] : store;
+  }
+  return r;
+}
+
 // Fixed-order sum p[0] + p[stride] + ... + p[(S-1)*stride] (left to right, so
 // results are deterministic); the loads are issued 16 at a time so the chain
 // costs ~S/16 L2 round trips instead of S (a 128-partial head gradient: 8).

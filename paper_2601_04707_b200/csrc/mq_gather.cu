@@ -12,7 +12,7 @@ constexpr int kGatherThreads = 256;
 // each warp keeps 4 float4 loads in flight before it stores.
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(
     const float* __restrict__ cache_tbl, int cache_pitch, const int32_t* __restrict__ slot_of,
-    const float* __restrict__ store, int store_pitch, const int32_t* __restrict__ ids,
+    StoreRef store, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ n_dev, int d4, float* __restrict__ out, int out_pitch,
     unsigned long long* __restrict__ hit_miss) {
   __shared__ unsigned int s_hits, s_miss;
@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(
       src = reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch);
       ++hits;
     } else {
-      src = reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
+      src = reinterpret_cast<const float4*>(store.row(id));
       ++miss;
     }
     float4* dst = reinterpret_cast<float4*>(out + row * out_pitch);
@@ -73,22 +73,25 @@ using namespace mq;
 
 extern "C" {
 
-int mq_gather(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
-              const float* store, int32_t store_pitch, const int32_t* ids, const int32_t* n_dev,
-              int32_t n_max, int32_t d, float* out, int32_t out_pitch,
-              unsigned long long* hit_miss, void* stream) {
-  MQ_CHECK_ARG(store && ids && n_dev && out, "mq_gather: null pointer");
-  MQ_CHECK_ARG(d >= 1, "mq_gather: d must be positive");
+static int gather_impl(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
+                       StoreRef store, const int32_t* ids, const int32_t* n_dev, int32_t n_max,
+                       int32_t d, float* out, int32_t out_pitch, unsigned long long* hit_miss,
+                       void* stream, const char* who) {
+  MQ_CHECK_ARG(ids && n_dev && out, "%s: null pointer", who);
+  MQ_CHECK_ARG(d >= 1, "%s: d must be positive", who);
   const int d4 = (d + 3) / 4;
-  MQ_CHECK_ARG(store_pitch % 4 == 0 && out_pitch % 4 == 0 && store_pitch >= 4 * d4 &&
+  MQ_CHECK_ARG(store.pitch % 4 == 0 && out_pitch % 4 == 0 && store.pitch >= 4 * d4 &&
                    out_pitch >= 4 * d4,
-               "mq_gather: pitches must be multiples of 4 floats covering d (d=%d, store %d, out %d)",
-               d, store_pitch, out_pitch);
-  MQ_CHECK_ARG(((uintptr_t)store | (uintptr_t)out) % 16 == 0, "mq_gather: tables must be 16B aligned");
+               "%s: pitches must be multiples of 4 floats covering d (d=%d, store %d, out %d)",
+               who, d, store.pitch, out_pitch);
+  MQ_CHECK_ARG((uintptr_t)out % 16 == 0, "%s: output must be 16B aligned", who);
+  for (int q = 0; q < store.n; ++q)
+    MQ_CHECK_ARG(store.base[q] && (uintptr_t)store.base[q] % 16 == 0,
+                 "%s: store table %d missing or not 16B aligned", who, q);
   if (slot_of) {
     MQ_CHECK_ARG(cache_tbl && hit_miss && cache_pitch % 4 == 0 && cache_pitch >= 4 * d4 &&
                      (uintptr_t)cache_tbl % 16 == 0,
-                 "mq_gather: cache table / counters invalid");
+                 "%s: cache table / counters invalid", who);
   }
   if (n_max <= 0) return MQ_OK;
   cudaStream_t s = as_stream(stream);
@@ -97,12 +100,32 @@ int mq_gather(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_o
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   {
     ProfScope ps(K_GATHER, s);
-    gather_kernel<<<blocks, kGatherThreads, 0, s>>>(cache_tbl, cache_pitch, slot_of, store,
-                                                    store_pitch, ids, n_dev, d4, out, out_pitch,
-                                                    hit_miss);
+    gather_kernel<<<blocks, kGatherThreads, 0, s>>>(cache_tbl, cache_pitch, slot_of, store, ids,
+                                                    n_dev, d4, out, out_pitch, hit_miss);
   }
-  MQ_LAUNCH_CHECK("gather");
+  MQ_LAUNCH_CHECK(who);
   return MQ_OK;
+}
+
+int mq_gather(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
+              const float* store, int32_t store_pitch, const int32_t* ids, const int32_t* n_dev,
+              int32_t n_max, int32_t d, float* out, int32_t out_pitch,
+              unsigned long long* hit_miss, void* stream) {
+  MQ_CHECK_ARG(store, "mq_gather: null store");
+  return gather_impl(cache_tbl, cache_pitch, slot_of, make_store(store, nullptr, 0, store_pitch),
+                     ids, n_dev, n_max, d, out, out_pitch, hit_miss, stream, "mq_gather");
+}
+
+int mq_gather_sharded(const float* cache_tbl, int32_t cache_pitch, const int32_t* slot_of,
+                      const float* const* shards, int32_t n_shards, int32_t store_pitch,
+                      const int32_t* ids, const int32_t* n_dev, int32_t n_max, int32_t d,
+                      float* out, int32_t out_pitch, unsigned long long* hit_miss,
+                      void* stream) {
+  MQ_CHECK_ARG(shards && n_shards >= 1 && n_shards <= MQ_MAX_PEERS,
+               "mq_gather_sharded: need 1..%d shards", MQ_MAX_PEERS);
+  return gather_impl(cache_tbl, cache_pitch, slot_of,
+                     make_store(nullptr, shards, n_shards, store_pitch), ids, n_dev, n_max, d, out,
+                     out_pitch, hit_miss, stream, "mq_gather_sharded");
 }
 
 int mq_gather_labels(const int32_t* all_labels, const int32_t* ids, const int32_t* n_dev,

@@ -256,7 +256,7 @@ constexpr int kGatherThreads = 256;
 
 __global__ void __launch_bounds__(kGatherThreads) gather_q_kernel(
     const float* __restrict__ cache_tbl, int cache_pitch, const int32_t* __restrict__ slot_of,
-    const float* __restrict__ store, int store_pitch, QP<const int32_t> ids, QP<const int32_t> n_dev,
+    StoreRef store, QP<const int32_t> ids, QP<const int32_t> n_dev,
     int d4, QP<float> out, int out_pitch, unsigned long long* __restrict__ hit_miss) {
   __shared__ unsigned int s_hits, s_miss;
   if (threadIdx.x == 0) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_q_kernel(
         src = reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch);
         ++hits;
       } else {
-        src = reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
+        src = reinterpret_cast<const float4*>(store.row(id));
         ++miss;
       }
       float4* dst = reinterpret_cast<float4*>(outq + row * out_pitch);
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_q_kernel(
       const int32_t slot = slot_of ? slot_of[id] : -1;
       hit = slot >= 0;
       my_src = hit ? reinterpret_cast<const float4*>(cache_tbl + (int64_t)slot * cache_pitch)
-                   : reinterpret_cast<const float4*>(store + (int64_t)id * store_pitch);
+                   : reinterpret_cast<const float4*>(store.row(id));
     }
     // warp-uniform counts (lane 0 reports them, as on the wide path)
     const unsigned hb = __ballot_sync(0xffffffffu, hit);
@@ -383,8 +383,13 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
   MQ_CHECK_ARG(d.num_hops >= 1 && d.num_hops <= MQ_MAX_HOPS, "mq_prep_batches: num_hops %d",
                d.num_hops);
   MQ_CHECK_ARG(d.row_off && d.col && d.targets && d.n_targets && d.key && d.dpos && d.first &&
-                   d.scratch && d.store && d.x0 && d.all_labels && d.labels,
+                   d.scratch && (d.store || d.n_shards >= 1) && d.x0 && d.all_labels && d.labels,
                "mq_prep_batches: null pointer");
+  MQ_CHECK_ARG(d.n_shards >= 0 && d.n_shards <= MQ_MAX_PEERS, "mq_prep_batches: n_shards %d",
+               d.n_shards);
+  for (int q = 0; q < d.n_shards; ++q)
+    MQ_CHECK_ARG(d.store_shard[q] && (uintptr_t)d.store_shard[q] % 16 == 0,
+                 "mq_prep_batches: shard %d missing or unaligned", q);
   MQ_CHECK_ARG((d.hot_arc == nullptr) == (d.hot_off == nullptr),
                "mq_prep_batches: hot_arc / hot_off must both be set or both NULL");
   MQ_CHECK_ARG(!d.slot_of || (d.cache_tbl && d.hit_miss), "mq_prep_batches: cache without table");
@@ -489,7 +494,8 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     const int cap = ceil_div(kNumSMs * 16, Q);
     if (blocks > cap) blocks = cap;
     gather_q_kernel<<<dim3(blocks, Q), kGatherThreads, 0, s>>>(
-        d.cache_tbl, d.cache_pitch, d.slot_of, d.store, d.store_pitch, cq(last.src_ids, last.src_s),
+        d.cache_tbl, d.cache_pitch, d.slot_of,
+        make_store(d.store, d.store_shard, d.n_shards, d.store_pitch), cq(last.src_ids, last.src_s),
         cq(last.counts, last.counts_s), dv4, qp(d.x0, d.x0_s), d.x0_pitch, d.hit_miss);
   }
   MQ_LAUNCH_CHECK("prep gather");

@@ -270,14 +270,8 @@ class TrainWorkspace:
         """transfer_stage (runtime.py:127-143) + target labels (samplers.py:532)."""
         g = sw.graph
         b = sw.bounds[-1]
-        if cache is None:
-            lib().mq_gather(None, 0, None, ptr(g.features), g.pitch, ptr(sw.input_ids),
-                            ptr(sw.n_input_dev), b.n_src_max, g.feature_dim, ptr(sw.x0), g.pitch,
-                            None, stream)
-        else:
-            lib().mq_gather(ptr(cache.table), g.pitch, ptr(cache.slot_of), ptr(g.features), g.pitch,
-                            ptr(sw.input_ids), ptr(sw.n_input_dev), b.n_src_max, g.feature_dim,
-                            ptr(sw.x0), g.pitch, ptr(cache.hit_miss), stream)
+        g.gather_rows(sw.input_ids, sw.n_input_dev, b.n_src_max, sw.x0, g.pitch, stream,
+                      cache=cache, hit_miss=cache.hit_miss if cache is not None else None)
         lib().mq_gather_labels(ptr(g.labels), ptr(sw.targets), ptr(sw.n_targets), sw.batch_size,
                                ptr(sw.labels), stream)
 

@@ -11,7 +11,11 @@ HBM layout:
   * ``features`` f32 [n, pitch], pitch = round_up(d, 4) floats so every row is
     16-byte aligned for vector loads (Reddit's 602-d rows are 2,408 B).
     Placement "hbm" keeps the table in device memory; "host" keeps it in
-    pinned host memory and the gather reads misses over the host link.
+    pinned host memory and the gather reads misses over the host link;
+    "sharded" (``shard_features``) partitions it by node across the ranks:
+    node v's row lives on rank v % G at row v // G, and the other ranks'
+    shards are mapped over NVLink (CUDA IPC), so the gather reads remote
+    rows peer-to-peer (BASELINE configs[4]).
   * ``labels`` int32 [n].
 """
 
@@ -19,6 +23,8 @@ from __future__ import annotations
 
 import numpy as np
 import torch
+
+import ctypes as C
 
 from ._lib import lib, ptr
 
@@ -44,8 +50,10 @@ class DeviceGraph:
     @classmethod
     def from_csr(cls, g, device=None, feature_placement: str = "hbm") -> "DeviceGraph":
         """Upload any GraphCSR-like object (reference ``GraphCSR`` or
-        ``synth.SynthGraph``).  ``feature_placement``: "hbm" or "host"."""
-        if feature_placement not in ("hbm", "host"):
+        ``synth.SynthGraph``).  ``feature_placement``: "hbm", "host" or
+        "sharded" (collective over torch.distributed: ``g.features`` holds
+        either every node's row or only this rank's rows v = rank, rank+G, ...)."""
+        if feature_placement not in ("hbm", "host", "sharded"):
             raise ValueError(f"unknown feature placement {feature_placement!r}")
         self = object.__new__(cls)
         dev = torch.device(device or "cuda")
@@ -61,6 +69,8 @@ class DeviceGraph:
         self.val_mask = np.asarray(_host(g.val_mask), dtype=bool)
         self.test_mask = np.asarray(_host(g.test_mask), dtype=bool)
         self.source = g
+        self.shards = None   # seed-partitioned store: device pointers of the G shards
+        self._shard_keep = None
         n = self.num_nodes
         if n >= INT32_MAX:
             raise ValueError("node ids must fit in int32")
@@ -88,6 +98,10 @@ class DeviceGraph:
             del row_off, col, scratch
             self.labels = _as_tensor(g.labels, torch.int32, dev)
             self.feature_placement = feature_placement
+            if feature_placement == "sharded":
+                self.features = None
+                self._install_shard(feats)
+                return self
             if feature_placement == "hbm":
                 if (isinstance(feats, torch.Tensor) and feats.device == dev
                         and feats.dtype == torch.float32 and feats.is_contiguous()
@@ -102,12 +116,97 @@ class DeviceGraph:
             self.features = table
         return self
 
+    # ---- seed-partitioned feature store
+    def shard_features(self, group=None):
+        """Collective: keep only this rank's rows of the (full) table and map
+        the other ranks' shards; the full table is released."""
+        if self.features is None:
+            raise ValueError("features are already sharded")
+        full = self.features
+        self.features = None
+        self._install_shard(full, group)
+        self.feature_placement = "sharded"
+        del full
+        torch.cuda.empty_cache()
+
+    def _install_shard(self, feats, group=None):
+        import torch.distributed as dist
+        from .peer import PeerArena, exchange_handles, open_handle
+        on = dist.is_available() and dist.is_initialized()
+        G, r = (dist.get_world_size(group), dist.get_rank(group)) if on else (1, 0)
+        if G > MQ_MAX_SHARDS:
+            raise ValueError(f"at most {MQ_MAX_SHARDS} feature shards")
+        n, d, P = self.num_nodes, self.feature_dim, self.pitch
+        rows = shard_rows(n, G, r)
+        if int(feats.shape[0]) == n:
+            own = feats[r::G]
+        elif int(feats.shape[0]) == rows:
+            own = feats
+        else:
+            raise ValueError(f"features must hold all {n} rows or this rank's {rows}")
+        arena = PeerArena(max(rows, 1) * P * 4, self.device)
+        stage = torch.zeros((max(rows, 1), P), dtype=torch.float32, device=self.device)
+        stage[:rows, :d] = _as_tensor(own, torch.float32, self.device)
+        lib().mq_memcpy_async(arena.ptr, ptr(stage), stage.numel() * 4,
+                              torch.cuda.current_stream(self.device).cuda_stream)
+        torch.cuda.synchronize(self.device)
+        del stage
+        infos = exchange_handles(arena.export(), group) if on else [(None, None)]
+        import os
+        ptrs, opened = [], []
+        for q, (pid, h) in enumerate(infos):
+            if q == r:
+                ptrs.append(arena.ptr)
+            elif pid == os.getpid():
+                raise RuntimeError("two ranks in one process: use use_local_shards")
+            else:
+                p = open_handle(h, self.device)
+                opened.append(p)
+                ptrs.append(p)
+        if on:
+            dist.barrier(group)
+        self.shards = ptrs
+        self._shard_keep = (arena, opened)
+        self.shard_rank, self.num_shards = r, G
+
+    def use_local_shards(self, world: int):
+        """Split this process's table into ``world`` node-partitioned shards
+        (one process standing in for G ranks; tests of the sharded gather)."""
+        if self.features is None or world < 1 or world > MQ_MAX_SHARDS:
+            raise ValueError("need a full table and 1..8 shards")
+        keep = [self.features[q::world].contiguous() for q in range(world)]
+        self.shards = [t.data_ptr() for t in keep]
+        self._shard_keep = keep
+        self.num_shards = world
+
+    def gather_rows(self, ids, n_dev, n_max: int, out, out_pitch: int, stream, cache=None,
+                    hit_miss=None):
+        """gather_features into ``out``: cache hits from the HBM table, misses
+        from the store (one table, pinned host, or the node-partitioned shards)."""
+        tbl = ptr(cache.table) if cache is not None else None
+        slot = ptr(cache.slot_of) if cache is not None else None
+        hm = ptr(hit_miss) if cache is not None else None
+        if self.shards is not None:
+            arr = (C.c_void_p * len(self.shards))(*self.shards)
+            lib().mq_gather_sharded(tbl, self.pitch, slot, arr, len(self.shards), self.pitch,
+                                    ptr(ids), ptr(n_dev), n_max, self.feature_dim, ptr(out),
+                                    out_pitch, hm, stream)
+        else:
+            lib().mq_gather(tbl, self.pitch, slot, ptr(self.features), self.pitch, ptr(ids),
+                            ptr(n_dev), n_max, self.feature_dim, ptr(out), out_pitch, hm, stream)
+
+    def require_full_table(self, what: str):
+        if self.features is None:
+            raise NotImplementedError(f"{what} reads the whole feature table; this graph's "
+                                      "features are sharded across ranks")
+
     # ---- reference-compatible views
     @property
     def num_edges(self) -> int:
         return self.num_arcs_stored
 
     def features_view(self) -> torch.Tensor:
+        self.require_full_table("features_view")
         return self.features[:, :self.feature_dim]
 
     def degree(self) -> torch.Tensor:
@@ -122,6 +221,14 @@ class DeviceGraph:
         lib().mq_in_degrees(ptr(self.col), self.num_nodes, self.num_arcs, ptr(self.loops),
                             ptr(deg), torch.cuda.current_stream(self.device).cuda_stream)
         return deg[:self.num_nodes]
+
+
+MQ_MAX_SHARDS = 8
+
+
+def shard_rows(num_nodes: int, world: int, rank: int) -> int:
+    """Rows of rank's shard: nodes rank, rank + world, ... < num_nodes."""
+    return max(0, (num_nodes - rank + world - 1) // world)
 
 
 def _host(a):

@@ -311,6 +311,7 @@ def full_forward(g, state: ModelState) -> torch.Tensor:
     dims = [g.feature_dim] + [int(w.shape[1]) for w in state.weights]
     if int(state.weights[0].shape[0]) != 2 * g.feature_dim:
         raise ValueError("model input width does not match the graph's features")
+    g.require_full_table("full_forward")
     ws = _eval_ws(g, dims)
     n = g.num_nodes
     h, ldh = g.features, g.pitch
@@ -379,6 +380,7 @@ def evaluate(g, state: ModelState, mask, chunk: int = 1 << 20) -> float:
         raise ValueError("model input width does not match the graph's features")
     n, L = g.num_nodes, len(state.weights)
     f32 = dict(dtype=torch.float32, device=dev)
+    g.require_full_table("evaluate")
     h, ldh = g.features, g.pitch
     keep = []
     for l in range(L - 1):

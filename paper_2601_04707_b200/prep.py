@@ -48,7 +48,8 @@ class PrepDesc(C.Structure):
                 ("slot_of", P), ("store", P),
                 ("x0", P), ("x0_s", I64), ("x0_pitch", I32), ("stage_mask", C.c_uint32),
                 ("hit_miss", P),
-                ("all_labels", P), ("labels", P), ("labels_s", I64)]
+                ("all_labels", P), ("labels", P), ("labels_s", I64),
+                ("store_shard", P * 8), ("n_shards", I32), ("pad2_", I32)]
 
 
 class PrepShared:
@@ -184,7 +185,13 @@ class PrepGroup:
         d.dpos, d.first, d.table_s = ptr(sh.dpos), ptr(sh.first), sh.dpos.stride(0)
         d.scratch, d.scratch_s = ptr(sh.scratch), sh.scratch_s
         d.row_off, d.col = ptr(g.row_off), ptr(g.col)
-        d.store, d.store_pitch = ptr(g.features), g.pitch
+        d.store_pitch = g.pitch
+        if g.shards is not None:  # seed-partitioned store (graph.DeviceGraph.shard_features)
+            d.n_shards = len(g.shards)
+            for q, p in enumerate(g.shards):
+                d.store_shard[q] = p
+        else:
+            d.store = ptr(g.features)
         if cache is not None:
             d.hot_arc, d.hot_off = ptr(cache.hot_arc), ptr(cache.hot_off)
             d.cache_tbl, d.cache_pitch = ptr(cache.table), g.pitch

@@ -135,10 +135,13 @@ def generate_numpy(num_nodes, num_arcs, feature_dim, num_classes, *, train=0.66,
 
 
 def generate_torch(num_nodes, num_arcs, feature_dim, num_classes, *, train=0.66,
-                   exponent=2.1, seed=0, device="cuda") -> SynthGraph:
+                   exponent=2.1, seed=0, device="cuda", feature_shard=None) -> SynthGraph:
     """Same construction with torch ops (GPU); arrays stay on ``device``.
 
     Masks are NumPy (host) like the reference's; row_offsets int64, col int32.
+    Features are drawn in fixed row chunks, so ``feature_shard=(G, r)`` —
+    keep only rows v = r, r + G, ... (the seed-partitioned store) — yields
+    exactly those rows of the unsharded table; labels always see every row.
     """
     import torch
 
@@ -170,17 +173,25 @@ def generate_torch(num_nodes, num_arcs, feature_dim, num_classes, *, train=0.66,
     row_offsets = torch.zeros(n + 1, dtype=torch.int64, device=device)
     torch.cumsum(counts, 0, out=row_offsets[1:])
     del counts
-    feats = torch.randn((n, feature_dim), generator=gen, device=device, dtype=torch.float32)
     proj = torch.randn((feature_dim, num_classes), generator=gen, device=device)
     labels = torch.empty(n, dtype=torch.int32, device=device)
-    for lo in range(0, n, 1 << 23):  # chunked: [n x C] logits would be 76 GB at papers
-        hi = min(n, lo + (1 << 23))
-        labels[lo:hi] = torch.argmax(feats[lo:hi] @ proj, dim=1).to(torch.int32)
+    G, r = feature_shard if feature_shard is not None else (1, 0)
+    feats = torch.empty(((n - r + G - 1) // G, feature_dim), dtype=torch.float32, device=device)
+    chunk = 1 << 20  # a multiple of every shard count <= 8
+    for lo in range(0, n, chunk):  # [n x C] logits would be 76 GB at papers
+        hi = min(n, lo + chunk)
+        x = torch.randn((hi - lo, feature_dim), generator=gen, device=device, dtype=torch.float32)
+        labels[lo:hi] = torch.argmax(x @ proj, dim=1).to(torch.int32)
+        first = (r - lo) % G  # first row of this chunk owned by shard r
+        feats[(lo + first - r) // G:(lo + first - r) // G + len(range(first, hi - lo, G))] = \
+            x[first::G]
+        del x
     tr, va, te = split_masks(n, ratios_for(train), seed + 4)
     return SynthGraph(n, row_offsets, col, feats, labels, num_classes, tr, va, te)
 
 
-def generate_shape(name: str, seed: int = 0, device: str | None = None, **overrides):
+def generate_shape(name: str, seed: int = 0, device: str | None = None, feature_shard=None,
+                   **overrides):
     spec = dict(SHAPES[name])
     spec.update(overrides)
     fanouts = spec.pop("fanouts")
@@ -190,7 +201,8 @@ def generate_shape(name: str, seed: int = 0, device: str | None = None, **overri
                            spec["num_classes"], train=train, seed=seed)
     else:
         g = generate_torch(spec["num_nodes"], spec["num_arcs"], spec["feature_dim"],
-                           spec["num_classes"], train=train, seed=seed, device=device)
+                           spec["num_classes"], train=train, seed=seed, device=device,
+                           feature_shard=feature_shard)
     return g, tuple(fanouts)
 
 
