@@ -607,6 +607,14 @@ int mq_racom_apply(const mq_peer_exchange* ex, int32_t optimizer /* 0 adam, 1 sg
 int mq_peer_state(const mq_peer_exchange* ex, unsigned long long* out4 /* pub, applied, min flag, max flag */,
                   void* stream);
 
+/* ------------------------------------------------------------- tracing
+ * Trace / TraceEvent (pipeline.py:30-98): when the stream reaches the call,
+ * append {globaltimer ns, tag << 32 | key_dev[2] (the slot's batch id) or
+ * 0xFFFFFFFF} at buf[2 * i] (i = atomicAdd(cursor, 1), dropped once i >=
+ * cap).  Launched dependent on its predecessor; capturable. */
+int mq_trace_stamp(unsigned long long* buf, int32_t cap, unsigned int* cursor, uint32_t tag,
+                   const uint32_t* key_dev, void* stream);
+
 /* ------------------------------------------------------------- utilities */
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): the step's
  * pinned-host result read-back as a node of a captured graph. */

@@ -128,6 +128,7 @@ SIGNATURES = {
     "mq_prof_read": (C.c_int, [P, P, I32]),
     "mq_launch_count": (I64, []),
     "mq_gather_sharded": (C.c_int, [P, I32, P, P, I32, I32, P, P, I32, I32, P, I32, P, P]),
+    "mq_trace_stamp": (C.c_int, [P, I32, P, U32, P, P]),
     "mq_peer_arena_bytes": (I64, [I64, I32]),
     "mq_peer_alloc": (C.c_int, [I64, P]),
     "mq_peer_free": (C.c_int, [P]),

@@ -65,6 +65,11 @@ class PipelineConfig:
     # batch k+1); 1: pipelined RaCoM, window k applied after batch k+1's
     # backward (every gradient misses exactly one update)
     staleness: int = 0
+    # device stage stamps for the returned Trace (sample / transfer /
+    # compute_fwd / compute_bwd / grad_share / grad_apply / sync spans from
+    # the GPU clock) and the queue statistics; False skips the stamp
+    # launches (5 per window) and returns a trace of windows only
+    trace: bool = True
 
     def validate(self) -> None:
         if self.num_devices < 1:
@@ -186,7 +191,7 @@ def _peer_for(replica, config, world, rank):
 def _runner_for(replica, g, cache, config, world, rank, multi, num_train, exchange=None):
     key = (id(g), id(cache), config.sampler.hop_fanouts, config.batch_size, config.optimizer,
            config.seed, world, rank, multi, num_train, config.use_graph, config.pipeline,
-           config.fused_step, config.queue_capacity, id(exchange))
+           config.fused_step, config.queue_capacity, id(exchange), config.trace)
     r = getattr(replica, "_runner", None)
     if r is None or r[0] != key:
         runner = StepRunner(g, replica, fanouts=config.sampler.hop_fanouts,
@@ -194,10 +199,86 @@ def _runner_for(replica, g, cache, config, world, rank, multi, num_train, exchan
                             optimizer=config.optimizer, seed=config.seed, world=world, rank=rank,
                             multi=multi, use_graph=config.use_graph,
                             pipeline=config.pipeline, fused=config.fused_step,
-                            queue_depth=config.queue_capacity, exchange=exchange)
+                            queue_depth=config.queue_capacity, exchange=exchange,
+                            trace_cap=_trace_cap(num_train, config, world) if config.trace else 0)
         replica._runner = (key, runner)
         return runner, True
     return r[1], False
+
+
+def _trace_cap(num_train, config, world):
+    windows = -(-num_train // (config.batch_size * world))
+    return 8 * windows + 64
+
+
+def device_trace(stamps, windows, Q: int, device: int, epoch: int, trace: Trace):
+    """Decode one replica's device stage stamps into the reference's trace
+    spans (pipeline.py:24-25 STAGES; the emit points of runtime.py:399-546)
+    and queue statistics.  ``windows`` = [(window, batch_id)] of this device.
+
+    * prep pass p (batched, Q windows) gives every batch of windows
+      [pQ, (p+1)Q): ``sample`` = [pass start, sample+relabel end],
+      ``enqueue_cpu`` (zero length at sample end), ``transfer`` =
+      [sample end, gather end];
+    * ``enqueue_dev`` = [gather end, compute start]: the time the prepared
+      batch waited in the device queue (slot ring);
+    * ``compute_fwd`` = [compute start, head end (loss, dlogits)],
+      ``compute_bwd`` = [head end, gradients done], ``grad_share`` =
+      [gradients done, packet published], ``grad_apply`` (batch = window)
+      = [published, update applied];
+    * ``sync`` spans from the model-average stamps.
+    Returns (queue_high_water {"cpu", "dev"}, queue_keys, sync spans added)."""
+    t0 = int(stamps[0, 0]) if len(stamps) else 0
+    by_tag = {}
+    for t, tag, bid in stamps:
+        by_tag.setdefault(int(tag), []).append((int(t) - t0, int(bid)))
+    from .trainer import (TAG_APPLY_END, TAG_BWD_END, TAG_COMPUTE_START, TAG_FWD_END,
+                          TAG_GATHER_END, TAG_PREP_START, TAG_SAMPLE_END, TAG_SHARE_END,
+                          TAG_SYNC_END, TAG_SYNC_START)
+    ps, se, ge = (by_tag.get(k, []) for k in (TAG_PREP_START, TAG_SAMPLE_END, TAG_GATHER_END))
+    cs, fe, be, sh, ae = (by_tag.get(k, []) for k in (TAG_COMPUTE_START, TAG_FWD_END,
+                                                      TAG_BWD_END, TAG_SHARE_END,
+                                                      TAG_APPLY_END))
+    ready, start = {}, {}
+    for k, (_, bid) in enumerate(windows):
+        p = k // Q
+        if p < len(ps) and p < len(se) and p < len(ge):
+            trace.add("sample", device, bid, epoch, ps[p][0], se[p][0])
+            trace.add("enqueue_cpu", device, bid, epoch, se[p][0], se[p][0])
+            trace.add("transfer", device, bid, epoch, se[p][0], ge[p][0])
+            ready[bid] = ge[p][0]
+        if k < len(cs) and k < len(fe) and k < len(be):
+            trace.add("compute_fwd", device, bid, epoch, cs[k][0], fe[k][0])
+            trace.add("compute_bwd", device, bid, epoch, fe[k][0], be[k][0])
+            start[bid] = cs[k][0]
+            if bid in ready:
+                trace.add("enqueue_dev", device, bid, epoch, ready[bid],
+                          max(ready[bid], cs[k][0]))
+        if k < len(be) and k < len(sh):
+            trace.add("grad_share", device, bid, epoch, be[k][0], sh[k][0])
+    for k in range(min(len(sh), len(ae))):
+        trace.add("grad_apply", device, k, epoch, sh[k][0], max(sh[k][0], ae[k][0]))
+    syncs = list(zip(by_tag.get(TAG_SYNC_START, []), by_tag.get(TAG_SYNC_END, [])))
+    for a, b in syncs:
+        trace.add("sync", device, -1, epoch, a[0], max(a[0], b[0]))
+    # queue occupancy from the same clock: the batched pass hands a whole group
+    # from sampling to transfer ("cpu"), prepared batches wait for compute ("dev")
+    def high_water(puts, gets):
+        evs = sorted([(t, 1) for t in puts] + [(t, -1) for t in gets], key=lambda x: (x[0], x[1]))
+        cur = hw = 0
+        for _, d in evs:
+            cur += d
+            hw = max(hw, cur)
+        return hw
+    bids = [bid for _, bid in windows]
+    cpu_put = [se[k // Q][0] for k in range(len(windows)) if k // Q < len(se)]
+    cpu_get = [ge[k // Q][0] for k in range(len(windows)) if k // Q < len(ge)]
+    hw = {"cpu": high_water(cpu_put, cpu_get) if cpu_put else 0,
+          "dev": high_water(list(ready.values()), list(start.values())) if ready else 0}
+    order = lambda d: [b for b in sorted(d, key=lambda b: (d[b], bids.index(b)))]  # noqa: E731
+    keys = {"cpu_put": bids[:len(cpu_put)], "cpu_get": bids[:len(cpu_get)],
+            "dev_put": order(ready), "dev_get": order(start)}
+    return hw, keys, len(syncs)
 
 
 def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
@@ -284,39 +365,54 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
     if cache is not None:
         delta = (cache.hit_miss - hm0).cpu().numpy()
         hits, misses = int(delta[0]), int(delta[1])
+
+    queue_hw, queue_keys = {}, {}
+    local_trace = Trace()
+    for d, r in zip(local_ranks, runners):
+        wins = [(k, bid) for k, (_, bid, _) in enumerate(per_device[d])]
+        if config.trace:
+            queue_hw[d], queue_keys[d], got = device_trace(r.read_trace(), wins, r.Q, d, epoch,
+                                                           local_trace)
+        else:
+            queue_hw[d] = {"cpu": 0, "dev": 0}
+            queue_keys[d] = {k: [b for _, b in wins]
+                             for k in ("cpu_put", "cpu_get", "dev_put", "dev_get")}
+            got = 0
+            per_win = gpu_ms / max(total_windows, 1)
+            for k, bid in wins:  # window spans only (no stamps)
+                a = k * per_win * MS_TO_NS
+                local_trace.add("compute_fwd", d, bid, epoch, a, a + per_win * MS_TO_NS)
+        t_end = int(gpu_ms * MS_TO_NS)
+        # elided syncs (identical replicas: the average is the identity) are
+        # zero-length, like the reference's barrier action with nothing to do
+        for _ in range(info["sync_count"] + info["epoch_sync"] - got):
+            local_trace.add("sync", d, -1, epoch, t_end, t_end)
     if dist_mode:
         import torch.distributed as dist
         gathered = [None] * world
-        dist.all_gather_object(gathered, (losses, hits, misses))
+        evs = [e.to_dict() for e in local_trace.events()]
+        dist.all_gather_object(gathered, (losses, hits, misses, queue_hw, queue_keys, evs))
         losses = {}
         hits = misses = 0
-        for l_, h_, m_ in gathered:
+        for l_, h_, m_, qh, qk, ev in gathered:
             losses.update(l_)
             hits += h_
             misses += m_
-    # coarse trace: one compute span per window, split fwd/bwd as the serial
-    # reference does with its duration models (runtime.py:332-333)
-    per_win = gpu_ms / max(total_windows, 1)
-    for d in local_ranks:
-        for k, (_, bid, _) in enumerate(per_device[d]):
-            a = k * per_win * MS_TO_NS
-            trace.add("compute_fwd", d, bid, epoch, a, a + per_win * MS_TO_NS / 2)
-            trace.add("compute_bwd", d, bid, epoch, a + per_win * MS_TO_NS / 2,
-                      a + per_win * MS_TO_NS)
-            trace.add("grad_apply", d, k, epoch, a + per_win * MS_TO_NS, a + per_win * MS_TO_NS)
-        t_end = total_windows * per_win * MS_TO_NS
-        for _ in range(info["sync_count"] + info["epoch_sync"]):
-            trace.add("sync", d, -1, epoch, t_end, t_end)
+            queue_hw.update(qh)
+            queue_keys.update(qk)
+            for e in ev:
+                trace.add(e["stage"], e["device"], e["batch"], e["epoch"], e["t_start_ns"],
+                          e["t_end_ns"])
+    else:
+        for e in local_trace.events():
+            trace.add(e.stage, e.device, e.batch, e.epoch, e.t_start_ns, e.t_end_ns)
     stats = EpochStats(
         epoch=epoch, losses=losses, batches=sum(len(x) for x in per_device),
         cache_hits=hits, cache_misses=misses, dropped_targets=0,
         sync_count=info["sync_count"], epoch_sync=info["epoch_sync"],
         elided_syncs=info["elided"],
         applied_windows={d: info["applied"] for d in range(config.num_devices)},
-        queue_high_water={d: {"cpu": 1 if per_device[d] else 0, "dev": 1 if per_device[d] else 0}
-                          for d in range(config.num_devices)},
-        queue_keys={d: {k: [b for _, b, _ in per_device[d]]
-                        for k in ("cpu_put", "cpu_get", "dev_put", "dev_get")}
-                    for d in range(config.num_devices)},
+        queue_high_water=queue_hw,
+        queue_keys=queue_keys,
         weight_traces=weight_traces, wall_ms=wall_ms)
     return stats, trace

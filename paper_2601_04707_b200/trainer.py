@@ -39,6 +39,12 @@ from .prep import PrepGroup, PrepShared
 DEFAULT_QUEUE_DEPTH = 8  # measured best on B200 (autotune.auto_queue_depth: 2 < 4 < 8)
 
 
+# device stage stamp tags (mq_trace_stamp; decoded by runtime.device_trace)
+TAG_PREP_START, TAG_SAMPLE_END, TAG_GATHER_END = 1, 2, 3
+TAG_COMPUTE_START, TAG_FWD_END, TAG_BWD_END, TAG_SHARE_END, TAG_APPLY_END = 10, 11, 12, 13, 14
+TAG_SYNC_START, TAG_SYNC_END = 20, 21
+
+
 class PeerTimeout(PipelineTimeout):
     """A rank waited past the timeout for a peer's window gradient (the
     reference's PipelineTimeout at the rendezvous, pipeline.py:101-106)."""
@@ -71,7 +77,7 @@ class StepRunner:
                  optimizer: str = "adam", seed: int = 0, world: int = 1, rank: int = 0,
                  multi: bool = False, use_graph: bool = True, pipeline: bool = True,
                  ring_len: int = 1 << 16, fused: bool = True, queue_depth: int | None = None,
-                 layer0: str = "auto", exchange=None):
+                 layer0: str = "auto", exchange=None, trace_cap: int = 0):
         if optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {optimizer!r}")
         Q = DEFAULT_QUEUE_DEPTH if queue_depth is None else int(queue_depth)
@@ -120,6 +126,11 @@ class StepRunner:
                        if self.multi and self.fx is None else None)
         self.stream = torch.cuda.Stream(device=dev)       # train stream
         self.prep_stream = torch.cuda.Stream(device=dev)  # sample + transfer stream
+        # device stage stamps (mq_trace_stamp): [cap][t_ns, tag << 32 | batch]
+        self.trace_cap = int(trace_cap)
+        self.trace_buf = (torch.zeros(2 * self.trace_cap, dtype=torch.int64, device=dev)
+                          if self.trace_cap else None)
+        self.trace_cur = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ev_prep = [torch.cuda.Event() for _ in self.groups]
         self.ev_train = [torch.cuda.Event() for _ in self.groups]
         self._desc = {}
@@ -144,6 +155,7 @@ class StepRunner:
         with torch.cuda.stream(self.stream):
             self.perm.copy_(staged, non_blocking=True)
             self.cursor.zero_()
+            self.trace_cur.zero_()
             for grp in self.groups:
                 grp.set_key(self.seed, epoch)
         self.epoch = epoch
@@ -169,23 +181,53 @@ class StepRunner:
                                                    self.world, self.rank)
         return self._desc[key]
 
+    def _stamp(self, tag: int, s, key=None):
+        if self.trace_buf is not None:
+            lib().mq_trace_stamp(ptr(self.trace_buf), self.trace_cap, ptr(self.trace_cur), tag,
+                                 ptr(key), s)
+
+    def _launch_prep(self, gi: int, host: bool, s):
+        """One batched prep pass over group gi; traced runs split it at the
+        sample | transfer boundary with stage stamps."""
+        grp, desc = self.groups[gi], self._prep_desc(gi, host)
+        if self.trace_buf is None:
+            grp.launch(desc, s)
+            return
+        from .prep import PREP_GATHER, PREP_LABELS, PREP_RELABEL, PREP_SAMPLE, PREP_SETUP
+        self._stamp(TAG_PREP_START, s)
+        try:
+            desc.stage_mask = PREP_SETUP | PREP_SAMPLE | PREP_RELABEL
+            grp.launch(desc, s)
+            self._stamp(TAG_SAMPLE_END, s)
+            desc.stage_mask = PREP_GATHER | PREP_LABELS
+            grp.launch(desc, s)
+        finally:
+            desc.stage_mask = 0
+        self._stamp(TAG_GATHER_END, s)
+
     def _enqueue_prep(self, sw, s, setup=True):
         """One batched prep pass filling the whole group that holds slot ``sw``."""
         gi = next(i for i, grp in enumerate(self.groups) if sw in grp.slots)
-        self.groups[gi].launch(self._prep_desc(gi, not setup), s)
+        self._launch_prep(gi, not setup, s)
 
     def _enqueue_train(self, sw, s, commit=True, ring=None):
         ring = self.loss_ring if ring is None else ring
+        self._stamp(TAG_COMPUTE_START, s, sw.key)
         if self.fused:
-            self.tw.launch_train(self.dm, s, sw, ring=ring if commit else None,
-                                 ring_len=self.ring_len, world=self.world)
+            for name, op in self.tw.train_ops(self.dm, sw, ring if commit else None,
+                                              self.ring_len, self.world):
+                op(s)
+                if name == "sage_head":  # loss + dlogits: the forward ends here
+                    self._stamp(TAG_FWD_END, s, sw.key)
         else:
             self.tw.launch_forward(self.dm, s, sw)
             self.tw.launch_loss(self.dm, s, sw)
             if commit:
                 lib().mq_step_commit(ptr(self.tw.loss), ptr(sw.key), self.world,
                                      ptr(ring), self.ring_len, s)
+            self._stamp(TAG_FWD_END, s, sw.key)
             self.tw.launch_backward(self.dm, s, sw)
+        self._stamp(TAG_BWD_END, s, sw.key)
         if self.fx is not None:
             self.fx.publish(self.dm.flat_g, self.tw.grad_src(self.dm) if self.fused else None,
                             sw.n_targets, s)
@@ -193,8 +235,13 @@ class StepRunner:
             src = self.tw.grad_src(self.dm) if self.fused else None
             lib().mq_pack_grads(ptr(self.dm.flat_g), self.dm.num_params, ptr(sw.n_targets),
                                 ptr(self.grad64), C.byref(src) if src is not None else None, s)
+        self._stamp(TAG_SHARE_END, s, sw.key)
 
     def _enqueue_update(self, s):
+        self._update(s)
+        self._stamp(TAG_APPLY_END, s)
+
+    def _update(self, s):
         if self.fx is not None:
             self.fx.apply(self.dm, self.optimizer, s)
         elif self.grad64 is None:
@@ -206,8 +253,7 @@ class StepRunner:
         """name -> fn(stream) for every graph this runner captures."""
         ph = {}
         for gi, grp in enumerate(self.groups):
-            ph[f"prep{gi}"] = (lambda s, gi=gi: self.groups[gi].launch(self._prep_desc(gi, False),
-                                                                       s))
+            ph[f"prep{gi}"] = (lambda s, gi=gi: self._launch_prep(gi, False, s))
             for q, sw in enumerate(grp.slots):
                 def train(s, sw=sw):
                     self._enqueue_train(sw, s)
@@ -244,6 +290,7 @@ class StepRunner:
         # starts with nothing pending
         self.finish()
         torch.cuda.synchronize(self.device)
+        self.trace_cur.zero_()
         for t, v in zip(self._state_tensors(), snap):
             t.copy_(v)
         self.tw.loss.zero_()
@@ -275,8 +322,7 @@ class StepRunner:
                     cur = torch.cuda.current_stream(self.device)
                     self.prep_stream.wait_stream(cur)
                     with torch.cuda.stream(self.prep_stream):
-                        self.groups[1 - gi].launch(self._prep_desc(1 - gi, False),
-                                                   self.prep_stream.cuda_stream)
+                        self._launch_prep(1 - gi, False, self.prep_stream.cuda_stream)
                     for q in range(self.Q):
                         ph = phases[f"train{gi}_{q}"]
                         ph(cur.cuda_stream)
@@ -395,6 +441,7 @@ class StepRunner:
     def state64(self) -> torch.Tensor:
         from .racom import _pack_state
         with torch.cuda.stream(self.stream):
+            self._stamp(TAG_SYNC_START, self.stream.cuda_stream)
             out = torch.empty(3 * self.dm.num_params, dtype=torch.float64, device=self.device)
             _pack_state(self.model, out)
         return out
@@ -403,6 +450,7 @@ class StepRunner:
         from .racom import _unpack_state
         with torch.cuda.stream(self.stream):
             _unpack_state(self.model, t, divisor)
+            self._stamp(TAG_SYNC_END, self.stream.cuda_stream)
 
     @property
     def step_count(self) -> int:
@@ -433,6 +481,20 @@ class StepRunner:
             hops.append((nd, ns, nnz))
             nd = ns
         return {"n_targets": c[0], "hops": hops}
+
+    def read_trace(self) -> np.ndarray:
+        """The epoch's stage stamps as int64 [k, 3] = (t_ns, tag, batch id), in
+        append order (stream order per stream)."""
+        if self.trace_buf is None:
+            return np.zeros((0, 3), dtype=np.int64)
+        torch.cuda.synchronize(self.device)
+        n = min(int(self.trace_cur.item()), self.trace_cap)
+        raw = self.trace_buf[:2 * n].view(n, 2).cpu().numpy()
+        out = np.empty((n, 3), dtype=np.int64)
+        out[:, 0] = raw[:, 0]
+        out[:, 1] = (raw[:, 1].view(np.uint64) >> np.uint64(32)).astype(np.int64)
+        out[:, 2] = (raw[:, 1].view(np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        return out
 
     def losses(self, n_windows: int) -> np.ndarray:
         self.stream.synchronize()
@@ -470,8 +532,7 @@ class StepRunner:
         self._grp_ev = [torch.cuda.Event() for _ in self.groups]
         phases = {}
         for gi, grp in enumerate(self.groups):
-            phases[f"hprep{gi}"] = (lambda s, gi=gi: self.groups[gi].launch(
-                self._prep_desc(gi, True), s))
+            phases[f"hprep{gi}"] = (lambda s, gi=gi: self._launch_prep(gi, True, s))
             for q, sw in enumerate(grp.slots):
                 def htrain(s, sw=sw):
                     self._enqueue_train(sw, s, commit=True, ring=self._loss_hring)
