@@ -141,6 +141,18 @@ class StepRunner:
         self.epoch = 0
         self._primed = False
         self._last = (0, 0)
+        self._join_current()
+
+    def _join_current(self):
+        """Order the runner's streams after the work already queued on the
+        caller's current stream: buffers, weights and the cache were created
+        (zero-filled, copied) there, and the step graphs run on the side
+        streams — without this a fill could land after the first prep pass
+        (found by compute-sanitizer racecheck: stale targets in the second
+        runner of a process)."""
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)
+        self.prep_stream.wait_stream(cur)
 
     # ---------------------------------------------------------------- epochs
     def begin_epoch(self, epoch: int, perm: np.ndarray):
@@ -150,7 +162,9 @@ class StepRunner:
         if perm.size != self.num_train:
             raise ValueError("permutation length changed; build a new StepRunner")
         staged = torch.from_numpy(perm.astype(np.int32)).pin_memory()
-        # an in-flight prep pass may still read perm / cursor
+        # the caller's queued work (model / cache updates) first, and an
+        # in-flight prep pass may still read perm / cursor
+        self._join_current()
         self.stream.wait_stream(self.prep_stream)
         with torch.cuda.stream(self.stream):
             self.perm.copy_(staged, non_blocking=True)
@@ -529,6 +543,7 @@ class StepRunner:
         # D2H read-back needs no copy node between the step's kernels
         self._loss_hring = torch.zeros(self.ring_len, dtype=torch.float64, pin_memory=True)
         self._win_ev = [torch.cuda.Event() for _ in range(2)]
+        self._join_current()
         self._grp_ev = [torch.cuda.Event() for _ in self.groups]
         phases = {}
         for gi, grp in enumerate(self.groups):
