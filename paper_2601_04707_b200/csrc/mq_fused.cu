@@ -527,6 +527,16 @@ constexpr int kHeadRows = 8;               // target rows per CTA: one warp per 
 #endif
 constexpr int kHeadWarps = MQ_HEAD_WARPS_PER_ROW * kHeadRows;
 constexpr int kHeadThreads = 32 * kHeadWarps;
+constexpr int kHeadKq = 8;  // k slices of the logits product
+constexpr int kHeadCq = 4;  // class slices of the dt product
+static_assert(kHeadRows == 8, "the dt product reads dlT as two float4 per class");
+
+__host__ __device__ inline int head_red_floats(int d, int C) {
+  const int d2p = (2 * d + 3) & ~3;
+  const int a = kHeadKq * kHeadRows * C, b = kHeadCq * kHeadRows * 2 * d;
+  return ((a > b ? a : b) + 3) & ~3;
+  (void)d2p;
+}
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
 __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
@@ -547,7 +557,9 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   float* Ws = smem;                 // [d2p][Cp]  (rows >= d2 zero)
   float* both = Ws + d2p * Cp;      // [R][d2p]   = [agg | h_dst | 0 pad]
   float* dl = both + R * d2p;       // [R][C]     logits, then dlogits
-  float* WsT = dl + R * C;          // [C][d2p]   W^T for dt = dl W^T (k contiguous)
+  float* dlT = dl + R * C;          // [C][R]     dlogits, class-major (dt operand)
+  float* red = dlT + R * C;         // slice sums of the logits / dt products
+  float* dts = red + head_red_floats(d, C);  // [R][d2p] dt = dl W^T
   __shared__ int32_t s_col[R][kHeadMaxEdges];
   __shared__ float s_val[R][kHeadMaxEdges];
   __shared__ int s_ne[R];
@@ -657,128 +669,153 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
   __syncthreads();
 
   htrace(2);
-  // 2. logits = both W: one (row, class) item per thread (all 256 busy),
-  //    float4 over k; consecutive classes read consecutive W columns.
-  for (int item = tid; item < R * C; item += kHeadThreads) {
-    const int r = item / C, c = item % C;
-    const float* br = both + r * d2p;
-    float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < d2p; k += 4) {
-      const float4 b = *reinterpret_cast<const float4*>(br + k);
-      acc0 = fmaf(b.x, Ws[(k + 0) * Cp + c], acc0);
-      acc1 = fmaf(b.y, Ws[(k + 1) * Cp + c], acc1);
-      acc0 = fmaf(b.z, Ws[(k + 2) * Cp + c], acc0);
-      acc1 = fmaf(b.w, Ws[(k + 3) * Cp + c], acc1);
+  // 2. logits = both W, register-blocked over the CTA's R rows: thread
+  //    (class c, k slice kq) reads each W element once and the R rows' k slice
+  //    as broadcasts; the kHeadKq slice sums are combined in slice order.
+  {
+    const int kr = ((d2p / 4 + kHeadKq - 1) / kHeadKq) * 4;
+    for (int item = tid; item < C * kHeadKq; item += kHeadThreads) {
+      const int c = item % C, kq = item / C;
+      const int k0 = kq * kr, k1 = min(d2p, k0 + kr);
+      float acc[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) acc[i] = 0.f;
+      for (int k = k0; k < k1; k += 4) {
+        const float w0 = Ws[(k + 0) * Cp + c], w1 = Ws[(k + 1) * Cp + c];
+        const float w2 = Ws[(k + 2) * Cp + c], w3 = Ws[(k + 3) * Cp + c];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const float4 x = *reinterpret_cast<const float4*>(both + i * d2p + k);
+          acc[i] = fmaf(x.w, w3, fmaf(x.z, w2, fmaf(x.y, w1, fmaf(x.x, w0, acc[i]))));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) red[(kq * R + i) * C + c] = acc[i];
     }
-    dl[r * C + c] = acc0 + acc1;
-  }
-  // W^T (smem -> smem, conflict-free: Cp is odd) for dt = dl W^T in phase 4
-  if (a.dh != nullptr) {
-    for (int c = warp; c < C; c += kHeadWarps)  // warp per class, lanes over k
-      for (int k = lane; k < d2p; k += 32) WsT[c * d2p + k] = Ws[k * Cp + c];
+    __syncthreads();
+    for (int item = tid; item < R * C; item += kHeadThreads) {
+      float v = 0.f;
+#pragma unroll
+      for (int kq = 0; kq < kHeadKq; ++kq) v += red[kq * R * C + item];
+      dl[item] = v;
+    }
   }
   __syncthreads();
 
   htrace(3);
-  // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot
+  // 3. summed softmax-CE (nn.py:141-156), dl <- softmax - onehot (row-major
+  //    for the dW partial, class-major in dlT for dt)
   if (row_warp) {
     float* x = dl + warp * C;
     double wloss = 0.0;
     int bad = 0;
     if (!live) {
-      for (int c = lane; c < C; c += 32) x[c] = 0.f;
+      for (int c = lane; c < C; c += 32) {
+        x[c] = 0.f;
+        dlT[c * R + warp] = 0.f;
+      }
     } else {
       lab = __shfl_sync(0xffffffffu, lab, 0);
       float m = -INFINITY;
       for (int c = lane; c < C; c += 32) m = fmaxf(m, x[c]);
 #pragma unroll
       for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      float s = 0.f;
-      for (int c = lane; c < C; c += 32) s += expf(x[c] - m);
+      float s = 0.f, shl = 0.f;
+      for (int c = lane; c < C; c += 32) {
+        const float sh = x[c] - m;
+        const float e = expf(sh);
+        if (c == lab) shl = sh;
+        s += e;
+        x[c] = e;
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       const float logd = logf(s);
       for (int c = lane; c < C; c += 32) {
-        const float sh = x[c] - m;
-        float p = expf(sh) / s;
+        float p = x[c] / s;
         if (c == lab) {
           p -= 1.f;
-          wloss += -(double)(sh - logd);
+          wloss += -(double)(shl - logd);
         }
         x[c] = p;
+        dlT[c * R + warp] = p;
         bad |= !isfinite(p);
       }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      wloss += __shfl_xor_sync(0xffffffffu, wloss, o);
-      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-    }
+    const unsigned any_loss = __ballot_sync(0xffffffffu, wloss != 0.0);
+    if (any_loss) wloss = __shfl_sync(0xffffffffu, wloss, __ffs(any_loss) - 1);
+    bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
       s_loss[warp] = wloss;
       if (bad) s_bad = 1;
     }
-    __syncwarp();
   }
+  __syncthreads();
 
   htrace(4);
-  // 4. dt = dl W^T -> dh: self half to the dst row, top half scattered over the
-  //    row's edges (dh zeroed for rows [0, n_src) beforehand).  A lane owns 4
-  //    consecutive k of [top | bot]; one v4 reduction per target row.
-  if (a.dh != nullptr && live) {
-    const float* x = dl + warp * C;
-    const bool v4 = (d & 3) == 0 && (a.lddh & 3) == 0 && ((uintptr_t)a.dh & 15) == 0;
-    if (v4) {
-      for (int kb = 4 * lane; kb < d2; kb += 128) {
-        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-        int c = 0;
-        for (; c + 2 <= C; c += 2) {
-          const float x0 = x[c], x1 = x[c + 1];
-          const float4 w0 = *reinterpret_cast<const float4*>(WsT + c * d2p + kb);
-          const float4 w1 = *reinterpret_cast<const float4*>(WsT + (c + 1) * d2p + kb);
-          a0.x = fmaf(x0, w0.x, a0.x);
-          a0.y = fmaf(x0, w0.y, a0.y);
-          a0.z = fmaf(x0, w0.z, a0.z);
-          a0.w = fmaf(x0, w0.w, a0.w);
-          a1.x = fmaf(x1, w1.x, a1.x);
-          a1.y = fmaf(x1, w1.y, a1.y);
-          a1.z = fmaf(x1, w1.z, a1.z);
-          a1.w = fmaf(x1, w1.w, a1.w);
-        }
-        if (c < C) {
-          const float x0 = x[c];
-          const float4 w0 = *reinterpret_cast<const float4*>(WsT + c * d2p + kb);
-          a0.x = fmaf(x0, w0.x, a0.x);
-          a0.y = fmaf(x0, w0.y, a0.y);
-          a0.z = fmaf(x0, w0.z, a0.z);
-          a0.w = fmaf(x0, w0.w, a0.w);
-        }
-        const float4 dt = make_float4(a0.x + a1.x, a0.y + a1.y, a0.z + a1.z, a0.w + a1.w);
-        if (kb >= d) {
-          atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)r * a.lddh + (kb - d)), dt);
-        } else {
-          for (int e = 0; e < ne; ++e) {
-            const float v = s_val[warp][e];
-            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)s_col[warp][e] * a.lddh + kb),
-                      make_float4(v * dt.x, v * dt.y, v * dt.z, v * dt.w));
+  // 4. dt = dl W^T (register-blocked like the logits: thread (k, class slice))
+  //    into dts, then dh += dt: the self half to the dst row, the top half
+  //    scattered over the row's edges (dh zeroed for rows [0, n_src)
+  //    beforehand) by both warps of each row.
+  if (a.dh != nullptr) {
+    const int cr = (C + kHeadCq - 1) / kHeadCq;
+    for (int item = tid; item < d2 * kHeadCq; item += kHeadThreads) {
+      const int k = item % d2, cq = item / d2;
+      const int c0 = cq * cr, c1 = min(C, c0 + cr);
+      float acc[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) acc[i] = 0.f;
+      for (int c = c0; c < c1; ++c) {
+        const float w = Ws[k * Cp + c];
+        const float4 p0 = *reinterpret_cast<const float4*>(dlT + c * R);
+        const float4 p1 = *reinterpret_cast<const float4*>(dlT + c * R + 4);
+        acc[0] = fmaf(p0.x, w, acc[0]);
+        acc[1] = fmaf(p0.y, w, acc[1]);
+        acc[2] = fmaf(p0.z, w, acc[2]);
+        acc[3] = fmaf(p0.w, w, acc[3]);
+        acc[4] = fmaf(p1.x, w, acc[4]);
+        acc[5] = fmaf(p1.y, w, acc[5]);
+        acc[6] = fmaf(p1.z, w, acc[6]);
+        acc[7] = fmaf(p1.w, w, acc[7]);
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) red[(cq * R + i) * d2 + k] = acc[i];
+    }
+    __syncthreads();
+    for (int item = tid; item < R * d2; item += kHeadThreads) {
+      float v = 0.f;
+#pragma unroll
+      for (int cq = 0; cq < kHeadCq; ++cq) v += red[cq * R * d2 + item];
+      dts[(item / d2) * d2p + item % d2] = v;
+    }
+    __syncthreads();
+    const int rw = warp % R;  // this warp's row; warps rw and rw + R share it
+    const int rr = blockIdx.x * R + rw;
+    if (rr < n) {
+      const int nrow = s_ne[rw];
+      const float* dtr = dts + rw * d2p;
+      const int t64 = (warp / R) * 32 + lane, nt = 32 * (kHeadWarps / R);
+      const bool v4 = (d & 3) == 0 && (a.lddh & 3) == 0 && ((uintptr_t)a.dh & 15) == 0;
+      if (v4) {
+        const int d4 = d >> 2;
+        for (int i = t64; i < (nrow + 1) * d4; i += nt) {
+          const int e = i / d4, j = 4 * (i % d4);
+          if (e == nrow) {
+            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)rr * a.lddh + j),
+                      *reinterpret_cast<const float4*>(dtr + d + j));
+          } else {
+            const float v = s_val[rw][e];
+            const float4 t = *reinterpret_cast<const float4*>(dtr + j);
+            atomicAdd(reinterpret_cast<float4*>(a.dh + (int64_t)s_col[rw][e] * a.lddh + j),
+                      make_float4(v * t.x, v * t.y, v * t.z, v * t.w));
           }
         }
-      }
-    } else {
-      for (int kb = 0; kb < d; kb += 32) {
-        const int k = kb + lane;
-        if (k >= d) continue;
-        float top = 0.f, bot = 0.f;
-        const float* wt = Ws + k * Cp;
-        const float* wb = Ws + (d + k) * Cp;
-        for (int c = 0; c < C; ++c) {
-          top = fmaf(x[c], wt[c], top);
-          bot = fmaf(x[c], wb[c], bot);
+      } else {
+        for (int i = t64; i < (nrow + 1) * d; i += nt) {
+          const int e = i / d, j = i % d;
+          if (e == nrow) atomicAdd(a.dh + (int64_t)rr * a.lddh + j, dtr[d + j]);
+          else atomicAdd(a.dh + (int64_t)s_col[rw][e] * a.lddh + j, s_val[rw][e] * dtr[j]);
         }
-        atomicAdd(a.dh + (int64_t)r * a.lddh + k, bot);
-        for (int e = 0; e < ne; ++e)
-          atomicAdd(a.dh + (int64_t)s_col[warp][e] * a.lddh + k, s_val[warp][e] * top);
       }
     }
   }
@@ -858,8 +895,9 @@ inline int head_rows(int) { return kHeadRows; }
 
 inline int64_t head_smem_bytes(int R, int d, int C) {
   const int Cp = C | 1, d2p = (2 * d + 3) & ~3;
-  // W, both, dl, W^T (+ the static edge stash)
-  return (int64_t)(d2p * Cp + R * d2p + R * C + C * d2p) * (int64_t)sizeof(float);
+  // W, both, dl, dlT, slice sums, dt (+ the static edge stash)
+  return (int64_t)(d2p * Cp + R * d2p + 2 * R * C + head_red_floats(d, C) + R * d2p) *
+         (int64_t)sizeof(float);
 }
 
 }  // namespace mq

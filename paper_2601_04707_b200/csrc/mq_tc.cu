@@ -37,6 +37,7 @@ constexpr int kThreads = 256;           // staging / epilogue warps 0-7
 constexpr int kBlock = kThreads + 32;    // + warp 8: TMEM owner and MMA issuer
 constexpr int kStages = 2;
 constexpr int kMaxN = 256;
+constexpr int kCoopTiles = 512;     // tiles covered by the cooperative split reduction
 constexpr int kMaxSplitsTc = 148;  // = SMs: a one-tile DW (d_in <= 128) still fills the GPU
 
 // ------------------------------------------------------------ PTX helpers
@@ -1028,11 +1029,81 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr, uint32_t lbo) {
          ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
 
+// Cooperative split reduction (deferred FWD / DW, S > 1): after a tile's S
+// split CTAs have stored their partials, each of them sums a 1/S row slice of
+// the tile over the S partials (fixed order p = 0..S-1, as fixed_order_sum)
+// and writes it into partial slot 0, and the kernel publishes nparts = 1: the
+// consumer (aggregation / optimizer) then reads ONE copy instead of S.  The S
+// CTAs of a tile meet on a per-tile arrival counter (all CTAs of the
+// persistent grid are co-resident: one per SM); the last to finish resets it.
+// coop[2 t] = arrivals, coop[2 t + 1] = departures; zero at rest.
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void coop_reduce_tile(float* __restrict__ part, int32_t* __restrict__ coop,
+                                                 int t, int s, int S, int Mout, int N, int etid) {
+  asm volatile("bar.sync 3, 128;" ::: "memory");  // the 4 epilogue warps stored this tile
+  if (etid == 0) {
+    __threadfence();
+    atomicAdd(&coop[2 * t], 1);
+    while (ld_acquire_gpu(&coop[2 * t]) < S) __nanosleep(40);
+    __threadfence();
+  }
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+  const int r0 = t * BM, nr = min(BM, Mout - r0);
+  const int lo = r0 + (s * nr) / S, hi = r0 + ((s + 1) * nr) / S;
+  const int64_t stride = (int64_t)Mout * N;
+  if ((N & 3) == 0) {
+    const int n4 = N >> 2;
+    for (int e = etid; e < (hi - lo) * n4; e += 128) {
+      const int64_t o = (int64_t)(lo + e / n4) * N + 4 * (e % n4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      int p = 0;
+      for (; p + 8 <= S; p += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldcg(reinterpret_cast<const float4*>(part + (p + u) * stride + o));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v.x += x[u].x;
+          v.y += x[u].y;
+          v.z += x[u].z;
+          v.w += x[u].w;
+        }
+      }
+      for (; p < S; ++p) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(part + p * stride + o));
+        v.x += x.x;
+        v.y += x.y;
+        v.z += x.z;
+        v.w += x.w;
+      }
+      *reinterpret_cast<float4*>(part + o) = v;
+    }
+  } else {
+    for (int e = etid; e < (hi - lo) * N; e += 128) {
+      const int64_t o = (int64_t)(lo + e / N) * N + e % N;
+      part[o] = fixed_order_sum(part + o, stride, S);
+    }
+  }
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+  if (etid == 0) {
+    __threadfence();
+    if (atomicAdd(&coop[2 * t + 1], 1) == S - 1) {
+      coop[2 * t + 1] = 0;
+      atomicExch(&coop[2 * t], 0);
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads2, 1)
     tc2_kernel(const __grid_constant__ Maps maps, Operands op, Geo geo, const int32_t* m_dev,
                int m_static, const int32_t* k_dev, int k_static, float* __restrict__ part,
-               int32_t* __restrict__ nparts_out, int ST) {
+               int32_t* __restrict__ nparts_out, int ST, int32_t* __restrict__ coop) {
   pdl_trigger();
   MQ_TL_BEGIN(MODE);
   if (threadIdx.x == 0) trace_at(0);
@@ -1047,10 +1118,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int K = k_dev ? *k_dev : k_static;
   const int Np = op.Np;
   const Work wk = work2(MODE, geo, M, K, gridDim.x);
+  // the S partials of a tile are summed in place (coop_reduce_tile)
+  const bool coop_on = coop != nullptr && wk.S > 1 && swapped(MODE);
   // published after the wait (see tc_gemm_kernel): the previous window's
   // optimizer may still read this counter when the grid starts
   auto publish_nparts = [&]() {
-    if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = wk.S;
+    if (nparts_out != nullptr && blockIdx.x == 0 && tid == 0) *nparts_out = coop_on ? 1 : wk.S;
   };
   const int G = (int)gridDim.x / wk.S;  // CTAs per split
   const int b = blockIdx.x;
@@ -1406,6 +1479,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         __syncwarp();
         if (warp == 10 && lane == 0 && ti < 1) trace_at(27);
         if (lane == 0) mbar_arrive(&acce[ab]);
+        if (coop_on) coop_reduce_tile(part, coop, t, s, wk.S, Mout, op.N, tid - 320);
         continue;
       }
       const int p = t * BM + q * 32 + lane;  // row in the (padded) M space
@@ -1532,11 +1606,18 @@ static bool tmap2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+inline int64_t tc_part_floats_base(int64_t m_max, int64_t n);
+static int g_tc_coop = -1;  // cooperative split reduction of the deferred FWD / DW (MQ_TC2_COOP)
+
 template <int MODE, class Epi>
 int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
             const int32_t* k_dev, int k_static, int k_max, float* part, const Epi& epi,
             cudaStream_t s, int kid, int kid_red, bool skip_reduce, int32_t* nparts_out) {
   using namespace tc;
+  if (g_tc_coop < 0) {
+    const char* e = getenv("MQ_TC2_COOP");
+    g_tc_coop = e ? atoi(e) : 0;
+  }
   if (!g_tc_v2 || op.Np > kMaxN2) return -1;
   // DW (X^T G, both operands MN-major) runs swapped, transposing X^T.  In the
   // fused step (deferred partials) it wins at every width (Reddit's 602-d
@@ -1598,10 +1679,17 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
     }();
     if (cap2 > 0 && grid > cap2) grid = cap2;
   }
+  // deferred swapped products (FWD Y parts, DW parts): the split CTAs of a
+  // tile sum their partials in place; counters live in the buffer's tail
+  int32_t* coop = nullptr;
+  const int64_t mrow = MODE == kDwCat ? 2 * ((m_max + 31) / 32 * 32) : (m_max < 1 ? 1 : m_max);
+  if (g_tc_coop && skip_reduce && nparts_out != nullptr && swapped(MODE) &&
+      (mrow + BM - 1) / BM <= kCoopTiles)
+    coop = reinterpret_cast<int32_t*>(part + tc_part_floats_base(m_max, op.N));
   {
     ProfScope ps(kid, s);
     MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2), (size_t)(ST * SB + 1024), s, mp,
-                     op, geo, m_dev, m_static, k_dev, k_static, part, nparts_out, ST));
+                     op, geo, m_dev, m_static, k_dev, k_static, part, nparts_out, ST, coop));
   }
   MQ_LAUNCH_CHECK("tc2_gemm");
   if (skip_reduce) return MQ_OK;
@@ -1669,11 +1757,16 @@ int run_tc_gemm(const tc::Operands& op, const int32_t* m_dev, int m_static, int 
 
 // floats of partials the tc path may write for an (m_max x n) output: the
 // device picks S <= ceil(grid / tiles_m), so S*M <= grid*BM + M.
-inline int64_t tc_part_floats(int64_t m_max, int64_t n) {
+inline int64_t tc_part_floats_base(int64_t m_max, int64_t n) {
   if (m_max < 1) m_max = 1;
   const int64_t a = (int64_t)tc::kMaxSplitsTc * m_max;
   const int64_t b = (int64_t)kNumSMs * tc::BM + m_max;
   return (a < b ? a : b) * n;
+}
+// + the cooperative reduction's per-tile counters (zeroed with the buffer,
+// left at zero by every launch)
+inline int64_t tc_part_floats(int64_t m_max, int64_t n) {
+  return tc_part_floats_base(m_max, n) + 2 * tc::kCoopTiles;
 }
 
 }  // namespace mq
