@@ -37,6 +37,7 @@ extern "C" {
 #define MQ_ERR_ARG 1
 #define MQ_ERR_CUDA 2
 #define MQ_ERR_STATE 3
+#define MQ_ERR_SAMPLING 4 /* SamplingError (samplers.py:23-24): empty candidates, zero norms */
 
 #define MQ_MAX_FANOUT 32
 /* ranks of one RaCoM exchange / shards of a partitioned feature store */
@@ -606,6 +607,74 @@ int mq_racom_apply(const mq_peer_exchange* ex, int32_t optimizer /* 0 adam, 1 sg
 /* counters[0..1] and the flag words of this rank's arena, read back (tests) */
 int mq_peer_state(const mq_peer_exchange* ex, unsigned long long* out4 /* pub, applied, min flag, max flag */,
                   void* stream);
+
+/* ------------------------------------------------- layer-wise samplers
+ * LADIES / FastGCN (samplers.py:233-495) and the GCN node-wise arm
+ * (samplers.py:178-191).  Graph = the loop-stripped CSR plus `loops` (stored
+ * self loops per node, NULL when none): the restricted Laplacian rows and
+ * a_hat_degrees are rebuilt from it exactly as the reference computes them
+ * on the stored CSR.  Draws follow the layer contract (oracle/layerwise.py):
+ * layer l of batch b reads uniforms from the Philox stream (seed, epoch;
+ * ctr (i, 0xFFFFFFFF, l, b)).  These calls are host-orchestrated and
+ * SYNCHRONISE their stream (the reference API they mirror returns arrays);
+ * their temporaries come from the stream-ordered allocator. */
+
+/* restricted-row offsets of prev (loop-stripped degree + loop entries),
+ * roff[n_prev + 1]; roff[n_prev] = entries.  scratch: mq_layer_scratch_bytes. */
+int64_t mq_layer_scratch_bytes(int64_t n_max);
+int mq_layer_entries(const int64_t* row_off, const int32_t* loops, const int32_t* prev,
+                     int32_t n_prev, int64_t* roff, void* scratch, void* stream);
+/* sample_ladies's target filter (samplers.py:453-458): targets with a stored
+ * out-degree > 0, in order; *count_dev = kept. */
+int mq_layer_live_targets(const int64_t* row_off, const int32_t* loops, const int32_t* targets,
+                          int32_t n, int32_t* out, int64_t* count_dev, void* scratch, void* stream);
+/* fastgcn_probs (samplers.py:314-318) over all nodes (flat: unsquared
+ * norms); cdf (optional, n_nodes) = the normalised cumulative sum the
+ * with-replacement draw searches (NumPy's choice(p) algorithm). */
+int mq_layer_fastgcn_probs(const int64_t* row_off, const int32_t* col, const int32_t* loops,
+                           int64_t n_nodes, int32_t flat, double* probs, double* cdf, void* stream);
+/* One layer-wise block (samplers.py:376-440).  probs_global == NULL: LADIES
+ * (candidates = sorted unique neighbours of prev, probabilities = squared or,
+ * with flat, unsquared restricted column norms, normalised by NumPy's
+ * pairwise sum; node_flags (n bytes, zero, left zero) and node_pos (n ints)
+ * are the caller's per-graph tables); else FastGCN over all nodes with the
+ * given probabilities (and cdf_global for mode 1).  mode: 0 = WOR with row
+ * normalisation, 1 = with replacement (counts / (s p)), 2 = debias (WOR with
+ * the recursive coefficients).  Outputs: rows/cols/values/effective
+ * [n_entries] (nnz used; rows nondecreasing, cols index src_ids), row_ptr
+ * [n_prev + 1], src_ids / sample_probs [budget] (n_src used, ascending node
+ * ids), counts[4] = {nnz, n_src, n_cand, s}.  Returns MQ_ERR_SAMPLING for an
+ * empty candidate set or all-zero norms. */
+int mq_layer_block(const int64_t* row_off, const int32_t* col, const int32_t* loops,
+                   int64_t n_nodes, const int32_t* prev, int32_t n_prev, const int64_t* roff,
+                   int64_t n_entries, const double* probs_global, const double* cdf_global,
+                   int32_t flat, int32_t mode, int32_t budget, uint64_t seed, uint64_t epoch,
+                   uint32_t batch, uint32_t layer, uint8_t* node_flags, int32_t* node_pos,
+                   int32_t* rows, int32_t* cols, double* values, double* effective,
+                   int32_t* row_ptr, int32_t* src_ids, double* sample_probs, int64_t* counts,
+                   void* stream);
+/* GCN arm of node_wise_block from the SAGE block of the same draws: per row
+ * the self entry (r, r, 1/deg_hat[v]) then the sampled entries with
+ * (n/s) / sqrt(deg_hat[v] deg_hat[u]).  Outputs sized nnz + n_dst. */
+int mq_gcn_block(const int64_t* row_off, const int32_t* loops, const int32_t* dst,
+                 const int32_t* src_ids, const int32_t* row_ptr, const int32_t* cols, int32_t n_dst,
+                 int32_t* row_ptr_out, int32_t* rows_out, int32_t* cols_out, double* vals_out,
+                 void* stream);
+/* NumPy's choice(p) cdf: cumsum(p) (sequential f64) / its last element */
+int mq_layer_cdf(const double* probs, int64_t n, double* cdf, void* stream);
+/* host reference of the layer uniforms (tests) */
+int mq_layer_uniforms_host(uint64_t seed, uint64_t epoch, uint32_t batch, uint32_t layer, int64_t n,
+                           double* out);
+
+/* GCN layer transform (nn.py:102-113, 159-180 gcn arm): z = agg W (relu_out
+ * = max(z, 0) when given); backward dW = agg^T dz and dt = dz W^T.  fp32
+ * split-K, fixed-order reduction (scratch: mq_linear_scratch_bytes). */
+int mq_gcn_linear_fwd(const float* agg, int32_t ldagg, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, float* z, int32_t ldz,
+                      float* relu_out, int32_t ldr, void* scratch, void* stream);
+int mq_gcn_linear_bwd(const float* agg, int32_t ldagg, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, const float* dz, int32_t lddz,
+                      float* dW, float* dt, int32_t lddt, void* scratch, void* stream);
 
 /* ------------------------------------------------------------- tracing
  * Trace / TraceEvent (pipeline.py:30-98): when the stream reaches the call,

@@ -11,8 +11,9 @@ from .cache import (DeviceCache, RefreshStream, cache_probs_degree, cache_probs_
                     weighted_sample_without_replacement)
 from .samplers import (Block, MiniBatch, PhiloxStream, SamplerParams, SamplingError,
                        build_minibatch, node_wise_block, sample_node_wise)
+from .layerwise import LayerBlock, fastgcn_probs, sample_fastgcn, sample_ladies
 from .nn import (ModelState, accuracy, adam_step, backward, batch_loss, evaluate, forward,
-                 full_forward, init_model,
+                 full_forward, gcn_forward, init_model,
                  loss_and_grads, sage_forward, sgd_step)
 from .racom import (DistExchange, LocalExchange, WindowDriver, apply_update, compute_sync_period,
                     staleness_cost, sync_models)

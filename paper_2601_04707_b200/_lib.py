@@ -138,6 +138,17 @@ SIGNATURES = {
     "mq_racom_publish": (C.c_int, [P, P, P, P, P]),
     "mq_racom_apply": (C.c_int, [P, I32, I32, P, P, P, P, P, I32, P, P, P]),
     "mq_peer_state": (C.c_int, [P, P, P]),
+    "mq_layer_scratch_bytes": (I64, [I64]),
+    "mq_layer_entries": (C.c_int, [P, P, P, I32, P, P, P]),
+    "mq_layer_live_targets": (C.c_int, [P, P, P, I32, P, P, P, P]),
+    "mq_layer_fastgcn_probs": (C.c_int, [P, P, P, I64, I32, P, P, P]),
+    "mq_layer_block": (C.c_int, [P, P, P, I64, P, I32, P, I64, P, P, I32, I32, I32, U64, U64,
+                                 U32, U32, P, P, P, P, P, P, P, P, P, P, P]),
+    "mq_gcn_block": (C.c_int, [P, P, P, P, P, P, I32, P, P, P, P, P]),
+    "mq_layer_uniforms_host": (C.c_int, [U64, U64, U32, U32, I64, P]),
+    "mq_layer_cdf": (C.c_int, [P, I64, P, P]),
+    "mq_gcn_linear_fwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, I32, P, I32, P, P]),
+    "mq_gcn_linear_bwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, I32, P, P, I32, P, P]),
 }
 
 _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
@@ -149,6 +160,14 @@ _INT_STATUS = {name for name, (res, _) in SIGNATURES.items()
 
 class MQError(RuntimeError):
     """A libmqgnn call failed (argument, CUDA or state error)."""
+
+
+class MQSamplingError(MQError):
+    """MQ_ERR_SAMPLING: the layer-wise sampler's SamplingError (empty
+    candidate set, all-zero column norms)."""
+
+
+MQ_ERR_SAMPLING = 4
 
 
 class _Lib:
@@ -173,6 +192,8 @@ class _Lib:
             rc = fn(*args)
             if rc != 0:
                 msg = self.dll.mq_last_error().decode(errors="replace")
+                if rc == MQ_ERR_SAMPLING:
+                    raise MQSamplingError(msg)
                 raise MQError(f"{name} failed ({rc}): {msg}")
             return rc
 

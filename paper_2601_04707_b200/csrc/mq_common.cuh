@@ -48,6 +48,17 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// resident blocks per SM of a kernel at this block size (>= 1)
+template <class K>
+inline int resident_blocks(K kernel, int threads, size_t smem = 0) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 1;
+  }
+  return n < 1 ? 1 : n;
+}
+
 constexpr int kNumSMs = 148;
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }

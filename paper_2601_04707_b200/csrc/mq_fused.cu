@@ -965,7 +965,14 @@ int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* 
   cudaStream_t s = as_stream(stream);
   const int warps = kAggThreads / 32;
   int blocks = ceil_div(n_dst_max < 1 ? 1 : n_dst_max, warps);
-  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  // one wave: the row bound is far above the live rows (Reddit: 11,264 vs
+  // ~2,000), and surplus blocks only queue behind the resident ones
+  {
+    static const int cap_parts = kNumSMs * resident_blocks(sage_aggregate_parts_kernel, kAggThreads);
+    static const int cap_plain = kNumSMs * resident_blocks(sage_aggregate_kernel, kAggThreads);
+    const int cap = y_nparts_dev ? cap_parts : cap_plain;
+    if (blocks > cap) blocks = cap;
+  }
   MQ_CHECK_ARG(!y_nparts_dev || (y_rows_dev && d_out % 2 == 0 && ldact % 2 == 0 &&
                                   ((uintptr_t)y & 7) == 0 && ((uintptr_t)act & 7) == 0),
                "mq_sage_aggregate: partial input needs y_rows_dev and even, aligned widths");
@@ -996,7 +1003,10 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
   cudaStream_t s = as_stream(stream);
   const int warps = kAggThreads / 32;
   int blocks = ceil_div(n_dst_max, warps);
-  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  {
+    static const int cap = kNumSMs * resident_blocks(sage_scatter_bwd_kernel, kAggThreads);
+    if (blocks > cap) blocks = cap;
+  }
   {
     ProfScope ps(K_SAGE_SCATTER, s);
     MQ_CUDA(launch_k(sage_scatter_bwd_kernel, dim3(blocks), dim3(kAggThreads), 0, s, row_ptr, cols, vals, n_dst_dev, dh, lddh,

@@ -78,4 +78,46 @@ int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t 
   return MQ_OK;
 }
 
+// ---- GCN arm (nn.py:102-113, 159-180): z = agg W, dW = agg^T dz, dt = dz W^T
+int mq_gcn_linear_fwd(const float* agg, int32_t ldagg, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, float* z, int32_t ldz,
+                      float* relu_out, int32_t ldr, void* scratch, void* stream) {
+  MQ_CHECK_ARG(agg && m_dev && W && (z || relu_out) && scratch, "mq_gcn_linear_fwd: null pointer");
+  MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldagg >= d_in && (!z || ldz >= d_out) &&
+                   (!relu_out || ldr >= d_out),
+               "mq_gcn_linear_fwd: bad dims");
+  if (m_max <= 0) return MQ_OK;
+  Dims dims{m_dev, 0, nullptr, d_in, d_out};
+  return run_gemm(ALoadRow{agg, ldagg}, BLoadRow{W, d_out, d_out}, EpiLinearFwd{z, ldz, relu_out, ldr},
+                  dims, m_max, d_in, kMaxSplits, reinterpret_cast<float*>(scratch), as_stream(stream),
+                  K_GCN_LINEAR, K_GCN_LINEAR_REDUCE);
+}
+
+int mq_gcn_linear_bwd(const float* agg, int32_t ldagg, const int32_t* m_dev, int32_t m_max,
+                      int32_t d_in, const float* W, int32_t d_out, const float* dz, int32_t lddz,
+                      float* dW, float* dt, int32_t lddt, void* scratch, void* stream) {
+  MQ_CHECK_ARG(agg && m_dev && W && dz && dW && scratch, "mq_gcn_linear_bwd: null pointer");
+  MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && ldagg >= d_in && ldagg % 4 == 0 && lddz >= d_out &&
+                   (uintptr_t)agg % 16 == 0 && (!dt || lddt >= d_in),
+               "mq_gcn_linear_bwd: agg needs a 16-byte-aligned pitch (multiple of 4) >= d_in");
+  cudaStream_t s = as_stream(stream);
+  float* part = reinterpret_cast<float*>(scratch);
+  {
+    // dW rows over the padded pitch (pad columns of agg are zero, dropped by the epilogue)
+    Dims dims{nullptr, ldagg, m_dev, 0, d_out};
+    int rc = run_gemm(ALoadConcatT{agg, agg, ldagg}, BLoadRow{dz, lddz, d_out},
+                      EpiDW{dW, ldagg, d_in, d_out}, dims, ldagg, m_max, kMaxSplits, part, s,
+                      K_GCN_LINEAR, K_GCN_LINEAR_REDUCE);
+    if (rc) return rc;
+  }
+  if (dt != nullptr && m_max > 0) {
+    Dims dims{m_dev, 0, nullptr, d_out, d_in};
+    int rc = run_gemm(ALoadRow{dz, lddz}, BLoadWT{W, d_out, d_out, d_in}, EpiStore{dt, lddt}, dims,
+                      m_max, d_out, (d_out + GBK - 1) / GBK, part, s, K_GCN_LINEAR,
+                      K_GCN_LINEAR_REDUCE);
+    if (rc) return rc;
+  }
+  return MQ_OK;
+}
+
 }  // extern "C"

@@ -56,7 +56,10 @@
   X(K_SAGE_AF_DW, "sage_linear_af_dw")          \
   X(K_INGEST, "ingest")                         \
   X(K_RACOM_PUBLISH, "racom_publish")           \
-  X(K_RACOM_APPLY, "racom_apply")
+  X(K_RACOM_APPLY, "racom_apply")               \
+  X(K_LAYERWISE, "layerwise")                   \
+  X(K_GCN_LINEAR, "gcn_linear")                 \
+  X(K_GCN_LINEAR_REDUCE, "gcn_linear_reduce")
 
 namespace mq {
 enum KernelId {

@@ -429,6 +429,48 @@ const PwPlan& pw_plan(int64_t n) {
 }
 
 }  // namespace rf
+
+// NumPy's pairwise sum of a device f64 array of host-known length into
+// *total (the refresh's level-parallel replay of the summation tree); the
+// tree's temporaries come from the stream-ordered allocator.
+int pairwise_total(const double* a, int64_t n, double* total, cudaStream_t s) {
+  MQ_CHECK_ARG(a && total && n > 0, "pairwise_total: bad arguments");
+  const rf::PwPlan& plan = rf::pw_plan(n);
+  const int64_t nl = (int64_t)plan.starts.size();
+  const int64_t ni = (int64_t)plan.left.size();
+  void* mem = nullptr;
+  const size_t bytes = 8 * (size_t)(nl + ni) + 8 * (size_t)nl + 4 * (size_t)(2 * ni) + 16;
+  MQ_CUDA(cudaMallocAsync(&mem, bytes, s));
+  double* sums = static_cast<double*>(mem);
+  int64_t* starts = reinterpret_cast<int64_t*>(sums + nl + ni);
+  int32_t* lft = reinterpret_cast<int32_t*>(starts + nl);
+  int32_t* rgt = lft + ni;
+  cudaError_t e = cudaMemcpyAsync(starts, plan.starts.data(), sizeof(int64_t) * nl,
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && ni)
+    e = cudaMemcpyAsync(lft, plan.left.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && ni)
+    e = cudaMemcpyAsync(rgt, plan.right.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    rf::pw_leaves_kernel<<<rf::grid_for(nl), rf::kThreads, 0, s>>>(a, starts, nl, n, sums);
+    int64_t lo = 0;
+    for (int64_t hi : plan.level_end) {
+      rf::pw_level_kernel<<<rf::grid_for(hi - lo), rf::kThreads, 0, s>>>(sums, lft, rgt, lo, hi, nl);
+      lo = hi;
+    }
+    rf::pw_total_kernel<<<1, 32, 0, s>>>(sums, plan.root, total);
+    e = cudaGetLastError();
+  }
+  // the host plan vectors are read by the async copies: keep them alive (the
+  // plan cache owns them) and free the device tree in stream order
+  cudaFreeAsync(mem, s);
+  if (e != cudaSuccess) {
+    set_error("pairwise_total: %s", cudaGetErrorString(e));
+    return MQ_ERR_CUDA;
+  }
+  return MQ_OK;
+}
+
 }  // namespace mq
 
 using namespace mq;

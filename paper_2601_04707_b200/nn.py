@@ -35,8 +35,8 @@ class ModelState:
 
     def __init__(self, weights, arch: str = "sage", learning_rate: float = 0.001,
                  step_count: int = 0, m=None, v=None, device=None):
-        if arch != "sage":
-            raise NotImplementedError("the B200 path implements the GraphSAGE arch")
+        if arch not in ("sage", "gcn"):
+            raise ValueError(f"unknown arch {arch!r}")
         dev = torch.device(device or (weights[0].device if isinstance(weights[0], torch.Tensor)
                                       and weights[0].is_cuda else "cuda"))
         self.arch = arch
@@ -85,13 +85,13 @@ class ModelState:
                 [v.cpu().numpy() for v in self.v])
 
 
-def glorot_weights(feature_dim, hidden_dim, num_classes, num_layers=2, seed=0):
-    """Same draws as nn.py:56-71 (NumPy default_rng(seed), SAGE fan-in 2x)."""
+def glorot_weights(feature_dim, hidden_dim, num_classes, num_layers=2, seed=0, arch="sage"):
+    """Same draws as nn.py:56-71 (NumPy default_rng(seed); SAGE fan-in 2x)."""
     rng = np.random.default_rng(seed)
     dims = [feature_dim] + [hidden_dim] * (num_layers - 1) + [num_classes]
     out = []
     for l in range(num_layers):
-        fan_in, fan_out = dims[l] * 2, dims[l + 1]
+        fan_in, fan_out = dims[l] * (2 if arch == "sage" else 1), dims[l + 1]
         limit = np.sqrt(6.0 / (fan_in + fan_out))
         out.append(rng.uniform(-limit, limit, size=(fan_in, fan_out)).astype(np.float32))
     return out
@@ -102,7 +102,9 @@ def init_model(feature_dim: int, hidden_dim: int, num_classes: int, num_layers: 
                dtype=np.float32, device=None) -> ModelState:
     if np.dtype(dtype) != np.float32:
         raise NotImplementedError("the device path trains in float32 (nn.py default)")
-    w = glorot_weights(feature_dim, hidden_dim, num_classes, num_layers, seed)
+    if arch not in ("sage", "gcn"):
+        raise ValueError(f"unknown arch {arch!r}")
+    w = glorot_weights(feature_dim, hidden_dim, num_classes, num_layers, seed, arch=arch)
     return ModelState(w, arch=arch, learning_rate=learning_rate, device=device)
 
 
@@ -162,7 +164,41 @@ def sage_forward(batch, state: ModelState, return_cache: bool = False):
     return (h, cache) if return_cache else h
 
 
-forward = sage_forward
+def gcn_forward(batch, state: ModelState, return_cache: bool = False):
+    """GCN arm (nn.py:102-113): agg = block_apply(effective values), z = agg W,
+    ReLU except the last layer."""
+    dev = state.device
+    stream = current_stream(dev)
+    h = batch.features.to(device=dev, dtype=torch.float32)
+    cache = {"inputs": [], "pre": []}
+    L = len(batch.layers)
+    for l, blk in enumerate(batch.layers):
+        d_in = int(h.shape[1])
+        ld = round_up(d_in, 4)
+        hp = _pitched(h, ld)
+        nd = blk.num_dst
+        nd_dev = torch.tensor([nd], dtype=torch.int32, device=dev)
+        agg = torch.zeros((max(nd, 1), ld), dtype=torch.float32, device=dev)
+        lib().mq_spmm_fwd(ptr(blk.row_ptr), ptr(blk.cols), ptr(blk.values), ptr(nd_dev), nd,
+                          ptr(hp), ld, d_in, ptr(agg), ld, stream)
+        W = state.weights[l]
+        d_out = int(W.shape[1])
+        z = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev)
+        r = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev) if l < L - 1 else None
+        scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+                          dtype=torch.float32, device=dev)
+        lib().mq_gcn_linear_fwd(ptr(agg), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out, ptr(z), d_out,
+                                ptr(r), d_out, ptr(scr), stream)
+        cache["inputs"].append((hp, agg, blk, nd_dev, d_in))
+        cache["pre"].append(z[:nd])
+        h = r[:nd] if l < L - 1 else z[:nd]
+    _finite_or_raise("gcn_forward output", h)
+    return (h, cache) if return_cache else h
+
+
+def forward(batch, state: ModelState, return_cache: bool = False):
+    fn = sage_forward if state.arch == "sage" else gcn_forward
+    return fn(batch, state, return_cache=return_cache)
 
 
 def batch_loss(logits: torch.Tensor, labels):
@@ -182,8 +218,47 @@ def batch_loss(logits: torch.Tensor, labels):
     return float(loss.item()), dl[:n]
 
 
+def _gcn_backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
+    """GCN arm of nn.py:159-180: dW = agg^T dz, dh = block_apply_t(dz W^T)."""
+    dev = state.device
+    stream = current_stream(dev)
+    L = len(batch.layers)
+    grads = [None] * L
+    dz = dlogits.contiguous().to(torch.float32)
+    lddz = int(dz.shape[1])
+    zero = torch.zeros(1, dtype=torch.int32, device=dev)
+    for l in range(L - 1, -1, -1):
+        hp, agg, blk, nd_dev, d_in = cache["inputs"][l]
+        ld = int(hp.shape[1])
+        nd = blk.num_dst
+        W = state.weights[l]
+        d_out = int(W.shape[1])
+        dW = torch.empty_like(W)
+        scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+                          dtype=torch.float32, device=dev)
+        dt = (torch.zeros((max(nd, 1), 2 * d_in), dtype=torch.float32, device=dev)
+              if l > 0 else None)
+        lib().mq_gcn_linear_bwd(ptr(agg), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out, ptr(dz), lddz,
+                                ptr(dW), ptr(dt), 2 * d_in, ptr(scr), stream)
+        grads[l] = dW
+        if l > 0:
+            ns = blk.num_src
+            counts = torch.tensor([ns, blk.nnz], dtype=torch.int32, device=dev)
+            dh = torch.empty((max(ns, 1), ld), dtype=torch.float32, device=dev)
+            # no self half: the init pass sees zero dst rows (every dh row starts at 0)
+            lib().mq_spmm_bwd(ptr(blk.rows), ptr(blk.cols), ptr(blk.values), ptr(counts), blk.nnz,
+                              ptr(zero), ns, ptr(dt), 2 * d_in, d_in, ptr(hp), ld, ptr(dh), ld,
+                              stream)
+            dz, lddz = dh, ld
+    for g in grads:
+        _finite_or_raise("backward", g)
+    return grads
+
+
 def backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
     """Weight gradients, last layer first (nn.py:159-180)."""
+    if state.arch == "gcn":
+        return _gcn_backward(batch, state, cache, dlogits)
     dev = state.device
     stream = current_stream(dev)
     L = len(batch.layers)

@@ -28,8 +28,7 @@ from .engine import SampleWorkspace, current_stream
 from .graph import DeviceGraph
 
 
-class SamplingError(RuntimeError):
-    """Raised when a layer cannot be built (samplers.py:23-24)."""
+from .layerwise import LayerBlock, SamplingError, gcn_block_from_sage, sample_fastgcn, sample_ladies
 
 
 @dataclass(frozen=True)
@@ -50,7 +49,7 @@ class PhiloxStream:
 class SamplerParams:
     method: str = "sage"
     fanout: object = 5            # int (every hop) or tuple (hop 0 = seeds)
-    nodes_per_layer: int = 512    # layer-wise methods: out of scope here
+    nodes_per_layer: int = 512    # layer-wise methods (ladies, fastgcn)
     num_layers: int = 2
     flat: bool = False
     debias: bool = False
@@ -208,37 +207,60 @@ def _run_hops(g, targets, fanouts, rng: PhiloxStream, cache, hop0: int = 0):
 
 
 # ---------------------------------------------------------------- public API
+def _gcn_arm(g: DeviceGraph, blk: Block) -> LayerBlock:
+    """The GCN rows of a SAGE block of the same draws (samplers.py:178-191)."""
+    row_ptr, rows, cols, vals = gcn_block_from_sage(g, blk, blk.dst_ids)
+    return LayerBlock(rows=rows, cols=cols, values=vals.to(torch.float32), src_ids=blk.src_ids,
+                      dst_ids=blk.dst_ids, row_ptr=row_ptr, exact=vals, exact_effective=vals,
+                      dst_in_src=blk.dst_in_src)
+
+
+def _check_arch(arch):
+    if arch not in ("sage", "gcn"):
+        raise ValueError(f"unknown arch {arch!r}")
+
+
 def node_wise_block(g: DeviceGraph, dst_ids, fanout: int, rng: PhiloxStream,
-                    arch: str = "sage", cached_mask=None) -> Block:
-    """One SAGE block (samplers.py:142-210) at hop ``rng.hop``."""
-    if arch != "sage":
-        raise NotImplementedError("the B200 path implements the GraphSAGE arm (DESIGN.md §6)")
-    return _run_hops(g, dst_ids, (fanout,), rng, _as_cache(g, cached_mask), hop0=rng.hop)[0]
+                    arch: str = "gcn", cached_mask=None):
+    """One node-wise block (samplers.py:142-210) at hop ``rng.hop``: the SAGE
+    arm (mean weights 1/s) or the GCN arm (normalised adjacency entries)."""
+    _check_arch(arch)
+    blk = _run_hops(g, dst_ids, (fanout,), rng, _as_cache(g, cached_mask), hop0=rng.hop)[0]
+    return _gcn_arm(g, blk) if arch == "gcn" else blk
 
 
 def sample_node_wise(g: DeviceGraph, targets, fanout, layers: int, rng: PhiloxStream,
-                     arch: str = "sage", cached_mask=None) -> list:
+                     arch: str = "gcn", cached_mask=None) -> list:
     """Top-down hops, blocks returned bottom-up (samplers.py:213-226)."""
-    if arch != "sage":
-        raise NotImplementedError("the B200 path implements the GraphSAGE arm (DESIGN.md §6)")
+    _check_arch(arch)
     fanouts = tuple(fanout) if isinstance(fanout, (tuple, list)) else (int(fanout),) * layers
     if len(fanouts) != layers:
         raise ValueError("one fanout per layer required")
     blocks = _run_hops(g, targets, fanouts, rng, _as_cache(g, cached_mask))
+    if arch == "gcn":
+        blocks = [_gcn_arm(g, b) for b in blocks]
     blocks.reverse()
     return blocks
 
 
 def build_minibatch(g: DeviceGraph, targets, params: SamplerParams, rng: PhiloxStream,
                     batch_id: int = 0, epoch: int = 0, cached_mask=None) -> MiniBatch:
-    """Node-wise batch assembly (samplers.py:502-540): blocks, labels, input
-    features (gathered on device) and the cache hit/miss count."""
-    if params.method not in ("sage",):
-        raise NotImplementedError(
-            f"method {params.method!r}: the B200 path implements GraphSAGE node-wise sampling")
+    """Batch assembly (samplers.py:502-540): the method's blocks, labels,
+    input features (gathered on device) and the cache hit/miss count."""
     cache = _as_cache(g, cached_mask)
-    blocks = sample_node_wise(g, targets, params.hop_fanouts, params.num_layers, rng,
-                              arch="sage", cached_mask=cache)
+    dropped = 0
+    if params.method in ("gcn", "sage"):
+        blocks = sample_node_wise(g, targets, params.hop_fanouts, params.num_layers, rng,
+                                  arch=params.method, cached_mask=cache)
+    elif params.method == "ladies":
+        blocks, dropped = sample_ladies(g, targets, params.nodes_per_layer, params.num_layers,
+                                        rng, flat=params.flat, debias=params.debias,
+                                        replace=params.replace)
+    elif params.method == "fastgcn":
+        blocks = sample_fastgcn(g, targets, params.nodes_per_layer, params.num_layers, rng,
+                                flat=params.flat, debias=params.debias)
+    else:
+        raise ValueError(f"unknown method {params.method!r}")
     kept = blocks[-1].dst_ids
     input_ids = blocks[0].src_ids
     hits = misses = 0
@@ -249,4 +271,4 @@ def build_minibatch(g: DeviceGraph, targets, params: SamplerParams, rng: PhiloxS
     return MiniBatch(batch_id=batch_id, epoch=epoch, target_ids=kept,
                      target_labels=g.labels[kept.long()], layers=tuple(blocks),
                      input_ids=input_ids, features=feats, cache_hits=hits, cache_misses=misses,
-                     method=params.method)
+                     dropped_targets=dropped, method=params.method)

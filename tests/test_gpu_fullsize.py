@@ -45,7 +45,7 @@ def test_hop0_bit_exact_vs_oracle_full_batch(reddit):
     sg, g, cache, mask, ro, col, fanouts = reddit
     rng = np.random.default_rng(1)
     tg = rng.choice(np.flatnonzero(g.train_mask), size=1024, replace=False)
-    blk = mq.node_wise_block(g, tg, 10, mq.PhiloxStream(0, 0, 7, 0), cached_mask=cache)
+    blk = mq.node_wise_block(g, tg, 10, mq.PhiloxStream(0, 0, 7, 0), arch="sage", cached_mask=cache)
     ref = osamp.node_wise_block(ro, col, tg, 10, seed=0, epoch=0, batch_id=7, hop=0,
                                 cached_mask=mask)
     r = blk.to_reference()

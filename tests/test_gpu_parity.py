@@ -99,7 +99,7 @@ def test_node_wise_block_any_hop_vs_oracle(golden_sampling, graphs, hop):
     for fanout in (1, 2, 7, 16, 25, 32):
         dst = rng.choice(2000, size=300, replace=False)
         for mask, c in ((None, None), (golden_sampling["g2/mask10"], cache)):
-            blk = node_wise_block(dg, dst, fanout, PhiloxStream(5, 6, 7, hop), cached_mask=c)
+            blk = node_wise_block(dg, dst, fanout, PhiloxStream(5, 6, 7, hop), arch="sage", cached_mask=c)
             ref = osamp.node_wise_block(g2.row_offsets, g2.col_indices, dst, fanout, seed=5,
                                         epoch=6, batch_id=7, hop=hop, cached_mask=mask)
             r = blk.to_reference()
@@ -115,7 +115,7 @@ def test_duplicate_targets_and_empty_rows(graphs):
     hg = HostGraph(ro, col, np.eye(5, 4, dtype=np.float32), np.zeros(5, np.int32), 2)
     dg = DeviceGraph.from_csr(hg)
     tg = np.array([1, 3, 4, 1, 0])
-    blk = node_wise_block(dg, tg, 2, PhiloxStream(1, 2, 3))
+    blk = node_wise_block(dg, tg, 2, PhiloxStream(1, 2, 3), arch="sage")
     ref = osamp.node_wise_block(hg.row_offsets, hg.col_indices, tg, 2, seed=1, epoch=2,
                                 batch_id=3, hop=0)
     r = blk.to_reference()
