@@ -74,11 +74,26 @@ inline int grid_for(int64_t n, int per = kT) {
   return (int)(g < 1 ? 1 : (g > kNumSMs * 16 ? kNumSMs * 16 : g));
 }
 
+// the device's default pool keeps freed blocks (the calls synchronise their
+// stream; a zero release threshold would unmap the pool at every sync)
+inline void keep_pool() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  (void)cudaGetLastError();
+}
+
 // stream-ordered temporaries, freed at scope exit
 struct Tmp {
   cudaStream_t s;
   std::vector<void*> ptrs;
-  explicit Tmp(cudaStream_t st) : s(st) {}
+  explicit Tmp(cudaStream_t st) : s(st) { keep_pool(); }
   ~Tmp() {
     for (void* p : ptrs) cudaFreeAsync(p, s);
   }
@@ -103,42 +118,50 @@ struct LoadRowLen {
   }
 };
 
-// warp per row: entries in sorted column order with the loop entries at v's
-// sorted place; rrow, rcol, rval (f64); candidate flags of stored entries
-__global__ void restricted_kernel(Graph g, const int32_t* __restrict__ prev, int n_prev,
-                                  const int64_t* __restrict__ roff, int32_t* __restrict__ rrow,
-                                  int32_t* __restrict__ rcol, double* __restrict__ rval,
-                                  uint8_t* __restrict__ flag) {
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < n_prev; r += gridDim.x * wpb) {
+// p[r] = #stripped neighbours of prev[r] below prev[r] (rows are sorted):
+// where the loop entries go
+__global__ void loop_pos_kernel(Graph g, const int32_t* __restrict__ prev, int n_prev,
+                                int64_t* __restrict__ lpos) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_prev; r += gridDim.x * blockDim.x) {
     const int v = prev[r];
-    const int64_t a = g.row_off[v], deg = g.stripped(v);
+    int64_t lo = g.row_off[v], hi = g.row_off[v + 1];
+    const int64_t a = lo;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (g.col[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    lpos[r] = lo - a;
+  }
+}
+
+// thread per restricted entry (hub rows spread over the grid): row by binary
+// search in roff; entries in sorted column order with the loop entries at
+// v's sorted place; rrow, rcol, rval (f64); candidate flags of stored entries
+__global__ void restricted_kernel(Graph g, const int32_t* __restrict__ prev, int n_prev,
+                                  const int64_t* __restrict__ roff, const int64_t* __restrict__ lpos,
+                                  int64_t ne, int32_t* __restrict__ rrow, int32_t* __restrict__ rcol,
+                                  double* __restrict__ rval, uint8_t* __restrict__ flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_prev;  // last r with roff[r] <= e
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (roff[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int r = lo, v = prev[r];
+    const int64_t i = e - roff[r], p = lpos[r];
     const int lc = g.loop_copies(v);
-    const int64_t base = roff[r];
     const double dv = g.deg_hat(v);
-    // p = #neighbours < v (rows are sorted)
-    int64_t p = 0;
-    for (int64_t i0 = 0; i0 < deg; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const bool lt = i < deg && g.col[a + i] < v;
-      p += __popc(__ballot_sync(0xffffffffu, lt));
-    }
-    for (int64_t i = lane; i < deg; i += 32) {
-      const int c = g.col[a + i];
-      const int64_t e = base + i + (i >= p ? lc : 0);
-      rrow[e] = r;
-      rcol[e] = c;
-      rval[e] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dv, g.deg_hat(c))));
-      if (flag) flag[c] = 1;
-    }
-    for (int k = lane; k < lc; k += 32) {
-      const int64_t e = base + p + k;
-      rrow[e] = r;
-      rcol[e] = v;
-      rval[e] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dv, dv)));
-    }
-    if (flag && lane == 0 && g.nloop(v) > 0) flag[v] = 1;
+    int c;
+    if (i < p) c = g.col[g.row_off[v] + i];
+    else if (i < p + lc) c = v;
+    else c = g.col[g.row_off[v] + i - lc];
+    rrow[e] = r;
+    rcol[e] = c;
+    rval[e] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dv, g.deg_hat(c))));
+    if (flag && (c != v || g.nloop(v) > 0)) flag[c] = 1;
   }
 }
 
@@ -509,10 +532,12 @@ int mq_layer_fastgcn_probs(const int64_t* row_off, const int32_t* col, const int
   MQ_TMP(int32_t, rrow, ne);
   MQ_TMP(int32_t, rcol, ne);
   MQ_TMP(double, rval, ne);
+  MQ_TMP(int64_t, lpos, n_nodes);
   {
     ProfScope ps(K_LAYERWISE, s);
-    lw::restricted_kernel<<<lw::grid_for(n_nodes, lw::kT / 32), lw::kT, 0, s>>>(
-        g, prev, (int32_t)n_nodes, roff, rrow, rcol, rval, nullptr);
+    lw::loop_pos_kernel<<<lw::grid_for(n_nodes), lw::kT, 0, s>>>(g, prev, (int32_t)n_nodes, lpos);
+    lw::restricted_kernel<<<lw::grid_for(ne), lw::kT, 0, s>>>(g, prev, (int32_t)n_nodes, roff, lpos,
+                                                             ne, rrow, rcol, rval, nullptr);
   }
   MQ_LAUNCH_CHECK("restricted");
   MQ_TMP(uint32_t, key, ne);
@@ -583,10 +608,12 @@ int mq_layer_block(const int64_t* row_off, const int32_t* col, const int32_t* lo
   MQ_TMP(double, rval, ne);
   MQ_TMP(char, scr, scan_scratch_bytes(n_nodes > ne ? n_nodes : ne));
   MQ_TMP(int64_t, hc, 4);  // n_cand, positive, nnz, n_uniq
+  MQ_TMP(int64_t, lpos, n_prev);
   {
     ProfScope ps(K_LAYERWISE, s);
-    lw::restricted_kernel<<<lw::grid_for(n_prev, lw::kT / 32), lw::kT, 0, s>>>(
-        g, prev, n_prev, roff, rrow, rcol, rval, probs_global ? nullptr : node_flags);
+    lw::loop_pos_kernel<<<lw::grid_for(n_prev), lw::kT, 0, s>>>(g, prev, n_prev, lpos);
+    lw::restricted_kernel<<<lw::grid_for(ne), lw::kT, 0, s>>>(
+        g, prev, n_prev, roff, lpos, ne, rrow, rcol, rval, probs_global ? nullptr : node_flags);
   }
   MQ_LAUNCH_CHECK("restricted");
 
