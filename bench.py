@@ -613,7 +613,7 @@ def run_ours(args):
             if kd.get("tflops"):
                 roof["tflops_fp32_equiv"] = kd["tflops"]
         focus = {}
-        for nm in ("prep_sample", "prep_relabel", "prep_gather", "sage_aggregate_l0",
+        for nm in ("prep_sample", "prep_relabel", "prep_gather", "prep_pass", "sage_aggregate_l0",
                    "sage_head", "sage_transform_l0", "sage_transform_bwd_l0",
                    "sage_scatter_bwd_l0", "optimizer"):
             if nm in kern:

@@ -76,17 +76,31 @@ __global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm,
 // through the per-epoch residency index; the row's gathers are issued from
 // register arrays so a row costs ~4 dependent round trips
 // (dst -> offsets -> hot arcs -> columns), not 2*fanout.
+// With `tbl` the kernel also does the relabel's per-row bookkeeping (the
+// sampled rows are independent of it): the dst mark (dpos[v] = max row,
+// src_ids prefix, samplers.py:155-156) and every pick's first-occurrence
+// slot (first[u] = min over slots r * fanout + i: the slot order is the
+// triplet order, so the minimum is the first occurrence, samplers.py:186-189).
+struct RelabelTables {
+  QP<int32_t> dpos, first, src_ids;
+  bool on;
+};
+
 template <int MAXK>
 __global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
     const int64_t* __restrict__ row_off, const int32_t* __restrict__ col,
     const int64_t* __restrict__ hot_arc, const int64_t* __restrict__ hot_off, QP<const int32_t> dst,
     QP<const int32_t> n_dst, QP<const uint32_t> key, int fanout, uint32_t hop, QP<int32_t> nbr,
-    QP<int32_t> cnt) {
+    QP<int32_t> cnt, RelabelTables tbl) {
   const int q = blockIdx.y;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= *n_dst.at(q)) return;
   const uint32_t* k = key.at(q);
   const int32_t v = dst.at(q)[r];
+  if (tbl.on) {
+    tbl.src_ids.at(q)[r] = v;
+    atomicMax(&tbl.dpos.at(q)[v], r);
+  }
   const int64_t beg = row_off[v];
   const int n = (int)(row_off[v + 1] - beg);
   int64_t hb = 0;
@@ -103,6 +117,11 @@ __global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
 #pragma unroll
     for (int i = 0; i < MAXK; ++i)
       if (i < n) out[i] = x[i];
+    if (tbl.on) {
+#pragma unroll
+      for (int i = 0; i < MAXK; ++i)
+        if (i < n) atomicMin(&tbl.first.at(q)[x[i]], r * fanout + i);
+    }
     cnt.at(q)[r] = n;
     return;
   }
@@ -118,6 +137,11 @@ __global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
 #pragma unroll
     for (int j = 0; j < MAXK; ++j)
       if (j < fanout) out[j] = x[j];
+    if (tbl.on) {
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j)
+        if (j < fanout) atomicMin(&tbl.first.at(q)[x[j]], r * fanout + j);
+    }
   } else if (hot_off != nullptr) {  // samplers.py:173-175: hot ++ choice(cold, f - |hot|)
     int64_t ha[MAXK];
 #pragma unroll
@@ -145,6 +169,14 @@ __global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
 #pragma unroll
     for (int j = 0; j < MAXK; ++j)
       if (j < k2) out[nh + j] = y[j];
+    if (tbl.on) {
+#pragma unroll
+      for (int i = 0; i < MAXK; ++i)
+        if (i < nh) atomicMin(&tbl.first.at(q)[x[i]], r * fanout + i);
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j)
+        if (j < k2) atomicMin(&tbl.first.at(q)[y[j]], r * fanout + nh + j);
+    }
   } else {  // samplers.py:176-177: choice(nbrs, f)
     fisher_yates<MAXK, int>(rs, n, fanout, pos);
 #pragma unroll
@@ -152,29 +184,16 @@ __global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
 #pragma unroll
     for (int j = 0; j < MAXK; ++j)
       if (j < fanout) out[j] = x[j];
+    if (tbl.on) {
+#pragma unroll
+      for (int j = 0; j < MAXK; ++j)
+        if (j < fanout) atomicMin(&tbl.first.at(q)[x[j]], r * fanout + j);
+    }
   }
   cnt.at(q)[r] = fanout;
 }
 
 // ------------------------------------------------------------ relabel
-struct QLoadCnt {
-  QP<const int32_t> cnt;
-  QP<const int32_t> n_dst;
-  __device__ int64_t size() const { return *n_dst.at(blockIdx.y); }
-  __device__ int64_t operator()(int64_t i) const { return cnt.at(blockIdx.y)[i]; }
-};
-struct QStoreRowPtr {
-  QP<int32_t> row_ptr;
-  QP<int32_t> counts;  // counts[1] = nnz
-  __device__ void operator()(int64_t i, int64_t excl, int64_t) const {
-    row_ptr.at(blockIdx.y)[i] = (int32_t)excl;
-  }
-  __device__ void total(int64_t n, int64_t t) const {
-    row_ptr.at(blockIdx.y)[n] = (int32_t)t;
-    counts.at(blockIdx.y)[1] = (int32_t)t;
-  }
-};
-
 __global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP<int32_t> dpos,
                               QP<int32_t> src_ids) {
   const int q = blockIdx.y;
@@ -185,46 +204,58 @@ __global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP
   atomicMax(&dpos.at(q)[v], i);
 }
 
+// first[u] = min slot r * fanout + i of every pick u (sample_q_kernel does
+// this inline; this kernel serves passes whose sampling ran separately)
 __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
-                               QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
-                               QP<const int32_t> dpos, QP<int32_t> first) {
+                               QP<const int32_t> n_dst, int fanout, QP<int32_t> first) {
   const int q = blockIdx.y;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int r = (int)(s / fanout), i = (int)(s % fanout);
   if (r >= *n_dst.at(q) || i >= cnt.at(q)[r]) return;
-  const int32_t u = nbr.at(q)[s];
-  if (dpos.at(q)[u] < 0) atomicMin(&first.at(q)[u], row_ptr.at(q)[r] + i);
+  atomicMin(&first.at(q)[nbr.at(q)[s]], (int32_t)s);
 }
 
-struct QLoadFirstFlag {
-  QP<const int32_t> nbr, cnt, row_ptr, n_dst, dpos, first;
+// One scan per hop over the slots r * fanout + i, two channels in one int64:
+// high 32 bits = the row's triplet count at its first slot (prefix ->
+// row_ptr), low 32 bits = the first-occurrence flag of a new node (prefix ->
+// its label) -- the row offsets and the labels in one decoupled-look-back pass.
+struct QLoadRowFlag {
+  QP<const int32_t> nbr, cnt, n_dst, dpos, first;
   int fanout;
   __device__ int64_t size() const { return (int64_t)(*n_dst.at(blockIdx.y)) * fanout; }
   __device__ int64_t operator()(int64_t s) const {
     const int q = blockIdx.y;
     const int r = (int)(s / fanout), i = (int)(s % fanout);
-    if (i >= cnt.at(q)[r]) return 0;
-    const int32_t u = nbr.at(q)[s];
-    return (dpos.at(q)[u] < 0 && first.at(q)[u] == row_ptr.at(q)[r] + i) ? 1 : 0;
+    const int c = cnt.at(q)[r];
+    int64_t v = i == 0 ? ((int64_t)c << 32) : 0;
+    if (i < c) {
+      const int32_t u = nbr.at(q)[s];
+      if (dpos.at(q)[u] < 0 && first.at(q)[u] == (int32_t)s) v |= 1;
+    }
+    return v;
   }
 };
-struct QStoreLabel {
+struct QStoreRowLabel {
   QP<const int32_t> nbr, n_dst;
-  QP<int32_t> dpos, src_ids, counts;
+  QP<int32_t> dpos, src_ids, counts, row_ptr;
+  int fanout;
   __device__ void operator()(int64_t s, int64_t excl, int64_t val) const {
-    if (!val) return;
     const int q = blockIdx.y;
+    if (s % fanout == 0) row_ptr.at(q)[s / fanout] = (int32_t)(excl >> 32);
+    if (!(val & 1)) return;
     const int32_t u = nbr.at(q)[s];
-    const int32_t lab = *n_dst.at(q) + (int32_t)excl;
+    const int32_t lab = *n_dst.at(q) + (int32_t)(excl & 0xFFFFFFFFll);
     src_ids.at(q)[lab] = u;
     dpos.at(q)[u] = lab;
   }
   __device__ void total(int64_t, int64_t t) const {
     const int q = blockIdx.y;
-    counts.at(q)[0] = *n_dst.at(q) + (int32_t)t;
+    const int nd = *n_dst.at(q);
+    row_ptr.at(q)[nd] = (int32_t)(t >> 32);
+    counts.at(q)[1] = (int32_t)(t >> 32);
+    counts.at(q)[0] = nd + (int32_t)(t & 0xFFFFFFFFll);
   }
 };
-
 __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
                               QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
                               QP<const int32_t> dpos, QP<int32_t> rows, QP<int32_t> cols,
@@ -241,14 +272,20 @@ __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
   vals.at(q)[e] = (float)(1.0 / (double)c);  // float32(1.0 / s), samplers.py:200 + nn.py:85
 }
 
+// Table restore, once per pass: every node a hop touched (dst marks, new
+// labels, first-occurrence slots of any pick) is in that hop's src list, and
+// each hop's src list contains the previous one's, so the last hop's src list
+// covers them all.  (Within a pass the next hop's mark overwrites each entry
+// with the same or a larger position: no restore between hops.)
 __global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> counts,
-                               QP<const int32_t> n_dst, QP<int32_t> dpos, QP<int32_t> first) {
+                               QP<int32_t> dpos, QP<int32_t> first) {
   const int q = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= counts.at(q)[0]) return;
-  const int32_t u = src_ids.at(q)[j];
-  dpos.at(q)[u] = -1;
-  if (j >= *n_dst.at(q)) first.at(q)[u] = INT_MAX;
+  const int n = counts.at(q)[0];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t u = src_ids.at(q)[j];
+    dpos.at(q)[u] = -1;
+    first.at(q)[u] = INT_MAX;
+  }
 }
 
 // ------------------------------------------------------------ gather
@@ -429,42 +466,35 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     const int64_t nd_s = h == 0 ? d.n_targets_s : d.hop[h - 1].counts_s;
     const int f = hp.fanout;
     const int64_t slots = (int64_t)hp.n_dst_max * f;
+    const bool relabel = (mask & MQ_PREP_RELABEL) != 0;
     if (mask & MQ_PREP_SAMPLE) {
       ProfScope ps(K_SAMPLE, s);
       const dim3 grid(ceil_div(hp.n_dst_max, 64), Q);
+      const RelabelTables tb{qp(d.dpos, d.table_s), qp(d.first, d.table_s),
+                             qp(hp.src_ids, hp.src_s), relabel};
       if (f <= 16)
         sample_q_kernel<16><<<grid, 64, 0, s>>>(
             d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
-            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s));
+            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s), tb);
       else
         sample_q_kernel<MQ_MAX_FANOUT><<<grid, 64, 0, s>>>(
             d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
-            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s));
-    }
-    MQ_LAUNCH_CHECK("prep sample");
-    if (!(mask & MQ_PREP_RELABEL)) continue;
-    int rc = launch_scan_q(QLoadCnt{cq(hp.cnt, hp.cnt_s), cq(nd, nd_s)},
-                           QStoreRowPtr{qp(hp.row_ptr, hp.row_ptr_s), qp(hp.counts, hp.counts_s)},
-                           hp.n_dst_max, Q, d.scratch, d.scratch_s, s, K_SCAN);
-    if (rc) return rc;
-    {
+            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s), tb);
+    } else if (relabel) {  // sampled earlier: the relabel's marks and first slots alone
       ProfScope ps(K_RELABEL_MARK, s);
       mark_q_kernel<<<dim3(ceil_div(hp.n_dst_max, 256), Q), 256, 0, s>>>(
           cq(dst, dst_s), cq(nd, nd_s), qp(d.dpos, d.table_s), qp(hp.src_ids, hp.src_s));
-    }
-    MQ_LAUNCH_CHECK("prep mark");
-    {
-      ProfScope ps(K_RELABEL_FIRST, s);
       first_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
-          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s), cq(nd, nd_s), f,
-          cq(d.dpos, d.table_s), qp(d.first, d.table_s));
+          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), f, qp(d.first, d.table_s));
     }
-    MQ_LAUNCH_CHECK("prep first");
-    rc = launch_scan_q(
-        QLoadFirstFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s),
-                       cq(nd, nd_s), cq(d.dpos, d.table_s), cq(d.first, d.table_s), f},
-        QStoreLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.dpos, d.table_s),
-                    qp(hp.src_ids, hp.src_s), qp(hp.counts, hp.counts_s)},
+    MQ_LAUNCH_CHECK("prep sample");
+    if (!relabel) continue;
+    int rc = launch_scan_q(
+        QLoadRowFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s),
+                     cq(d.dpos, d.table_s), cq(d.first, d.table_s), f},
+        QStoreRowLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.dpos, d.table_s),
+                       qp(hp.src_ids, hp.src_s), qp(hp.counts, hp.counts_s),
+                       qp(hp.row_ptr, hp.row_ptr_s), f},
         slots, Q, d.scratch, d.scratch_s, s, K_RELABEL_FLAG);
     if (rc) return rc;
     {
@@ -475,11 +505,13 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
           qp(hp.vals, hp.edge_s));
     }
     MQ_LAUNCH_CHECK("prep cols");
-    {
+    if (h == d.num_hops - 1) {
       ProfScope ps(K_RELABEL_CLEAN, s);
-      clean_q_kernel<<<dim3(ceil_div(slots + hp.n_dst_max, 256), Q), 256, 0, s>>>(
-          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), cq(nd, nd_s),
-          qp(d.dpos, d.table_s), qp(d.first, d.table_s));
+      int cb = ceil_div(slots + hp.n_dst_max, 256);
+      const int cap = ceil_div(kNumSMs * 8, Q);
+      clean_q_kernel<<<dim3(cb < cap ? cb : cap, Q), 256, 0, s>>>(
+          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), qp(d.dpos, d.table_s),
+          qp(d.first, d.table_s));
     }
     MQ_LAUNCH_CHECK("prep clean");
   }

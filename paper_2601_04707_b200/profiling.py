@@ -55,6 +55,9 @@ def op_models(counts: dict, dims: list, fanouts, Q: int, cached: bool, n_params:
     m["prep_relabel"] = {"bytes": Q * relab, "units": f"{Q} batches x {L} hops"}
     m["prep_gather"] = {"bytes": Q * (2 * 4 * feature_dim * n_in + 8 * n_in),
                         "units": f"{Q} batches"}
+    m["prep_pass"] = {"bytes": m["prep_sample"]["bytes"] + m["prep_relabel"]["bytes"]
+                      + m["prep_gather"]["bytes"] + Q * 12 * B,
+                      "units": f"{Q} batches (sample + relabel + gather + labels)"}
     for l in range(L - 1):
         nd, ns, nnz = hops[L - 1 - l]
         d, dout = dims[l], dims[l + 1]
@@ -106,8 +109,11 @@ def op_table(runner, reps: int = 20, iters: int = 3) -> dict:
     ops = list(runner.tw.train_ops(dm, sw, ring=None, ring_len=0, world=runner.world))
     ops.append(("optimizer", lambda s: runner.tw.launch_optimizer(dm, runner.optimizer, s)))
     host = runner._prep_desc(gi, True)  # host-staged descriptor: no batch plan
+    # prep_relabel alone re-runs the marks / first slots that the full pass
+    # folds into the sampler; prep_pass is the whole batched pass as the step runs it
     for name, mask in (("prep_sample", PREP_SAMPLE), ("prep_relabel", PREP_RELABEL),
-                       ("prep_gather", PREP_GATHER)):
+                       ("prep_gather", PREP_GATHER),
+                       ("prep_pass", PREP_SAMPLE | PREP_RELABEL | PREP_GATHER | PREP_LABELS)):
         def prep_op(s, mask=mask):
             host.stage_mask = mask
             try:
