@@ -690,13 +690,6 @@ int mq_trace_stamp(unsigned long long* buf, int32_t cap, unsigned int* cursor, u
 int mq_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 /* cudaMemsetAsync (a scatter target's clear inside a captured step). */
 int mq_memset_async(void* dst, int32_t value, int64_t bytes, void* stream);
-/* Instantiate a captured cudaGraph_t (use_node_priority: each kernel node
- * keeps the priority of the stream it was captured on, so the train
- * stream's kernels win SM slots over the concurrent prep pass), launch it,
- * destroy it. */
-int mq_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out);
-int mq_graph_launch(void* exec, void* stream);
-int mq_graph_destroy(void* exec);
 /* exclusive prefix sum of int32 counts into int32 offsets (n+1 entries). */
 int mq_scan_i32(const int32_t* in, const int32_t* n_dev, int32_t n_max, int32_t* out,
                 void* scratch, void* stream);

@@ -152,24 +152,4 @@ int mq_set_pdl(int32_t on) {
 
 int mq_get_pdl(void) { return mq::g_pdl_on.load() ? 1 : 0; }
 
-int mq_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out) {
-  MQ_CHECK_ARG(graph && exec_out, "mq_graph_instantiate: null pointer");
-  cudaGraphExec_t ex = nullptr;
-  const unsigned long long flags = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0;
-  MQ_CUDA(cudaGraphInstantiateWithFlags(&ex, static_cast<cudaGraph_t>(graph), flags));
-  *exec_out = ex;
-  return MQ_OK;
-}
-
-int mq_graph_launch(void* exec, void* stream) {
-  MQ_CHECK_ARG(exec, "mq_graph_launch: null exec");
-  MQ_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), mq::as_stream(stream)));
-  return MQ_OK;
-}
-
-int mq_graph_destroy(void* exec) {
-  if (exec) MQ_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
-  return MQ_OK;
-}
-
 }  // extern "C"

@@ -968,9 +968,10 @@ int mq_sage_aggregate(const int32_t* row_ptr, const int32_t* cols, const float* 
   // one wave: the row bound is far above the live rows (Reddit: 11,264 vs
   // ~2,000), and surplus blocks only queue behind the resident ones
   {
+    static const bool one_wave = getenv("MQ_AGG_ONE_WAVE") == nullptr || atoi(getenv("MQ_AGG_ONE_WAVE"));
     static const int cap_parts = kNumSMs * resident_blocks(sage_aggregate_parts_kernel, kAggThreads);
     static const int cap_plain = kNumSMs * resident_blocks(sage_aggregate_kernel, kAggThreads);
-    const int cap = y_nparts_dev ? cap_parts : cap_plain;
+    const int cap = one_wave ? (y_nparts_dev ? cap_parts : cap_plain) : kNumSMs * 8;
     if (blocks > cap) blocks = cap;
   }
   MQ_CHECK_ARG(!y_nparts_dev || (y_rows_dev && d_out % 2 == 0 && ldact % 2 == 0 &&
@@ -1004,7 +1005,9 @@ int mq_sage_scatter_bwd(const int32_t* row_ptr, const int32_t* cols, const float
   const int warps = kAggThreads / 32;
   int blocks = ceil_div(n_dst_max, warps);
   {
-    static const int cap = kNumSMs * resident_blocks(sage_scatter_bwd_kernel, kAggThreads);
+    static const bool one_wave = getenv("MQ_AGG_ONE_WAVE") == nullptr || atoi(getenv("MQ_AGG_ONE_WAVE"));
+    static const int cap = one_wave ? kNumSMs * resident_blocks(sage_scatter_bwd_kernel, kAggThreads)
+                                    : kNumSMs * 8;
     if (blocks > cap) blocks = cap;
   }
   {

@@ -581,42 +581,13 @@ def current_stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-class PriorityGraph:
-    """A captured step graph instantiated with per-node priorities
-    (mq_graph_instantiate): kernels captured on the high-priority train
-    stream keep their priority inside the graph, so the concurrent prep
-    pass only takes the SM slots the train chain leaves free.  Keeps the
-    torch CUDAGraph (and its memory pool) alive."""
-
-    def __init__(self):
-        self.graph = torch.cuda.CUDAGraph(keep_graph=True)
-        self.exec = None
-
-    def finish(self):
-        import ctypes as C
-        h = C.c_void_p()
-        lib().mq_graph_instantiate(C.c_void_p(self.graph.raw_cuda_graph()), 1, C.byref(h))
-        self.exec = h.value
-
-    def replay(self):
-        lib().mq_graph_launch(self.exec, torch.cuda.current_stream().cuda_stream)
-
-    def __del__(self):
-        try:
-            if self.exec:
-                lib().mq_graph_destroy(self.exec)
-        except Exception:  # interpreter shutdown
-            pass
-
-
 class capture_graph:
     """torch.cuda.graph with Python's cyclic GC paused: a CUDAGraph of an
     earlier runner collected mid-capture would destroy its graph exec inside
     the capture and invalidate it (cudaErrorStreamCaptureInvalidated)."""
 
     def __init__(self, graph, stream):
-        self._prio = graph if isinstance(graph, PriorityGraph) else None
-        self._ctx = torch.cuda.graph(self._prio.graph if self._prio else graph, stream=stream)
+        self._ctx = torch.cuda.graph(graph, stream=stream)
 
     def __enter__(self):
         import gc
@@ -628,10 +599,7 @@ class capture_graph:
     def __exit__(self, *exc):
         import gc
         try:
-            r = self._ctx.__exit__(*exc)
-            if self._prio is not None and exc[0] is None:
-                self._prio.finish()
-            return r
+            return self._ctx.__exit__(*exc)
         finally:
             if self._was:
                 gc.enable()

@@ -17,7 +17,7 @@ import torch
 
 from ._lib import lib
 from .engine import capture_graph
-from .prep import PREP_GATHER, PREP_RELABEL, PREP_SAMPLE
+from .prep import PREP_GATHER, PREP_LABELS, PREP_RELABEL, PREP_SAMPLE
 
 
 def _time(fn, stream, reps: int, iters: int) -> float:

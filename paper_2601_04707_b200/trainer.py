@@ -32,14 +32,10 @@ import numpy as np
 import torch
 
 from ._lib import lib, ptr
-from .engine import FusedTrainWorkspace, PriorityGraph, TrainWorkspace, capture_graph
+from .engine import FusedTrainWorkspace, TrainWorkspace, capture_graph
 from .pipeline import PipelineTimeout
 from .prep import PrepGroup, PrepShared
 
-# train-stream priority (torch: lower = higher); MQ_TRAIN_PRIORITY=0 turns the
-# prioritised graphs off (A/B)
-import os as _os
-_TRAIN_PRIORITY = -int(_os.environ.get("MQ_TRAIN_PRIORITY", "1"))
 
 DEFAULT_QUEUE_DEPTH = 8  # measured best on B200 (autotune.auto_queue_depth: 2 < 4 < 8)
 
@@ -129,9 +125,7 @@ class StepRunner:
         self.loss_ring = torch.zeros(self.ring_len, dtype=torch.float64, device=dev)
         self.grad64 = (torch.zeros(self.dm.num_params + 1, dtype=torch.float64, device=dev)
                        if self.multi and self.fx is None else None)
-        # the train chain is latency-bound: its stream outranks the prep pass
-        # (graphs keep per-node priorities, engine.PriorityGraph)
-        self.stream = torch.cuda.Stream(device=dev, priority=_TRAIN_PRIORITY)  # train stream
+        self.stream = torch.cuda.Stream(device=dev)       # train stream
         self.prep_stream = torch.cuda.Stream(device=dev)  # sample + transfer stream
         # device stage stamps (mq_trace_stamp): [cap][t_ns, tag << 32 | batch]
         self.trace_cap = int(trace_cap)
@@ -320,7 +314,7 @@ class StepRunner:
 
     def _capture(self, phases):
         for name, fn in phases.items():
-            graph = PriorityGraph() if _TRAIN_PRIORITY < 0 else torch.cuda.CUDAGraph()
+            graph = torch.cuda.CUDAGraph()
             before = lib().mq_launch_count()
             with capture_graph(graph, self.stream):
                 fn(torch.cuda.current_stream().cuda_stream)
