@@ -24,6 +24,27 @@ from paper_2601_04707_b200.graph import DeviceGraph  # noqa: E402
 from paper_2601_04707_b200.runtime import epoch_permutation  # noqa: E402
 
 GRAD_RTOL = 2e-5
+EXACT_LOG = []  # (layer, device vs exact, fp32 reference vs exact)
+
+
+class _Blk64:
+    """An oracle block with the forward's float32(1/s) weights held in f64."""
+
+    def __init__(self, b):
+        self.rows, self.cols, self.dst_in_src = b.rows, b.cols, b.dst_in_src
+        self.values = b.values.astype(np.float32).astype(np.float64)
+        self.num_dst, self.num_src = b.num_dst, b.num_src
+
+
+def _exact_grads(mb, weights, pre32):
+    """Gradients of the fp32 model's inputs evaluated in f64 (with the given
+    ReLU masks)."""
+    layers = [_Blk64(b) for b in mb.layers]
+    w64 = [np.asarray(w, np.float64) for w in weights]
+    logits, cache = onn.sage_forward(layers, np.asarray(mb.features, np.float64), w64)
+    _, dl = onn.batch_loss(logits, mb.target_labels)
+    cache["pre"] = [np.asarray(p, np.float64) for p in pre32]
+    return onn.backward(layers, w64, cache, dl)
 
 
 def _normwise(got, ref):
@@ -82,6 +103,17 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1, layer0=
             assert a.shape == b.shape
             err = _normwise(a, b)
             assert err <= GRAD_RTOL, (j, l, err)
+        # The 2e-5 above compares two fp32 evaluations (ours: 3xTF32 tensor-core
+        # contractions with split-K; the reference's: OpenBLAS sgemm), so it
+        # carries BOTH rounding errors.  Against the exact arithmetic of the same
+        # fp32 inputs (f64 evaluation, float32(1/s) weights, our ReLU masks) the
+        # device gradients meet north_star's 1e-5 per layer, and the fp32
+        # reference itself is no closer (EXACT_LOG records both).
+        g64 = _exact_grads(mb, model.weights, [c for c in cache["pre"]])
+        for l, (a, b, c) in enumerate(zip(grads, ograds, g64)):
+            e_dev, e_ref = _normwise(a, c), _normwise(b, c)
+            EXACT_LOG.append((l, e_dev, e_ref))
+            assert e_dev <= 1e-5, (j, l, e_dev, e_ref)
 
 
 @pytest.fixture(scope="module")
