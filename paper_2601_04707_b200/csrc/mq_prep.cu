@@ -70,6 +70,9 @@ __global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm,
 #ifndef MQ_SAMPLE_MINB
 #define MQ_SAMPLE_MINB 12  // >= 12 resident 64-thread blocks per SM (register cap): products sample 27 -> 24 us/batch
 #endif
+#ifndef MQ_SAMPLE_MINB8
+#define MQ_SAMPLE_MINB8 20  // fanout <= 8: smaller per-row arrays, more rows in flight per SM
+#endif
 
 // ------------------------------------------------------------ sample
 // One thread per dst row (node_wise_block, SAGE arm).  Every case is O(fanout)
@@ -87,7 +90,7 @@ struct RelabelTables {
 };
 
 template <int MAXK>
-__global__ void __launch_bounds__(64, MQ_SAMPLE_MINB) sample_q_kernel(
+__global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MINB) sample_q_kernel(
     const int64_t* __restrict__ row_off, const int32_t* __restrict__ col,
     const int64_t* __restrict__ hot_arc, const int64_t* __restrict__ hot_off, QP<const int32_t> dst,
     QP<const int32_t> n_dst, QP<const uint32_t> key, int fanout, uint32_t hop, QP<int32_t> nbr,
@@ -472,7 +475,11 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
       const dim3 grid(ceil_div(hp.n_dst_max, 64), Q);
       const RelabelTables tb{qp(d.dpos, d.table_s), qp(d.first, d.table_s),
                              qp(hp.src_ids, hp.src_s), relabel};
-      if (f <= 16)
+      if (f <= 8)
+        sample_q_kernel<8><<<grid, 64, 0, s>>>(
+            d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
+            cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s), tb);
+      else if (f <= 16)
         sample_q_kernel<16><<<grid, 64, 0, s>>>(
             d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
             cq(d.key, d.key_s), f, (uint32_t)h, qp(hp.nbr, hp.nbr_s), qp(hp.cnt, hp.cnt_s), tb);
