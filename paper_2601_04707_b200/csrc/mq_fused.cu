@@ -514,13 +514,17 @@ __device__ __forceinline__ void htrace(int i) {
 __device__ __forceinline__ void htrace(int) {}
 #endif
 
-constexpr int kHeadRows = 8;               // target rows per CTA: one warp per row
-// two warps per target row: the row phases (aggregation, CE, dt) use the
-// first kHeadRows warps, the dense phases (logits, W^T, dW partial) all of them
-// (logits 3.55 -> 2.62 us, dW partial 1.8 -> 1.2 us per CTA; spreading the dt
-// scatter over all warps as well measured slower: 3.8 -> 4.2 us)
+#ifndef MQ_HEAD_ROWS
+#define MQ_HEAD_ROWS 4
+#endif
+constexpr int kHeadRows = MQ_HEAD_ROWS;    // target rows per CTA: one warp per row
+// four warps per target row (4 rows, 512 threads, 256 CTAs at Reddit's batch,
+// two per SM): the row phases (aggregation, CE) use the first kHeadRows
+// warps, the dense phases (logits, dt, dW partial) and the dt scatter all of
+// them.  Measured on the Reddit step: 8 rows x 2 warps 54.1 us/step (head
+// 10.6 us), 4 x 2 55.1 (11.1), 4 x 4 53.0 (10.2).
 #ifndef MQ_HEAD_WARPS_PER_ROW
-#define MQ_HEAD_WARPS_PER_ROW 2
+#define MQ_HEAD_WARPS_PER_ROW 4
 #endif
 #if defined(MQ_HEAD_LATE_TRIGGER) && MQ_HEAD_WARPS_PER_ROW > 1
 #error "MQ_HEAD_LATE_TRIGGER with the multi-warp head faulted intermittently (DESIGN.md 7b): unsupported"
@@ -529,7 +533,7 @@ constexpr int kHeadWarps = MQ_HEAD_WARPS_PER_ROW * kHeadRows;
 constexpr int kHeadThreads = 32 * kHeadWarps;
 constexpr int kHeadKq = 8;  // k slices of the logits product
 constexpr int kHeadCq = 4;  // class slices of the dt product
-static_assert(kHeadRows == 8, "the dt product reads dlT as two float4 per class");
+static_assert(kHeadRows % 4 == 0, "the dt product reads dlT as float4 per class");
 
 __host__ __device__ inline int head_red_floats(int d, int C) {
   const int d2p = (2 * d + 3) & ~3;
@@ -539,7 +543,7 @@ __host__ __device__ inline int head_red_floats(int d, int C) {
 }
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
-__global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
+__global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sage_head_kernel(HeadArgs a) {
 // The scatter that follows launches at the head's trigger.  With 8-warp CTAs
 // a trigger after the dW partials was faster (60.2 -> 58.8 us/step); with the
 // 16-warp head the entry trigger is (58.1 vs 59.3 us/step), and the late
@@ -767,16 +771,14 @@ __global__ void __launch_bounds__(kHeadThreads) sage_head_kernel(HeadArgs a) {
       for (int i = 0; i < R; ++i) acc[i] = 0.f;
       for (int c = c0; c < c1; ++c) {
         const float w = Ws[k * Cp + c];
-        const float4 p0 = *reinterpret_cast<const float4*>(dlT + c * R);
-        const float4 p1 = *reinterpret_cast<const float4*>(dlT + c * R + 4);
-        acc[0] = fmaf(p0.x, w, acc[0]);
-        acc[1] = fmaf(p0.y, w, acc[1]);
-        acc[2] = fmaf(p0.z, w, acc[2]);
-        acc[3] = fmaf(p0.w, w, acc[3]);
-        acc[4] = fmaf(p1.x, w, acc[4]);
-        acc[5] = fmaf(p1.y, w, acc[5]);
-        acc[6] = fmaf(p1.z, w, acc[6]);
-        acc[7] = fmaf(p1.w, w, acc[7]);
+#pragma unroll
+        for (int i4 = 0; i4 < R / 4; ++i4) {
+          const float4 p = *reinterpret_cast<const float4*>(dlT + c * R + 4 * i4);
+          acc[4 * i4 + 0] = fmaf(p.x, w, acc[4 * i4 + 0]);
+          acc[4 * i4 + 1] = fmaf(p.y, w, acc[4 * i4 + 1]);
+          acc[4 * i4 + 2] = fmaf(p.z, w, acc[4 * i4 + 2]);
+          acc[4 * i4 + 3] = fmaf(p.w, w, acc[4 * i4 + 3]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < R; ++i) red[(cq * R + i) * d2 + k] = acc[i];
