@@ -530,7 +530,10 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     const int warps = kGatherThreads / 32;
     // narrow rows: 32 rows per warp pass; wide rows: one row per warp pass
     int blocks = ceil_div(last.n_src_max, dv4 > 32 ? warps : warps * 32);
-    const int cap = ceil_div(kNumSMs * 16, Q);
+    // blocks per SM across the Q slots (MQ_PREP_GATHER_BPS): the pass runs
+    // beside the latency-bound train chain, whose CTAs must find room
+    static const int bps = getenv("MQ_PREP_GATHER_BPS") ? atoi(getenv("MQ_PREP_GATHER_BPS")) : 4;
+    const int cap = ceil_div(kNumSMs * bps, Q);
     if (blocks > cap) blocks = cap;
     gather_q_kernel<<<dim3(blocks, Q), kGatherThreads, 0, s>>>(
         d.cache_tbl, d.cache_pitch, d.slot_of,
