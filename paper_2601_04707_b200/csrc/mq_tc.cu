@@ -1103,7 +1103,8 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads2, 1)
     tc2_kernel(const __grid_constant__ Maps maps, Operands op, Geo geo, const int32_t* m_dev,
                int m_static, const int32_t* k_dev, int k_static, float* __restrict__ part,
-               int32_t* __restrict__ nparts_out, int ST, int32_t* __restrict__ coop) {
+               int32_t* __restrict__ nparts_out, int ST, int32_t* __restrict__ coop,
+               int stage_on) {
   pdl_trigger();
   MQ_TL_BEGIN(MODE);
   if (threadIdx.x == 0) trace_at(0);
@@ -1454,13 +1455,57 @@ __global__ void __launch_bounds__(kThreads2, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter
+    const int etid = tid - 320;  // 0..127 over the four epilogue warps
     uint32_t ti = 0;
     const bool vec = (op.N & 3) == 0 && (ldd & 3) == 0 && ((uintptr_t)dst & 15) == 0;
+    // swapped modes storing whole rows (partial tiles, or an output whose
+    // pitch is N): each 32-row chunk goes TMEM -> registers -> a shared
+    // staging buffer (double-buffered, conflict-free: lanes are consecutive
+    // features) -> ONE bulk async copy of its contiguous rows.  The
+    // per-thread 4-byte global stores this replaces were bound by the SM's
+    // store path (~0.9 us per 16 KB chunk with all CTAs storing).
+    // (only CTAs that loop over several tiles: there the next tile's MMAs
+    // overlap the copies; a one-tile split-K CTA measured no gain in-step)
+    const bool bulk = SW && stage_on && ldd == op.N && vec && (stage_on > 1 || wk.tiles_m > G);
+    float* stage = reinterpret_cast<float*>(smem + ST * SB);
+    int chunk = 0;
     for (int t = t_first; t < wk.tiles_m; t += G, ++ti) {
       const uint32_t ab = ti & 1;
       mbar_wait(&accf[ab], (ti >> 1) & 1);
       if (warp == 10 && lane == 0 && ti < 2) trace_at(26 + 2 * (int)ti);
       tc_fence_after();
+      if (bulk) {
+        const int n = q * 32 + lane;
+        for (int cb = 0; cb < BM; cb += 32, ++chunk) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * (uint32_t)cstride + (uint32_t)cb, v);
+          const int r0 = t * BM + cb;
+          const int nr = min(32, M - r0);
+          float* sb = stage + (chunk & 1) * (32 * op.N);
+          // the copy that read this buffer two chunks ago has finished reading
+          if (etid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          if (n < op.N) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) sb[u * op.N + n] = relu ? fmaxf(v[u], 0.f) : v[u];
+          }
+          fence_async_smem();
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+          if (etid == 0 && nr > 0) {
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                "cp.async.bulk.commit_group;" ::"l"(dst + (int64_t)r0 * ldd),
+                "r"(smem_u32(sb)), "r"((uint32_t)(nr * op.N * 4))
+                : "memory");
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (warp == 10 && lane == 0 && ti < 1) trace_at(27);
+        if (lane == 0) mbar_arrive(&acce[ab]);
+        if (coop_on) coop_reduce_tile(part, coop, t, s, wk.S, Mout, op.N, tid - 320);
+        continue;
+      }
       if (SW) {  // TMEM lane = output feature n, column = row of the tile
         const int n = q * 32 + lane;
         if (32 * q < op.N) {  // warp-uniform
@@ -1511,6 +1556,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
       if (warp == 10 && lane == 0 && ti < 1) trace_at(27);
       if (lane == 0) mbar_arrive(&acce[ab]);
     }
+  }
+  // the bulk copies' global writes, complete and ordered for the generic
+  // proxy before the grid signals completion (a programmatic dependent
+  // launch reads them right after its griddepcontrol.wait)
+  if (tid == 320) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
   }
   tc_fence_before();
   __syncthreads();
@@ -1608,6 +1661,8 @@ static bool tmap2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows
 
 inline int64_t tc_part_floats_base(int64_t m_max, int64_t n);
 static int g_tc_coop = -1;  // cooperative split reduction of the deferred FWD / DW (MQ_TC2_COOP)
+// bulk (TMA-engine) epilogue stores of the swapped modes (MQ_TC2_BULK=0: per-thread stores)
+static const int g_tc_bulk = getenv("MQ_TC2_BULK") ? atoi(getenv("MQ_TC2_BULK")) : 1;
 
 template <int MODE, class Epi>
 int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
@@ -1625,9 +1680,26 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
   // measures faster on v1 (21 vs 29 us with its split reduction)
   if (MODE == kDw && op.d_in > 128 && !skip_reduce && g_tc_v2 < 3) return -1;
   const int SB = stage2_bytes(MODE, op.Np);
-  int ST = (kSmemBudget - 1024) / SB;
+  // swapped modes: a double-buffered 32-row staging area for the bulk
+  // epilogue, reserved only where CTAs loop over many tiles (a host-known
+  // row count above one tile per CTA, or a short K that leaves the product
+  // unsplit): the extra 32 KB of shared memory per CTA alone cost the
+  // Reddit step ~4 us (fewer co-resident CTAs of the neighbouring kernels).
+  // DW (bit 2) stays off: its bulk stores raced with the dependent launch
+  // in the fused step (tests/test_gpu_fused.py, intermittently).
+  const bool many_tiles = (m_dev == nullptr && (m_static + BM - 1) / BM > kNumSMs) || k_max <= 256;
+  const int stage_bytes =
+      swapped(MODE) && (g_tc_bulk & (MODE == kDw ? 2 : 1)) && (many_tiles || (g_tc_bulk & 4))
+          ? 2 * 32 * op.Np * 4
+          : 0;
+  int ST = (kSmemBudget - 1024 - stage_bytes) / SB;
   if (ST > kMaxStages2) ST = kMaxStages2;
   if (ST > max_stages_tmem(MODE, op.Np)) ST = max_stages_tmem(MODE, op.Np);
+  {  // experiment knob: fewer stages = a smaller shared-memory footprint
+    static const int cap_st = getenv("MQ_TC2_MAX_STAGES") ? atoi(getenv("MQ_TC2_MAX_STAGES")) : 0;
+    if (cap_st >= 2 && ST > cap_st) ST = cap_st;
+  }
+  ST &= ~1;  // an odd stage count hung the products step (MQ_TC2_MAX_STAGES=3): even only
   if (ST < 2) return -1;
   Maps mp;
   Geo geo{0, 0};
@@ -1688,8 +1760,10 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
     coop = reinterpret_cast<int32_t*>(part + tc_part_floats_base(m_max, op.N));
   {
     ProfScope ps(kid, s);
-    MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2), (size_t)(ST * SB + 1024), s, mp,
-                     op, geo, m_dev, m_static, k_dev, k_static, part, nparts_out, ST, coop));
+    MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2),
+                     (size_t)(ST * SB + 1024 + stage_bytes), s, mp, op, geo, m_dev, m_static, k_dev,
+                     k_static, part, nparts_out, ST, coop,
+                     stage_bytes > 0 ? (g_tc_bulk & 4 ? 2 : 1) : 0));
   }
   MQ_LAUNCH_CHECK("tc2_gemm");
   if (skip_reduce) return MQ_OK;
