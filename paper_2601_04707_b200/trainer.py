@@ -332,17 +332,21 @@ class StepRunner:
         self._warm(phases)
         self._capture(phases)
         if self.pipeline and not self._host_exchange:
+            # whole groups, plus the leading k < Q windows of a group (an
+            # epoch's last group, the tail of a steps() call): every window a
+            # group-aligned caller issues runs inside a group graph
             for gi in range(2):
-                def group(s, gi=gi):
-                    cur = torch.cuda.current_stream(self.device)
-                    self.prep_stream.wait_stream(cur)
-                    with torch.cuda.stream(self.prep_stream):
-                        self._launch_prep(1 - gi, False, self.prep_stream.cuda_stream)
-                    for q in range(self.Q):
-                        ph = phases[f"train{gi}_{q}"]
-                        ph(cur.cuda_stream)
-                    cur.wait_stream(self.prep_stream)
-                self._capture({f"group{gi}": group})
+                for k in range(1, self.Q + 1):
+                    def group(s, gi=gi, k=k):
+                        cur = torch.cuda.current_stream(self.device)
+                        self.prep_stream.wait_stream(cur)
+                        with torch.cuda.stream(self.prep_stream):
+                            self._launch_prep(1 - gi, False, self.prep_stream.cuda_stream)
+                        for q in range(k):
+                            ph = phases[f"train{gi}_{q}"]
+                            ph(cur.cuda_stream)
+                        cur.wait_stream(self.prep_stream)
+                    self._capture({f"group{gi}" if k == self.Q else f"group{gi}_{k}": group})
         if self.pipeline and not self._primed:
             self._prologue()
 
@@ -431,22 +435,23 @@ class StepRunner:
         Q = self.Q
         while done < n:
             k = self.windows_done
-            if (self.use_graph and self.pipeline and "group0" in self.graphs and k % Q == 0
-                    and n - done >= Q):
+            if self.use_graph and self.pipeline and "group0" in self.graphs and k % Q == 0:
                 if not self._primed:
                     self._prologue()
                 gi = (k // Q) % 2
+                c = min(Q, n - done)
                 with torch.cuda.stream(self.stream):
                     # the group graph joins its own prep branch; prep(1-gi)
                     # overwrites the other half, whose last trains preceded it
                     self.stream.wait_event(self.ev_prep[gi])
-                    self.graphs[f"group{gi}"].replay()
-                self.ev_train[gi].record(self.stream)
+                    self.graphs[f"group{gi}" if c == Q else f"group{gi}_{c}"].replay()
+                if c == Q:  # (a partial group's last window records it, compute_window)
+                    self.ev_train[gi].record(self.stream)
                 self.ev_prep[1 - gi].record(self.stream)
-                self._last = (gi, Q - 1)
-                self.dm.host_steps += Q
-                self.windows_done += Q
-                done += Q
+                self._last = (gi, c - 1)
+                self.dm.host_steps += c
+                self.windows_done += c
+                done += c
             else:
                 self.compute_window()
                 self.apply_window()
@@ -559,10 +564,11 @@ class StepRunner:
             self._capture(phases)
             groups = {}
             for gi, grp in enumerate(self.groups):
-                def hgroup(s, gi=gi):
-                    for q in range(Q):
-                        phases[f"htrain{gi}_{q}"](s)
-                groups[f"hgroup{gi}"] = hgroup
+                for k in range(1, Q + 1):  # whole groups and a last partial one
+                    def hgroup(s, gi=gi, k=k):
+                        for q in range(k):
+                            phases[f"htrain{gi}_{q}"](s)
+                    groups[f"hgroup{gi}" if k == Q else f"hgroup{gi}_{k}"] = hgroup
             self._capture(groups)
         self._hphases = phases
 
@@ -659,13 +665,14 @@ class StepRunner:
                 stage_and_prep(j)
             self.stream.wait_event(self.ev_prep[gi])
             ids = [bid for bid, _ in chunk]
-            if self.use_graph and len(chunk) == Q and f"hgroup{gi}" in self.graphs:
+            gname = f"hgroup{gi}" if len(chunk) == Q else f"hgroup{gi}_{len(chunk)}"
+            if self.use_graph and gname in self.graphs:
                 yield from drain(0 if clash(ids) else 1)
                 with torch.cuda.stream(self.stream):
-                    self.graphs[f"hgroup{gi}"].replay()
+                    self.graphs[gname].replay()
                 ev = self._grp_ev[gi]
                 ev.record(self.stream)
-                self.dm.host_steps += Q
+                self.dm.host_steps += len(chunk)
                 pending.append((ev, ids))
             else:
                 for q, bid in enumerate(ids):
