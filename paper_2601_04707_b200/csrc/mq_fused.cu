@@ -755,6 +755,27 @@ __global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sag
     }
   }
   __syncthreads();
+  // the batch loss and this CTA's completion count, right after the CE: no
+  // global write of the thread is pending yet, so its fence is cheap (at the
+  // kernel's end it waited on the dt atomics and dW stores: ~1 us per CTA).
+  // The last CTA to get here commits the loss to the epoch's loss ring.
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < R; ++w) t += s_loss[w];
+    if (t != 0.0) atomicAdd(a.loss_acc, t);
+    if (s_bad) atomicOr(a.nonfinite, 1);
+    if (a.ring != nullptr) {
+      __threadfence();
+      if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
+        __threadfence();
+        const int k = (int)((a.key[2] / (uint32_t)a.world) % (uint32_t)a.ring_len);
+        volatile double* la = a.loss_acc;
+        a.ring[k] = *la;
+        *la = 0.0;
+        *a.done = 0;
+      }
+    }
+  }
 
   htrace(4);
   // 4. dt = dl W^T (register-blocked like the logits: thread (k, class slice))
@@ -822,12 +843,6 @@ __global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sag
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < R; ++w) t += s_loss[w];
-    if (t != 0.0) atomicAdd(a.loss_acc, t);
-    if (s_bad) atomicOr(a.nonfinite, 1);
-  }
 
   htrace(5);
   // 5. this CTA's dW partial = both^T dl: thread (k octet, class), 8 k per item
@@ -865,22 +880,7 @@ __global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sag
   pdl_trigger();
 #endif
   // 6. dW stays as per-CTA partials: the optimizer reduces them in fixed CTA
-  //    order (mq_grad_src), so no grid-wide barrier is needed here.  The last
-  //    CTA to finish commits the batch loss to the epoch's loss ring.
-  if (a.ring != nullptr) {
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      if (atomicAdd(a.done, 1) == (int)gridDim.x - 1) {
-        __threadfence();
-        const int k = (int)((a.key[2] / (uint32_t)a.world) % (uint32_t)a.ring_len);
-        volatile double* la = a.loss_acc;
-        a.ring[k] = *la;
-        *la = 0.0;
-        *a.done = 0;
-      }
-    }
-  }
+  //    order (mq_grad_src), so no grid-wide barrier is needed here.
   htrace(7);
   MQ_TL_END(6);
 }

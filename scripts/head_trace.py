@@ -41,7 +41,7 @@ print("head phases (us from entry):", " ".join(f"{i}:{(t[i] - t[0]) / 1e3:.2f}" 
 print("  1 W/W^T staged, 2 aggregated, 3 logits, 4 CE, 5 dt atomics, 6 dW partial, 7 end")
 cta = (C.c_ulonglong * (256 * 8))()
 lib().dll.mq_debug_head_cta(cta)
-n_cta = -(-1024 // 8)
+n_cta = -(-1024 // int(os.environ.get("MQ_HEAD_ROWS_TRACE", "4")))
 rows = [[int(cta[8 * b + i]) for i in range(8)] for b in range(n_cta)]
 t0 = min(r[0] for r in rows)
 import statistics as _st
