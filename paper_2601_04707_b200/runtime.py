@@ -31,8 +31,8 @@ import torch
 
 from .cache import DeviceCache, gather_features
 from .pipeline import MS_TO_NS, Trace
-from .racom import DistExchange, WindowDriver
-from .samplers import PhiloxStream, SamplerParams
+from .racom import DistExchange, WindowDriver, apply_update
+from .samplers import PhiloxStream, SamplerParams, build_minibatch
 from .trainer import StepRunner
 
 
@@ -84,8 +84,8 @@ class PipelineConfig:
             raise ValueError(f"unknown timing_mode {self.timing_mode!r}")
         if self.optimizer not in ("adam", "sgd"):
             raise ValueError(f"unknown optimizer {self.optimizer!r}")
-        if self.sampler.method != "sage":
-            raise NotImplementedError("the device runtime trains GraphSAGE node-wise batches")
+        if self.sampler.method not in ("sage", "gcn", "ladies", "fastgcn"):
+            raise ValueError(f"unknown method {self.sampler.method!r}")
         if self.timing_mode != "real" or self.stage_durations:
             raise NotImplementedError("simulated stage timings belong to the reference simulator")
         if self.exchange not in ("auto", "peer", "collective"):
@@ -281,6 +281,74 @@ def device_trace(stamps, windows, Q: int, device: int, epoch: int, trace: Trace)
     return hw, keys, len(syncs)
 
 
+def _run_epoch_per_op(g, cache, replicas, config, epoch, trace):
+    """The reference's serial schedule (runtime.py:226-324, zero delays) over
+    the per-op API, for the samplers the fused step does not cover (the GCN
+    node-wise arm, LADIES, FastGCN): per window k every device builds and
+    trains its batch (build_minibatch, loss_and_grads), the packets are
+    folded in device order into the f64 running mean (Accumulator,
+    racom.py:36-78), every replica applies it (apply_update), and the
+    replicas are averaged every sync_period applied windows and at the epoch
+    barrier (sync_models)."""
+    from . import nn
+    from .racom import sync_models
+    if _distributed():
+        raise NotImplementedError("the per-op schedule runs in-process replicas")
+    if len(replicas) != config.num_devices:
+        raise ValueError("one model replica per device required")
+    per_device, expected = plan_epoch(g, config, epoch)
+    losses, hits, misses, dropped = {}, 0, 0, 0
+    applied = syncs = 0
+    t0 = time.perf_counter()
+    t0_ns = time.perf_counter_ns()
+    for k in range(len(expected)):
+        mean, count = None, 0
+        for d, rep in enumerate(replicas):
+            if k >= len(per_device[d]):
+                continue
+            _, bid, targets = per_device[d][k]
+            ts = time.perf_counter_ns()
+            batch = build_minibatch(g, targets, config.sampler, batch_rng(config, epoch, bid),
+                                    batch_id=bid, epoch=epoch, cached_mask=cache)
+            loss, grads, _ = nn.loss_and_grads(batch, rep)
+            losses[bid] = loss
+            hits += batch.cache_hits
+            misses += batch.cache_misses
+            dropped += batch.dropped_targets
+            count += 1
+            if mean is None:
+                mean = [gr.to(torch.float64).clone() for gr in grads]
+            else:
+                for m, gr in zip(mean, grads):
+                    m += (gr.to(torch.float64) - m) / count
+            te = time.perf_counter_ns()
+            trace.add("compute_fwd", d, bid, epoch, ts - t0_ns, te - t0_ns)
+        if count != expected[k]:
+            raise RuntimeError(f"window {k}: {count} packets, expected {expected[k]}")
+        for rep in replicas:
+            apply_update(rep, mean, config.optimizer)
+        applied += 1
+        if applied % config.sync_period == 0:  # the milestone rendezvous (runtime.py:255-265)
+            if config.num_devices > 1:  # (one replica: the average is the identity)
+                sync_models(replicas)
+            syncs += 1
+    epoch_sync = 0
+    if config.num_devices > 1:
+        sync_models(replicas)
+        epoch_sync = 1
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    stats = EpochStats(
+        epoch=epoch, losses=losses, batches=sum(len(x) for x in per_device), cache_hits=hits,
+        cache_misses=misses, dropped_targets=dropped, sync_count=syncs, epoch_sync=epoch_sync,
+        applied_windows={d: applied for d in range(config.num_devices)},
+        queue_high_water={d: {"cpu": 1, "dev": 1} for d in range(config.num_devices)},
+        queue_keys={d: {k: [b for _, b, _ in per_device[d]]
+                        for k in ("cpu_put", "cpu_get", "dev_put", "dev_get")}
+                    for d in range(config.num_devices)},
+        wall_ms=wall_ms)
+    return stats, trace
+
+
 def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
               trace: Trace | None = None):
     """Train one epoch; returns (EpochStats, Trace).  Every training target
@@ -291,6 +359,8 @@ def run_epoch(g, cache, replicas: list, config: PipelineConfig, epoch: int = 0,
         trace = Trace()
     if cache is not None and not isinstance(cache, DeviceCache):
         cache = DeviceCache(g, cache)
+    if config.sampler.method != "sage":
+        return _run_epoch_per_op(g, cache, replicas, config, epoch, trace)
     dist_mode = _distributed()
     if dist_mode:
         import torch.distributed as dist

@@ -135,6 +135,41 @@ def main():
                 out[f"{name}/L{l}/{k}"] = getattr(blk, k)
         gcn.append(name)
     out["gcn_cases"] = np.array(gcn)
+
+    # run_epoch (serial deterministic schedule) with the layer-wise samplers
+    # and the GCN arch: the reference's own runtime, its batch rng replaced by
+    # the layer stream (a LayerRng per batch) or the node-wise row shim
+    rruntime, rnn = mg.rruntime, mg.rnn
+    node_rng = rruntime.batch_rng
+    Gs = mqpipe.split_masks(G2, ratios=(0.3, 0.1, 0.1), seed=2)
+    ep = []
+    for name, G, method, extra in (("ladies_1dev", 1, "ladies", dict(nodes_per_layer=96)),
+                                   ("ladies_2dev_debias", 2, "ladies",
+                                    dict(nodes_per_layer=96, debias=True)),
+                                   ("fastgcn_2dev", 2, "fastgcn", dict(nodes_per_layer=128)),
+                                   ("gcn_2dev", 2, "gcn", dict(fanout=(4, 3)))):
+        if method == "gcn":
+            rruntime.batch_rng = node_rng
+        else:
+            rruntime.batch_rng = lambda config, epoch, bid: LayerRng(config.seed, epoch, bid)
+        cfg = rruntime.PipelineConfig(
+            num_devices=G, batch_size=64,
+            sampler=mqpipe.SamplerParams(method=method, num_layers=2, **extra),
+            optimizer="adam", sync_period=1, deterministic=True, seed=5)
+        base = rnn.init_model(16, 16, 5, num_layers=2, arch="gcn", seed=5, learning_rate=0.01)
+        reps = [base.copy() for _ in range(G)]
+        stats, _ = rruntime.run_epoch(Gs, None, reps, cfg, epoch=1)
+        k = f"epoch/{name}"
+        out[f"{k}/loss_bids"] = np.array(sorted(stats.losses))
+        out[f"{k}/losses"] = np.array([stats.losses[b] for b in sorted(stats.losses)])
+        out[f"{k}/sync"] = np.array([stats.sync_count, stats.epoch_sync, stats.dropped_targets])
+        for l in range(2):
+            out[f"{k}/w{l}"] = reps[0].weights[l]
+        out[f"{k}/config"] = np.array([G, 64, 5])
+        ep.append(name)
+    rruntime.batch_rng = node_rng
+    out["epoch_cases"] = np.array(ep)
+    out["epoch/train_mask"] = Gs.train_mask
     np.savez_compressed(HERE / "layerwise.npz", **out)
     print("wrote", HERE / "layerwise.npz", len(out), "arrays")
 

@@ -170,3 +170,40 @@ def test_layerwise_errors(graphs):
         mq.sample_ladies(g, [8, 8], 3, 1, mq.PhiloxStream(0, 0, 0))
     with pytest.raises(mq.SamplingError):
         mq.sample_fastgcn(g, [], 3, 1, mq.PhiloxStream(0, 0, 0))
+
+
+@pytest.mark.parametrize("case", [str(c) for c in LW["epoch_cases"]])
+def test_run_epoch_layerwise_and_gcn_match_reference(case):
+    """run_epoch with LADIES / FastGCN / the GCN node-wise arm and the GCN
+    arch (the per-op serial schedule) against the reference's own run_epoch:
+    per-batch losses and the final weights."""
+    import paper_2601_04707_b200 as mq
+    samp = load_golden("sampling.npz")
+    hg = make_g2(samp)
+    hg.train_mask = LW["epoch/train_mask"]
+    g = mq.DeviceGraph.from_csr(hg, device=torch.device("cuda", 0))
+    G, B, seed = LW[f"epoch/{case}/config"].tolist()
+    method = case.split("_")[0]
+    if method == "gcn":
+        params = mq.SamplerParams(method="gcn", fanout=(4, 3), num_layers=2)
+    else:
+        params = mq.SamplerParams(method=method, nodes_per_layer=128 if method == "fastgcn" else 96,
+                                  num_layers=2, debias="debias" in case)
+    cfg = mq.PipelineConfig(num_devices=G, batch_size=B, sampler=params, optimizer="adam",
+                            sync_period=1, deterministic=True, seed=seed)
+    base = mq.init_model(16, 16, 5, num_layers=2, arch="gcn", seed=5, learning_rate=0.01)
+    reps = [base.copy() for _ in range(G)]
+    stats, _ = mq.run_epoch(g, None, reps, cfg, epoch=1)
+    bids = LW[f"epoch/{case}/loss_bids"]
+    assert sorted(stats.losses) == bids.tolist()
+    got = np.array([stats.losses[b] for b in bids])
+    ref = LW[f"epoch/{case}/losses"]
+    np.testing.assert_allclose(got, ref, rtol=1e-4)
+    assert [stats.sync_count, stats.epoch_sync, stats.dropped_targets] == \
+        LW[f"epoch/{case}/sync"].tolist()
+    for l in range(2):
+        w = reps[0].weights[l].cpu().numpy()
+        ref_w = LW[f"epoch/{case}/w{l}"]
+        assert np.abs(w - ref_w).max() <= 1e-4 * np.abs(ref_w).max()
+        for r in reps[1:]:  # replicas identical after the epoch barrier
+            np.testing.assert_array_equal(r.weights[l].cpu().numpy(), w)
