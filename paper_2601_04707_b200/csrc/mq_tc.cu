@@ -1466,22 +1466,33 @@ __global__ void __launch_bounds__(kThreads2, 1)
     // store path (~0.9 us per 16 KB chunk with all CTAs storing).
     // (only CTAs that loop over several tiles: there the next tile's MMAs
     // overlap the copies; a one-tile split-K CTA measured no gain in-step)
-    const bool bulk = SW && stage_on && ldd == op.N && vec && (stage_on > 1 || wk.tiles_m > G);
-    float* stage = reinterpret_cast<float*>(smem + ST * SB);
+    // staging: the reserved area (stage_on & 3), or -- for a CTA's LAST tile,
+    // whose MMAs have consumed every pipeline stage (stage_on & 4) -- the
+    // pipeline's own stage memory, so no extra shared memory is reserved
+    const bool bulk_ok = SW && ldd == op.N && vec;
+    const bool bulk_res = bulk_ok && (stage_on & 3) && ((stage_on & 3) > 1 || wk.tiles_m > G);
+    const bool bulk_last = bulk_ok && (stage_on & 4);
     int chunk = 0;
     for (int t = t_first; t < wk.tiles_m; t += G, ++ti) {
       const uint32_t ab = ti & 1;
       mbar_wait(&accf[ab], (ti >> 1) & 1);
       if (warp == 10 && lane == 0 && ti < 2) trace_at(26 + 2 * (int)ti);
       tc_fence_after();
+      const bool bulk = bulk_res || (bulk_last && t + G >= wk.tiles_m);
+      float* stage = reinterpret_cast<float*>(bulk_res ? smem + ST * SB : smem);
       if (bulk) {
         const int n = q * 32 + lane;
-        for (int cb = 0; cb < BM; cb += 32, ++chunk) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * (uint32_t)cstride + (uint32_t)cb, v);
+        for (int cb = 0; cb < BM; cb += 32) {
           const int r0 = t * BM + cb;
           const int nr = min(32, M - r0);
+          // chunks past the last row issue no copy and must not take a
+          // buffer turn: the read-wait below lets the most recent copy run
+          // on, which must be the OTHER buffer's
+          if (nr <= 0) continue;
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * (uint32_t)cstride + (uint32_t)cb, v);
           float* sb = stage + (chunk & 1) * (32 * op.N);
+          ++chunk;
           // the copy that read this buffer two chunks ago has finished reading
           if (etid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           asm volatile("bar.sync 3, 128;" ::: "memory");
@@ -1491,7 +1502,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           }
           fence_async_smem();
           asm volatile("bar.sync 3, 128;" ::: "memory");
-          if (etid == 0 && nr > 0) {
+          if (etid == 0) {
             asm volatile(
                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
                 "cp.async.bulk.commit_group;" ::"l"(dst + (int64_t)r0 * ldd),
@@ -1661,8 +1672,14 @@ static bool tmap2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows
 
 inline int64_t tc_part_floats_base(int64_t m_max, int64_t n);
 static int g_tc_coop = -1;  // cooperative split reduction of the deferred FWD / DW (MQ_TC2_COOP)
-// bulk (TMA-engine) epilogue stores of the swapped modes (MQ_TC2_BULK=0: per-thread stores)
-static const int g_tc_bulk = getenv("MQ_TC2_BULK") ? atoi(getenv("MQ_TC2_BULK")) : 1;
+// bulk (async-copy engine) epilogue stores of the swapped modes, MQ_TC2_BULK bits:
+//   8  a CTA's last tile stages through the pipeline's own stage memory
+//      (default: Reddit 54.4 -> 49.4 us/step, products 429 -> 421 us/step)
+//   1  FWD: a reserved 32 KB staging area for every tile of many-tile CTAs
+//   2  the same for DW;  4  reserve it whatever the tile count
+// (bits 1/2/4 cost more than they save in-step: the larger shared-memory
+// footprint alone slowed the Reddit step ~4 us and products ~3 %)
+static const int g_tc_bulk = getenv("MQ_TC2_BULK") ? atoi(getenv("MQ_TC2_BULK")) : 8;
 
 template <int MODE, class Epi>
 int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_max,
@@ -1680,13 +1697,10 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
   // measures faster on v1 (21 vs 29 us with its split reduction)
   if (MODE == kDw && op.d_in > 128 && !skip_reduce && g_tc_v2 < 3) return -1;
   const int SB = stage2_bytes(MODE, op.Np);
-  // swapped modes: a double-buffered 32-row staging area for the bulk
-  // epilogue, reserved only where CTAs loop over many tiles (a host-known
-  // row count above one tile per CTA, or a short K that leaves the product
-  // unsplit): the extra 32 KB of shared memory per CTA alone cost the
-  // Reddit step ~4 us (fewer co-resident CTAs of the neighbouring kernels).
-  // DW (bit 2) stays off: its bulk stores raced with the dependent launch
-  // in the fused step (tests/test_gpu_fused.py, intermittently).
+  // swapped modes: an optional double-buffered 32-row staging area for the
+  // bulk epilogue of every tile (MQ_TC2_BULK bits 1/2/4), reserved only
+  // where CTAs loop over many tiles (a host-known row count above one tile
+  // per CTA, or a short K that leaves the product unsplit)
   const bool many_tiles = (m_dev == nullptr && (m_static + BM - 1) / BM > kNumSMs) || k_max <= 256;
   const int stage_bytes =
       swapped(MODE) && (g_tc_bulk & (MODE == kDw ? 2 : 1)) && (many_tiles || (g_tc_bulk & 4))
@@ -1763,7 +1777,8 @@ int run_tc2(const tc::Operands& op, const int32_t* m_dev, int m_static, int m_ma
     MQ_CUDA(launch_k(tc2_kernel<MODE>, dim3(grid), dim3(kThreads2),
                      (size_t)(ST * SB + 1024 + stage_bytes), s, mp, op, geo, m_dev, m_static, k_dev,
                      k_static, part, nparts_out, ST, coop,
-                     stage_bytes > 0 ? (g_tc_bulk & 4 ? 2 : 1) : 0));
+                     (stage_bytes > 0 ? (g_tc_bulk & 4 ? 2 : 1) : 0) |
+                         (swapped(MODE) && (g_tc_bulk & 8) ? 4 : 0)));
   }
   MQ_LAUNCH_CHECK("tc2_gemm");
   if (skip_reduce) return MQ_OK;

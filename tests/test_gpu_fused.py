@@ -7,6 +7,8 @@ the identical batch; loss and gradients agree up to fp32 re-association:
 loss rel 1e-5, gradients max|a-b| <= 2e-5 * max|b| per layer.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -70,6 +72,8 @@ def _fused_vs_oracle(hg, fanouts, hidden, B, seed, mask=None, windows=1, layer0=
     if layer0 != "auto":
         assert runner.tw.af0 == (layer0 == "af")
     runner.begin_epoch(0, perm)
+    if os.environ.get("MQ_TEST_DEFERRED_FIRST"):
+        runner.tw.grad_src(state.dev)  # diagnostics: the deferred path from window 0
     s = runner.stream
     for j in range(windows):
         q = j % runner.Q  # one batched prep pass fills Q slots
