@@ -167,3 +167,46 @@ def test_aggregate_first_layer(tc_kernel, rows, d_in, d_out):
     dz = dh[:rows].astype(np.float64) * (got > 0)
     ref_dw = np.concatenate([agg, h], 1).astype(np.float64)[:rows].T @ dz
     assert _normwise(dw, ref_dw) <= 2 * RTOL
+
+
+@pytest.mark.parametrize("rows,d_in,d_out", [(3262, 602, 64), (1131, 32, 32), (1000, 64, 64),
+                                             (1323, 16, 32), (97, 64, 8)])
+def test_deferred_partials_repeated(rows, d_in, d_out):
+    """The deferred transform / weight-gradient partials (the fused step's
+    path; bulk async-copy epilogue on each CTA's last tile), summed over the
+    published split count, against fp64 -- 20 repetitions, since a staging
+    buffer reused while its previous copy still reads it shows up only
+    intermittently."""
+    rng = np.random.default_rng(rows * 7 + d_in)
+    ld = (d_in + 3) // 4 * 4
+    h = np.zeros((rows, ld), np.float32)
+    h[:, :d_in] = rng.standard_normal((rows, d_in))
+    W = (rng.standard_normal((2 * d_in, d_out)) / np.sqrt(d_in)).astype(np.float32)
+    g = rng.standard_normal((rows, 2 * d_out)).astype(np.float32)
+    th, tW, tg = (torch.from_numpy(x).cuda() for x in (h, W, g))
+    m_dev = torch.tensor([rows], dtype=torch.int32, device="cuda")
+    scr = torch.zeros(int(lib().mq_sage_fused_scratch_bytes(rows, d_in, d_out)) // 4 + 1,
+                      dtype=torch.float32, device="cuda")
+    yp = torch.zeros(int(lib().mq_sage_y_parts_bytes(rows, d_out)) // 4 + 1, dtype=torch.float32,
+                     device="cuda")
+    dwp = torch.zeros(int(lib().mq_sage_dw_parts_bytes(d_in, d_out)) // 4 + 1,
+                      dtype=torch.float32, device="cuda")
+    ny = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nw = torch.zeros(1, dtype=torch.int32, device="cuda")
+    h64, W64, g64 = h[:, :d_in].astype(np.float64), W.astype(np.float64), g.astype(np.float64)
+    ref_y = h64 @ np.concatenate([W64[:d_in], W64[d_in:]], axis=1)
+    ref_dw = np.concatenate([h64.T @ g64[:, :d_out], h64.T @ g64[:, d_out:]], axis=0)
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(20):
+        lib().mq_sage_transform(ptr(th), ld, ptr(m_dev), rows, d_in, ptr(tW), d_out, None,
+                                ptr(scr), ptr(yp), ptr(ny), s)
+        lib().mq_sage_transform_bwd(ptr(th), ld, ptr(m_dev), rows, d_in, ptr(tW), d_out, ptr(tg),
+                                    None, None, ld, ptr(scr), ptr(dwp), ptr(nw), s)
+        torch.cuda.synchronize()
+        S = int(ny.item())
+        y = yp[:S * rows * 2 * d_out].view(S, rows, 2 * d_out).double().sum(0).cpu().numpy()
+        assert _normwise(y, ref_y) <= RTOL
+        S = int(nw.item())
+        p = dwp[:S * d_in * 2 * d_out].view(S, d_in, 2 * d_out).double().sum(0).cpu().numpy()
+        dw = np.concatenate([p[:, :d_out], p[:, d_out:]], axis=0)
+        assert _normwise(dw, ref_dw) <= RTOL
