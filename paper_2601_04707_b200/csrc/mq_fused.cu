@@ -514,36 +514,30 @@ __device__ __forceinline__ void htrace(int i) {
 __device__ __forceinline__ void htrace(int) {}
 #endif
 
-#ifndef MQ_HEAD_ROWS
-#define MQ_HEAD_ROWS 4
-#endif
-constexpr int kHeadRows = MQ_HEAD_ROWS;    // target rows per CTA: one warp per row
-// four warps per target row (4 rows, 512 threads, 256 CTAs at Reddit's batch,
-// two per SM): the row phases (aggregation, CE) use the first kHeadRows
+// Two CTA shapes, both 512 threads: 4 target rows x 4 warps (256 CTAs at a
+// batch of 1024, two per SM) when two CTAs' shared memory fits on an SM,
+// else 8 rows x 2 warps (one wave of 128 CTAs; papers' 172 classes need
+// ~120 KB per CTA).  The row phases (aggregation, CE) use the first R
 // warps, the dense phases (logits, dt, dW partial) and the dt scatter all of
-// them.  Measured on the Reddit step: 8 rows x 2 warps 54.1 us/step (head
-// 10.6 us), 4 x 2 55.1 (11.1), 4 x 4 53.0 (10.2).
-#ifndef MQ_HEAD_WARPS_PER_ROW
-#define MQ_HEAD_WARPS_PER_ROW 4
-#endif
-#if defined(MQ_HEAD_LATE_TRIGGER) && MQ_HEAD_WARPS_PER_ROW > 1
+// them.  Measured on the Reddit step: 8 x 2 50.2 us/step, 4 x 4 49.3,
+// 8 x 4 52.2, 4 x 2 55.1 (an earlier build).
+#if defined(MQ_HEAD_LATE_TRIGGER)
 #error "MQ_HEAD_LATE_TRIGGER with the multi-warp head faulted intermittently (DESIGN.md 7b): unsupported"
 #endif
-constexpr int kHeadWarps = MQ_HEAD_WARPS_PER_ROW * kHeadRows;
-constexpr int kHeadThreads = 32 * kHeadWarps;
 constexpr int kHeadKq = 8;  // k slices of the logits product
 constexpr int kHeadCq = 4;  // class slices of the dt product
-static_assert(kHeadRows % 4 == 0, "the dt product reads dlT as float4 per class");
 
-__host__ __device__ inline int head_red_floats(int d, int C) {
-  const int d2p = (2 * d + 3) & ~3;
-  const int a = kHeadKq * kHeadRows * C, b = kHeadCq * kHeadRows * 2 * d;
+__host__ __device__ inline int head_red_floats(int R, int d, int C) {
+  const int a = kHeadKq * R * C, b = kHeadCq * R * 2 * d;
   return ((a > b ? a : b) + 3) & ~3;
-  (void)d2p;
 }
 constexpr int kHeadMaxEdges = MQ_MAX_FANOUT;  // a seeds-block row has <= fanout triplets
 
-__global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sage_head_kernel(HeadArgs a) {
+template <int R, int WPR>
+__global__ void __launch_bounds__(32 * WPR * R, 2) sage_head_kernel(HeadArgs a) {
+  static_assert(R % 4 == 0, "the dt product reads dlT as float4 per class");
+  constexpr int kHeadWarps = WPR * R;
+  constexpr int kHeadThreads = 32 * kHeadWarps;
 // The scatter that follows launches at the head's trigger.  With 8-warp CTAs
 // a trigger after the dW partials was faster (60.2 -> 58.8 us/step); with the
 // 16-warp head the entry trigger is (58.1 vs 59.3 us/step), and the late
@@ -556,14 +550,13 @@ __global__ void __launch_bounds__(kHeadThreads, kHeadThreads <= 256 ? 4 : 2) sag
   MQ_TL_BEGIN(6);
   htrace(0);
   extern __shared__ __align__(16) float smem[];
-  constexpr int R = kHeadRows;
   const int d = a.d, d2 = 2 * a.d, d2p = (d2 + 3) & ~3, C = a.C, Cp = a.Cp;
   float* Ws = smem;                 // [d2p][Cp]  (rows >= d2 zero)
   float* both = Ws + d2p * Cp;      // [R][d2p]   = [agg | h_dst | 0 pad]
   float* dl = both + R * d2p;       // [R][C]     logits, then dlogits
   float* dlT = dl + R * C;          // [C][R]     dlogits, class-major (dt operand)
   float* red = dlT + R * C;         // slice sums of the logits / dt products
-  float* dts = red + head_red_floats(d, C);  // [R][d2p] dt = dl W^T
+  float* dts = red + head_red_floats(R, d, C);  // [R][d2p] dt = dl W^T
   __shared__ int32_t s_col[R][kHeadMaxEdges];
   __shared__ float s_val[R][kHeadMaxEdges];
   __shared__ int s_ne[R];
@@ -893,13 +886,17 @@ __global__ void head_dw_reduce_kernel(const float* __restrict__ part, int nparts
     dW[o] = fixed_order_sum(part + o, total, nparts);
 }
 
-inline int head_rows(int) { return kHeadRows; }
-
 inline int64_t head_smem_bytes(int R, int d, int C) {
   const int Cp = C | 1, d2p = (2 * d + 3) & ~3;
   // W, both, dl, dlT, slice sums, dt (+ the static edge stash)
-  return (int64_t)(d2p * Cp + R * d2p + 2 * R * C + head_red_floats(d, C) + R * d2p) *
+  return (int64_t)(d2p * Cp + R * d2p + 2 * R * C + head_red_floats(R, d, C) + R * d2p) *
          (int64_t)sizeof(float);
+}
+
+// target rows per CTA: 4 while two CTAs (+ their static stash and the
+// per-CTA reservation) fit in an SM's 228 KB, else 8
+inline int head_rows(int d, int C) {
+  return 2 * (head_smem_bytes(4, d, C) + 4096) <= 228 * 1024 ? 4 : 8;
 }
 
 }  // namespace mq
@@ -1106,7 +1103,7 @@ int mq_sage_transform_bwd(const float* h, int32_t ldh, const int32_t* m_dev, int
 }
 
 int64_t mq_sage_head_scratch_bytes(int32_t n_dst_max, int32_t d, int32_t n_classes) {
-  const int R = head_rows(n_dst_max < 1 ? 1 : n_dst_max);
+  const int R = head_rows(d, n_classes);
   const int64_t G = (n_dst_max + R - 1) / R;
   return 256 + G * 2 * d * (int64_t)n_classes * (int64_t)sizeof(float);
 }
@@ -1124,17 +1121,17 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                "mq_sage_head: bad dims");
   MQ_CHECK_ARG(!loss_ring || (key_dev && ring_len > 0 && world >= 1), "mq_sage_head: bad ring");
   if (n_dst_max <= 0) return MQ_OK;
-  const int R = head_rows(n_dst_max);
+  const int R = head_rows(d, n_classes);
   const int G = ceil_div(n_dst_max, R);
   const int64_t smem = head_smem_bytes(R, d, n_classes);
   MQ_CHECK_ARG(smem <= 220 * 1024, "mq_sage_head: d=%d, classes=%d need %lld B of shared memory", d,
                n_classes, (long long)smem);
   cudaStream_t s = as_stream(stream);
-  static thread_local int64_t configured = 0;
-  if (smem > configured) {  // (static smem counts against the 48 KB default too)
-    MQ_CUDA(cudaFuncSetAttribute(sage_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    configured = smem;
+  auto kern = R == 4 ? sage_head_kernel<4, 4> : sage_head_kernel<8, 2>;
+  static thread_local int64_t configured[2] = {0, 0};
+  if (smem > configured[R == 8]) {  // (static smem counts against the 48 KB default too)
+    MQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[R == 8] = smem;
   }
   HeadArgs a;
   a.row_ptr = row_ptr;
@@ -1162,7 +1159,7 @@ int mq_sage_head(const int32_t* row_ptr, const int32_t* cols, const float* vals,
   a.R = R;
   {
     ProfScope ps(K_SAGE_HEAD, s);
-    MQ_CUDA(launch_k(sage_head_kernel, dim3(G), dim3(kHeadThreads), smem, s, a));
+    MQ_CUDA(launch_k(kern, dim3(G), dim3(512), smem, s, a));
   }
   MQ_LAUNCH_CHECK("sage_head");
   if (dW != nullptr) {
@@ -1189,7 +1186,7 @@ int mq_sage_head_grad_seg(int32_t n_dst_max, int32_t d, int32_t n_classes, void*
                           int64_t offset, mq_grad_seg* out) {
   MQ_CHECK_ARG(scratch && out && n_dst_max >= 1 && d >= 1 && n_classes >= 1,
                "mq_sage_head_grad_seg: bad arguments");
-  const int R = head_rows(n_dst_max);
+  const int R = head_rows(d, n_classes);
   memset(out, 0, sizeof(*out));
   out->part = reinterpret_cast<const float*>(reinterpret_cast<char*>(scratch) + 256);
   out->nparts = ceil_div(n_dst_max, R);
