@@ -157,7 +157,9 @@ int mq_relabel(const int32_t* dst, const int32_t* n_dst_dev, int32_t n_dst_max,
  * mq_gather_labels, bit-identical to the single-batch entry points.  Every
  * per-slot array is given as slot 0's pointer plus a stride (elements) to the
  * next slot.  dpos / first are node-indexed tables per slot (stride
- * table_s) holding -1 / INT32_MAX on entry, restored on exit; scratch holds
+ * table_s) holding -1 / INT32_MAX on entry, restored on exit, INTERLEAVED:
+ * node u's dpos at dpos[2u], its first at first[2u] with first = dpos + 1
+ * (one 8-byte pair per node); scratch holds
  * Q regions of mq_prep_scratch_bytes(max n_dst_max, its fanout) each
  * (scratch_s bytes apart).  When cursor != NULL, cursor[0] (window) advances
  * by Q and cursor[1] must be 0 at rest. */

@@ -21,6 +21,11 @@
 namespace mq {
 namespace prep {
 
+// The relabel's node tables interleave per node: dpos(u) at [2u], first(u)
+// at [2u + 1] (mq_prep_desc.first = dpos + 1): the scan's two random reads
+// of a node, and the sampler's two atomics, share one 32-byte sector.
+constexpr int64_t kTbl = 2;
+
 template <class T>
 struct QP {
   T* p;
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
   const int32_t v = dst.at(q)[r];
   if (tbl.on) {
     tbl.src_ids.at(q)[r] = v;
-    atomicMax(&tbl.dpos.at(q)[v], r);
+    atomicMax(&tbl.dpos.at(q)[kTbl * (int64_t)v], r);
   }
   const int64_t beg = row_off[v];
   const int n = (int)(row_off[v + 1] - beg);
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < n) atomicMin(&tbl.first.at(q)[x[i]], r * fanout + i);
+        if (i < n) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[i]], r * fanout + i);
     }
     cnt.at(q)[r] = n;
     return;
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.first.at(q)[x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[j]], r * fanout + j);
     }
   } else if (hot_off != nullptr) {  // samplers.py:173-175: hot ++ choice(cold, f - |hot|)
     int64_t ha[MAXK];
@@ -175,10 +180,10 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < nh) atomicMin(&tbl.first.at(q)[x[i]], r * fanout + i);
+        if (i < nh) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[i]], r * fanout + i);
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < k2) atomicMin(&tbl.first.at(q)[y[j]], r * fanout + nh + j);
+        if (j < k2) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)y[j]], r * fanout + nh + j);
     }
   } else {  // samplers.py:176-177: choice(nbrs, f)
     fisher_yates<MAXK, int>(rs, n, fanout, pos);
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.first.at(q)[x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[j]], r * fanout + j);
     }
   }
   cnt.at(q)[r] = fanout;
@@ -204,7 +209,7 @@ __global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP
   if (i >= *n_dst.at(q)) return;
   const int32_t v = dst.at(q)[i];
   src_ids.at(q)[i] = v;
-  atomicMax(&dpos.at(q)[v], i);
+  atomicMax(&dpos.at(q)[kTbl * (int64_t)v], i);
 }
 
 // first[u] = min slot r * fanout + i of every pick u (sample_q_kernel does
@@ -215,7 +220,7 @@ __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int r = (int)(s / fanout), i = (int)(s % fanout);
   if (r >= *n_dst.at(q) || i >= cnt.at(q)[r]) return;
-  atomicMin(&first.at(q)[nbr.at(q)[s]], (int32_t)s);
+  atomicMin(&first.at(q)[kTbl * (int64_t)nbr.at(q)[s]], (int32_t)s);
 }
 
 // One scan per hop over the slots r * fanout + i, two channels in one int64:
@@ -233,7 +238,7 @@ struct QLoadRowFlag {
     int64_t v = i == 0 ? ((int64_t)c << 32) : 0;
     if (i < c) {
       const int32_t u = nbr.at(q)[s];
-      if (dpos.at(q)[u] < 0 && first.at(q)[u] == (int32_t)s) v |= 1;
+      if (dpos.at(q)[kTbl * (int64_t)u] < 0 && first.at(q)[kTbl * (int64_t)u] == (int32_t)s) v |= 1;
     }
     return v;
   }
@@ -249,7 +254,7 @@ struct QStoreRowLabel {
     const int32_t u = nbr.at(q)[s];
     const int32_t lab = *n_dst.at(q) + (int32_t)(excl & 0xFFFFFFFFll);
     src_ids.at(q)[lab] = u;
-    dpos.at(q)[u] = lab;
+    dpos.at(q)[kTbl * (int64_t)u] = lab;
   }
   __device__ void total(int64_t, int64_t t) const {
     const int q = blockIdx.y;
@@ -271,7 +276,7 @@ __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
   if (i >= c) return;
   const int e = row_ptr.at(q)[r] + i;
   rows.at(q)[e] = r;
-  cols.at(q)[e] = dpos.at(q)[nbr.at(q)[s]];
+  cols.at(q)[e] = dpos.at(q)[kTbl * (int64_t)nbr.at(q)[s]];
   vals.at(q)[e] = (float)(1.0 / (double)c);  // float32(1.0 / s), samplers.py:200 + nn.py:85
 }
 
@@ -286,8 +291,8 @@ __global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> coun
   const int n = counts.at(q)[0];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int32_t u = src_ids.at(q)[j];
-    dpos.at(q)[u] = -1;
-    first.at(q)[u] = INT_MAX;
+    dpos.at(q)[kTbl * (int64_t)u] = -1;
+    first.at(q)[kTbl * (int64_t)u] = INT_MAX;
   }
 }
 

@@ -60,8 +60,11 @@ class PrepShared:
         dev = g.device
         self.Q = int(Q)
         bounds = hop_bounds(batch_size, fanouts, g.num_nodes)
-        self.dpos = torch.full((Q, g.num_nodes), -1, dtype=torch.int32, device=dev)
-        self.first = torch.full((Q, g.num_nodes), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        # interleaved node tables: [..., 0] = dpos (-1 at rest), [..., 1] = first
+        self.tbl = torch.empty((Q, g.num_nodes, 2), dtype=torch.int32, device=dev)
+        self.tbl[..., 0] = -1
+        self.tbl[..., 1] = 2 ** 31 - 1
+        self.dpos, self.first = self.tbl[..., 0], self.tbl[..., 1]
         per = max(int(lib().mq_prep_scratch_bytes(b.n_dst_max, b.fanout)) for b in bounds)
         self.scratch_s = per
         self.scratch = torch.zeros(Q * per, dtype=torch.uint8, device=dev)
@@ -182,7 +185,7 @@ class PrepGroup:
             hp.edge_s = hb.rows.stride(0)
             hp.src_ids, hp.src_s = ptr(hb.src_ids), hb.src_ids.stride(0)
             hp.counts, hp.counts_s = ptr(hb.counts), hb.counts.stride(0)
-        d.dpos, d.first, d.table_s = ptr(sh.dpos), ptr(sh.first), sh.dpos.stride(0)
+        d.dpos, d.first, d.table_s = ptr(sh.tbl), ptr(sh.tbl) + 4, sh.tbl.stride(0)
         d.scratch, d.scratch_s = ptr(sh.scratch), sh.scratch_s
         d.row_off, d.col = ptr(g.row_off), ptr(g.col)
         d.store_pitch = g.pitch
