@@ -285,9 +285,10 @@ def run_reference_arm(args):
     del sg
     if device:
         torch.cuda.empty_cache()
-    # warm-up batches are not timed; each timed step is one batch, capped so
-    # the whole arm stays within a few minutes
-    w = min(args.warmup, 3)
+    # warm-up batches (W of them, as the driver asked; a cap far above any
+    # driver W keeps a mistaken W from running for hours) are not timed; each
+    # timed step is one batch, capped so the whole arm stays within minutes
+    w = min(args.warmup, 64)
     cpu_oracle_run(ro, col, feats, labels, mask, perm, fanouts, args, 60.0, w, workers=1)
     budget = float(os.environ.get("MQ_REF_BUDGET_S", 90.0))
     seeds, nb, dt, cores = cpu_oracle_run(ro, col, feats, labels, mask, perm[w * args.batch:],
