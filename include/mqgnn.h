@@ -227,6 +227,8 @@ int mq_gather_sharded(const float* cache_tbl, int32_t cache_pitch, const int32_t
 /* ---------------------------------------------------------- SAGE numerics
  * block_apply (nn.py:79-89): agg[r] = sum over the row's triplets, in order,
  * of float32(val) * h[col] — sequential fp32 adds, bit-identical to np.add.at. */
+/* y = max(x, 0) elementwise (the per-op forward's hidden activation). */
+int mq_relu(const float* x, float* y, int64_t n, void* stream);
 int mq_spmm_fwd(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                 const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh,
                 int32_t d, float* agg, int32_t ldagg, void* stream);
@@ -667,6 +669,12 @@ int mq_layer_cdf(const double* probs, int64_t n, double* cdf, void* stream);
 /* host reference of the layer uniforms (tests) */
 int mq_layer_uniforms_host(uint64_t seed, uint64_t epoch, uint32_t batch, uint32_t layer, int64_t n,
                            double* out);
+
+/* dt = dz W^T alone (the per-op SAGE backward when its dW runs on the
+ * tensor cores, mq_sage_linear_af_bwd); scratch: mq_linear_scratch_bytes. */
+int mq_sage_linear_dt(const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                      int32_t d_out, const float* dz, int32_t lddz, float* dt, int32_t lddt,
+                      void* scratch, void* stream);
 
 /* GCN layer transform (nn.py:102-113, 159-180 gcn arm): z = agg W (relu_out
  * = max(z, 0) when given); backward dW = agg^T dz and dt = dz W^T.  fp32

@@ -147,6 +147,8 @@ SIGNATURES = {
     "mq_gcn_block": (C.c_int, [P, P, P, P, P, P, I32, P, P, P, P, P]),
     "mq_layer_uniforms_host": (C.c_int, [U64, U64, U32, U32, I64, P]),
     "mq_layer_cdf": (C.c_int, [P, I64, P, P]),
+    "mq_relu": (C.c_int, [P, P, I64, P]),
+    "mq_sage_linear_dt": (C.c_int, [P, I32, I32, P, I32, P, I32, P, I32, P, P]),
     "mq_gcn_linear_fwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, I32, P, I32, P, P]),
     "mq_gcn_linear_bwd": (C.c_int, [P, I32, P, I32, I32, P, I32, P, I32, P, P, I32, P, P]),
 }

@@ -78,6 +78,20 @@ int mq_sage_linear_bwd(const float* agg, int32_t ldagg, const float* h, int32_t 
   return MQ_OK;
 }
 
+// dt = dz W^T alone (the per-op backward when dW runs on the tensor cores)
+int mq_sage_linear_dt(const int32_t* m_dev, int32_t m_max, int32_t d_in, const float* W,
+                      int32_t d_out, const float* dz, int32_t lddz, float* dt, int32_t lddt,
+                      void* scratch, void* stream) {
+  MQ_CHECK_ARG(m_dev && W && dz && dt && scratch, "mq_sage_linear_dt: null pointer");
+  MQ_CHECK_ARG(d_in >= 1 && d_out >= 1 && lddz >= d_out && lddt >= 2 * d_in,
+               "mq_sage_linear_dt: bad dims");
+  if (m_max <= 0) return MQ_OK;
+  Dims dims{m_dev, 0, nullptr, d_out, 2 * d_in};
+  return run_gemm(ALoadRow{dz, lddz}, BLoadWT{W, d_out, d_out, 2 * d_in}, EpiStore{dt, lddt}, dims,
+                  m_max, d_out, (d_out + GBK - 1) / GBK, reinterpret_cast<float*>(scratch),
+                  as_stream(stream), K_LINEAR_BWD_X, K_LINEAR_BWD_X_REDUCE);
+}
+
 // ---- GCN arm (nn.py:102-113, 159-180): z = agg W, dW = agg^T dz, dt = dz W^T
 int mq_gcn_linear_fwd(const float* agg, int32_t ldagg, const int32_t* m_dev, int32_t m_max,
                       int32_t d_in, const float* W, int32_t d_out, float* z, int32_t ldz,

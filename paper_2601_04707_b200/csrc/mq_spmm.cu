@@ -109,11 +109,28 @@ __global__ void spmm_bwd_mask_kernel(const int32_t* __restrict__ counts, int d,
   }
 }
 
+// y = max(x, 0) elementwise (the per-op forward's activation)
+__global__ void relu_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fmaxf(x[i], 0.f);
+}
+
 }  // namespace mq
 
 using namespace mq;
 
 extern "C" {
+
+int mq_relu(const float* x, float* y, int64_t n, void* stream) {
+  MQ_CHECK_ARG(x && y && n >= 0, "mq_relu: bad arguments");
+  if (n == 0) return MQ_OK;
+  int64_t b = (n + 255) / 256;
+  if (b > kNumSMs * 16) b = kNumSMs * 16;
+  relu_kernel<<<(int)b, 256, 0, as_stream(stream)>>>(x, y, n);
+  MQ_LAUNCH_CHECK("relu");
+  return MQ_OK;
+}
 
 int mq_spmm_fwd(const int32_t* row_ptr, const int32_t* cols, const float* vals,
                 const int32_t* n_dst_dev, int32_t n_dst_max, const float* h, int32_t ldh, int32_t d,

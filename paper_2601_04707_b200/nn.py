@@ -133,6 +133,14 @@ def _pitched(x: torch.Tensor, ld: int) -> torch.Tensor:
     return out
 
 
+def _tc_linear_ok(d_in: int, d_out: int) -> bool:
+    """The per-op SAGE transform runs on the tensor cores (tcgen05 3xTF32, the
+    aggregate-first kernels of the fused step) where their shape rules allow;
+    otherwise the fp32 split-K FFMA GEMM."""
+    return (lib().mq_get_gemm_backend() == 1 and d_in >= 4 and d_in % 4 == 0
+            and d_out <= 256)
+
+
 def sage_forward(batch, state: ModelState, return_cache: bool = False):
     """Per layer: agg = segment-mean SpMM, z = [agg | h_dst] W, ReLU except last."""
     dev = state.device
@@ -153,10 +161,18 @@ def sage_forward(batch, state: ModelState, return_cache: bool = False):
         d_out = int(W.shape[1])
         z = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev)
         r = torch.empty((max(nd, 1), d_out), dtype=torch.float32, device=dev) if l < L - 1 else None
-        scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
-                          dtype=torch.float32, device=dev)
-        lib().mq_sage_linear_fwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,
-                                 ptr(z), d_out, ptr(r), d_out, ptr(scr), stream)
+        if _tc_linear_ok(d_in, d_out):  # z = [agg | h_dst] W on tcgen05, then relu
+            part = torch.empty(int(lib().mq_full_linear_cat_part_floats(nd, d_out)),
+                               dtype=torch.float32, device=dev)
+            lib().mq_full_linear_cat(ptr(agg), ld, ptr(hp), ld, nd, d_in, ptr(W), d_out, ptr(z),
+                                     d_out, 0, ptr(part), stream)
+            if r is not None:
+                lib().mq_relu(ptr(z), ptr(r), nd * d_out, stream)
+        else:
+            scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
+                              dtype=torch.float32, device=dev)
+            lib().mq_sage_linear_fwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W),
+                                     d_out, ptr(z), d_out, ptr(r), d_out, ptr(scr), stream)
         cache["inputs"].append((hp, agg, blk, nd_dev, d_in))
         cache["pre"].append(z[:nd])
         h = r[:nd] if l < L - 1 else z[:nd]
@@ -218,6 +234,38 @@ def batch_loss(logits: torch.Tensor, labels):
     return float(loss.item()), dl[:n]
 
 
+def _tc_weight_grad(agg, hp, ld, nd_dev, nd, d_in, dz, lddz, d_out, dW, stream):
+    """dW = [agg | h]^T dz (nn.py:167-170) through the aggregate-first weight
+    gradient kernel (tcgen05, split-K partials [S][2 d_in][d_out]) and one
+    fixed-order reduction into dW."""
+    from ._lib import GradSrc
+    import ctypes as C
+    dev = dW.device
+    parts = torch.empty(int(lib().mq_sage_af_dw_parts_bytes(d_in, d_out)) // 4 + 1,
+                        dtype=torch.float32, device=dev)
+    nparts = torch.zeros(1, dtype=torch.int32, device=dev)
+    dzc = dz if (dz.is_contiguous() and lddz % 4 == 0) else None
+    if dzc is None:  # a 16-byte-aligned pitch for the tensor-map operand
+        lp = (d_out + 3) // 4 * 4
+        dzc = torch.zeros((max(nd, 1), lp), dtype=torch.float32, device=dev)
+        dzc[:nd, :d_out] = dz[:nd, :d_out]
+        lddz = lp
+    ones = torch.ones((max(nd, 1), lddz), dtype=torch.float32, device=dev)
+    lib().mq_sage_linear_af_bwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(dzc), lddz,
+                                ptr(ones), lddz, d_out, ptr(parts), ptr(nparts), stream)
+    src = GradSrc()
+    seg = src.seg[0]
+    seg.part = ptr(parts)
+    seg.nparts_dev = ptr(nparts)
+    seg.stride = 2 * d_in * d_out
+    seg.offset = 0
+    seg.size = 2 * d_in * d_out
+    seg.nparts = 0
+    seg.kind = 0
+    src.nseg = 1
+    lib().mq_grad_reduce(C.byref(src), ptr(dW), 2 * d_in * d_out, ptr(dW), stream)
+
+
 def _gcn_backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
     """GCN arm of nn.py:159-180: dW = agg^T dz, dh = block_apply_t(dz W^T)."""
     dev = state.device
@@ -275,8 +323,18 @@ def backward(batch, state: ModelState, cache, dlogits: torch.Tensor) -> list:
         scr = torch.empty(int(lib().mq_linear_scratch_bytes(nd, d_in, d_out)) // 4 + 1,
                           dtype=torch.float32, device=dev)
         dt = torch.empty((max(nd, 1), 2 * d_in), dtype=torch.float32, device=dev) if l > 0 else None
-        lib().mq_sage_linear_bwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W), d_out,
-                                 ptr(dz), lddz, ptr(dW), ptr(dt), 2 * d_in, ptr(scr), stream)
+        if _tc_linear_ok(d_in, d_out) and nd > 0:
+            # dW = [agg | h_dst]^T dz on tcgen05 (deferred split-K partials,
+            # reduced in fixed order); dz is already masked, so the kernel's
+            # (act > 0) mask gets ones
+            _tc_weight_grad(agg, hp, ld, nd_dev, nd, d_in, dz, lddz, d_out, dW, stream)
+            if dt is not None:  # dt = dz W^T: K = d_out, the FFMA GEMM
+                lib().mq_sage_linear_dt(ptr(nd_dev), nd, d_in, ptr(W), d_out, ptr(dz), lddz,
+                                        ptr(dt), 2 * d_in, ptr(scr), stream)
+        else:
+            lib().mq_sage_linear_bwd(ptr(agg), ld, ptr(hp), ld, ptr(nd_dev), nd, d_in, ptr(W),
+                                     d_out, ptr(dz), lddz, ptr(dW), ptr(dt), 2 * d_in, ptr(scr),
+                                     stream)
         grads[l] = dW
         if l > 0:
             ns = blk.num_src
