@@ -225,3 +225,30 @@ def test_spmm_backward_vs_oracle(golden_sampling, graphs):
                       b.num_src, ptr(dtt), 2 * d, d, None, 0, ptr(dh), d,
                       torch.cuda.current_stream().cuda_stream)
     assert_close_normwise(dh.cpu().numpy(), ref, rtol=1e-6, what="spmm_bwd")
+
+
+def test_per_op_tcgen05_matches_ffma(golden_sampling, graphs):
+    """The per-op SAGE transform / weight gradient on tcgen05 (3xTF32, split-K
+    partials summed by mq_grad_reduce) against the FFMA split-K path at a
+    wider hidden size, with a class count whose dlogits pitch (5) needs the
+    16-byte-aligned copy."""
+    dg = graphs["g2"]
+    params = SamplerParams("sage", (10, 5, 3), num_layers=3)
+    tg = np.random.default_rng(11).choice(2000, 512, replace=False)
+    mb = build_minibatch(dg, tg, params, PhiloxStream(9, 0, 1), batch_id=1)
+    state = mnn.init_model(16, 64, 5, num_layers=3, seed=3, learning_rate=0.01)
+    out = {}
+    old = lib().mq_get_gemm_backend()
+    try:
+        for be in (1, 0):
+            lib().mq_set_gemm_backend(be)
+            logits, fc = mnn.forward(mb, state, return_cache=True)
+            loss, dl = mnn.batch_loss(logits, mb.target_labels)
+            grads = mnn.backward(mb, state, fc, dl)
+            out[be] = (logits.cpu().numpy(), loss, [g.cpu().numpy() for g in grads])
+    finally:
+        lib().mq_set_gemm_backend(old)
+    assert_close_normwise(out[1][0], out[0][0], rtol=2e-5, what="logits")
+    assert out[1][1] == pytest.approx(out[0][1], rel=1e-5)
+    for l, (a, b) in enumerate(zip(out[1][2], out[0][2])):
+        assert_close_normwise(a, b, rtol=2e-5, what=f"grad{l}")
