@@ -156,10 +156,10 @@ int mq_relabel(const int32_t* dst, const int32_t* n_dst_dev, int32_t n_dst_max,
  * n_targets / key) -> [mq_sample_hop -> mq_relabel] per hop -> mq_gather +
  * mq_gather_labels, bit-identical to the single-batch entry points.  Every
  * per-slot array is given as slot 0's pointer plus a stride (elements) to the
- * next slot.  dpos / first are node-indexed tables per slot (stride
- * table_s) holding -1 / INT32_MAX on entry, restored on exit, INTERLEAVED:
- * node u's dpos at dpos[2u], its first at first[2u] with first = dpos + 1
- * (one 8-byte pair per node); scratch holds
+ * next slot.  node_rank is a node-indexed int32 table per slot (stride
+ * table_s) holding INT32_MAX on entry, restored on exit (one word per node:
+ * -(position + 1) for a node in the current src list, else its first pick
+ * slot; reserved_ must be NULL); scratch holds
  * Q regions of mq_prep_scratch_bytes(max n_dst_max, its fanout) each
  * (scratch_s bytes apart).  When cursor != NULL, cursor[0] (window) advances
  * by Q and cursor[1] must be 0 at rest. */
@@ -180,7 +180,7 @@ typedef struct mq_prep_desc {
   int32_t* n_targets; int64_t n_targets_s;
   uint32_t* key;      int64_t key_s;      /* {seed mod 2^32, epoch, batch} per slot */
   mq_prep_hop hop[MQ_MAX_HOPS];
-  int32_t* dpos; int32_t* first; int64_t table_s;
+  int32_t* node_rank; void* reserved_; int64_t table_s;
   void* scratch; int64_t scratch_s;
   const int64_t* row_off; const int32_t* col; const int64_t* hot_arc; const int64_t* hot_off;
   const float* cache_tbl; int32_t cache_pitch, store_pitch;

@@ -21,11 +21,18 @@
 namespace mq {
 namespace prep {
 
-// The relabel's node tables interleave per node: dpos(u) at [2u], first(u)
-// at [2u + 1] (mq_prep_desc.first = dpos + 1): the scan's two random reads
-// of a node, and the sampler's two atomics, share one 32-byte sector.
-constexpr int64_t kTbl = 2;
-
+// The relabel keeps ONE int32 word per node and slot (mq_prep_desc.node_rank,
+// INT32_MAX at rest), so a products-sized table (8 slots x 2.4M nodes x 4 B)
+// stays L2-resident:
+//   w[u] = -(p + 1)  u is in the current src list at position p (dst marks
+//                    -(r + 1) and new labels are both stored this way);
+//   w[u] = s >= 0    u's first pick slot s = r * fanout + i this hop
+//                    (atomicMin: the slot order is the triplet order);
+//   w[u] = INT32_MAX u untouched.
+// Marks and picks are both atomicMin (order-free); a scan tile flags u iff
+// w[u] == s, which no stored label (negative) can alias.  The next hop's dst
+// list is this hop's src list, so its marks are already in place: only hop 0
+// marks.
 template <class T>
 struct QP {
   T* p;
@@ -85,13 +92,14 @@ __global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm,
 // register arrays so a row costs ~4 dependent round trips
 // (dst -> offsets -> hot arcs -> columns), not 2*fanout.
 // With `tbl` the kernel also does the relabel's per-row bookkeeping (the
-// sampled rows are independent of it): the dst mark (dpos[v] = max row,
-// src_ids prefix, samplers.py:155-156) and every pick's first-occurrence
-// slot (first[u] = min over slots r * fanout + i: the slot order is the
-// triplet order, so the minimum is the first occurrence, samplers.py:186-189).
+// sampled rows are independent of it): the src_ids prefix and, at hop 0,
+// the dst mark (w[v] = -(max row + 1), samplers.py:155-156), and every
+// pick's first-occurrence slot (w[u] = min over slots r * fanout + i: the
+// slot order is the triplet order, so the minimum is the first occurrence,
+// samplers.py:186-189).
 struct RelabelTables {
-  QP<int32_t> dpos, first, src_ids;
-  bool on;
+  QP<int32_t> w, src_ids;
+  bool on, mark;
 };
 
 template <int MAXK>
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
   const int32_t v = dst.at(q)[r];
   if (tbl.on) {
     tbl.src_ids.at(q)[r] = v;
-    atomicMax(&tbl.dpos.at(q)[kTbl * (int64_t)v], r);
+    if (tbl.mark) atomicMin(&tbl.w.at(q)[v], -(r + 1));
   }
   const int64_t beg = row_off[v];
   const int n = (int)(row_off[v + 1] - beg);
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < n) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[i]], r * fanout + i);
+        if (i < n) atomicMin(&tbl.w.at(q)[x[i]], r * fanout + i);
     }
     cnt.at(q)[r] = n;
     return;
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(&tbl.w.at(q)[x[j]], r * fanout + j);
     }
   } else if (hot_off != nullptr) {  // samplers.py:173-175: hot ++ choice(cold, f - |hot|)
     int64_t ha[MAXK];
@@ -180,10 +188,10 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < nh) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[i]], r * fanout + i);
+        if (i < nh) atomicMin(&tbl.w.at(q)[x[i]], r * fanout + i);
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < k2) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)y[j]], r * fanout + nh + j);
+        if (j < k2) atomicMin(&tbl.w.at(q)[y[j]], r * fanout + nh + j);
     }
   } else {  // samplers.py:176-177: choice(nbrs, f)
     fisher_yates<MAXK, int>(rs, n, fanout, pos);
@@ -195,32 +203,32 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.first.at(q)[kTbl * (int64_t)x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(&tbl.w.at(q)[x[j]], r * fanout + j);
     }
   }
   cnt.at(q)[r] = fanout;
 }
 
 // ------------------------------------------------------------ relabel
-__global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP<int32_t> dpos,
-                              QP<int32_t> src_ids) {
+__global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP<int32_t> w,
+                              QP<int32_t> src_ids, bool mark) {
   const int q = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_dst.at(q)) return;
   const int32_t v = dst.at(q)[i];
   src_ids.at(q)[i] = v;
-  atomicMax(&dpos.at(q)[kTbl * (int64_t)v], i);
+  if (mark) atomicMin(&w.at(q)[v], -(i + 1));
 }
 
-// first[u] = min slot r * fanout + i of every pick u (sample_q_kernel does
+// w[u] = min slot r * fanout + i of every pick u (sample_q_kernel does
 // this inline; this kernel serves passes whose sampling ran separately)
 __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
-                               QP<const int32_t> n_dst, int fanout, QP<int32_t> first) {
+                               QP<const int32_t> n_dst, int fanout, QP<int32_t> w) {
   const int q = blockIdx.y;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int r = (int)(s / fanout), i = (int)(s % fanout);
   if (r >= *n_dst.at(q) || i >= cnt.at(q)[r]) return;
-  atomicMin(&first.at(q)[kTbl * (int64_t)nbr.at(q)[s]], (int32_t)s);
+  atomicMin(&w.at(q)[nbr.at(q)[s]], (int32_t)s);
 }
 
 // One scan per hop over the slots r * fanout + i, two channels in one int64:
@@ -228,7 +236,7 @@ __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
 // row_ptr), low 32 bits = the first-occurrence flag of a new node (prefix ->
 // its label) -- the row offsets and the labels in one decoupled-look-back pass.
 struct QLoadRowFlag {
-  QP<const int32_t> nbr, cnt, n_dst, dpos, first;
+  QP<const int32_t> nbr, cnt, n_dst, w;
   int fanout;
   __device__ int64_t size() const { return (int64_t)(*n_dst.at(blockIdx.y)) * fanout; }
   __device__ int64_t operator()(int64_t s) const {
@@ -237,15 +245,14 @@ struct QLoadRowFlag {
     const int c = cnt.at(q)[r];
     int64_t v = i == 0 ? ((int64_t)c << 32) : 0;
     if (i < c) {
-      const int32_t u = nbr.at(q)[s];
-      if (dpos.at(q)[kTbl * (int64_t)u] < 0 && first.at(q)[kTbl * (int64_t)u] == (int32_t)s) v |= 1;
+      if (__ldcg(&w.at(q)[nbr.at(q)[s]]) == (int32_t)s) v |= 1;
     }
     return v;
   }
 };
 struct QStoreRowLabel {
   QP<const int32_t> nbr, n_dst;
-  QP<int32_t> dpos, src_ids, counts, row_ptr;
+  QP<int32_t> w, src_ids, counts, row_ptr;
   int fanout;
   __device__ void operator()(int64_t s, int64_t excl, int64_t val) const {
     const int q = blockIdx.y;
@@ -254,7 +261,7 @@ struct QStoreRowLabel {
     const int32_t u = nbr.at(q)[s];
     const int32_t lab = *n_dst.at(q) + (int32_t)(excl & 0xFFFFFFFFll);
     src_ids.at(q)[lab] = u;
-    dpos.at(q)[kTbl * (int64_t)u] = lab;
+    w.at(q)[u] = -(lab + 1);
   }
   __device__ void total(int64_t, int64_t t) const {
     const int q = blockIdx.y;
@@ -266,7 +273,7 @@ struct QStoreRowLabel {
 };
 __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
                               QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
-                              QP<const int32_t> dpos, QP<int32_t> rows, QP<int32_t> cols,
+                              QP<const int32_t> w, QP<int32_t> rows, QP<int32_t> cols,
                               QP<float> vals) {
   const int q = blockIdx.y;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -276,23 +283,21 @@ __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
   if (i >= c) return;
   const int e = row_ptr.at(q)[r] + i;
   rows.at(q)[e] = r;
-  cols.at(q)[e] = dpos.at(q)[kTbl * (int64_t)nbr.at(q)[s]];
+  cols.at(q)[e] = -(w.at(q)[nbr.at(q)[s]] + 1);
   vals.at(q)[e] = (float)(1.0 / (double)c);  // float32(1.0 / s), samplers.py:200 + nn.py:85
 }
 
 // Table restore, once per pass: every node a hop touched (dst marks, new
 // labels, first-occurrence slots of any pick) is in that hop's src list, and
 // each hop's src list contains the previous one's, so the last hop's src list
-// covers them all.  (Within a pass the next hop's mark overwrites each entry
-// with the same or a larger position: no restore between hops.)
+// covers them all.
 __global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> counts,
-                               QP<int32_t> dpos, QP<int32_t> first) {
+                               QP<int32_t> w) {
   const int q = blockIdx.y;
   const int n = counts.at(q)[0];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int32_t u = src_ids.at(q)[j];
-    dpos.at(q)[kTbl * (int64_t)u] = -1;
-    first.at(q)[kTbl * (int64_t)u] = INT_MAX;
+    w.at(q)[u] = INT_MAX;
   }
 }
 
@@ -427,7 +432,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
   MQ_CHECK_ARG(Q >= 1 && Q <= 65535, "mq_prep_batches: nslots %d out of range", Q);
   MQ_CHECK_ARG(d.num_hops >= 1 && d.num_hops <= MQ_MAX_HOPS, "mq_prep_batches: num_hops %d",
                d.num_hops);
-  MQ_CHECK_ARG(d.row_off && d.col && d.targets && d.n_targets && d.key && d.dpos && d.first &&
+  MQ_CHECK_ARG(d.row_off && d.col && d.targets && d.n_targets && d.key && d.node_rank &&
                    d.scratch && (d.store || d.n_shards >= 1) && d.x0 && d.all_labels && d.labels,
                "mq_prep_batches: null pointer");
   MQ_CHECK_ARG(d.n_shards >= 0 && d.n_shards <= MQ_MAX_PEERS, "mq_prep_batches: n_shards %d",
@@ -478,8 +483,8 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     if (mask & MQ_PREP_SAMPLE) {
       ProfScope ps(K_SAMPLE, s);
       const dim3 grid(ceil_div(hp.n_dst_max, 64), Q);
-      const RelabelTables tb{qp(d.dpos, d.table_s), qp(d.first, d.table_s),
-                             qp(hp.src_ids, hp.src_s), relabel};
+      const RelabelTables tb{qp(d.node_rank, d.table_s), qp(hp.src_ids, hp.src_s), relabel,
+                             h == 0};
       if (f <= 8)
         sample_q_kernel<8><<<grid, 64, 0, s>>>(
             d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
@@ -495,16 +500,18 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     } else if (relabel) {  // sampled earlier: the relabel's marks and first slots alone
       ProfScope ps(K_RELABEL_MARK, s);
       mark_q_kernel<<<dim3(ceil_div(hp.n_dst_max, 256), Q), 256, 0, s>>>(
-          cq(dst, dst_s), cq(nd, nd_s), qp(d.dpos, d.table_s), qp(hp.src_ids, hp.src_s));
+          cq(dst, dst_s), cq(nd, nd_s), qp(d.node_rank, d.table_s), qp(hp.src_ids, hp.src_s),
+          h == 0);
       first_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
-          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), f, qp(d.first, d.table_s));
+          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), f,
+          qp(d.node_rank, d.table_s));
     }
     MQ_LAUNCH_CHECK("prep sample");
     if (!relabel) continue;
     int rc = launch_scan_q(
         QLoadRowFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s),
-                     cq(d.dpos, d.table_s), cq(d.first, d.table_s), f},
-        QStoreRowLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.dpos, d.table_s),
+                     cq(d.node_rank, d.table_s), f},
+        QStoreRowLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.node_rank, d.table_s),
                        qp(hp.src_ids, hp.src_s), qp(hp.counts, hp.counts_s),
                        qp(hp.row_ptr, hp.row_ptr_s), f},
         slots, Q, d.scratch, d.scratch_s, s, K_RELABEL_FLAG);
@@ -513,7 +520,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
       ProfScope ps(K_RELABEL_COLS, s);
       cols_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
           cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s), cq(nd, nd_s), f,
-          cq(d.dpos, d.table_s), qp(hp.rows, hp.edge_s), qp(hp.cols, hp.edge_s),
+          cq(d.node_rank, d.table_s), qp(hp.rows, hp.edge_s), qp(hp.cols, hp.edge_s),
           qp(hp.vals, hp.edge_s));
     }
     MQ_LAUNCH_CHECK("prep cols");
@@ -522,8 +529,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
       int cb = ceil_div(slots + hp.n_dst_max, 256);
       const int cap = ceil_div(kNumSMs * 8, Q);
       clean_q_kernel<<<dim3(cb < cap ? cb : cap, Q), 256, 0, s>>>(
-          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), qp(d.dpos, d.table_s),
-          qp(d.first, d.table_s));
+          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), qp(d.node_rank, d.table_s));
     }
     MQ_LAUNCH_CHECK("prep clean");
   }

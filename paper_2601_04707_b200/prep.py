@@ -41,7 +41,7 @@ class PrepDesc(C.Structure):
                 ("targets", P), ("targets_s", I64), ("n_targets", P), ("n_targets_s", I64),
                 ("key", P), ("key_s", I64),
                 ("hop", PrepHop * MQ_MAX_HOPS),
-                ("dpos", P), ("first", P), ("table_s", I64),
+                ("node_rank", P), ("reserved_", P), ("table_s", I64),
                 ("scratch", P), ("scratch_s", I64),
                 ("row_off", P), ("col", P), ("hot_arc", P), ("hot_off", P),
                 ("cache_tbl", P), ("cache_pitch", I32), ("store_pitch", I32),
@@ -60,11 +60,9 @@ class PrepShared:
         dev = g.device
         self.Q = int(Q)
         bounds = hop_bounds(batch_size, fanouts, g.num_nodes)
-        # interleaved node tables: [..., 0] = dpos (-1 at rest), [..., 1] = first
-        self.tbl = torch.empty((Q, g.num_nodes, 2), dtype=torch.int32, device=dev)
-        self.tbl[..., 0] = -1
-        self.tbl[..., 1] = 2 ** 31 - 1
-        self.dpos, self.first = self.tbl[..., 0], self.tbl[..., 1]
+        # the relabel's node-rank words, one int32 per node and slot (INT32_MAX
+        # at rest): 4 B x nodes x Q, L2-resident up to products-sized graphs
+        self.tbl = torch.full((Q, g.num_nodes), 2 ** 31 - 1, dtype=torch.int32, device=dev)
         per = max(int(lib().mq_prep_scratch_bytes(b.n_dst_max, b.fanout)) for b in bounds)
         self.scratch_s = per
         self.scratch = torch.zeros(Q * per, dtype=torch.uint8, device=dev)
@@ -185,7 +183,7 @@ class PrepGroup:
             hp.edge_s = hb.rows.stride(0)
             hp.src_ids, hp.src_s = ptr(hb.src_ids), hb.src_ids.stride(0)
             hp.counts, hp.counts_s = ptr(hb.counts), hb.counts.stride(0)
-        d.dpos, d.first, d.table_s = ptr(sh.tbl), ptr(sh.tbl) + 4, sh.tbl.stride(0)
+        d.node_rank, d.table_s = ptr(sh.tbl), sh.tbl.stride(0)
         d.scratch, d.scratch_s = ptr(sh.scratch), sh.scratch_s
         d.row_off, d.col = ptr(g.row_off), ptr(g.col)
         d.store_pitch = g.pitch
