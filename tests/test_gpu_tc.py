@@ -30,6 +30,8 @@ SHAPES = [  # (rows, d_in, d_out)
     (5000, 64, 64),    # several items per CTA on the forward
     (700, 16, 8),      # N = 16: the narrowest UMMA tile (one 32-column TMEM load)
     (40000, 100, 64),  # many items per CTA: the async ring crosses item boundaries
+    (97000, 64, 64),   # products-shaped hidden layer: resident weights (kFwdR)
+    (50000, 30, 13),   # resident weights with odd widths (N = 26 padded to 32)
 ]
 
 
@@ -136,7 +138,8 @@ def test_transform_bwd_deterministic(tc_kernel, rows, d_in, d_out):
 
 
 @pytest.mark.parametrize("rows,d_in,d_out", [(2604, 100, 64), (777, 16, 16), (97, 64, 8),
-                                             (30000, 100, 64), (0, 16, 16)])
+                                             (30000, 100, 64), (0, 16, 16),
+                                             (100000, 100, 64), (60000, 16, 16)])
 def test_aggregate_first_layer(tc_kernel, rows, d_in, d_out):
     """mq_sage_linear_af (act = relu([agg | h] W)) and mq_sage_linear_af_bwd
     (dW = [agg | h]^T (dh * (act > 0))) against fp64."""
