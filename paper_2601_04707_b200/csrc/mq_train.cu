@@ -107,17 +107,18 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;  // element within the segment
     const int np = sg.nparts;
     float acc = 0.f;
-    if (j < sg.size) {
-      float tv[16];
+    if (j < sg.size) {  // warp q sums partials q, q + 8, ... in order, 16 loads in flight
+      for (int base = 0; base < np; base += 128) {
+        float tv[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int p = q + 8 * u;
-        tv[u] = p < np ? __ldcg(sg.part + (int64_t)p * sg.stride + j) : 0.f;
+        for (int u = 0; u < 16; ++u) {
+          const int p = base + q + 8 * u;
+          tv[u] = p < np ? __ldcg(sg.part + (int64_t)p * sg.stride + j) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (base + q + 8 * u < np) acc += tv[u];
       }
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (q + 8 * u < np) acc += tv[u];
-      for (int p = q + 128; p < np; p += 8) acc += __ldcg(sg.part + (int64_t)p * sg.stride + j);
     }
     red[q][lane] = acc;
     __syncthreads();
