@@ -49,7 +49,9 @@ def main(path):
             a[k] += num(r[i])
     tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
               "ms": 1e3}.get(unit.get("t", "ns"), 1e-3)
-    bscale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit.get("rd", "byte"), 1e-6)
+    bs = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+    rscale = bs.get(unit.get("rd", "byte"), 1e-6)  # each column carries its own unit
+    wscale = bs.get(unit.get("wr", "byte"), 1e-6)
     sscale = 1.0 if unit.get("smem", "").startswith("Kbyte") else 1 / 1024
     print("| kernel | launches | time us (ncu, cold) | DRAM read MB | DRAM write MB | DRAM % peak "
           "| SM thr % | tensor pipe % | warps active % | grid | regs | dyn smem KB |")
@@ -57,7 +59,7 @@ def main(path):
     for nm, a in agg.items():
         n = a["n"]
         g = lambda k, s=1.0: a[k] / n * s if k in a else float("nan")
-        print(f"| {nm} | {n} | {g('t', tscale):.2f} | {g('rd', bscale):.3f} | {g('wr', bscale):.3f} "
+        print(f"| {nm} | {n} | {g('t', tscale):.2f} | {g('rd', rscale):.3f} | {g('wr', wscale):.3f} "
               f"| {g('dram'):.1f} | {g('sm'):.1f} | {g('tc'):.1f} | {g('warps'):.1f} | {g('grid'):.0f} "
               f"| {g('regs'):.0f} | {g('smem') * sscale:.0f} |")
 
