@@ -521,6 +521,7 @@ def run_ours(args):
                 "share": per_step[nm] / tot, "units": rec.get("units"),
                 "bytes_per_launch": rec.get("bytes"), "gbps": rec.get("gbps"),
                 "flops_per_launch": rec.get("flops"), "tflops": rec.get("tflops"),
+                "sector_gbps": rec.get("sector_gbps"),
             }
         per_kernel["_counts"] = tab["counts"]
     if world > 1:  # the other ranks' next steps wait on rank 0's exchange
@@ -638,6 +639,9 @@ def run_ours(args):
                              "units": k["units"]}
                 if k.get("tflops"):
                     focus[nm]["tflops_fp32_equiv"] = k["tflops"]
+                if k.get("sector_gbps"):  # random-access kernels: 32 B per touch
+                    focus[nm]["sector_gbps"] = k["sector_gbps"]
+                    focus[nm]["frac_hbm_sector"] = k["sector_gbps"] / hbm
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "warmup_windows_run": args.warmup + extra_warm,

@@ -46,13 +46,23 @@ def op_models(counts: dict, dims: list, fanouts, Q: int, cached: bool, n_params:
     B = counts["n_targets"]
     C = num_classes
     m = {}
-    samp = relab = 0.0
-    for nd, ns, nnz in hops:
+    samp = relab = samp_sec = relab_sec = 0.0
+    for h, (nd, ns, nnz) in enumerate(hops):
         samp += nd * (4 + 16 + (16 if cached else 0) + 4) + nnz * (4 + 4 + (8 if cached else 0))
         relab += 4 * (nnz + nd) + 4 * (nnz + ns) + 4 * (nd + 1)
+        # the same work counted in the 32-byte sectors a random access moves:
+        # sampler = offsets (+ hot offsets) per row and one column sector per
+        # pick (+ its hot-arc entry); relabel = one node-word sector per
+        # first-slot atomic, flag read and column read per pick, per label
+        # store, per hop-0 mark and per restore (last hop)
+        samp_sec += 32 * (nd * (2 if cached else 1) + nnz * (2 if cached else 1))
+        relab_sec += 32 * (3 * nnz + (ns - nd) + (nd if h == 0 else 0)
+                           + (ns if h == L - 1 else 0))
     n_in = hops[-1][1]
-    m["prep_sample"] = {"bytes": Q * samp, "units": f"{Q} batches x {L} hops"}
-    m["prep_relabel"] = {"bytes": Q * relab, "units": f"{Q} batches x {L} hops"}
+    m["prep_sample"] = {"bytes": Q * samp, "sector_bytes": Q * (samp + samp_sec),
+                        "units": f"{Q} batches x {L} hops"}
+    m["prep_relabel"] = {"bytes": Q * relab, "sector_bytes": Q * (relab + relab_sec),
+                         "units": f"{Q} batches x {L} hops"}
     m["prep_gather"] = {"bytes": Q * (2 * 4 * feature_dim * n_in + 8 * n_in),
                         "units": f"{Q} batches"}
     m["prep_pass"] = {"bytes": m["prep_sample"]["bytes"] + m["prep_relabel"]["bytes"]
@@ -143,6 +153,8 @@ def op_table(runner, reps: int = 20, iters: int = 3) -> dict:
         sec = rec["us"] * 1e-6
         if md.get("bytes"):
             rec["gbps"] = md["bytes"] / sec / 1e9
+        if md.get("sector_bytes"):
+            rec["sector_gbps"] = md["sector_bytes"] / sec / 1e9
         if md.get("flops"):
             rec["tflops"] = md["flops"] / sec / 1e12
     return {"counts": counts, "ops": out}

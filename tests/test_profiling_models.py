@@ -48,3 +48,17 @@ def test_models_stay_within_touchable_bytes():
     for name, v in m.items():
         q = 8 if name.startswith("prep_") else 1
         assert v["bytes"] <= 3 * big * q, (name, v["bytes"])
+
+
+def test_sector_models_of_the_random_access_prep():
+    """prep_sample / prep_relabel also carry a 32-byte-sector count (one
+    sector per random touch on top of the compulsory bytes)."""
+    m = _models()
+    hops, Q, L = COUNTS["hops"], 8, 3
+    relab_sec = sum(32 * (3 * nnz + (ns - nd) + (nd if h == 0 else 0) + (ns if h == L - 1 else 0))
+                    for h, (nd, ns, nnz) in enumerate(hops))
+    assert m["prep_relabel"]["sector_bytes"] == m["prep_relabel"]["bytes"] + Q * relab_sec
+    samp_sec = sum(32 * (2 * nd + 2 * nnz) for nd, ns, nnz in hops)  # cached: hot offsets / arcs
+    assert m["prep_sample"]["sector_bytes"] == m["prep_sample"]["bytes"] + Q * samp_sec
+    for k in ("prep_sample", "prep_relabel"):
+        assert m[k]["sector_bytes"] > m[k]["bytes"]
