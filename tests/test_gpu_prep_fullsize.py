@@ -61,3 +61,19 @@ def test_products_group_vs_oracle(placement):
     hg = _Host(g)
     _device_plan_vs_oracle(hg, g, cache, mask, fanouts, 1024, seed=1, epoch=2,
                            check_slots=8 if placement == "hbm" else 2)
+
+
+def test_products_fused_step_vs_oracle():
+    """The fused training step at the products shape (3 layers, aggregate-
+    first 100-d input layer, 1024 seeds, the real prep pass): loss at rel
+    1e-5 and per-layer gradients within 1e-5 of the exact (f64) evaluation of
+    the same fp32 model on the oracle's identical batch, two windows."""
+    from conftest import HostGraph
+    from test_gpu_fused import _fused_vs_oracle
+    g, _, mask, fanouts = _shape("products")
+    h = _Host(g)
+    hg = HostGraph(h.row_offsets, h.col_indices, h.features, h.labels, g.num_classes,
+                   train_mask=g.train_mask)
+    del g
+    torch.cuda.empty_cache()
+    _fused_vs_oracle(hg, tuple(fanouts), 64, 1024, seed=3, mask=mask, windows=2, layer0="af")
