@@ -218,8 +218,19 @@ __global__ void seg_sum_kernel(const double* __restrict__ sq, const int64_t* __r
                                double* __restrict__ out) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_cand;
        p += (int64_t)gridDim.x * blockDim.x) {
+    // sequential in entry order (np.add.at), 16 loads in flight: a hub
+    // candidate's chain costs its adds, not one memory latency per entry
     double acc = 0.0;
-    for (int64_t e = lo[p]; e < hi[p]; ++e) acc = __dadd_rn(acc, sq[e]);
+    int64_t e = lo[p];
+    const int64_t e1 = hi[p];
+    for (; e + 16 <= e1; e += 16) {
+      double t[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = __ldg(&sq[e + u]);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, t[u]);
+    }
+    for (; e < e1; ++e) acc = __dadd_rn(acc, sq[e]);
     out[p] = flat ? __dsqrt_rn(acc) : acc;
   }
 }
@@ -267,8 +278,19 @@ __global__ void iota_kernel(int32_t* __restrict__ a, int32_t n) {
 // cdf = cumsum(p) (sequential, as np.cumsum), then cdf /= cdf[-1]
 __global__ void cumsum_kernel(const double* __restrict__ p, int64_t n, double* __restrict__ cdf) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  double acc = 0.0;
-  for (int64_t i = 0; i < n; ++i) {
+  double acc = 0.0;  // np.cumsum's sequential order; loads batched 16 ahead
+  int64_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    double t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t[u] = __ldg(&p[i + u]);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      acc = __dadd_rn(acc, t[u]);
+      cdf[i + u] = acc;
+    }
+  }
+  for (; i < n; ++i) {
     acc = __dadd_rn(acc, p[i]);
     cdf[i] = acc;
   }
