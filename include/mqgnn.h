@@ -156,10 +156,14 @@ int mq_relabel(const int32_t* dst, const int32_t* n_dst_dev, int32_t n_dst_max,
  * n_targets / key) -> [mq_sample_hop -> mq_relabel] per hop -> mq_gather +
  * mq_gather_labels, bit-identical to the single-batch entry points.  Every
  * per-slot array is given as slot 0's pointer plus a stride (elements) to the
- * next slot.  node_rank is a node-indexed int32 table per slot (stride
- * table_s) holding INT32_MAX on entry, restored on exit (one word per node:
- * -(position + 1) for a node in the current src list, else its first pick
- * slot; reserved_ must be NULL); scratch holds
+ * next slot.  node_rank holds the relabel's rank words per slot (stride
+ * table_s int32; one word per node: -(position + 1) for a node in the
+ * current src list, else its first pick slot), restored on exit: with
+ * hash_lg == 0 a node-indexed table [num_nodes] holding INT32_MAX; with
+ * hash_lg = k > 0 an open-addressing hash of 2^k (key, word) int32 pairs
+ * (key 0 / word INT32_MAX at rest) followed by the last hop's n_src_max
+ * position entries, for graphs whose node-indexed tables would not fit
+ * (reserved_ must be NULL); scratch holds
  * Q regions of mq_prep_scratch_bytes(max n_dst_max, its fanout) each
  * (scratch_s bytes apart).  When cursor != NULL, cursor[0] (window) advances
  * by Q and cursor[1] must be 0 at rest. */
@@ -193,7 +197,7 @@ typedef struct mq_prep_desc {
    * node v's row lives on shard v % n_shards at row v / n_shards, pitch
    * store_pitch — one table per rank, the others' mapped over NVLink P2P
    * (mq_ipc_open), so misses of remote rows are read peer-to-peer */
-  const float* store_shard[MQ_MAX_PEERS]; int32_t n_shards, pad2_;
+  const float* store_shard[MQ_MAX_PEERS]; int32_t n_shards, hash_lg;
 } mq_prep_desc;
 #define MQ_PREP_SETUP 1u
 #define MQ_PREP_SAMPLE 2u

@@ -23,7 +23,8 @@ namespace prep {
 
 // The relabel keeps ONE int32 word per node and slot (mq_prep_desc.node_rank,
 // INT32_MAX at rest), so a products-sized table (8 slots x 2.4M nodes x 4 B)
-// stays L2-resident:
+// stays L2-resident (RankTbl below: a hash of the touched nodes instead when
+// the node-indexed table would not fit):
 //   w[u] = -(p + 1)  u is in the current src list at position p (dst marks
 //                    -(r + 1) and new labels are both stored this way);
 //   w[u] = s >= 0    u's first pick slot s = r * fanout + i this hop
@@ -44,6 +45,59 @@ template <class T>
 inline QP<T> qp(T* p, int64_t s) {
   return QP<T>{p, s};
 }
+
+// The rank words of one slot: node-indexed (lg == 0: word of u at [u]) or,
+// for graphs whose node-indexed tables would span GBs (8 slots x 111M nodes),
+// an open-addressing hash of 2^lg (key, word) pairs -- key u + 1 (0 = empty)
+// at [2h], its word at [2h + 1], linear probing from a multiplicative home --
+// followed by hpos[position] = the entry of the src list's node at that
+// position (the restore walks it: deleting entries by lookup would cut the
+// probe chains of entries not yet deleted).  The same words, the same
+// atomics and the same scan: only the address of a node's word changes.
+struct RankTbl {
+  int32_t* base;
+  int64_t s;  // int32 elements between slots
+  int lg;     // 0: node-indexed
+  __device__ __forceinline__ int32_t* slot(int q) const { return base + (int64_t)q * s; }
+  __device__ __forceinline__ uint32_t home(int32_t u) const {
+    return ((uint32_t)u * 0x9E3779B1u) >> (32 - lg);
+  }
+  // entry of u, which some earlier access of this pass inserted
+  __device__ __forceinline__ uint32_t find(int q, int32_t u) const {
+    const int32_t* t = slot(q);
+    const uint32_t m = (1u << lg) - 1;
+    uint32_t h = home(u);
+    while (__ldcg(t + 2 * h) != u + 1) h = (h + 1) & m;
+    return h;
+  }
+  // entry of u, inserted if absent (concurrent inserts of u agree on one)
+  __device__ __forceinline__ uint32_t claim(int q, int32_t u) const {
+    int32_t* t = slot(q);
+    const uint32_t m = (1u << lg) - 1;
+    uint32_t h = home(u);
+    for (;;) {
+      const int32_t k = __ldcg(t + 2 * h);
+      if (k == u + 1) return h;
+      if (k == 0) {
+        const int32_t old = atomicCAS(t + 2 * h, 0, u + 1);
+        if (old == 0 || old == u + 1) return h;
+      }
+      h = (h + 1) & m;
+    }
+  }
+  __device__ __forceinline__ int32_t* word(int q, int32_t u, bool insert) const {
+    if (lg == 0) return slot(q) + u;
+    return slot(q) + 2 * (insert ? claim(q, u) : find(q, u)) + 1;
+  }
+  __device__ __forceinline__ int32_t* hpos(int q) const { return slot(q) + (2ll << lg); }
+  // the word of u for a node taking src position p (records hpos[p])
+  __device__ __forceinline__ int32_t* word_at(int q, int32_t u, int32_t p, bool insert) const {
+    if (lg == 0) return slot(q) + u;
+    const uint32_t h = insert ? claim(q, u) : find(q, u);
+    hpos(q)[p] = (int32_t)h;
+    return slot(q) + 2 * h + 1;
+  }
+};
 
 // ------------------------------------------------------------ batch setup
 // slot q <- window cursor[0] + q: batch j = window*world + rank (round-robin
@@ -98,7 +152,8 @@ __global__ void setup_q_kernel(const int32_t* __restrict__ perm, int64_t n_perm,
 // slot order is the triplet order, so the minimum is the first occurrence,
 // samplers.py:186-189).
 struct RelabelTables {
-  QP<int32_t> w, src_ids;
+  RankTbl w;
+  QP<int32_t> src_ids;
   bool on, mark;
 };
 
@@ -115,7 +170,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
   const int32_t v = dst.at(q)[r];
   if (tbl.on) {
     tbl.src_ids.at(q)[r] = v;
-    if (tbl.mark) atomicMin(&tbl.w.at(q)[v], -(r + 1));
+    if (tbl.mark) atomicMin(tbl.w.word_at(q, v, r, true), -(r + 1));
   }
   const int64_t beg = row_off[v];
   const int n = (int)(row_off[v + 1] - beg);
@@ -136,7 +191,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < n) atomicMin(&tbl.w.at(q)[x[i]], r * fanout + i);
+        if (i < n) atomicMin(tbl.w.word(q, x[i], true), r * fanout + i);
     }
     cnt.at(q)[r] = n;
     return;
@@ -156,7 +211,7 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.w.at(q)[x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(tbl.w.word(q, x[j], true), r * fanout + j);
     }
   } else if (hot_off != nullptr) {  // samplers.py:173-175: hot ++ choice(cold, f - |hot|)
     int64_t ha[MAXK];
@@ -188,10 +243,10 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int i = 0; i < MAXK; ++i)
-        if (i < nh) atomicMin(&tbl.w.at(q)[x[i]], r * fanout + i);
+        if (i < nh) atomicMin(tbl.w.word(q, x[i], true), r * fanout + i);
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < k2) atomicMin(&tbl.w.at(q)[y[j]], r * fanout + nh + j);
+        if (j < k2) atomicMin(tbl.w.word(q, y[j], true), r * fanout + nh + j);
     }
   } else {  // samplers.py:176-177: choice(nbrs, f)
     fisher_yates<MAXK, int>(rs, n, fanout, pos);
@@ -203,32 +258,32 @@ __global__ void __launch_bounds__(64, MAXK <= 8 ? MQ_SAMPLE_MINB8 : MQ_SAMPLE_MI
     if (tbl.on) {
 #pragma unroll
       for (int j = 0; j < MAXK; ++j)
-        if (j < fanout) atomicMin(&tbl.w.at(q)[x[j]], r * fanout + j);
+        if (j < fanout) atomicMin(tbl.w.word(q, x[j], true), r * fanout + j);
     }
   }
   cnt.at(q)[r] = fanout;
 }
 
 // ------------------------------------------------------------ relabel
-__global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, QP<int32_t> w,
+__global__ void mark_q_kernel(QP<const int32_t> dst, QP<const int32_t> n_dst, RankTbl w,
                               QP<int32_t> src_ids, bool mark) {
   const int q = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *n_dst.at(q)) return;
   const int32_t v = dst.at(q)[i];
   src_ids.at(q)[i] = v;
-  if (mark) atomicMin(&w.at(q)[v], -(i + 1));
+  if (mark) atomicMin(w.word_at(q, v, i, true), -(i + 1));
 }
 
 // w[u] = min slot r * fanout + i of every pick u (sample_q_kernel does
 // this inline; this kernel serves passes whose sampling ran separately)
 __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
-                               QP<const int32_t> n_dst, int fanout, QP<int32_t> w) {
+                               QP<const int32_t> n_dst, int fanout, RankTbl w) {
   const int q = blockIdx.y;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int r = (int)(s / fanout), i = (int)(s % fanout);
   if (r >= *n_dst.at(q) || i >= cnt.at(q)[r]) return;
-  atomicMin(&w.at(q)[nbr.at(q)[s]], (int32_t)s);
+  atomicMin(w.word(q, nbr.at(q)[s], true), (int32_t)s);
 }
 
 // One scan per hop over the slots r * fanout + i, two channels in one int64:
@@ -236,7 +291,8 @@ __global__ void first_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
 // row_ptr), low 32 bits = the first-occurrence flag of a new node (prefix ->
 // its label) -- the row offsets and the labels in one decoupled-look-back pass.
 struct QLoadRowFlag {
-  QP<const int32_t> nbr, cnt, n_dst, w;
+  QP<const int32_t> nbr, cnt, n_dst;
+  RankTbl w;
   int fanout;
   __device__ int64_t size() const { return (int64_t)(*n_dst.at(blockIdx.y)) * fanout; }
   __device__ int64_t operator()(int64_t s) const {
@@ -245,14 +301,15 @@ struct QLoadRowFlag {
     const int c = cnt.at(q)[r];
     int64_t v = i == 0 ? ((int64_t)c << 32) : 0;
     if (i < c) {
-      if (__ldcg(&w.at(q)[nbr.at(q)[s]]) == (int32_t)s) v |= 1;
+      if (__ldcg(w.word(q, nbr.at(q)[s], false)) == (int32_t)s) v |= 1;
     }
     return v;
   }
 };
 struct QStoreRowLabel {
   QP<const int32_t> nbr, n_dst;
-  QP<int32_t> w, src_ids, counts, row_ptr;
+  RankTbl w;
+  QP<int32_t> src_ids, counts, row_ptr;
   int fanout;
   __device__ void operator()(int64_t s, int64_t excl, int64_t val) const {
     const int q = blockIdx.y;
@@ -261,7 +318,7 @@ struct QStoreRowLabel {
     const int32_t u = nbr.at(q)[s];
     const int32_t lab = *n_dst.at(q) + (int32_t)(excl & 0xFFFFFFFFll);
     src_ids.at(q)[lab] = u;
-    w.at(q)[u] = -(lab + 1);
+    *w.word_at(q, u, lab, false) = -(lab + 1);
   }
   __device__ void total(int64_t, int64_t t) const {
     const int q = blockIdx.y;
@@ -273,7 +330,7 @@ struct QStoreRowLabel {
 };
 __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
                               QP<const int32_t> row_ptr, QP<const int32_t> n_dst, int fanout,
-                              QP<const int32_t> w, QP<int32_t> rows, QP<int32_t> cols,
+                              RankTbl w, QP<int32_t> rows, QP<int32_t> cols,
                               QP<float> vals) {
   const int q = blockIdx.y;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -283,7 +340,7 @@ __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
   if (i >= c) return;
   const int e = row_ptr.at(q)[r] + i;
   rows.at(q)[e] = r;
-  cols.at(q)[e] = -(w.at(q)[nbr.at(q)[s]] + 1);
+  cols.at(q)[e] = -(*w.word(q, nbr.at(q)[s], false) + 1);
   vals.at(q)[e] = (float)(1.0 / (double)c);  // float32(1.0 / s), samplers.py:200 + nn.py:85
 }
 
@@ -291,13 +348,18 @@ __global__ void cols_q_kernel(QP<const int32_t> nbr, QP<const int32_t> cnt,
 // labels, first-occurrence slots of any pick) is in that hop's src list, and
 // each hop's src list contains the previous one's, so the last hop's src list
 // covers them all.
-__global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> counts,
-                               QP<int32_t> w) {
+__global__ void clean_q_kernel(QP<const int32_t> src_ids, QP<const int32_t> counts, RankTbl w) {
   const int q = blockIdx.y;
   const int n = counts.at(q)[0];
+  int32_t* t = w.slot(q);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int32_t u = src_ids.at(q)[j];
-    w.at(q)[u] = INT_MAX;
+    if (w.lg == 0) {
+      t[src_ids.at(q)[j]] = INT_MAX;
+    } else {  // (duplicate hop-0 targets share an entry: restored twice, harmlessly)
+      const int32_t h = w.hpos(q)[j];
+      t[2 * h] = 0;
+      t[2 * h + 1] = INT_MAX;
+    }
   }
 }
 
@@ -465,6 +527,12 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     MQ_LAUNCH_CHECK("prep setup");
   }
 
+  MQ_CHECK_ARG(d.hash_lg == 0 || (d.hash_lg >= 4 && d.hash_lg <= 30 &&
+                                   d.table_s >= (2ll << d.hash_lg) +
+                                                    d.hop[d.num_hops - 1].n_src_max),
+               "mq_prep_batches: hash_lg %d does not fit table_s", d.hash_lg);
+  const RankTbl rt{d.node_rank, d.table_s, d.hash_lg};
+
   // 2. hops: sample + relabel (samplers.py:213-226 hop chain)
   for (int h = 0; h < d.num_hops; ++h) {
     const mq_prep_hop& hp = d.hop[h];
@@ -483,8 +551,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     if (mask & MQ_PREP_SAMPLE) {
       ProfScope ps(K_SAMPLE, s);
       const dim3 grid(ceil_div(hp.n_dst_max, 64), Q);
-      const RelabelTables tb{qp(d.node_rank, d.table_s), qp(hp.src_ids, hp.src_s), relabel,
-                             h == 0};
+      const RelabelTables tb{rt, qp(hp.src_ids, hp.src_s), relabel, h == 0};
       if (f <= 8)
         sample_q_kernel<8><<<grid, 64, 0, s>>>(
             d.row_off, d.col, d.hot_arc, d.hot_off, cq(dst, dst_s), cq(nd, nd_s),
@@ -500,18 +567,15 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
     } else if (relabel) {  // sampled earlier: the relabel's marks and first slots alone
       ProfScope ps(K_RELABEL_MARK, s);
       mark_q_kernel<<<dim3(ceil_div(hp.n_dst_max, 256), Q), 256, 0, s>>>(
-          cq(dst, dst_s), cq(nd, nd_s), qp(d.node_rank, d.table_s), qp(hp.src_ids, hp.src_s),
-          h == 0);
+          cq(dst, dst_s), cq(nd, nd_s), rt, qp(hp.src_ids, hp.src_s), h == 0);
       first_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
-          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), f,
-          qp(d.node_rank, d.table_s));
+          cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), f, rt);
     }
     MQ_LAUNCH_CHECK("prep sample");
     if (!relabel) continue;
     int rc = launch_scan_q(
-        QLoadRowFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s),
-                     cq(d.node_rank, d.table_s), f},
-        QStoreRowLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), qp(d.node_rank, d.table_s),
+        QLoadRowFlag{cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(nd, nd_s), rt, f},
+        QStoreRowLabel{cq(hp.nbr, hp.nbr_s), cq(nd, nd_s), rt,
                        qp(hp.src_ids, hp.src_s), qp(hp.counts, hp.counts_s),
                        qp(hp.row_ptr, hp.row_ptr_s), f},
         slots, Q, d.scratch, d.scratch_s, s, K_RELABEL_FLAG);
@@ -520,7 +584,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
       ProfScope ps(K_RELABEL_COLS, s);
       cols_q_kernel<<<dim3(ceil_div(slots, 256), Q), 256, 0, s>>>(
           cq(hp.nbr, hp.nbr_s), cq(hp.cnt, hp.cnt_s), cq(hp.row_ptr, hp.row_ptr_s), cq(nd, nd_s), f,
-          cq(d.node_rank, d.table_s), qp(hp.rows, hp.edge_s), qp(hp.cols, hp.edge_s),
+          rt, qp(hp.rows, hp.edge_s), qp(hp.cols, hp.edge_s),
           qp(hp.vals, hp.edge_s));
     }
     MQ_LAUNCH_CHECK("prep cols");
@@ -529,7 +593,7 @@ int mq_prep_batches(const mq_prep_desc* pd, void* stream) {
       int cb = ceil_div(slots + hp.n_dst_max, 256);
       const int cap = ceil_div(kNumSMs * 8, Q);
       clean_q_kernel<<<dim3(cb < cap ? cb : cap, Q), 256, 0, s>>>(
-          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), qp(d.node_rank, d.table_s));
+          cq(hp.src_ids, hp.src_s), cq(hp.counts, hp.counts_s), rt);
     }
     MQ_LAUNCH_CHECK("prep clean");
   }

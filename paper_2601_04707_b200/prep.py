@@ -16,6 +16,7 @@ workspaces expect (targets, hops[h].row_ptr, x0, labels, ...).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -23,6 +24,11 @@ from ._lib import I32, I64, P, lib, ptr
 from .engine import hop_bounds
 
 MQ_MAX_HOPS = 4
+# node-indexed relabel tables up to 16 GB (all slots): the hashed layout is
+# a memory saver, not a speed-up (papers shape 2.30M -> 2.17M seeds/s, products
+# 2.53M -> 2.31M with it forced: probes and the key CAS cost more than the
+# smaller span saves)
+RANK_TABLE_BYTES = 16 << 30
 PREP_SETUP, PREP_SAMPLE, PREP_RELABEL, PREP_GATHER, PREP_LABELS = 1, 2, 4, 8, 16
 
 
@@ -49,7 +55,7 @@ class PrepDesc(C.Structure):
                 ("x0", P), ("x0_s", I64), ("x0_pitch", I32), ("stage_mask", C.c_uint32),
                 ("hit_miss", P),
                 ("all_labels", P), ("labels", P), ("labels_s", I64),
-                ("store_shard", P * 8), ("n_shards", I32), ("pad2_", I32)]
+                ("store_shard", P * 8), ("n_shards", I32), ("hash_lg", I32)]
 
 
 class PrepShared:
@@ -62,7 +68,24 @@ class PrepShared:
         bounds = hop_bounds(batch_size, fanouts, g.num_nodes)
         # the relabel's node-rank words, one int32 per node and slot (INT32_MAX
         # at rest): 4 B x nodes x Q, L2-resident up to products-sized graphs
-        self.tbl = torch.full((Q, g.num_nodes), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        # (papers-sized: 8 x 111M x 4 B = 3.5 GB).  Past RANK_TABLE_BYTES a hash
+        # of the touched nodes per slot instead: 2^k (key, word) pairs, load
+        # <= 0.8 at the bound on a pass's distinct nodes (~0.3 in practice),
+        # then the position -> entry list (MQ_PREP_HASH=1 / 0 forces it)
+        n_src = bounds[-1].n_src_max
+        force = os.environ.get("MQ_PREP_HASH")
+        direct = Q * g.num_nodes * 4
+        self.hash_lg = 0
+        if force == "1" or (force != "0" and direct > RANK_TABLE_BYTES):
+            lg = max(4, (int(1.25 * n_src) - 1).bit_length())
+            if force == "1" or (2 << lg) + n_src < g.num_nodes:
+                self.hash_lg = lg
+        if self.hash_lg:
+            cap = 1 << self.hash_lg
+            self.tbl = torch.zeros((Q, 2 * cap + n_src), dtype=torch.int32, device=dev)
+            self.tbl[:, 1:2 * cap:2] = 2 ** 31 - 1
+        else:
+            self.tbl = torch.full((Q, g.num_nodes), 2 ** 31 - 1, dtype=torch.int32, device=dev)
         per = max(int(lib().mq_prep_scratch_bytes(b.n_dst_max, b.fanout)) for b in bounds)
         self.scratch_s = per
         self.scratch = torch.zeros(Q * per, dtype=torch.uint8, device=dev)
@@ -183,7 +206,7 @@ class PrepGroup:
             hp.edge_s = hb.rows.stride(0)
             hp.src_ids, hp.src_s = ptr(hb.src_ids), hb.src_ids.stride(0)
             hp.counts, hp.counts_s = ptr(hb.counts), hb.counts.stride(0)
-        d.node_rank, d.table_s = ptr(sh.tbl), sh.tbl.stride(0)
+        d.node_rank, d.table_s, d.hash_lg = ptr(sh.tbl), sh.tbl.stride(0), sh.hash_lg
         d.scratch, d.scratch_s = ptr(sh.scratch), sh.scratch_s
         d.row_off, d.col = ptr(g.row_off), ptr(g.col)
         d.store_pitch = g.pitch

@@ -67,11 +67,29 @@ def _run_group(g, cache, fanouts, batches, seed, epoch, placement_cache=None):
     return grp
 
 
-def test_prep_pass_matches_reference_digests(golden_sampling, hosts):
+@pytest.fixture(params=["direct", "hash"])
+def rank_table(request, monkeypatch):
+    """The relabel's rank words node-indexed, or hashed (the papers-scale
+    layout, forced here on the small golden graphs)."""
+    monkeypatch.setenv("MQ_PREP_HASH", "1" if request.param == "hash" else "0")
+    return request.param
+
+
+def _table_at_rest(grp):
+    t = grp.shared.tbl
+    if grp.shared.hash_lg:
+        cap = 1 << grp.shared.hash_lg
+        assert int(t[:, 0:2 * cap:2].abs().sum()) == 0  # every key empty again
+        assert bool((t[:, 1:2 * cap:2] == 2 ** 31 - 1).all())
+    else:
+        assert bool((t == 2 ** 31 - 1).all())
+
+
+def test_prep_pass_matches_reference_digests(golden_sampling, hosts, rank_table):
     """Every golden batch, prepared by the batched production pass in a full
     group of 8 slots (the group's other slots hold other batches of the same
     graph, or the same batches under other slots), reproduces the reference's
-    digest, labels and hit/miss counts."""
+    digest, labels and hit/miss counts; the rank words are back at rest."""
     gs = golden_sampling
     devs = {k: mq.DeviceGraph.from_csr(h) for k, h in hosts.items()}
     checked = 0
@@ -90,6 +108,8 @@ def test_prep_pass_matches_reference_digests(golden_sampling, hosts):
             order = [items[i % len(items)] for i in range(Q)]
             batches = [(bid, gs[f"{p}/targets"]) for bid, p in order]
             grp = _run_group(g, cache, fo, batches, seed, epoch)
+            assert (grp.shared.hash_lg > 0) == (rank_table == "hash")
+            _table_at_rest(grp)
             tot_hits = tot_miss = 0
             for q, (bid, p) in enumerate(order):
                 targets, layers, digest, hits = golden_batch(gs, p)

@@ -77,3 +77,12 @@ def test_products_fused_step_vs_oracle():
     del g
     torch.cuda.empty_cache()
     _fused_vs_oracle(hg, tuple(fanouts), 64, 1024, seed=3, mask=mask, windows=2, layer0="af")
+
+
+def test_products_group_vs_oracle_hashed_ranks(monkeypatch):
+    """The same products-shape group with the relabel's rank words in the
+    hashed layout (the one papers-sized graphs use)."""
+    monkeypatch.setenv("MQ_PREP_HASH", "1")
+    g, cache, mask, fanouts = _shape("products")
+    _device_plan_vs_oracle(_Host(g), g, cache, mask, fanouts, 1024, seed=4, epoch=1,
+                           check_slots=4)
