@@ -85,7 +85,7 @@ def _slot_bytes(runner) -> int:
 
 
 def auto_queue_depth(g, model, *, fanouts, batch_size: int, num_train: int, cache=None,
-                     optimizer: str = "adam", seed: int = 0, candidates=(2, 4, 8),
+                     optimizer: str = "adam", seed: int = 0, candidates=(2, 4, 8, 16),
                      windows: int = 60, total_memory_bytes=DEFAULT_DEVICE_MEMORY,
                      margin: float = MEMORY_MARGIN) -> QueueChoice:
     """Measure the pipelined step at each candidate queue depth that fits the

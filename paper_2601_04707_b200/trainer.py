@@ -37,7 +37,7 @@ from .pipeline import PipelineTimeout
 from .prep import PrepGroup, PrepShared
 
 
-DEFAULT_QUEUE_DEPTH = 8  # measured best on B200 (autotune.auto_queue_depth: 2 < 4 < 8)
+DEFAULT_QUEUE_DEPTH = 16  # measured on B200: 2 < 4 < 8 < 16 (Reddit 20.70M -> 20.92M seeds/s, e2e +2 %)
 
 
 # device stage stamp tags (mq_trace_stamp; decoded by runtime.device_trace)
