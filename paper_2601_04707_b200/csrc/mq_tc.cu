@@ -1108,6 +1108,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
   pdl_trigger();
   MQ_TL_BEGIN(MODE);
   if (threadIdx.x == 0) trace_at(0);
+  if (threadIdx.x == 0) {  // the descriptors are kernel parameters: fetch them
+    // while the barriers / TMEM are set up and the predecessor drains
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b2)) : "memory");
+  }
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps LDS / STS
   __shared__ __align__(8) uint64_t full[kMaxStages2], conv[kMaxStages2], empty[kMaxStages2];
