@@ -60,24 +60,31 @@ __device__ __forceinline__ double grad_count(const double* g64, double scale, in
   return (g64 != nullptr && scale == 0.0) ? g64[n] : 1.0;
 }
 
-// Adam update of element i with gradient g (nn.py:191-206, NumPy-2 f32 op order)
-__device__ __forceinline__ bool adam_elem(float* __restrict__ w, float* __restrict__ m,
-                                          float* __restrict__ v, int64_t i, float g, float bc1,
-                                          float bc2, float lr) {
+// Adam update of element i with gradient g (nn.py:191-206, NumPy-2 f32 op order),
+// given the element's current w / m / v (loaded by the caller ahead of the
+// gradient's partial sums, so their latency overlaps)
+__device__ __forceinline__ bool adam_elem_v(float* __restrict__ w, float* __restrict__ m,
+                                            float* __restrict__ v, int64_t i, float w0, float m0,
+                                            float v0, float g, float bc1, float bc2, float lr) {
   const float b1 = (float)0.9, b2 = (float)0.999;
   const float c1 = (float)(1.0 - 0.9), c2 = (float)(1.0 - 0.999), eps = (float)1e-8;
-  float mi = __fmul_rn(m[i], b1);                         // m *= beta1
+  float mi = __fmul_rn(m0, b1);                           // m *= beta1
   mi = __fadd_rn(mi, __fmul_rn(c1, g));                   // m += (1-beta1)*g
-  float vi = __fmul_rn(v[i], b2);                         // v *= beta2
+  float vi = __fmul_rn(v0, b2);                           // v *= beta2
   vi = __fadd_rn(vi, __fmul_rn(__fmul_rn(c2, g), g));     // v += (1-beta2)*g*g
   const float mh = __fdiv_rn(mi, bc1);                    // m / (1 - beta1**t)
   const float vh = __fdiv_rn(vi, bc2);                    // v / (1 - beta2**t)
   const float upd = __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps));
-  const float wi = __fsub_rn(w[i], upd);                  // w -= lr*mh/(sqrt(vh)+eps)
+  const float wi = __fsub_rn(w0, upd);                    // w -= lr*mh/(sqrt(vh)+eps)
   m[i] = mi;
   v[i] = vi;
   w[i] = wi;
   return !finite_f(wi);
+}
+__device__ __forceinline__ bool adam_elem(float* __restrict__ w, float* __restrict__ m,
+                                          float* __restrict__ v, int64_t i, float g, float bc1,
+                                          float bc2, float lr) {
+  return adam_elem_v(w, m, v, i, w[i], m[i], v[i], g, bc1, bc2, lr);
 }
 
 inline GradSrc make_src(const mq_grad_src* src) {

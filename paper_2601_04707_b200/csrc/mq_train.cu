@@ -133,7 +133,9 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
     for (int64_t i = (int64_t)(blockIdx.x - coop_blocks) * blockDim.x + threadIdx.x; i < n;
          i += nb * blockDim.x) {
       if (i >= c_lo && i < c_hi) continue;
-      bad |= adam_elem(w, m, v, i, load_grad(src, g32, g64, scale, count, i), bc1, bc2, lr);
+      const float w0 = w[i], m0 = m[i], v0 = v[i];  // in flight with the partials
+      bad |= adam_elem_v(w, m, v, i, w0, m0, v0, load_grad(src, g32, g64, scale, count, i), bc1,
+                         bc2, lr);
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
