@@ -83,14 +83,12 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
   MQ_TL_BEGIN(8);
   __shared__ float red[8][33];
   const int t = step[0] + 1;  // this update's step number (nn.py:194 t += 1)
-  if (t < 1) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);  // step counter wrapped
-    step_arrive(step, t);
-    return;
-  }
+  // a wrapped counter skips the updates (flag 2); no early return, so the
+  // element loads below do not wait on the step -> bias chain
+  const bool wrapped = t < 1;
   // the table ends at float32(1 - beta**t) == 1.0f for both betas (t > ~17.3k),
   // so every later step reads its last row exactly (mqgnn.h mq_adam)
-  const int tb = t < bias_len ? t : bias_len;
+  const int tb = wrapped ? 1 : (t < bias_len ? t : bias_len);
   const float bc1 = bias[2 * (tb - 1)], bc2 = bias[2 * (tb - 1) + 1];
   const float lr = *lr_dev;  // float32(learning_rate), read per launch (graph replays follow it)
   const double count = grad_count(g64, scale, n);
@@ -122,7 +120,7 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
     }
     red[q][lane] = acc;
     __syncthreads();
-    if (q == 0 && j < sg.size) {
+    if (q == 0 && j < sg.size && !wrapped) {
       float g = 0.f;
 #pragma unroll
       for (int r = 0; r < 8; ++r) g += red[r][lane];
@@ -134,10 +132,11 @@ __global__ void adam_kernel(float* __restrict__ w, float* __restrict__ m, float*
          i += nb * blockDim.x) {
       if (i >= c_lo && i < c_hi) continue;
       const float w0 = w[i], m0 = m[i], v0 = v[i];  // in flight with the partials
-      bad |= adam_elem_v(w, m, v, i, w0, m0, v0, load_grad(src, g32, g64, scale, count, i), bc1,
-                         bc2, lr);
+      const float g = load_grad(src, g32, g64, scale, count, i);
+      if (!wrapped) bad |= adam_elem_v(w, m, v, i, w0, m0, v0, g, bc1, bc2, lr);
     }
   }
+  if (wrapped && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(nonfinite, 2);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
   step_arrive(step, t);
   MQ_TL_END(8);
