@@ -419,9 +419,15 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
   const int n = *n_dst_dev;  // the block (prep output) ahead of the wait; dh / act / G after
   int r = blockIdx.x * warps + (threadIdx.x >> 5);
   int pe0 = 0, pe1 = 0;
+  int32_t pcol = 0;  // the first row's first 32 triplets, also ahead of the wait
+  float pval = 0.f;
   if (r < n) {
     pe0 = row_ptr[r];
     pe1 = row_ptr[r + 1];
+    if (pe0 + lane < pe1) {
+      pcol = __ldg(&cols[pe0 + lane]);
+      pval = __ldg(&vals[pe0 + lane]);
+    }
   }
   pdl_wait();
   const int ldg = 2 * N;
@@ -445,7 +451,10 @@ __global__ void __launch_bounds__(kAggThreads) sage_scatter_bwd_kernel(
           const int me = eb + lane;
           int32_t my_col = 0;
           float my_val = 0.f;
-          if (me < e1) {
+          if (first && eb == e0) {
+            my_col = pcol;
+            my_val = pval;
+          } else if (me < e1) {
             my_col = __ldg(&cols[me]);
             my_val = __ldg(&vals[me]);
           }
