@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--profile-steps", type=int, default=20,
                     help="launches per op in the per-kernel graph timing (0: skip)")
-    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--e2e-steps", type=int, default=600)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--queue-depth", default=None,
                     help="batches per batched prep pass (MQ-GNN queue depth Q), or 'auto'")
@@ -532,14 +532,23 @@ def run_ours(args):
         if fx is not None:  # epoch boundary: nothing held back by a lagged exchange
             runner.finish()
         runner.capture_host_input()
-        perm_e2e = epoch_permutation(g.train_mask, args.seed, 100)
         B = args.batch
         # the round-robin deal (runtime.py:111-113): this rank's batches j = rank, rank + N, ...
-        nb = min(args.e2e_steps, len(perm_e2e) // (B * world))
-        host_batches = [(j * world + rank,
-                         torch.from_numpy(perm_e2e[(j * world + rank) * B:
-                                                   (j * world + rank + 1) * B].astype(np.int32))
-                         .pin_memory()) for j in range(nb)]
+        # over as many fresh epoch permutations as --e2e-steps needs (distinct
+        # targets and batch ids throughout: one epoch of the Reddit shape is
+        # only ~150 windows, too short to amortise the first group's prep)
+        host_batches, ep = [], 100
+        while len(host_batches) < args.e2e_steps:
+            perm_e2e = epoch_permutation(g.train_mask, args.seed, ep)
+            per = len(perm_e2e) // (B * world)
+            if per == 0:
+                break
+            for j in range(min(per, args.e2e_steps - len(host_batches))):
+                host_batches.append((len(host_batches) * world + rank, torch.from_numpy(
+                    perm_e2e[(j * world + rank) * B:(j * world + rank + 1) * B]
+                    .astype(np.int32)).pin_memory()))
+            ep += 1
+        nb = len(host_batches)
         for _ in runner.run_host_batches(host_batches[:5]):
             pass
         e0 = torch.cuda.Event(enable_timing=True)
