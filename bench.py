@@ -261,6 +261,28 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def host_link_peak(dev, nbytes=512 << 20, reps=10):
+    """Measured host -> device rate of this box's link: a pinned host buffer
+    copied into HBM by the copy engine (best of ``reps``, CUDA events).  The
+    host-store gather reads the same pinned memory over the same link with
+    SM loads, so this is its ceiling."""
+    import torch
+
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = None
+    for _ in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    del src, dst
+    return nbytes / (best * 1e-3) / 1e9
+
+
 def traffic_table():
     """Per-launch DRAM bytes of each kernel from the committed ncu capture."""
     files = sorted((ROOT / "profiles").glob("traffic_*.json"))
@@ -524,6 +546,24 @@ def run_ours(args):
                 "sector_gbps": rec.get("sector_gbps"),
             }
         per_kernel["_counts"] = tab["counts"]
+    # ---- host-miss gather against the host link (configs[3]: features in
+    # pinned host memory, only the GNS cache table in HBM): the misses of
+    # one prep pass cross the link inside prep_gather
+    host_link = None
+    if rank == 0 and args.feature_placement == "host" and "prep_gather" in per_kernel:
+        hr = cache.hit_rate()
+        n_in = int(per_kernel["_counts"]["hops"][-1][1])
+        miss_bytes = (1.0 - hr) * runner.Q * n_in * 4 * g.feature_dim
+        us = per_kernel["prep_gather"]["avg_launch_us"]
+        peak = host_link_peak(dev)
+        ach = miss_bytes / (us * 1e-6) / 1e9
+        host_link = {"bound": "host link", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "miss_rate": 1.0 - hr,
+                     "miss_bytes_per_pass": miss_bytes, "prep_gather_us": us,
+                     "units": f"{runner.Q} batches x {n_in} input rows x {g.feature_dim} f32",
+                     "peak_source": "measured: 512 MiB pinned host -> HBM copy_, best of 10, "
+                                    "CUDA events (copy engine; the gather reads the link "
+                                    "with SM loads and can exceed it)"}
     if world > 1:  # the other ranks' next steps wait on rank 0's exchange
         dist.barrier()
     # ----------------------------- e2e through the host-buffer entry point ---
@@ -678,6 +718,7 @@ def run_ours(args):
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "per_epoch": epoch_extra,
             "cache": {"mode": cache_mode, "fraction": args.cache_fraction,
                       "resident": cache.size, "hit_rate": cache.hit_rate()},
+            "host_link": host_link,
             "gpu_launches": int(round(n_kernels * args.steps)), "kernels_per_step": n_kernels,
             "wall_s_timed": t_wall, "setup": setup,
         }

@@ -272,9 +272,12 @@ inline StoreRef make_store(const float* store, const float* const* shards, int n
 // Fixed-order sum p[0] + p[stride] + ... + p[(S-1)*stride] (left to right, so
 // results are deterministic); the loads are issued 16 at a time so the chain
 // costs ~S/16 L2 round trips instead of S (a 128-partial head gradient: 8).
+#ifndef MQ_SUM_BATCH
+#define MQ_SUM_BATCH 16  // partial loads in flight per batch of fixed_order_sum
+#endif
 __device__ __forceinline__ float fixed_order_sum(const float* __restrict__ p, int64_t stride,
                                                  int S) {
-  constexpr int kB = 16;
+  constexpr int kB = MQ_SUM_BATCH;
   float v = 0.f;
   int s = 0;
   for (; s + kB <= S; s += kB) {

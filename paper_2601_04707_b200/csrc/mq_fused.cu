@@ -30,6 +30,9 @@
 
 #include "mq_gemm.cuh"
 
+#ifndef MQ_AGG_U
+#define MQ_AGG_U 4  // neighbour rows per batch of split-partial loads in sage_aggregate_parts
+#endif
 #ifndef MQ_AGG_SU
 #define MQ_AGG_SU 4  // split partials loaded per batch in sage_aggregate_parts
 #endif
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(kAggThreads) sage_aggregate_parts_kernel(
     ZeroRange z1) {
   pdl_trigger();
   MQ_TL_BEGIN(5);
-  constexpr int U = 4, SU = MQ_AGG_SU;
+  constexpr int U = MQ_AGG_U, SU = MQ_AGG_SU;
   const int lane = threadIdx.x & 31;
   const int warps = kAggThreads / 32;
   // the block (prep output) is read ahead of the wait; the partials are not

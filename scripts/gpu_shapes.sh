@@ -12,5 +12,5 @@ for f in 0.001 0.01 0.1; do
       --e2e-steps 50 --cache-fraction $f --feature-placement $p > $OUT/sweep_${f}_${p}.jsonl 2> $OUT/sweep_${f}_${p}.err
   done
 done
-for f in $OUT/*.jsonl; do echo "$f :: $(python -c "import json; b=json.loads(open('$f').readline()); print(round(b['value']/1e6,3),'M/s', round(b['ms_per_step']*1e3,1),'us/step', 'e2e', round(b['e2e']['value']/1e6,3) if b.get('e2e') else None, 'hits', b.get('cache_hit_rate'))" 2>&1 | tail -1)"; done
+for f in $OUT/*.jsonl; do echo "$f :: $(python -c "import json; b=json.loads(open('$f').readline()); print(round(b['value']/1e6,3),'M/s', round(b['ms_per_step']*1e3,1),'us/step', 'e2e', round(b['e2e']['value']/1e6,3) if b.get('e2e') else None, 'hits', (b.get('cache') or {}).get('hit_rate'), 'host_link', {k: (b['host_link'] or {}).get(k) for k in ('achieved','peak','frac')} if b.get('host_link') else None)" 2>&1 | tail -1)"; done
 tail -n 3 $OUT/*.err
