@@ -460,11 +460,18 @@ def run_ours(args):
     plan_sizes = np.minimum(args.batch, np.maximum(
         0, n_train - np.arange(windows * world) * args.batch))
 
+    # MQ_BENCH_EPOCH_TIMES=1: train-stream events at every epoch boundary
+    # (diagnostic; the per-epoch device times go to stderr)
+    epoch_evs = [] if os.environ.get("MQ_BENCH_EPOCH_TIMES") else None
+
     def run_windows(n):
         """n windows; a single replica issues whole slot groups as one graph each."""
         left = n
         while left > 0:
             if runner.windows_done >= windows:
+                if epoch_evs is not None:
+                    epoch_evs.append(torch.cuda.Event(enable_timing=True))
+                    epoch_evs[-1].record(runner.stream)
                 runner.finish()  # a lagged exchange applies its held-back window
                 epoch[0] += 1
                 runner.begin_epoch(epoch[0], epoch_permutation(g.train_mask, args.seed, epoch[0]))
@@ -520,6 +527,10 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    if epoch_evs:
+        marks = [e for e in epoch_evs if e.query()]
+        print(json.dumps({"epoch_ms": [round(a.elapsed_time(b), 3)
+                                       for a, b in zip(marks, marks[1:])]}), file=sys.stderr)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

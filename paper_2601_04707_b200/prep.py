@@ -174,10 +174,14 @@ class PrepGroup:
         self.slots = [SlotView(self, q) for q in range(Q)]
 
     def set_key(self, seed: int, epoch: int):
-        import numpy as np
-        k = torch.from_numpy(np.array([seed & 0xFFFFFFFF, epoch & 0xFFFFFFFF, 0],
-                                      dtype=np.uint32).view(np.int32))
-        self.key[:, 0:2].copy_(k[0:2].to(self.key.device).expand(self.Q, 2))
+        # fills with the words' int32 bit patterns: kernel arguments, no
+        # pageable host copy (which would block the host until the stream
+        # drains, e.g. at every epoch boundary)
+        def i32(x):
+            x &= 0xFFFFFFFF
+            return x - (1 << 32) if x >= 1 << 31 else x
+        self.key[:, 0].fill_(i32(seed))
+        self.key[:, 1].fill_(i32(epoch))
 
     def desc(self, cache, perm, cursor, world: int, rank: int) -> PrepDesc:
         """Descriptor of one pass; cursor=None means host-staged targets."""

@@ -25,6 +25,7 @@ in-process replicas) -> update graph.
 from __future__ import annotations
 
 import gc
+import os
 
 import ctypes as C
 
@@ -142,6 +143,16 @@ class StepRunner:
         self.epoch = 0
         self._primed = False
         self._last = (0, 0)
+        # epoch-boundary overlap (single replica, group graphs): g0 is the slot
+        # group an epoch starts on; when the previous epoch ended with its
+        # train-only last-group graph (_tail_clean), the next epoch's first
+        # prep runs on the prep stream while that group still trains, in the
+        # OTHER group's slots (g0 alternates), instead of after it
+        self.g0 = 0
+        self._tail_clean = False
+        self._perm_stage = None
+        self._perm_i = 0
+        self._epoch_windows = -(-self.num_train // (self.batch_size * self.world))
         self._join_current()
 
     def _join_current(self):
@@ -162,29 +173,58 @@ class StepRunner:
         perm = np.asarray(perm)
         if perm.size != self.num_train:
             raise ValueError("permutation length changed; build a new StepRunner")
-        staged = torch.from_numpy(perm.astype(np.int32)).pin_memory()
-        # the caller's queued work (model / cache updates) first, and an
-        # in-flight prep pass may still read perm / cursor
+        # two persistent pinned staging rows, reused every other epoch once the
+        # copy that read them has executed (with a fresh pinned tensor per
+        # epoch, a host running epochs ahead of the device hit one 10-60 ms
+        # device stall in ~half the 10-epoch bench runs, measured per epoch)
+        if self._perm_stage is None:
+            self._perm_stage = [torch.empty(perm.size, dtype=torch.int32, pin_memory=True)
+                                for _ in range(2)]
+            self._perm_ev = [torch.cuda.Event() for _ in range(2)]
+        si = self._perm_i
+        self._perm_i ^= 1
+        self._perm_ev[si].synchronize()
+        staged = self._perm_stage[si]
+        staged.numpy()[:] = perm
+        # the caller's queued work (model / cache updates) first
         self._join_current()
-        self.stream.wait_stream(self.prep_stream)
-        with torch.cuda.stream(self.stream):
+        overlap = (self._tail_clean and self.pipeline and self.use_graph and not self.multi
+                   and self.trace_buf is None and self.windows_done == self._epoch_windows
+                   and os.environ.get("MQ_EPOCH_OVERLAP", "1") != "0")
+        if overlap:
+            # the last group (self._last[0]) may still be training: the prep
+            # stream alone switches perm / cursor / keys (only prep passes read
+            # perm and cursor; the trains read key[2], set_key writes key[0:2])
+            # and prepares the other group once its previous trains are done
+            self.g0 = 1 - self._last[0]
+            self.prep_stream.wait_event(self.ev_train[self.g0])
+            cs = self.prep_stream
+        else:
+            # an in-flight prep pass may still read perm / cursor
+            self.stream.wait_stream(self.prep_stream)
+            self.g0 = 0
+            cs = self.stream
+        with torch.cuda.stream(cs):
             self.perm.copy_(staged, non_blocking=True)
+            self._perm_ev[si].record(cs)
             self.cursor.zero_()
-            self.trace_cur.zero_()
+            if not overlap:
+                self.trace_cur.zero_()
             for grp in self.groups:
                 grp.set_key(self.seed, epoch)
         self.epoch = epoch
         self.windows_done = 0
-        n_windows = -(-self.num_train // (self.batch_size * self.world))
-        self.dm.ensure_bias(self.dm.host_steps + n_windows + 8)
+        self._tail_clean = False
+        self.dm.ensure_bias(self.dm.host_steps + self._epoch_windows + 8)
         self._primed = False
         if self.pipeline and (self.graphs or not self.use_graph):
-            self._prologue()
+            self._prologue(overlap)
 
-    def _prologue(self):
-        self.prep_stream.wait_stream(self.stream)
-        self._run("prep0", self.prep_stream)
-        self.ev_prep[0].record(self.prep_stream)
+    def _prologue(self, overlap: bool = False):
+        if not overlap:
+            self.prep_stream.wait_stream(self.stream)
+        self._run(f"prep{self.g0}", self.prep_stream)
+        self.ev_prep[self.g0].record(self.prep_stream)
         self._primed = True
 
     # --------------------------------------------------------------- enqueue
@@ -347,6 +387,15 @@ class StepRunner:
                             ph(cur.cuda_stream)
                         cur.wait_stream(self.prep_stream)
                     self._capture({f"group{gi}" if k == self.Q else f"group{gi}_{k}": group})
+            if not self.multi and self.trace_buf is None:
+                # an epoch's last group without the forked prep of the group
+                # after it (the next epoch's first prep replaces that fork)
+                c = (self._epoch_windows - 1) % self.Q + 1
+                for gi in range(2):
+                    def tgroup(s, gi=gi, c=c):
+                        for q in range(c):
+                            phases[f"train{gi}_{q}"](s)
+                    self._capture({f"tgroup{gi}_{c}": tgroup})
         if self.pipeline and not self._primed:
             self._prologue()
 
@@ -383,10 +432,11 @@ class StepRunner:
     def compute_window(self):
         k, Q = self.windows_done, self.Q
         q = k % Q
+        self._tail_clean = False
         if self.pipeline:
             if not self._primed:
                 self._prologue()
-            gi = (k // Q) % 2
+            gi = (k // Q + self.g0) % 2
             if q == 0:  # the next group fills the other half while this one trains
                 nxt = 1 - gi
                 self.prep_stream.wait_event(self.ev_train[nxt])
@@ -438,16 +488,24 @@ class StepRunner:
             if self.use_graph and self.pipeline and "group0" in self.graphs and k % Q == 0:
                 if not self._primed:
                     self._prologue()
-                gi = (k // Q) % 2
+                gi = (k // Q + self.g0) % 2
                 c = min(Q, n - done)
+                # the epoch's last group: train-only graph (begin_epoch forks
+                # the next epoch's first prep beside it)
+                tail = f"tgroup{gi}_{c}"
+                last = k + c == epoch_windows and tail in self.graphs
                 with torch.cuda.stream(self.stream):
                     # the group graph joins its own prep branch; prep(1-gi)
                     # overwrites the other half, whose last trains preceded it
                     self.stream.wait_event(self.ev_prep[gi])
-                    self.graphs[f"group{gi}" if c == Q else f"group{gi}_{c}"].replay()
-                if c == Q:  # (a partial group's last window records it, compute_window)
-                    self.ev_train[gi].record(self.stream)
-                self.ev_prep[1 - gi].record(self.stream)
+                    self.graphs[tail if last else
+                                f"group{gi}" if c == Q else f"group{gi}_{c}"].replay()
+                # every group graph marks its trains done (the overlapped
+                # prologue waits on the group it overwrites)
+                self.ev_train[gi].record(self.stream)
+                if not last:
+                    self.ev_prep[1 - gi].record(self.stream)
+                self._tail_clean = last
                 self._last = (gi, c - 1)
                 self.dm.host_steps += c
                 self.windows_done += c
@@ -629,6 +687,7 @@ class StepRunner:
 
     def _run_host_batches(self, batches):
         Q = self.Q
+        self._tail_clean = False
         chunks = [batches[i:i + Q] for i in range(0, len(batches), Q)]
         prep_s = self.prep_stream if self.pipeline else self.stream
         ngroups = len(self.groups)

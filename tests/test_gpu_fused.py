@@ -261,3 +261,50 @@ def test_group_graphs_match_window_graphs(golden_sampling):
     np.testing.assert_allclose(outs[1][0], outs[0][0], rtol=1e-5)
     for a, b in zip(outs[1][1], outs[0][1]):
         assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+@pytest.mark.gpu
+def test_epoch_boundary_overlap_matches_serial(golden_sampling):
+    """steps() across epochs: each epoch's last group runs train-only and the
+    next epoch's first prep runs beside it in the other slot group (g0
+    alternates).  Losses of every epoch and the final weights match the
+    per-window schedule whose epoch boundaries are fully serialised."""
+    hg = make_g2(golden_sampling)
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, golden_sampling["g2/mask10"])
+    B, E = 64, 4
+    perms = [epoch_permutation(hg.train_mask, 5, e) for e in range(E)]
+    n_win = -(-perms[0].size // B)
+    outs = []
+    for overlapped in (False, True):
+        st = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        r = mq.StepRunner(g, st, fanouts=(4, 3), batch_size=B, num_train=perms[0].size,
+                          cache=cache, seed=5, queue_depth=3)
+        r.begin_epoch(0, perms[0])
+        r.capture()
+        c_last = (n_win - 1) % 3 + 1
+        assert f"tgroup0_{c_last}" in r.graphs and f"tgroup1_{c_last}" in r.graphs
+        losses, starts = [], []
+        for e in range(E):
+            if e:
+                r.begin_epoch(e, perms[e])
+            starts.append(r.g0)
+            if overlapped:
+                assert r.steps(n_win) == n_win
+                assert r._tail_clean
+            else:
+                for _ in range(n_win):
+                    r.step()
+            # the epoch's losses copied on the train stream: no host sync, so
+            # the next begin_epoch really overlaps this epoch's last group
+            with torch.cuda.stream(r.stream):
+                losses.append(r.loss_ring[:n_win].clone())
+        r.check_finite()
+        losses = [x.cpu().numpy() for x in losses]
+        if overlapped and -(-n_win // 3) % 2 == 1:  # odd group count: the start group alternates
+            assert starts == [0, 1, 0, 1]
+        outs.append((losses, [w.cpu().numpy() for w in st.weights]))
+    for a, b in zip(outs[1][0], outs[0][0]):
+        np.testing.assert_allclose(a, b, rtol=1e-5)
+    for a, b in zip(outs[1][1], outs[0][1]):
+        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
