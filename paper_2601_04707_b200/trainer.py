@@ -150,6 +150,7 @@ class StepRunner:
         # OTHER group's slots (g0 alternates), instead of after it
         self.g0 = 0
         self._tail_clean = False
+        self._pending_prep = None  # group whose prep a train-only tail deferred
         self._perm_stage = None
         self._perm_i = 0
         self._epoch_windows = -(-self.num_train // (self.batch_size * self.world))
@@ -215,6 +216,7 @@ class StepRunner:
         self.epoch = epoch
         self.windows_done = 0
         self._tail_clean = False
+        self._pending_prep = None  # the new epoch's prologue prepares its first group
         self.dm.ensure_bias(self.dm.host_steps + self._epoch_windows + 8)
         self._primed = False
         if self.pipeline and (self.graphs or not self.use_graph):
@@ -388,14 +390,17 @@ class StepRunner:
                         cur.wait_stream(self.prep_stream)
                     self._capture({f"group{gi}" if k == self.Q else f"group{gi}_{k}": group})
             if not self.multi and self.trace_buf is None:
-                # an epoch's last group without the forked prep of the group
-                # after it (the next epoch's first prep replaces that fork)
-                c = (self._epoch_windows - 1) % self.Q + 1
+                # train-only groups, without the forked prep of the group after
+                # them: an epoch's last group (the next epoch's first prep
+                # replaces that fork) and a steps() call's partial tail (the
+                # fork waits until more windows are asked for)
+                sizes = set(range(1, self.Q)) | {(self._epoch_windows - 1) % self.Q + 1}
                 for gi in range(2):
-                    def tgroup(s, gi=gi, c=c):
-                        for q in range(c):
-                            phases[f"train{gi}_{q}"](s)
-                    self._capture({f"tgroup{gi}_{c}": tgroup})
+                    for c in sorted(sizes):
+                        def tgroup(s, gi=gi, c=c):
+                            for q in range(c):
+                                phases[f"train{gi}_{q}"](s)
+                        self._capture({f"tgroup{gi}_{c}": tgroup})
         if self.pipeline and not self._primed:
             self._prologue()
 
@@ -429,9 +434,20 @@ class StepRunner:
 
     # RaCoM protocol (racom.WindowDriver): compute -> exchange grad64 -> apply.
     # A lone replica's train graph already contains its update.
+    def _flush_prep(self):
+        """Issue the next group's prep that a train-only tail held back."""
+        p = self._pending_prep
+        if p is None:
+            return
+        self._pending_prep = None
+        self.prep_stream.wait_event(self.ev_train[p])  # its previous trains
+        self._run(f"prep{p}", self.prep_stream)
+        self.ev_prep[p].record(self.prep_stream)
+
     def compute_window(self):
         k, Q = self.windows_done, self.Q
         q = k % Q
+        self._flush_prep()
         self._tail_clean = False
         if self.pipeline:
             if not self._primed:
@@ -483,6 +499,7 @@ class StepRunner:
         n = min(n, epoch_windows - self.windows_done)
         done = 0
         Q = self.Q
+        self._flush_prep()
         while done < n:
             k = self.windows_done
             if self.use_graph and self.pipeline and "group0" in self.graphs and k % Q == 0:
@@ -494,16 +511,21 @@ class StepRunner:
                 # the next epoch's first prep beside it)
                 tail = f"tgroup{gi}_{c}"
                 last = k + c == epoch_windows and tail in self.graphs
+                # this call's partial tail mid-epoch: train only as well; the
+                # next group's prep is issued by the next call (_flush_prep)
+                defer = not last and c < Q and tail in self.graphs
                 with torch.cuda.stream(self.stream):
                     # the group graph joins its own prep branch; prep(1-gi)
                     # overwrites the other half, whose last trains preceded it
                     self.stream.wait_event(self.ev_prep[gi])
-                    self.graphs[tail if last else
+                    self.graphs[tail if last or defer else
                                 f"group{gi}" if c == Q else f"group{gi}_{c}"].replay()
                 # every group graph marks its trains done (the overlapped
                 # prologue waits on the group it overwrites)
                 self.ev_train[gi].record(self.stream)
-                if not last:
+                if defer:
+                    self._pending_prep = 1 - gi
+                elif not last:
                     self.ev_prep[1 - gi].record(self.stream)
                 self._tail_clean = last
                 self._last = (gi, c - 1)
@@ -687,6 +709,7 @@ class StepRunner:
 
     def _run_host_batches(self, batches):
         Q = self.Q
+        self._flush_prep()
         self._tail_clean = False
         chunks = [batches[i:i + Q] for i in range(0, len(batches), Q)]
         prep_s = self.prep_stream if self.pipeline else self.stream

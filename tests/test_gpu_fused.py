@@ -308,3 +308,39 @@ def test_epoch_boundary_overlap_matches_serial(golden_sampling):
         np.testing.assert_allclose(a, b, rtol=1e-5)
     for a, b in zip(outs[1][1], outs[0][1]):
         assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+@pytest.mark.gpu
+def test_steps_tails_defer_the_next_prep(golden_sampling):
+    """steps() calls that end inside a slot group run the tail train-only and
+    hold the next group's prep back until the next call (_flush_prep); calls
+    of 5 and 4 windows mix group graphs, deferred tails and single windows and
+    still train like one window at a time."""
+    hg = make_g2(golden_sampling)
+    g = DeviceGraph.from_csr(hg)
+    cache = mq.DeviceCache(g, golden_sampling["g2/mask10"])
+    perm = epoch_permutation(hg.train_mask, 5, 0)
+    B = 64
+    n_win = -(-perm.size // B)
+    outs = []
+    for chunked in (False, True):
+        st = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        r = mq.StepRunner(g, st, fanouts=(4, 3), batch_size=B, num_train=perm.size, cache=cache,
+                          seed=5, queue_depth=3)
+        r.begin_epoch(0, perm)
+        r.capture()
+        done, deferred = 0, 0
+        while done < n_win:
+            if chunked:
+                done += r.steps(5 if (done // 5) % 2 == 0 else 4)
+                deferred += r._pending_prep is not None
+            else:
+                r.step()
+                done += 1
+        if chunked:
+            assert deferred > 0
+        r.check_finite()
+        outs.append((r.losses(n_win), [w.cpu().numpy() for w in st.weights]))
+    np.testing.assert_allclose(outs[1][0], outs[0][0], rtol=1e-5)
+    for a, b in zip(outs[1][1], outs[0][1]):
+        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
