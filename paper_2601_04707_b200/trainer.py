@@ -189,7 +189,7 @@ class StepRunner:
         staged.numpy()[:] = perm
         # the caller's queued work (model / cache updates) first
         self._join_current()
-        overlap = (self._tail_clean and self.pipeline and self.use_graph and not self.multi
+        overlap = (self._tail_clean and self.pipeline and self.use_graph
                    and self.trace_buf is None and self.windows_done == self._epoch_windows
                    and os.environ.get("MQ_EPOCH_OVERLAP", "1") != "0")
         if overlap:
@@ -389,7 +389,7 @@ class StepRunner:
                             ph(cur.cuda_stream)
                         cur.wait_stream(self.prep_stream)
                     self._capture({f"group{gi}" if k == self.Q else f"group{gi}_{k}": group})
-            if not self.multi and self.trace_buf is None:
+            if self.trace_buf is None:
                 # train-only groups, without the forked prep of the group after
                 # them: an epoch's last group (the next epoch's first prep
                 # replaces that fork) and a steps() call's partial tail (the

@@ -265,3 +265,73 @@ def test_straggler_injection_changes_nothing(tmp_path):
             assert np.abs(b[f"w{l}"] - w).max() <= 1e-6 * np.abs(w).max()
     for l in range(2):
         np.testing.assert_array_equal(slow[0][f"w{l}"], slow[1][f"w{l}"])
+
+
+def _steps_worker(rank, world, port, out_dir, mode):
+    """One rank: a StepRunner over the in-graph peer exchange trains 3 epochs,
+    either through steps() in 5- / 4-window calls (group graphs, deferred
+    tails, single windows, epoch-boundary overlap: the bench's multi-rank
+    path) or through step(), one window at a time (serialised boundaries).
+    One graph runner per process, as in the bench and run_epoch (DESIGN 7b:
+    a second graph runner with a fresh exchange in the same processes
+    trains wrong)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    import paper_2601_04707_b200 as mq
+    from paper_2601_04707_b200.graph import DeviceGraph
+    from paper_2601_04707_b200.runtime import epoch_permutation
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gs = load_golden("sampling.npz")
+        hg = make_g2(gs)
+        g = DeviceGraph.from_csr(hg)
+        cache = mq.DeviceCache(g, gs["g2/mask10"])
+        B = 64
+        perms = [epoch_permutation(hg.train_mask, 5, e) for e in range(3)]
+        windows = -(-perms[0].size // (B * world))
+        st = mq.init_model(16, 16, 5, num_layers=2, seed=5, learning_rate=0.01)
+        fx = mq.PeerExchange(st.dev.num_params, g.device, lag=0, ring=4)
+        r = mq.StepRunner(g, st, fanouts=(4, 3), batch_size=B, num_train=perms[0].size,
+                          cache=cache, seed=5, world=world, rank=rank, multi=True,
+                          queue_depth=3, exchange=fx)
+        r.begin_epoch(0, perms[0])
+        r.capture()
+        losses = []
+        for e in range(3):
+            if e:
+                r.finish()
+                r.begin_epoch(e, perms[e])
+            done, c = 0, 0
+            while done < windows:
+                if mode == "chunked":
+                    done += r.steps(5 if c % 2 == 0 else 4, windows)
+                else:
+                    r.step()
+                    done += 1
+                c += 1
+            with torch.cuda.stream(r.stream):  # no host sync between epochs
+                losses.append(r.loss_ring[:windows].clone())
+        r.finish()
+        r.check_finite()
+        np.savez(os.path.join(out_dir, f"rank{rank}_{mode}.npz"),
+                 losses=np.concatenate([x.cpu().numpy() for x in losses]),
+                 **{f"w{l}": w.cpu().numpy() for l, w in enumerate(st.weights)})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_steps_match_windows(tmp_path):
+    world = 2
+    for mode in ("chunked", "windows"):
+        mp.start_processes(_steps_worker, args=(world, _free_port(), str(tmp_path), mode),
+                           nprocs=world, join=True, start_method="spawn")
+    for rank in range(world):
+        c = np.load(tmp_path / f"rank{rank}_chunked.npz")
+        w = np.load(tmp_path / f"rank{rank}_windows.npz")
+        np.testing.assert_allclose(c["losses"], w["losses"], rtol=1e-5)
+        for l in range(2):
+            assert np.abs(c[f"w{l}"] - w[f"w{l}"]).max() <= 1e-5 * np.abs(w[f"w{l}"]).max()
+    for l in range(2):  # the ranks fold the same packets in the same order
+        a = np.load(tmp_path / "rank0_chunked.npz")[f"w{l}"]
+        np.testing.assert_array_equal(a, np.load(tmp_path / "rank1_chunked.npz")[f"w{l}"])
